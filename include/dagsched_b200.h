@@ -1,0 +1,204 @@
+/* dagsched_b200 — C-ABI drop-in boundary for the DAG-scheduler hot path on B200.
+ *
+ * The reference (arxiv/paper_2602_20826, /root/reference/proj) has no FFI: its
+ * boundary is the C++ library API of static lib `dagsched`
+ * (proj/include/dagsched/*.hpp). This header is the thin C layer underneath the
+ * kept C++ API (include/dagsched/*.hpp in this repo); every entry point names
+ * the reference function it replaces.
+ *
+ * Rules: POD structs only; the caller owns every buffer; no exceptions cross
+ * this boundary; every function returns a DS_* status and sets a thread-local
+ * message readable with ds_last_error().
+ */
+#ifndef DAGSCHED_B200_H
+#define DAGSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ----------------------------------------------------------- status codes */
+#define DS_OK 0
+#define DS_EINVAL 1      /* std::invalid_argument: bad Platform / GenConfig / args  */
+#define DS_EOVERFLOW 3   /* std::overflow_error: exact value outside the ABI range */
+#define DS_ECUDA 4       /* CUDA runtime error                                     */
+#define DS_EINVARIANT 5  /* std::logic_error: scheduler/simulator invariant broken */
+#define DS_ETOOBIG 6     /* DAG larger than DS_MAX_NODES                           */
+#define DS_ENOMEM 7
+#define DS_ENODEV 8      /* no CUDA device / extension cannot run                  */
+/* ValidationError family (dag.cpp:22-138, scheduler.cpp:177-182), one code per
+ * message so parity can be checked per DAG. Checked in the reference's order. */
+#define DS_E_EMPTY 10      /* "task has no nodes"                         dag.cpp:26  */
+#define DS_E_DUP_ID 11     /* "duplicate node id"                         dag.cpp:30-34 */
+#define DS_E_LOAD 12       /* "load ... below minimum"                    dag.cpp:35-41 */
+#define DS_E_PERIOD 13     /* "period must be positive"                   dag.cpp:42-44 */
+#define DS_E_EDGE 14       /* "edge ... references unknown node"          dag.cpp:57-60 */
+#define DS_E_SELFLOOP 15   /* "cycle detected: self-loop"                 dag.cpp:61-64 */
+#define DS_E_CYCLE 16      /* "cycle detected involving nodes"            dag.cpp:89-95 */
+#define DS_E_SOURCES 17    /* "expected a single source node"             dag.cpp:102-105 */
+#define DS_E_SINKS 18      /* "expected a single sink node"               dag.cpp:106-108 */
+#define DS_E_LOAD_TMIN 19  /* "load below the platform time unit"         scheduler.cpp:177-182 */
+
+/* Largest DAG the device path accepts (node-index masks are 4 x 64 bits). */
+#define DS_MAX_NODES 256
+
+/* Bound slots / method mask bits. Methods mirror experiment.hpp:14
+ * (Method::{proposed, greedy, greedy_unaware, graham_para}); LOWER is
+ * lower_bound (analysis.cpp:72-81). */
+#define DS_BOUND_PROPOSED 0
+#define DS_BOUND_GREEDY 1
+#define DS_BOUND_GREEDY_UNAWARE 2
+#define DS_BOUND_GRAHAM_PARA 3
+#define DS_BOUND_LOWER 4
+#define DS_N_BOUNDS 5
+#define DS_M_PROPOSED (1u << DS_BOUND_PROPOSED)
+#define DS_M_GREEDY (1u << DS_BOUND_GREEDY)
+#define DS_M_GREEDY_UNAWARE (1u << DS_BOUND_GREEDY_UNAWARE)
+#define DS_M_GRAHAM_PARA (1u << DS_BOUND_GRAHAM_PARA)
+#define DS_M_LOWER (1u << DS_BOUND_LOWER)
+#define DS_M_ALL 0x1fu
+
+/* Flags for the batch entry points. */
+#define DS_F_DEVICE_PTRS 1u /* batch and result pointers are device memory on `device` */
+#define DS_F_PINNED 2u      /* (corpus generation) allocate host arrays pinned         */
+
+/* --------------------------------------------------------------- inputs */
+/* Platform (exec_model.hpp:11-19): M identical SMs and the time floor t_min. */
+typedef struct ds_platform {
+    int32_t sm_count;
+    int32_t reserved;
+    int64_t tmin_num;
+    int64_t tmin_den;
+} ds_platform;
+
+/* Packed batch of DAGs (the batch form of std::vector<DagTask>).
+ * DAG d owns nodes [node_off[d], node_off[d+1]) in ascending-id order — the
+ * local index of a node is the rank of its id, which is how every "ties by
+ * id" rule of the reference is preserved — and edges
+ * [edge_off[d], edge_off[d+1]), each packed as (from_local << 16) | to_local.
+ * Loads are exact rationals load_num/load_den (den > 0, need not be reduced);
+ * load_den == NULL means every denominator is 1. */
+typedef struct ds_dag_batch {
+    uint64_t n_dags;
+    const uint32_t* node_off; /* [n_dags + 1] */
+    const uint32_t* edge_off; /* [n_dags + 1] */
+    const int64_t* load_num;  /* [node_off[n_dags]] */
+    const int64_t* load_den;  /* [node_off[n_dags]] or NULL */
+    const uint32_t* edges;    /* [edge_off[n_dags]] */
+} ds_dag_batch;
+
+/* Per-DAG results of the batched analysis (evaluate_corpus + lower_bound). */
+typedef struct ds_results {
+    int32_t* status;   /* [n_dags] DS_OK or a per-DAG DS_E* / DS_EOVERFLOW code   */
+    int64_t* bounds;   /* [n_dags * 10]: bound k at (2k, 2k+1) = (num, den), reduced,
+                          den > 0; 0/0 when the method bit was not requested       */
+    uint16_t* n_groups;/* optional [n_dags]: executed balanced groups (may be NULL) */
+} ds_results;
+
+/* GenConfig (generator.hpp:15-28). */
+typedef struct ds_gen_config {
+    int32_t depth_min, depth_max, max_width, integer_loads;
+    int64_t avg_load_num, avg_load_den;
+    double load_jitter, edge_density;
+    uint64_t seed;
+    int64_t tmin_num, tmin_den;
+    int32_t exact_mean, reserved;
+} ds_gen_config;
+
+/* ------------------------------------------------- schedule detail output */
+/* EntityRecord (scheduler.hpp:31-39) minus preds, in creation order: for each
+ * executed group its launches (launch order) then its members (id order). */
+typedef struct ds_entity_rec {
+    uint16_t origin;      /* local node index (EntityId::origin)                 */
+    uint16_t generation;  /* EntityId::generation                                */
+    uint8_t part;         /* 0 whole, 1 parallel, 2 residual (EntityId::Part)    */
+    uint8_t launched;     /* EntityRecord::launched                              */
+    uint16_t group;       /* executed-group index                                */
+    int32_t parallelism;  /* SMs held                                            */
+    int32_t reserved;
+    int64_t load_num, load_den;  /* EntityRecord::load                           */
+    int64_t exec_num, exec_den;  /* EntityRecord::exec (= duration for launches) */
+    int64_t res_num, res_den;    /* parallel segments: residual load left behind  */
+} ds_entity_rec;
+
+/* GroupPlan (scheduler.hpp:56-64) plus what is needed to materialise the
+ * augmented graph (extra deps) on the host. */
+typedef struct ds_group_rec {
+    int64_t resp_num, resp_den;  /* GroupPlan::response                          */
+    int32_t spare_sms;           /* GroupPlan::spare_sms                         */
+    uint16_t div_group;          /* index of the division group it executes      */
+    uint16_t bottleneck;         /* entity index (within the DAG) of v_R         */
+    uint16_t first_entity;       /* launches then members, contiguous            */
+    uint16_t n_launches;
+    uint16_t n_members;
+    uint16_t reserved;
+    uint64_t unlaunched[4];      /* node mask: candidates not launched whole
+                                    (they get the extra dep v_R -> candidate)    */
+} ds_group_rec;
+
+/* Capacities: entities per DAG <= 2 n, executed groups per DAG <= n. Slot bases
+ * are 2*node_off[d] for entities and node_off[d] for groups. */
+typedef struct ds_scheme_out {
+    int32_t* status;          /* [n_dags]                                        */
+    uint16_t* n_entities;     /* [n_dags]                                        */
+    uint16_t* n_groups;       /* [n_dags]                                        */
+    uint16_t* n_div_groups;   /* [n_dags] size of the division Π                 */
+    int16_t* node_block;      /* [N] block index of each node (build_blocks)     */
+    int16_t* node_div_group;  /* [N] division group of each node (build_groups)  */
+    ds_entity_rec* entities;  /* [2N]                                            */
+    ds_group_rec* groups;     /* [N]                                             */
+    int64_t* bounds;          /* [n_dags * 10] as in ds_results                  */
+} ds_scheme_out;
+
+/* ------------------------------------------------------------- functions */
+const char* ds_last_error(void);
+const char* ds_version(void);
+int ds_device_count(int* count);
+
+/* Batched bound analysis — replaces evaluate_corpus (experiment.cpp:52-79 with
+ * method_bound :27-39) plus lower_bound (analysis.cpp:72-81). One warp per DAG.
+ * Host pointers (pinned or pageable) unless DS_F_DEVICE_PTRS; `stream` is a
+ * cudaStream_t (NULL = a library stream). Synchronous for host pointers,
+ * asynchronous on `stream` for device pointers. */
+int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform,
+                     uint32_t method_mask, ds_results* out, int device, void* stream,
+                     uint32_t flags);
+
+/* Same, sharded as contiguous DAG ranges over `devices` (one host thread per
+ * device, no collective), host pointers only; results land in DAG order. */
+int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platform,
+                           uint32_t method_mask, ds_results* out, const int* devices,
+                           int n_devices);
+
+/* Full schedule detail — replaces schedule() (scheduler.cpp:175-427) and
+ * build_blocks/build_groups (division.cpp:10-126) for a batch; host pointers. */
+int ds_schedule_batch(const ds_dag_batch* batch, const ds_platform* platform,
+                      ds_scheme_out* out, int device);
+
+/* Corpus generation on the host — replaces generate_corpus (generator.cpp:98-108)
+ * with identical RNG call order; parallel over seeds. The handle owns packed
+ * arrays (pinned when DS_F_PINNED) exposed through ds_corpus_view. */
+int ds_corpus_generate(const ds_gen_config* cfg, int64_t count, uint32_t flags,
+                       void** handle);
+int ds_corpus_view(void* handle, ds_dag_batch* view);
+void ds_corpus_free(void* handle);
+
+/* Timed-analysis session: uploads a batch once and replays the kernel on it
+ * (bench.py's device-resident `value` leg). */
+int ds_session_create(const ds_dag_batch* batch, const ds_platform* platform,
+                      uint32_t method_mask, int device, void** session);
+/* Launches the analysis kernel on the session's stream; returns the kernel's
+ * duration in ms measured with CUDA events on that stream. */
+int ds_session_run(void* session, float* kernel_ms);
+/* Copies results of the last run back to host buffers. */
+int ds_session_results(void* session, ds_results* out);
+int ds_session_free(void* session);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DAGSCHED_B200_H */

@@ -1,0 +1,142 @@
+"""TEST INFRASTRUCTURE — ctypes bindings for the two CPU checkers.
+
+* ``Checker("ref")``    -> oracle/_ref/libdagsched_ref.so, the reference's own
+  sources compiled against oracle/shim (see oracle/Makefile).
+* ``Checker("oracle")`` -> oracle/_build/libdagsched_oracle.so, the independent
+  restatement in oracle/src.
+
+Both implement oracle/oracle_api.h over the packed batch format of
+include/dagsched_b200.h. Never imported by the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+
+from paper_2602_20826_b200 import _abi
+from paper_2602_20826_b200.batch import DagBatch, from_arrays
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIBS = {
+    "ref": os.path.join(HERE, "_ref", "libdagsched_ref.so"),
+    "oracle": os.path.join(HERE, "_build", "libdagsched_oracle.so"),
+}
+PREFIX = {"ref": "ref_", "oracle": "orc_"}
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(LIBS[kind])
+
+
+def platform(sm_count: int, t_min=1) -> _abi.ds_platform:
+    t = Fraction(t_min)
+    return _abi.ds_platform(int(sm_count), 0, t.numerator, t.denominator)
+
+
+def gen_config(depth_min=5, depth_max=8, max_width=8, avg_load=20, load_jitter=0.5,
+               edge_density=0.2, seed=1, integer_loads=True, exact_mean=False,
+               t_min=1) -> _abi.ds_gen_config:
+    a, t = Fraction(avg_load), Fraction(t_min)
+    return _abi.ds_gen_config(depth_min, depth_max, max_width, int(integer_loads),
+                              a.numerator, a.denominator, float(load_jitter),
+                              float(edge_density), int(seed), t.numerator, t.denominator,
+                              int(exact_mean), 0)
+
+
+class Checker:
+    def __init__(self, kind: str = "ref"):
+        if not available(kind):
+            raise FileNotFoundError(f"{LIBS[kind]} not built (make -C oracle)")
+        self.kind = kind
+        self.lib = C.CDLL(LIBS[kind])
+        p = PREFIX[kind]
+        self._f = {}
+        sig = {
+            "last_error": (C.c_char_p, []),
+            "free": (None, [C.c_void_p]),
+            "corpus_from_packed": (C.c_void_p, [C.POINTER(_abi.ds_dag_batch), C.c_int64, C.c_int64, C.c_void_p]),
+            "corpus_generate": (C.c_void_p, [C.POINTER(_abi.ds_gen_config), C.c_int64]),
+            "corpus_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+            "corpus_pack": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5),
+            "corpus_free": (None, [C.c_void_p]),
+            "corpus_evaluate": (C.c_double, [C.c_void_p, C.POINTER(_abi.ds_platform), C.c_uint32, C.c_int, C.c_void_p, C.c_void_p]),
+            "scheme_json": (C.c_void_p, [C.c_void_p, C.c_uint64, C.POINTER(_abi.ds_platform)]),
+            "analyze_json": (C.c_void_p, [C.c_void_p, C.c_uint64, C.POINTER(_abi.ds_platform)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(self.lib, p + name)
+            fn.restype = res
+            fn.argtypes = args
+            self._f[name] = fn
+
+    def error(self) -> str:
+        return (self._f["last_error"]() or b"").decode()
+
+    # ---------------------------------------------------------------- corpora
+    def corpus(self, batch: DagBatch, min_load=1) -> "Corpus":
+        m = Fraction(min_load)
+        st = np.zeros(batch.n_dags, np.int32)
+        cb = batch.as_c(with_den=True)
+        h = self._f["corpus_from_packed"](C.byref(cb), m.numerator, m.denominator, st.ctypes.data)
+        return Corpus(self, h, batch.n_dags, st)
+
+    def generate(self, count: int, **cfg) -> "Corpus":
+        g = gen_config(**cfg)
+        h = self._f["corpus_generate"](C.byref(g), int(count))
+        if not h:
+            raise ValueError(self.error())
+        return Corpus(self, h, count, np.zeros(count, np.int32))
+
+
+class Corpus:
+    def __init__(self, chk: Checker, handle, n_dags: int, parse_status: np.ndarray):
+        self.chk, self.h, self.n_dags, self.parse_status = chk, handle, n_dags, parse_status
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.chk._f["corpus_free"](self.h)
+            self.h = None
+
+    def pack(self) -> DagBatch:
+        n, nn, ne = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.chk._f["corpus_size"](self.h, C.byref(n), C.byref(nn), C.byref(ne))
+        node_off = np.zeros(n.value + 1, np.uint32)
+        edge_off = np.zeros(n.value + 1, np.uint32)
+        ln = np.zeros(nn.value, np.int64)
+        ld = np.zeros(nn.value, np.int64)
+        ed = np.zeros(ne.value, np.uint32)
+        rc = self.chk._f["corpus_pack"](self.h, node_off.ctypes.data, edge_off.ctypes.data,
+                                        ln.ctypes.data, ld.ctypes.data, ed.ctypes.data)
+        if rc != 0:
+            raise ValueError(self.chk.error())
+        return from_arrays(node_off, edge_off, ln, ld, ed)
+
+    def evaluate(self, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, parallel=True):
+        """-> (status int32[n], bounds int64[n, 10], seconds)."""
+        st = self.parse_status.copy()
+        b = np.zeros((self.n_dags, 10), np.int64)
+        pl = platform(sm_count, t_min)
+        secs = self.chk._f["corpus_evaluate"](self.h, C.byref(pl), mask, int(parallel),
+                                              st.ctypes.data, b.ctypes.data)
+        return st, b, secs
+
+    def _json(self, fn: str, d: int, sm_count: int, t_min):
+        pl = platform(sm_count, t_min)
+        p = self.chk._f[fn](self.h, d, C.byref(pl))
+        if not p:
+            raise RuntimeError(self.chk.error())
+        try:
+            return json.loads(C.string_at(p).decode())
+        finally:
+            self.chk._f["free"](p)
+
+    def scheme(self, d: int, sm_count: int, t_min=1) -> dict:
+        """write_scheme() JSON of schedule(task d) (task_io.cpp:94-148)."""
+        return self._json("scheme_json", d, sm_count, t_min)
+
+    def analyze(self, d: int, sm_count: int, t_min=1) -> dict:
+        return self._json("analyze_json", d, sm_count, t_min)

@@ -1,0 +1,57 @@
+/* TEST INFRASTRUCTURE — oracle only (tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs). Never part of the product.
+ *
+ * One C interface, two implementations:
+ *   oracle/_ref/libdagsched_ref.so   the reference's own sources
+ *                                    (/root/reference/proj/src/*.cpp) compiled
+ *                                    unmodified against oracle/shim/ (prefix ref_)
+ *   oracle/_build/libdagsched_oracle.so  the independent restatement in
+ *                                    oracle/src/ (prefix orc_)
+ * Both speak the packed batch format of include/dagsched_b200.h (ds_dag_batch):
+ * per DAG a contiguous node range in id order (local index = rank of the id)
+ * and a contiguous edge range of (from << 16) | to local-index pairs.
+ *
+ * Bounds layout: bounds[d * 10 + 2 * k + {0: num, 1: den}], k in
+ * DS_BOUND_{PROPOSED, GREEDY, GREEDY_UNAWARE, GRAHAM_PARA, LOWER}; a bound that
+ * was not requested is written as 0/0. Status codes are the DS_* codes.
+ */
+#ifndef DAGSCHED_ORACLE_API_H
+#define DAGSCHED_ORACLE_API_H
+
+#include <stdint.h>
+
+#include "../include/dagsched_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORACLE_DECLARE(P)                                                            \
+    const char* P##last_error(void);                                                 \
+    void P##free(void* p);                                                           \
+    /* corpus handle: parsed DagTasks held in the implementation's own types */      \
+    void* P##corpus_from_packed(const ds_dag_batch* batch, int64_t min_load_num,     \
+                                int64_t min_load_den, int32_t* status);              \
+    void* P##corpus_generate(const ds_gen_config* cfg, int64_t count);               \
+    int P##corpus_size(void* h, uint64_t* n_dags, uint64_t* n_nodes,                 \
+                       uint64_t* n_edges);                                           \
+    int P##corpus_pack(void* h, uint32_t* node_off, uint32_t* edge_off,              \
+                       int64_t* load_num, int64_t* load_den, uint32_t* edges);       \
+    void P##corpus_free(void* h);                                                    \
+    /* evaluate_corpus (+ lower_bound) over the handle; returns wall seconds */      \
+    double P##corpus_evaluate(void* h, const ds_platform* plat, uint32_t method_mask,\
+                              int parallel, int32_t* status, int64_t* bounds);       \
+    /* one DAG (index d of the handle) -> JSON text, caller frees with P##free */   \
+    char* P##scheme_json(void* h, uint64_t d, const ds_platform* plat);              \
+    char* P##analyze_json(void* h, uint64_t d, const ds_platform* plat);
+
+ORACLE_DECLARE(ref_)
+ORACLE_DECLARE(orc_)
+
+#undef ORACLE_DECLARE
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
