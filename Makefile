@@ -1,0 +1,44 @@
+# Build of the product library (sm_100a) and the test-only CPU checkers.
+#
+#   make            -> paper_2602_20826_b200/_lib/libdagsched_b200.so   (product)
+#                      oracle/_build/libdagsched_oracle.so               (checker)
+#                      oracle/_ref/libdagsched_ref.so  (only if /root/reference exists)
+# nvcc cross-compiles for sm_100a here; no GPU is needed to build.
+
+NVCC    ?= /usr/local/cuda/bin/nvcc
+CXX     ?= g++
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_2602_20826_b200
+LIBDIR  := $(PKG)/_lib
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v --expt-relaxed-constexpr
+CXXFLAGS:= -std=c++17 -O3 -fPIC -fopenmp -fvisibility=hidden -I/usr/local/cuda/include -Wall -Wno-comment
+LDOMP   := -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp -lpthread
+
+CU_SRCS := $(PKG)/csrc/capi.cu
+CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/dagsched_b200.h
+
+.PHONY: all product oracle ref clean
+all: product oracle ref
+
+product: $(LIBDIR)/libdagsched_b200.so
+
+$(LIBDIR)/capi.o: $(PKG)/csrc/capi.cu $(CU_DEPS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(LIBDIR)/ptxas_capi.txt || (cat $(LIBDIR)/ptxas_capi.txt; false)
+
+$(LIBDIR)/host_gen.o: $(PKG)/csrc/host_gen.cpp include/dagsched_b200.h
+	@mkdir -p $(LIBDIR)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libdagsched_b200.so: $(LIBDIR)/capi.o $(LIBDIR)/host_gen.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --exclude-libs,ALL $(LDOMP)
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; else echo "no /root/reference: using prebuilt oracle/_ref if present"; fi
+
+clean:
+	rm -rf $(LIBDIR)
+	$(MAKE) -C oracle clean

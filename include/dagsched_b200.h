@@ -80,7 +80,9 @@ typedef struct ds_platform {
  * id" rule of the reference is preserved — and edges
  * [edge_off[d], edge_off[d+1]), each packed as (from_local << 16) | to_local.
  * Loads are exact rationals load_num/load_den (den > 0, need not be reduced);
- * load_den == NULL means every denominator is 1. */
+ * load_den == NULL means every denominator is 1. Array indices are relative
+ * to the first offset: node i of the batch is load_num[i - node_off[0]], so a
+ * sub-batch is just shifted pointers (see ds_analyze_batch_multi). */
 typedef struct ds_dag_batch {
     uint64_t n_dags;
     const uint32_t* node_off; /* [n_dags + 1] */
@@ -154,6 +156,9 @@ typedef struct ds_scheme_out {
 } ds_scheme_out;
 
 /* ------------------------------------------------------------- functions */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 const char* ds_last_error(void);
 const char* ds_version(void);
 int ds_device_count(int* count);
@@ -196,6 +201,10 @@ int ds_session_run(void* session, float* kernel_ms);
 /* Copies results of the last run back to host buffers. */
 int ds_session_results(void* session, ds_results* out);
 int ds_session_free(void* session);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }

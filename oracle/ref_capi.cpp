@@ -113,11 +113,11 @@ void* ref_corpus_from_packed(const ds_dag_batch* b, int64_t min_num, int64_t min
         std::vector<DagNode> nodes;
         std::vector<std::pair<NodeId, NodeId>> edges;
         for (uint32_t i = b->node_off[d]; i < b->node_off[d + 1]; ++i) {
-            int64_t den = b->load_den ? b->load_den[i] : 1;
-            nodes.push_back(DagNode{i - b->node_off[d], rat(b->load_num[i], den)});
+            int64_t den = b->load_den ? b->load_den[i - b->node_off[0]] : 1;
+            nodes.push_back(DagNode{i - b->node_off[d], rat(b->load_num[i - b->node_off[0]], den)});
         }
         for (uint32_t e = b->edge_off[d]; e < b->edge_off[d + 1]; ++e) {
-            edges.emplace_back(b->edges[e] >> 16, b->edges[e] & 0xffffu);
+            edges.emplace_back(b->edges[e - b->edge_off[0]] >> 16, b->edges[e - b->edge_off[0]] & 0xffffu);
         }
         int st = guarded([&] {
             c->tasks.push_back(DagTask::make(std::move(nodes), std::move(edges),

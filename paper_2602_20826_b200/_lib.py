@@ -1,0 +1,195 @@
+"""Loader and thin Python bindings for libdagsched_b200.so (the C-ABI).
+
+The product path is the CUDA library; there is no CPU fallback. If the
+library is missing or no CUDA device is visible, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from .batch import DagBatch, combine_status
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libdagsched_b200.so")
+
+_lock = threading.Lock()
+_lib = None
+
+
+class DagschedError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_abi.STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _sig(lib):
+    P = C.POINTER
+    table = {
+        "ds_last_error": (C.c_char_p, []),
+        "ds_version": (C.c_char_p, []),
+        "ds_device_count": (C.c_int, [P(C.c_int)]),
+        "ds_analyze_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
+                                       P(_abi.ds_results), C.c_int, C.c_void_p, C.c_uint32]),
+        "ds_analyze_batch_multi": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
+                                             P(_abi.ds_results), P(C.c_int), C.c_int]),
+        "ds_schedule_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform),
+                                        P(_abi.ds_scheme_out), C.c_int]),
+        "ds_corpus_generate": (C.c_int, [P(_abi.ds_gen_config), C.c_int64, C.c_uint32, P(C.c_void_p)]),
+        "ds_corpus_view": (C.c_int, [C.c_void_p, P(_abi.ds_dag_batch)]),
+        "ds_corpus_free": (None, [C.c_void_p]),
+        "ds_session_create": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
+                                        C.c_int, P(C.c_void_p)]),
+        "ds_session_run": (C.c_int, [C.c_void_p, P(C.c_float)]),
+        "ds_session_results": (C.c_int, [C.c_void_p, P(_abi.ds_results)]),
+        "ds_session_free": (C.c_int, [C.c_void_p]),
+    }
+    for name, (res, args) in table.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+def lib():
+    """The loaded product library (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DagschedError(_abi.DS_ENODEV, f"{LIB_PATH} not built (run `make` or __graft_entry__.build())")
+            _lib = _sig(C.CDLL(LIB_PATH))
+        return _lib
+
+
+def check(rc: int):
+    if rc != _abi.DS_OK:
+        raise DagschedError(rc, lib().ds_last_error().decode())
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    rc = lib().ds_device_count(C.byref(n))
+    return n.value if rc == _abi.DS_OK else 0
+
+
+def platform(sm_count: int, t_min=1) -> _abi.ds_platform:
+    from fractions import Fraction
+    t = Fraction(t_min)
+    return _abi.ds_platform(int(sm_count), 0, t.numerator, t.denominator)
+
+
+def gen_config(depth_min=5, depth_max=8, max_width=8, avg_load=20, load_jitter=0.5,
+               edge_density=0.2, seed=1, integer_loads=True, exact_mean=False, t_min=1):
+    from fractions import Fraction
+    a, t = Fraction(avg_load), Fraction(t_min)
+    return _abi.ds_gen_config(depth_min, depth_max, max_width, int(integer_loads),
+                              a.numerator, a.denominator, float(load_jitter), float(edge_density),
+                              int(seed), t.numerator, t.denominator, int(exact_mean), 0)
+
+
+def _results(n: int, with_groups=True):
+    st = np.zeros(n, np.int32)
+    b = np.zeros((n, 10), np.int64)
+    ng = np.zeros(n, np.uint16) if with_groups else None
+    r = _abi.ds_results(st.ctypes.data, b.ctypes.data, ng.ctypes.data if ng is not None else None)
+    return st, b, ng, r
+
+
+def analyze(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
+    """Batched bound analysis on one GPU -> (status[n], bounds[n, 10], n_groups[n])."""
+    st, b, ng, r = _results(batch.n_dags)
+    cb = batch.as_c()
+    pl = platform(sm_count, t_min)
+    check(lib().ds_analyze_batch(C.byref(cb), C.byref(pl), mask, C.byref(r), device, None, 0))
+    return combine_status(batch.pack_status, st), b, ng
+
+
+def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = _abi.DS_M_ALL):
+    st, b, ng, r = _results(batch.n_dags)
+    cb = batch.as_c()
+    pl = platform(sm_count, t_min)
+    devs = (C.c_int * len(devices))(*devices)
+    check(lib().ds_analyze_batch_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
+    return combine_status(batch.pack_status, st), b, ng
+
+
+class Corpus:
+    """Host-generated corpus (product generator, generator.cpp semantics)."""
+
+    def __init__(self, count: int, pinned: bool = False, **cfg):
+        self.h = C.c_void_p()
+        g = gen_config(**cfg)
+        check(lib().ds_corpus_generate(C.byref(g), int(count), _abi.DS_F_PINNED if pinned else 0,
+                                       C.byref(self.h)))
+        self.view = _abi.ds_dag_batch()
+        check(lib().ds_corpus_view(self.h, C.byref(self.view)))
+        v = self.view
+        n = v.n_dags
+        self.n_dags = n
+
+        def arr(ptr, count, ct, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(count,)).view(dt)
+
+        self.node_off = arr(v.node_off, n + 1, C.c_uint32, np.uint32)
+        self.edge_off = arr(v.edge_off, n + 1, C.c_uint32, np.uint32)
+        nn, ne = int(self.node_off[-1]), int(self.edge_off[-1])
+        self.load_num = arr(v.load_num, nn, C.c_int64, np.int64)
+        self.load_den = arr(v.load_den, nn, C.c_int64, np.int64)
+        self.edges = arr(v.edges, ne, C.c_uint32, np.uint32)
+
+    def batch(self) -> DagBatch:
+        """Zero-copy DagBatch view (valid while this object lives)."""
+        b = DagBatch(self.node_off, self.edge_off, self.load_num, self.load_den, self.edges,
+                     np.zeros(self.n_dags, np.int32))
+        b._owner = self
+        return b
+
+    def close(self):
+        if self.h:
+            lib().ds_corpus_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Session:
+    """Device-resident batch; ``run()`` replays the analysis kernel(s)."""
+
+    def __init__(self, batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
+        self.h = C.c_void_p()
+        self.n = batch.n_dags
+        cb = batch.as_c()
+        pl = platform(sm_count, t_min)
+        check(lib().ds_session_create(C.byref(cb), C.byref(pl), mask, device, C.byref(self.h)))
+
+    def run(self) -> float:
+        ms = C.c_float(0)
+        check(lib().ds_session_run(self.h, C.byref(ms)))
+        return ms.value
+
+    def results(self):
+        st, b, ng, r = _results(self.n)
+        check(lib().ds_session_results(self.h, C.byref(r)))
+        return st, b, ng
+
+    def close(self):
+        if self.h:
+            lib().ds_session_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

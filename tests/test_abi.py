@@ -1,0 +1,107 @@
+"""CPU suite: the C-ABI library builds, loads and exports every symbol the
+header declares; ctypes layouts match the C compiler's; host-side pieces
+(corpus generator, packer) are exact; the device entry points fail loudly
+without a GPU instead of falling back to the CPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import bindings
+from paper_2602_20826_b200 import _abi, _lib
+from paper_2602_20826_b200.batch import combine_status, pack
+from tests import helpers
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dagsched_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        subprocess.run(["make", "-C", ROOT, "product"], check=True, capture_output=True)
+    return _lib.lib()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(ds_\w+)\(", text, re.M)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert len(names) >= 12
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ds_\w+)", out))
+    assert set(names) <= exported, set(names) - exported
+    for n in names:
+        assert hasattr(lib, n)
+
+
+def test_struct_layouts_match_c():
+    structs = ["ds_platform", "ds_dag_batch", "ds_results", "ds_gen_config", "ds_entity_rec",
+               "ds_group_rec", "ds_scheme_out"]
+    src = '#include <stdio.h>\n#include "dagsched_b200.h"\nint main(){\n' + "".join(
+        f'printf("{s} %zu\\n", sizeof({s}));\n' for s in structs) + "return 0;}\n"
+    with tempfile.TemporaryDirectory() as d:
+        with open(os.path.join(d, "s.c"), "w") as f:
+            f.write(src)
+        exe = os.path.join(d, "s")
+        subprocess.run(["gcc", "-I", os.path.dirname(HEADER), os.path.join(d, "s.c"), "-o", exe], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True).stdout
+    sizes = dict(line.split() for line in out.strip().splitlines())
+    for s in structs:
+        assert int(sizes[s]) == C.sizeof(getattr(_abi, s)), s
+
+
+@pytest.mark.parametrize("cfg", [dict(seed=1), dict(seed=12345, avg_load=200, max_width=16),
+                                 dict(seed=3, integer_loads=False, avg_load=5),
+                                 dict(seed=11, exact_mean=True, integer_loads=False, avg_load=7),
+                                 dict(seed=4, t_min="1/2", avg_load=9)])
+def test_host_generator_matches_reference_generator(lib, cfg):
+    """ds_corpus_generate (product, host C++) is bit-identical to the
+    reference's generate_corpus (generator.cpp:24-108)."""
+    chk = bindings.Checker("ref" if bindings.available("ref") else "oracle")
+    want = chk.generate(3000, **cfg).pack()
+    got = _lib.Corpus(3000, **cfg).batch()
+    for k in ("node_off", "edge_off", "load_num", "load_den", "edges"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+
+
+def test_generator_rejects_bad_config(lib):
+    with pytest.raises(_lib.DagschedError):
+        _lib.Corpus(10, depth_min=1)
+    with pytest.raises(_lib.DagschedError):
+        _lib.Corpus(10, load_jitter=2.0)
+    with pytest.raises(_lib.DagschedError):
+        _lib.Corpus(0)
+
+
+def test_packer_status_order():
+    # dag.cpp order: empty, duplicate id, load, edges (first in sorted order), cycle/sources/sinks
+    b = pack([([], []), ([(1, 1), (1, 2)], []), ([(0, 1)], [(0, 9)]), ([(0, 1), (1, 1)], [(1, 1), (0, 5)]),
+              ([(0, "1/2")], [(0, 7)])])
+    assert list(b.pack_status) == [_abi.DS_E_EMPTY, _abi.DS_E_DUP_ID, _abi.DS_E_EDGE, _abi.DS_E_EDGE,
+                                   _abi.DS_E_EDGE]
+    dev = np.array([0, 0, 0, 0, _abi.DS_E_LOAD], np.int32)
+    assert list(combine_status(b.pack_status, dev))[-1] == _abi.DS_E_LOAD  # load check precedes edges
+
+
+def test_fixture_packing_matches_raw():
+    for case in helpers.fixtures():
+        if case["status"] == 0:
+            a, b = helpers.fixture_batch(case), helpers.fixture_raw_batch(case)
+            assert np.array_equal(a.load_num, b.load_num)
+            assert sorted(set(b.edges.tolist())) == a.edges.tolist()
+
+
+def test_device_path_fails_loudly_without_gpu(lib):
+    if _lib.device_count() > 0:
+        pytest.skip("GPU present")
+    b = pack([([1, 2, 1], [(0, 1), (1, 2)])])
+    with pytest.raises(_lib.DagschedError):
+        _lib.analyze(b, 8)

@@ -1,0 +1,181 @@
+"""GPU parity suite for K1 (batched bound analysis) through the C-ABI.
+
+Every result is compared with the reference's own outputs (tests/golden,
+produced by the reference sources compiled in oracle/_ref) or with the
+restated oracle on seeded corpora. Integer/rational work: bit-exact.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import bindings
+from paper_2602_20826_b200 import _abi, _lib, scheme
+from paper_2602_20826_b200.batch import pack
+from tests import helpers
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return bindings.Checker("oracle")
+
+
+def test_fixtures_bounds_and_status():
+    for case in helpers.fixtures():
+        b = helpers.fixture_batch(case)
+        st, bounds, _ = _lib.analyze(b, case["sm_count"], case["t_min"])
+        assert int(st[0]) == case["status"], case["name"]
+        assert [int(x) for x in bounds[0]] == case["bounds"], case["name"]
+
+
+def test_fixture_schemes_match_reference_write_scheme():
+    for case in helpers.fixtures():
+        if case["status"] != 0:
+            continue
+        b = helpers.fixture_batch(case)
+        schemes, st = scheme.schedule_batch(b, case["sm_count"], case["t_min"])
+        got = scheme.to_reference_json(schemes[0])
+        assert helpers.normalise_scheme(got) == helpers.normalise_scheme(case["scheme"]), case["name"]
+
+
+@pytest.mark.parametrize("name,tag", [("corpus_default.npz", "default"), ("corpus_variants.npz", "heavy"),
+                                      ("corpus_variants.npz", "fractional"), ("corpus_variants.npz", "wide")])
+def test_golden_corpora(name, tag):
+    b, res, _ = helpers.corpus(name, tag)
+    for M, (st_ref, b_ref) in res.items():
+        st, bounds, _ = _lib.analyze(b, M)
+        assert np.array_equal(st, st_ref), M
+        bad = np.nonzero((bounds != b_ref).any(1))[0]
+        assert len(bad) == 0, (M, bad[:5], bounds[bad[:1]], b_ref[bad[:1]])
+
+
+def test_golden_schemes_group_membership_and_quotas():
+    b, _, _ = helpers.corpus()
+    recs = list(helpers.schemes())
+    for M in (8, 32, 148):
+        sub = b.slice(0, 120)
+        schemes, st = scheme.schedule_batch(sub, M)
+        for rec in recs:
+            if rec["sm_count"] != M:
+                continue
+            got = scheme.to_reference_json(schemes[rec["dag"]])
+            assert helpers.normalise_scheme(got) == helpers.normalise_scheme(rec["scheme"]), (M, rec["dag"])
+
+
+@pytest.mark.parametrize("cfg,Ms", [
+    (dict(seed=2024), (1, 2, 5, 8, 32, 64, 148, 1000)),
+    (dict(seed=7, avg_load=200, max_width=12), (8, 148, 300)),
+    (dict(seed=99, integer_loads=False, avg_load=5), (4, 148)),
+    (dict(seed=5, t_min="1/2", avg_load=9), (6, 148)),
+    (dict(seed=31, exact_mean=True, integer_loads=False, avg_load=7), (16, 148)),
+    (dict(seed=13, depth_min=6, depth_max=10, max_width=24, avg_load=40), (32, 148)),  # n > 64: W=4 kernel
+])
+def test_seeded_corpora_vs_oracle(orc, cfg, Ms):
+    n = 4000
+    gen = _lib.Corpus(n, **cfg)
+    b = gen.batch()
+    c = orc.corpus(b, min_load=cfg.get("t_min", 1))
+    for M in Ms:
+        tmin = cfg.get("t_min", 1)
+        st_o, b_o, _ = c.evaluate(M, tmin)
+        st, bounds, _ = _lib.analyze(b, M, tmin)
+        assert np.array_equal(st, st_o), M
+        bad = np.nonzero((bounds != b_o).any(1))[0]
+        assert len(bad) == 0, (M, bad[:5])
+
+
+def test_method_mask_subsets(orc):
+    b = _lib.Corpus(500, seed=3).batch()
+    _, full, _ = _lib.analyze(b, 148)
+    for mask in (1, 2, 4, 8, 16, 5, 0x1E):
+        st, part, _ = _lib.analyze(b, 148, mask=mask)
+        for k in range(5):
+            cols = part[:, 2 * k:2 * k + 2]
+            if mask >> k & 1:
+                assert np.array_equal(cols, full[:, 2 * k:2 * k + 2])
+            else:
+                assert not cols.any()
+
+
+def test_invalid_and_edge_dags():
+    dags = [
+        ([], []),                                          # empty
+        ([(0, 1), (0, 2)], []),                            # duplicate id
+        ([(0, 1), (1, 1)], [(0, 1), (1, 0)]),              # cycle
+        ([(0, 1)], [(0, 0)]),                              # self loop
+        ([(0, 1), (1, 1), (2, 1)], [(0, 2), (1, 2)]),      # two sources
+        ([(0, 1), (1, 1), (2, 1)], [(0, 1), (0, 2)]),      # two sinks
+        ([(0, "1/2")], []),                                # load below t_min
+        ([(0, 5)], []),                                    # single node
+        (list(range(1, 258)), [(i, i + 1) for i in range(256)]),  # 257 nodes: too big
+        ([(5, 3), (9, 4), (40, 2)], [(5, 9), (9, 40), (5, 40), (5, 9)]),  # sparse ids + duplicate edge
+    ]
+    b = pack(dags)
+    st, bounds, _ = _lib.analyze(b, 4)
+    assert list(st[:8]) == [_abi.DS_E_EMPTY, _abi.DS_E_DUP_ID, _abi.DS_E_CYCLE, _abi.DS_E_SELFLOOP,
+                            _abi.DS_E_SOURCES, _abi.DS_E_SINKS, _abi.DS_E_LOAD, _abi.DS_OK]
+    assert st[8] == _abi.DS_ETOOBIG
+    assert st[9] == _abi.DS_OK
+    assert not bounds[:7].any()
+
+
+def test_session_and_multi_and_device_pointers():
+    torch = pytest.importorskip("torch")
+    b = _lib.Corpus(20000, seed=8).batch()
+    st, bounds, ng = _lib.analyze(b, 148)
+    s = _lib.Session(b, 148)
+    for _ in range(3):
+        ms = s.run()
+        assert ms > 0
+    st2, b2, ng2 = s.results()
+    assert np.array_equal(st, st2) and np.array_equal(bounds, b2) and np.array_equal(ng, ng2)
+    st3, b3, _ = _lib.analyze_multi(b, 148, devices=[0, 0, 0])
+    assert np.array_equal(st, st3) and np.array_equal(bounds, b3)
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(getattr(b, k).view(np.int32) if getattr(b, k).dtype == np.uint32
+                             else getattr(b, k)).to(dev) for k in ("node_off", "edge_off", "load_num", "edges")}
+    out_st = torch.zeros(b.n_dags, dtype=torch.int32, device=dev)
+    out_b = torch.zeros(b.n_dags * 10, dtype=torch.int64, device=dev)
+    cb = _abi.ds_dag_batch(b.n_dags, t["node_off"].data_ptr(), t["edge_off"].data_ptr(), t["load_num"].data_ptr(),
+                           None, t["edges"].data_ptr())
+    r = _abi.ds_results(out_st.data_ptr(), out_b.data_ptr(), None)
+    pl = _lib.platform(148)
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), 0,
+                                           C.c_void_p(stream), _abi.DS_F_DEVICE_PTRS))
+    torch.cuda.synchronize()
+    assert np.array_equal(out_st.cpu().numpy(), st)
+    assert np.array_equal(out_b.cpu().numpy().reshape(-1, 10), bounds)
+
+
+def test_full_size_properties_and_sampled_parity(orc):
+    """BASELINE config C5 at full size (1M DAGs, M=148): size-independent
+    properties on every DAG plus oracle parity on a 20k random sample."""
+    n = 1_000_000
+    b = _lib.Corpus(n, seed=1).batch()
+    st, bounds, ng = _lib.analyze(b, 148)
+    assert (st == 0).all()
+    q = lambda k: bounds[:, 2 * k].astype(np.float64) / bounds[:, 2 * k + 1]
+    prop, gr, gu, gp, lo = (q(k) for k in range(5))
+    assert (bounds[:, 1::2] > 0).all()
+    eps = 1e-9
+    assert (lo <= prop + eps).all() and (lo <= gr + eps).all() and (lo <= gp + eps).all()
+    assert (gr <= gu + eps).all()
+    assert (ng >= 1).all()
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(n, 20000, replace=False))
+    sub = pack_subset(b, idx)
+    st_o, b_o, _ = orc.corpus(sub).evaluate(148)
+    assert np.array_equal(st_o, st[idx]) and np.array_equal(b_o, bounds[idx])
+
+
+def pack_subset(b, idx):
+    from paper_2602_20826_b200.batch import from_arrays
+    no, eo, ln, ld, ed = [0], [0], [], [], []
+    for d in idx:
+        n0, n1, e0, e1 = b.node_off[d], b.node_off[d + 1], b.edge_off[d], b.edge_off[d + 1]
+        ln.append(b.load_num[n0:n1]); ld.append(b.load_den[n0:n1]); ed.append(b.edges[e0:e1])
+        no.append(no[-1] + n1 - n0); eo.append(eo[-1] + e1 - e0)
+    return from_arrays(no, eo, np.concatenate(ln), np.concatenate(ld), np.concatenate(ed))
