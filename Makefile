@@ -14,23 +14,23 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden
 CXXFLAGS:= -std=c++17 -O3 -fPIC -fopenmp -fvisibility=hidden -I/usr/local/cuda/include -Wall -Wno-comment
 LDOMP   := -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp -lpthread
 
-CU_SRCS := $(PKG)/csrc/capi.cu
-CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/dagsched_b200.h
+CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o
+CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/dagsched_b200.h
 
 .PHONY: all product oracle ref clean
 all: product oracle ref
 
 product: $(LIBDIR)/libdagsched_b200.so
 
-$(LIBDIR)/capi.o: $(PKG)/csrc/capi.cu $(CU_DEPS)
+$(LIBDIR)/%.o: $(PKG)/csrc/%.cu $(CU_DEPS) $(PKG)/csrc/k1_main.cu
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(LIBDIR)/ptxas_capi.txt || (cat $(LIBDIR)/ptxas_capi.txt; false)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(LIBDIR)/ptxas_$*.txt || (cat $(LIBDIR)/ptxas_$*.txt; false)
 
 $(LIBDIR)/host_gen.o: $(PKG)/csrc/host_gen.cpp include/dagsched_b200.h
 	@mkdir -p $(LIBDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(LIBDIR)/libdagsched_b200.so: $(LIBDIR)/capi.o $(LIBDIR)/host_gen.o
+$(LIBDIR)/libdagsched_b200.so: $(CU_OBJS) $(LIBDIR)/host_gen.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --exclude-libs,ALL $(LDOMP)
 
 oracle:

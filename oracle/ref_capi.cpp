@@ -250,6 +250,7 @@ double ref_corpus_evaluate(void* h, const ds_platform* p, uint32_t mask, int par
         bool ok = true;
         for (std::size_t m = 0; m < methods.size(); ++m) ok &= put(rows[i][m], b + 2 * slot[m]);
         if (mask & DS_M_LOWER) ok &= put(lowers[i], b + 2 * DS_BOUND_LOWER);
+        if (!ok) for (int k = 0; k < 10; ++k) b[k] = 0;  // failed DAGs carry no bounds
         if (status) status[d] = ok ? DS_OK : DS_EOVERFLOW;
     }
     return std::chrono::duration<double>(t1 - t0).count();

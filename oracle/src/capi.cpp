@@ -185,6 +185,7 @@ double orc_corpus_evaluate(void* h, const ds_platform* p, uint32_t mask, int par
                 }
             }
         }
+        if (st != DS_OK) for (int k = 0; k < 10; ++k) b[k] = 0;  // failed DAGs carry no bounds
         if (status) status[d] = st;
     };
     auto t0 = std::chrono::steady_clock::now();

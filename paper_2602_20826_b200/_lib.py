@@ -100,13 +100,24 @@ def _results(n: int, with_groups=True):
     return st, b, ng, r
 
 
+def _finish(batch: DagBatch, st, b, ng):
+    """Merge packer (id-level) and device validation; failed DAGs carry no bounds."""
+    status = combine_status(batch.pack_status, st)
+    bad = status != _abi.DS_OK
+    if bad.any():
+        b[bad] = 0
+        if ng is not None:
+            ng[bad] = 0
+    return status, b, ng
+
+
 def analyze(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
     """Batched bound analysis on one GPU -> (status[n], bounds[n, 10], n_groups[n])."""
     st, b, ng, r = _results(batch.n_dags)
     cb = batch.as_c()
     pl = platform(sm_count, t_min)
     check(lib().ds_analyze_batch(C.byref(cb), C.byref(pl), mask, C.byref(r), device, None, 0))
-    return combine_status(batch.pack_status, st), b, ng
+    return _finish(batch, st, b, ng)
 
 
 def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = _abi.DS_M_ALL):
@@ -115,7 +126,7 @@ def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = 
     pl = platform(sm_count, t_min)
     devs = (C.c_int * len(devices))(*devices)
     check(lib().ds_analyze_batch_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
-    return combine_status(batch.pack_status, st), b, ng
+    return _finish(batch, st, b, ng)
 
 
 class Corpus:

@@ -10,9 +10,18 @@
 // Layout: a DAG of n <= 64*W nodes lives in the warp's shared-memory slice
 // (SoA per node, W-word node masks). Node-parallel work (closure rounds,
 // W^anc, ranks, head / candidate tests, per-node bounds) maps node v to lane
-// v % 32 (2W nodes per lane); the inherently sequential parts of the greedy
-// (group loop, apportion shed/fill, launch loop) run warp-uniformly over
-// masks, so there is no divergence and no shuffle traffic in them.
+// v % 32; the inherently sequential parts of the greedy (group loop,
+// apportion shed/fill, launch loop) run warp-uniformly over masks, so they
+// neither diverge nor shuffle.
+//
+// Code size is a first-class constraint: the kernel is latency bound and its
+// first version (everything inlined, 32.5k SASS instructions) spent 86% of its
+// stall samples on instruction fetch. Every phase below is an out-of-line
+// function and every rational op goes through one out-of-line copy (rat.cuh).
+//
+// Word width T: u64 for every DAG; DAGs whose u64 pass overflowed are re-run
+// with T = u128 (k1_analyse_retry) so results are exact wherever the
+// reference's 128-bit Boost rationals hold them.
 //
 // Parity rules reproduced: join order ascending W^anc
 // ties id; heads = ungrouped block members whose unique in-block predecessor
@@ -31,27 +40,26 @@ namespace ds {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <int W>
+template <int W, class T>
 struct WarpState {
     static constexpr int N = 64 * W;
     u64 pred[N][W], succ[N][W], anc[N][W], desc[N][W];
-    u64 divg[N][W];              // division groups, in order
-    u64 ln[N], ld[N];            // original load
-    u64 pn[N], pd[N];            // pending load (residual after a split)
-    u64 xn[N], xd[N];            // W^anc, later per-member exec
-    u64 rn[N], rd[N];            // apportion remainder (unreduced)
-    u64 cn[N], cd[N];            // critical-path prefix (lower bound)
-    int mmax[N];                 // max_parallelism(original load)
-    int mq[N];                   // apportioned parallelism
-    int cap[N];                  // min(max_parallelism(pending load), M)
-    short rank[N];               // position in (W^anc desc, id asc)
-    short order[N];              // node at rank r
-    short jorder[N];             // joins in (W^anc asc, id asc)
-    short done[N];               // executed group that completed the origin, -1 pending
-    unsigned short gen[N];       // split generation counter
-    unsigned char level[N];      // 1 + longest predecessor chain (hop count)
-    unsigned char ppart[N];      // pending entity part (0 whole, 2 residual)
-    u64 rmask[W];                // rank-space scratch
+    u64 divg[N][W];   // division groups, in order
+    T ln[N], ld[N];   // original load
+    T pn[N], pd[N];   // pending load (residual after a split)
+    T xn[N], xd[N];   // W^anc, later per-member exec
+    T rn[N], rd[N];   // apportion remainder (unreduced)
+    T cn[N], cd[N];   // critical-path prefix (lower bound)
+    int mmax[N];      // max_parallelism(original load)
+    int mq[N];        // apportioned parallelism
+    int cap[N];       // min(max_parallelism(pending load), M)
+    short rank[N];    // position in (W^anc desc, id asc)
+    short order[N];   // node at rank r
+    short jorder[N];  // joins in (W^anc asc, id asc)
+    unsigned short gen[N];   // split generation counter
+    unsigned char ppart[N];  // pending entity part (0 whole, 2 residual)
+    u64 rmask[W];            // rank-space scratch
+    T bn[DS_N_BOUNDS], bd[DS_N_BOUNDS];  // results
 };
 
 template <int W>
@@ -75,6 +83,12 @@ struct Mask {
     }
     __device__ __forceinline__ bool test(int i) const { return (w[i >> 6] >> (i & 63)) & 1; }
     __device__ __forceinline__ void set(int i) { w[i >> 6] |= 1ull << (i & 63); }
+    __device__ __forceinline__ bool eq(const Mask& o) const {
+        bool e = true;
+#pragma unroll
+        for (int k = 0; k < W; ++k) e &= w[k] == o.w[k];
+        return e;
+    }
 };
 
 template <int W>
@@ -85,26 +99,36 @@ __device__ __forceinline__ Mask<W> load_mask(const u64 (&m)[W]) {
     return r;
 }
 
-// Uniform mask from a per-node predicate evaluated by the owning lanes.
+// Uniform mask from a per-node predicate evaluated by the owning lanes. The
+// predicate body is instantiated once per mask word.
 template <int W, class Pred>
 __device__ __forceinline__ Mask<W> ballot_nodes(int lane, Pred pred) {
     Mask<W> r;
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-        const u32 lo = __ballot_sync(FULL, pred(k * 64 + lane));
-        const u32 hi = __ballot_sync(FULL, pred(k * 64 + 32 + lane));
-        r.w[k] = u64(lo) | (u64(hi) << 32);
+        u64 acc = 0;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            acc |= u64(__ballot_sync(FULL, pred(k * 64 + h * 32 + lane))) << (32 * h);
+        }
+        r.w[k] = acc;
     }
     return r;
 }
 
-// Iterate the set bits of a uniform mask in ascending node order.
+// Set bits of a uniform mask, ascending.
 template <int W, class F>
 __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
+#pragma unroll 1
         for (u64 x = m.w[k]; x; x &= x - 1) f(k * 64 + __ffsll(x) - 1);
     }
+}
+
+template <class T>
+__device__ __forceinline__ bool fits_i64(T v) {
+    return (v >> 63) == 0;
 }
 
 struct DetailOut {
@@ -114,46 +138,38 @@ struct DetailOut {
     short* node_div_group;
 };
 
-// Analyse DAG `d`. All lanes of the warp call this with identical arguments.
-// Returns the DS_* status; writes bounds (and detail records when DETAIL).
-template <int W, bool DETAIL>
-__device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u64* __restrict__ lnum,
-                           const u64* __restrict__ lden, const u32* __restrict__ edges, const int n_edges,
-                           const Plat P, const u32 mask, Rat (&bound)[DS_N_BOUNDS], int& n_groups_out,
-                           DetailOut det, int& n_ent_out, int& n_div_out) {
-    constexpr int N = WarpState<W>::N;
-    bool ovf = false;
-    n_groups_out = 0;
-    n_ent_out = 0;
-    n_div_out = 0;
-    if (n <= 0) return DS_E_EMPTY;
-    if (n > N) return DS_ETOOBIG;
-
-    // ---------------------------------------------------------------- loads
-    // dag.cpp:35-41 (load >= min_load; min_load = t_min on this path)
-    bool bad_load = false, bad_arg = false, frac = false;
-    for (int v = lane; v < N; v += 32) {
-        if (v < n) {
-            long long a = (long long)lnum[v];
-            long long b = lden ? (long long)lden[v] : 1;
-            if (b == 0) bad_arg = true;
-            if (b < 0) {
-                a = -a;
-                b = -b;
-            }
-            Rat l = a > 0 && b > 0 ? rat_reduce(u64(a), u64(b)) : Rat{0, 1};
-            if (a <= 0 || rat_cmp(l, P.tmin) < 0) bad_load = true;
-            frac |= l.d != 1;
-            S.ln[v] = l.n;
-            S.ld[v] = l.d;
-            S.pn[v] = l.n;
-            S.pd[v] = l.d;
-            S.mmax[v] = (a > 0 && b > 0) ? max_par(l, P) : 1;
-            S.done[v] = -1;
-            S.gen[v] = 0;
-            S.ppart[v] = 0;
-            S.level[v] = 0;
+// --------------------------------------------------------------- phase: loads
+// dag.cpp:35-41 (load >= min_load; min_load = t_min on this path).
+// Returns status | (integer_loads << 8).
+template <int W, class T>
+__device__ __noinline__ int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* __restrict__ lnum,
+                                   const u64* __restrict__ lden, const PlatT<T> P) {
+    bool bad_load = false, bad_arg = false, frac = false, ovf = false;
+#pragma unroll 1
+    for (int v = lane; v < n; v += 32) {
+        long long a = (long long)lnum[v];
+        long long b = lden ? (long long)lden[v] : 1;
+        if (b == 0) bad_arg = true;
+        if (b < 0) {
+            a = -a;
+            b = -b;
         }
+        RatT<T> l{0, 1};
+        if (a > 0 && b > 0) l = n_reduce<T>(T(u64(a)), T(u64(b)));
+        if (a <= 0 || n_cmp(l, P.tmin) < 0) bad_load = true;
+        frac |= l.d != 1;
+        S.ln[v] = l.n;
+        S.ld[v] = l.d;
+        S.pn[v] = l.n;
+        S.pd[v] = l.d;
+        int mp = 1;
+        if (a > 0 && b > 0) {
+            mp = n_max_par(l, P);
+            if (mp < 0) ovf = true;
+        }
+        S.mmax[v] = mp;
+        S.gen[v] = 0;
+        S.ppart[v] = 0;
 #pragma unroll
         for (int k = 0; k < W; ++k) {
             S.pred[v][k] = 0;
@@ -164,13 +180,18 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
     }
     if (__any_sync(FULL, bad_arg)) return DS_EINVAL;
     if (__any_sync(FULL, bad_load)) return DS_E_LOAD;
-    const bool integer_loads = !__any_sync(FULL, frac);
-    __syncwarp();
+    if (__any_sync(FULL, ovf)) return DS_EOVERFLOW;
+    return DS_OK | ((!__any_sync(FULL, frac)) << 8);
+}
 
-    // ---------------------------------------------------------------- edges
-    // dag.cpp:48-67: checked in sorted (from, to) order; first failure wins.
+// --------------------------------------------------------------- phase: edges
+// dag.cpp:48-67: checked in sorted (from, to) order; the first failure wins.
+template <int W, class T>
+__device__ __noinline__ int p_edges(WarpState<W, T>& S, const int lane, const int n, const u32* __restrict__ edges,
+                                    const int n_edges) {
     u32 first_bad = 0xffffffffu;
     int bad_kind = 0;
+#pragma unroll 1
     for (int e = lane; e < n_edges; e += 32) {
         const u32 w = edges[e];
         const int u = int(w >> 16), v = int(w & 0xffffu);
@@ -184,215 +205,246 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
             atomicOr(&S.pred[v][u >> 6], 1ull << (u & 63));
         }
     }
-    {
-        const u32 m = __reduce_min_sync(FULL, first_bad);
-        if (m != 0xffffffffu) {
-            const u32 who = __ballot_sync(FULL, first_bad == m);
-            return __shfl_sync(FULL, bad_kind, __ffs(who) - 1);
-        }
-    }
+    const u32 m = __reduce_min_sync(FULL, first_bad);
     __syncwarp();
+    if (m == 0xffffffffu) return DS_OK;
+    const u32 who = __ballot_sync(FULL, first_bad == m);
+    return __shfl_sync(FULL, bad_kind, __ffs(who) - 1);
+}
 
-    Mask<W> V;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        const int lo = k * 64, hi = lo + 64;
-        V.w[k] = n >= hi ? ~0ull : (n <= lo ? 0ull : ((1ull << (n - lo)) - 1));
-    }
-
-    // ------------------------------------------- closure (Kahn, level-synchronous)
-    // dag.cpp:69-124. Round r makes ready every node whose predecessors are
-    // all processed; a node's round is 1 + the longest predecessor chain (the
-    // hop count graham_para needs). No progress with nodes left = cycle.
-    const bool want_lower = mask & DS_M_LOWER;
-    if (want_lower) {
+// ------------------------------------------------------------ phase: closure
+// dag.cpp:69-124, level-synchronous Kahn. Round r makes ready every node whose
+// predecessors (successors when !FWD) are all processed; round = 1 + longest
+// chain, so the number of rounds is the hop-count critical path graham_para
+// needs. With FWD and `lower`, also the weighted critical path of
+// lower_bound (analysis.cpp:11-24, 72-81). Returns rounds, or -1 on a cycle,
+// or -2 on overflow.
+template <int W, class T, bool FWD>
+__device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const int n, const bool lower,
+                                      const PlatT<T> P) {
+    bool ovf = false;
+    if (FWD && lower) {
+#pragma unroll 1
         for (int v = lane; v < n; v += 32) {
-            Rat w = exec_time(Rat{S.ln[v], S.ld[v]}, min(S.mmax[v], P.M), P, ovf);
+            const RatT<T> w = n_exec(RatT<T>{S.ln[v], S.ld[v]}, min(S.mmax[v], P.M), P);
+            ovf |= w.d == 0;
             S.cn[v] = w.n;  // weight; replaced by the path prefix below
             S.cd[v] = w.d;
         }
+        __syncwarp();
     }
-    Mask<W> done_m;
-    done_m.clear();
+    Mask<W> done;
+    done.clear();
     int rounds = 0;
+#pragma unroll 1
     for (;;) {
         const Mask<W> R = ballot_nodes<W>(lane, [&](int v) {
-            if (v >= n || done_m.test(v)) return false;
+            if (v >= n || done.test(v)) return false;
             bool ok = true;
 #pragma unroll
-            for (int k = 0; k < W; ++k) ok &= (S.pred[v][k] & ~done_m.w[k]) == 0;
+            for (int k = 0; k < W; ++k) ok &= ((FWD ? S.pred[v][k] : S.succ[v][k]) & ~done.w[k]) == 0;
             return ok;
         });
         if (!R.any()) break;
         ++rounds;
-        for (int v = lane; v < N; v += 32) {
+#pragma unroll 1
+        for (int v = lane; v < n; v += 32) {
             if (!R.test(v)) continue;
             u64 a[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) a[k] = 0;
-            Rat best{0, 1};
-            const Mask<W> pm = load_mask<W>(S.pred[v]);
+            RatT<T> best{0, 1};
+            const Mask<W> pm = load_mask<W>(FWD ? S.pred[v] : S.succ[v]);
             for_bits<W>(pm, [&](int p) {
 #pragma unroll
-                for (int k = 0; k < W; ++k) a[k] |= S.anc[p][k];
+                for (int k = 0; k < W; ++k) a[k] |= FWD ? S.anc[p][k] : S.desc[p][k];
                 a[p >> 6] |= 1ull << (p & 63);
-                if (want_lower) best = rat_max(best, Rat{S.cn[p], S.cd[p]});
+                if (FWD && lower) {
+                    const RatT<T> c{S.cn[p], S.cd[p]};
+                    if (n_cmp(c, best) > 0) best = c;
+                }
             });
 #pragma unroll
-            for (int k = 0; k < W; ++k) S.anc[v][k] = a[k];
-            S.level[v] = (unsigned char)min(rounds, 255);
-            if (want_lower) {
-                Rat c = rat_add(best, Rat{S.cn[v], S.cd[v]}, ovf);
+            for (int k = 0; k < W; ++k) {
+                if (FWD) S.anc[v][k] = a[k];
+                else S.desc[v][k] = a[k];
+            }
+            if (FWD && lower) {
+                const RatT<T> c = n_add(best, RatT<T>{S.cn[v], S.cd[v]});
+                ovf |= c.d == 0;
                 S.cn[v] = c.n;
                 S.cd[v] = c.d;
             }
         }
 #pragma unroll
-        for (int k = 0; k < W; ++k) done_m.w[k] |= R.w[k];
+        for (int k = 0; k < W; ++k) done.w[k] |= R.w[k];
         __syncwarp();
     }
-    {
-        bool all = true;
-#pragma unroll
-        for (int k = 0; k < W; ++k) all &= done_m.w[k] == V.w[k];
-        if (!all) return DS_E_CYCLE;
-    }
-    // dag.cpp:97-108: exactly one source and one sink
-    {
-        const Mask<W> src = ballot_nodes<W>(lane, [&](int v) {
-            if (v >= n) return false;
-            u64 a = 0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) a |= S.pred[v][k];
-            return a == 0;
-        });
-        if (src.popc() != 1) return DS_E_SOURCES;
-        const Mask<W> snk = ballot_nodes<W>(lane, [&](int v) {
-            if (v >= n) return false;
-            u64 a = 0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) a |= S.succ[v][k];
-            return a == 0;
-        });
-        if (snk.popc() != 1) return DS_E_SINKS;
-    }
-    // descendants: reverse rounds over successors
-    done_m.clear();
-    for (;;) {
-        const Mask<W> R = ballot_nodes<W>(lane, [&](int v) {
-            if (v >= n || done_m.test(v)) return false;
-            bool ok = true;
-#pragma unroll
-            for (int k = 0; k < W; ++k) ok &= (S.succ[v][k] & ~done_m.w[k]) == 0;
-            return ok;
-        });
-        if (!R.any()) break;
-        for (int v = lane; v < N; v += 32) {
-            if (!R.test(v)) continue;
-            u64 a[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) a[k] = 0;
-            const Mask<W> sm = load_mask<W>(S.succ[v]);
-            for_bits<W>(sm, [&](int s) {
-#pragma unroll
-                for (int k = 0; k < W; ++k) a[k] |= S.desc[s][k];
-                a[s >> 6] |= 1ull << (s & 63);
-            });
-#pragma unroll
-            for (int k = 0; k < W; ++k) S.desc[v][k] = a[k];
-        }
-#pragma unroll
-        for (int k = 0; k < W; ++k) done_m.w[k] |= R.w[k];
-        __syncwarp();
-    }
+    if (__any_sync(FULL, ovf)) return -2;
+    return done.popc() == n ? rounds : -1;
+}
 
-    // ---------------------------------------------------------------- bounds
-    // analysis.cpp:40-81 (node-parallel sums; canonical rationals)
-    if (mask & (DS_M_GREEDY | DS_M_GREEDY_UNAWARE | DS_M_GRAHAM_PARA | DS_M_LOWER)) {
-        Rat g{0, 1}, gu{0, 1}, tot{0, 1};
-        u64 units = 0;
-        for (int v = lane; v < n; v += 32) {
-            const Rat l{S.ln[v], S.ld[v]};
-            if (mask & DS_M_GREEDY) g = rat_add(g, exec_time(l, min(S.mmax[v], P.M), P, ovf), ovf);
-            if (mask & DS_M_GREEDY_UNAWARE) gu = rat_add(gu, exec_time(l, S.mmax[v], P, ovf), ovf);
-            if (mask & DS_M_GRAHAM_PARA) units += rat_ceil(rat_div(l, P.tmin, ovf));
-            if (mask & DS_M_LOWER) tot = rat_add(tot, l, ovf);
-        }
-        if (mask & DS_M_GREEDY) bound[DS_BOUND_GREEDY] = warp_sum(g, ovf);
-        if (mask & DS_M_GREEDY_UNAWARE) bound[DS_BOUND_GREEDY_UNAWARE] = warp_sum(gu, ovf);
-        if (mask & DS_M_GRAHAM_PARA) {
+// dag.cpp:97-108: exactly one source and one sink.
+template <int W, class T>
+__device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int n) {
+    const Mask<W> src = ballot_nodes<W>(lane, [&](int v) {
+        if (v >= n) return false;
+        u64 a = 0;
 #pragma unroll
-            for (int o = 16; o; o >>= 1) units += __shfl_xor_sync(FULL, units, o);
-            // chain = (longest hop path) * t_min; bound = chain + (work - chain) / M
-            const Rat work = rat_mul_int(P.tmin, units, ovf);
-            const Rat chain = rat_mul_int(P.tmin, u64(rounds), ovf);
-            bound[DS_BOUND_GRAHAM_PARA] =
-                rat_add(chain, rat_div_int(rat_sub(work, chain, ovf), u64(P.M), ovf), ovf);
+        for (int k = 0; k < W; ++k) a |= S.pred[v][k];
+        return a == 0;
+    });
+    if (src.popc() != 1) return DS_E_SOURCES;
+    const Mask<W> snk = ballot_nodes<W>(lane, [&](int v) {
+        if (v >= n) return false;
+        u64 a = 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) a |= S.succ[v][k];
+        return a == 0;
+    });
+    if (snk.popc() != 1) return DS_E_SINKS;
+    return DS_OK;
+}
+
+// ------------------------------------------------------------- phase: bounds
+// analysis.cpp:40-81 — greedy, greedy_unaware, graham_para, lower_bound.
+template <int W, class T>
+__device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const int n, const int rounds,
+                                     const PlatT<T> P, const u32 mask) {
+    RatT<T> g{0, 1}, gu{0, 1}, tot{0, 1}, cp{0, 1};
+    T units = 0;
+    bool ovf = false;
+#pragma unroll 1
+    for (int v = lane; v < n; v += 32) {
+        const RatT<T> l{S.ln[v], S.ld[v]};
+        if (mask & DS_M_GREEDY) g = n_add(g, n_exec(l, min(S.mmax[v], P.M), P));
+        if (mask & DS_M_GREEDY_UNAWARE) gu = n_add(gu, n_exec(l, S.mmax[v], P));
+        if (mask & DS_M_GRAHAM_PARA) {  // ceil(load / t_min) unit nodes
+            T u;
+            if (P.tmin.n == 1 && P.tmin.d == 1 && l.d == 1) {
+                u = l.n;
+            } else {
+                const RatT<T> q = n_div(l, P.tmin);
+                ovf |= q.d == 0;
+                u = n_ceil(q);
+            }
+            units = addc(units, u, ovf);
         }
         if (mask & DS_M_LOWER) {
-            tot = warp_sum(tot, ovf);
-            Rat cp{0, 1};
-            for (int v = lane; v < n; v += 32) cp = rat_max(cp, Rat{S.cn[v], S.cd[v]});
-            cp = warp_max(cp);
-            bound[DS_BOUND_LOWER] = rat_max(rat_div_int(tot, u64(P.M), ovf), cp);
+            tot = n_add(tot, l);
+            const RatT<T> c{S.cn[v], S.cd[v]};
+            if (n_cmp(c, cp) > 0) cp = c;
         }
     }
+    ovf |= g.d == 0 || gu.d == 0 || tot.d == 0;
+#pragma unroll 1
+    for (int o = 16; o; o >>= 1) {
+        g = n_add(g, RatT<T>{shfl_xor_w(g.n, o), shfl_xor_w(g.d, o)});
+        gu = n_add(gu, RatT<T>{shfl_xor_w(gu.n, o), shfl_xor_w(gu.d, o)});
+        tot = n_add(tot, RatT<T>{shfl_xor_w(tot.n, o), shfl_xor_w(tot.d, o)});
+        units = addc(units, shfl_xor_w(units, o), ovf);
+        const RatT<T> c{shfl_xor_w(cp.n, o), shfl_xor_w(cp.d, o)};
+        if (n_cmp(c, cp) > 0) cp = c;
+    }
+    ovf |= g.d == 0 || gu.d == 0 || tot.d == 0;
+    if (lane == 0) {
+        if (mask & DS_M_GREEDY) {
+            S.bn[DS_BOUND_GREEDY] = g.n;
+            S.bd[DS_BOUND_GREEDY] = g.d;
+        }
+        if (mask & DS_M_GREEDY_UNAWARE) {
+            S.bn[DS_BOUND_GREEDY_UNAWARE] = gu.n;
+            S.bd[DS_BOUND_GREEDY_UNAWARE] = gu.d;
+        }
+        if (mask & DS_M_GRAHAM_PARA) {
+            // chain = (longest hop path) * t_min; bound = chain + (work - chain) / M
+            const RatT<T> work = n_mul_int(P.tmin, units);
+            const RatT<T> chain = n_mul_int(P.tmin, T(rounds));
+            const RatT<T> r = n_add(chain, n_div_int(n_sub(work, chain), T(P.M)));
+            ovf |= work.d == 0 || chain.d == 0 || r.d == 0;
+            S.bn[DS_BOUND_GRAHAM_PARA] = r.n;
+            S.bd[DS_BOUND_GRAHAM_PARA] = r.d;
+        }
+        if (mask & DS_M_LOWER) {
+            const RatT<T> wf = n_div_int(tot, T(P.M));
+            ovf |= wf.d == 0;
+            const RatT<T> r = n_cmp(wf, cp) < 0 ? cp : wf;
+            S.bn[DS_BOUND_LOWER] = r.n;
+            S.bd[DS_BOUND_LOWER] = r.d;
+        }
+    }
+    __syncwarp();
+    return __any_sync(FULL, ovf) ? DS_EOVERFLOW : DS_OK;
+}
 
-    const bool need_sched = (mask & DS_M_PROPOSED) || DETAIL;
-    if (!need_sched) return __any_sync(FULL, ovf) ? DS_EOVERFLOW : DS_OK;
-
-    // ----------------------------------------------------------- W^anc, ranks
-    // dag.cpp:126-135 W^anc = load + sum of ancestors' loads
+// --------------------------------------------------------- phase: W^anc, ranks
+// dag.cpp:126-135 W^anc = load + sum of ancestors' loads; ranks in
+// (W^anc desc, id asc) for heads (division.cpp:88-93) and candidates
+// (scheduler.cpp:275-280); joins in (W^anc asc, id asc) (dag.cpp:218-230).
+// Returns the join count, or -1 on overflow.
+template <int W, class T>
+__device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int n, const bool integer) {
+    bool ovf = false;
+#pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         const Mask<W> am = load_mask<W>(S.anc[v]);
-        if (integer_loads) {
-            u64 s = S.ln[v];
+        if (integer) {
+            T s = S.ln[v];
             for_bits<W>(am, [&](int u) { s = addc(s, S.ln[u], ovf); });
             S.xn[v] = s;
             S.xd[v] = 1;
         } else {
-            Rat s{S.ln[v], S.ld[v]};
-            for_bits<W>(am, [&](int u) { s = rat_add(s, Rat{S.ln[u], S.ld[u]}, ovf); });
+            RatT<T> s{S.ln[v], S.ld[v]};
+            for_bits<W>(am, [&](int u) { s = n_add(s, RatT<T>{S.ln[u], S.ld[u]}); });
+            ovf |= s.d == 0;
             S.xn[v] = s.n;
             S.xd[v] = s.d;
         }
     }
     __syncwarp();
-    // rank in (W^anc desc, id asc) — heads (division.cpp:88-93) and
-    // candidates (scheduler.cpp:275-280); join order (W^anc asc, id asc,
-    // dag.cpp:218-230) among joins.
-    int n_joins = 0;
-    {
-        const Mask<W> J = ballot_nodes<W>(lane, [&](int v) {
-            if (v >= n) return false;
-            int c = 0;
+    const Mask<W> J = ballot_nodes<W>(lane, [&](int v) {
+        if (v >= n) return false;
+        int c = 0;
 #pragma unroll
-            for (int k = 0; k < W; ++k) c += __popcll(S.pred[v][k]);
-            return c >= 2;
-        });
-        n_joins = J.popc();
-        for (int v = lane; v < n; v += 32) {
-            const Rat wv{S.xn[v], S.xd[v]};
-            int r = 0, jr = 0;
-            const bool isj = J.test(v);
-            for (int u = 0; u < n; ++u) {
-                const Rat wu{S.xn[u], S.xd[u]};
-                const int c = integer_loads ? (wu.n < wv.n ? -1 : (wu.n > wv.n ? 1 : 0)) : rat_cmp(wu, wv);
-                r += (c > 0) || (c == 0 && u < v);
-                if (isj) jr += J.test(u) && ((c < 0) || (c == 0 && u < v));
-            }
-            S.rank[v] = short(r);
-            S.order[r] = short(v);
-            if (isj) S.jorder[jr] = short(v);
+        for (int k = 0; k < W; ++k) c += __popcll(S.pred[v][k]);
+        return c >= 2;
+    });
+#pragma unroll 1
+    for (int v = lane; v < n; v += 32) {
+        const RatT<T> wv{S.xn[v], S.xd[v]};
+        int r = 0, jr = 0;
+        const bool isj = J.test(v);
+#pragma unroll 1
+        for (int u = 0; u < n; ++u) {
+            int c;
+            if (integer) c = S.xn[u] < wv.n ? -1 : (S.xn[u] > wv.n ? 1 : 0);
+            else c = n_cmp(RatT<T>{S.xn[u], S.xd[u]}, wv);
+            r += (c > 0) || (c == 0 && u < v);
+            jr += isj && J.test(u) && ((c < 0) || (c == 0 && u < v));
         }
+        S.rank[v] = short(r);
+        S.order[r] = short(v);
+        if (isj) S.jorder[jr] = short(v);
     }
     __syncwarp();
+    if (__any_sync(FULL, ovf)) return -1;
+    return J.popc();
+}
 
-    // -------------------------------------------------------------- division
-    // division.cpp:10-30 blocks in join order + residual; :67-126 groups.
-    int n_div = 0;
-    Mask<W> assigned;
+// ----------------------------------------------------------- phase: division
+// division.cpp:10-30 blocks in join order + residual; :67-126 groups.
+template <int W, class T, bool DETAIL>
+__device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const int n, const int n_joins,
+                                       const int M, DetailOut det) {
+    Mask<W> V, assigned;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int lo = k * 64;
+        V.w[k] = n >= lo + 64 ? ~0ull : (n <= lo ? 0ull : ((1ull << (n - lo)) - 1));
+    }
     assigned.clear();
+    int n_div = 0;
+#pragma unroll 1
     for (int b = 0; b <= n_joins; ++b) {
         Mask<W> B;
         if (b < n_joins) {
@@ -406,12 +458,14 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
 #pragma unroll
         for (int k = 0; k < W; ++k) assigned.w[k] |= B.w[k];
         if (DETAIL) {
+#pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 if (B.test(v)) det.node_block[v] = short(b);
             }
         }
         Mask<W> grouped;
         grouped.clear();
+#pragma unroll 1
         for (;;) {
             // heads: ungrouped members whose in-block predecessor is grouped or absent
             const Mask<W> H = ballot_nodes<W>(lane, [&](int v) {
@@ -423,10 +477,11 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
             });
             if (!H.any()) break;
             Mask<W> sel = H;
-            if (H.popc() > P.M) {  // keep the top-M by rank
+            if (H.popc() > M) {  // Rule 1: keep the top-M by rank
 #pragma unroll
                 for (int k = 0; k < W; ++k) S.rmask[k] = 0;
                 __syncwarp();
+#pragma unroll 1
                 for (int v = lane; v < n; v += 32) {
                     if (H.test(v)) atomicOr(&S.rmask[S.rank[v] >> 6], 1ull << (S.rank[v] & 63));
                 }
@@ -441,17 +496,18 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
                         if (k * 64 + 64 <= r) below += __popcll(w);
                         else if (k * 64 < r) below += __popcll(w & ((1ull << (r - k * 64)) - 1));
                     }
-                    return below < P.M;
+                    return below < M;
                 });
                 __syncwarp();
             }
             // Rule 2: any selected head with m^max >= M -> the max-m^max head alone
             int mx = 0;
+#pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 if (sel.test(v)) mx = max(mx, S.mmax[v]);
             }
             mx = __reduce_max_sync(FULL, mx);
-            if (mx >= P.M) {
+            if (mx >= M) {
                 const Mask<W> top = ballot_nodes<W>(lane, [&](int v) {
                     return v < n && sel.test(v) && S.mmax[v] == mx;
                 });
@@ -469,6 +525,7 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
                 S.divg[n_div][k] = sel.w[k];
             }
             if (DETAIL) {
+#pragma unroll 1
                 for (int v = lane; v < n; v += 32) {
                     if (sel.test(v)) det.node_div_group[v] = short(n_div);
                 }
@@ -477,65 +534,95 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
         }
     }
     __syncwarp();
-    n_div_out = n_div;
+    return n_div;
+}
 
-    // --------------------------------------------------------------- schedule
-    // scheduler.cpp:214-359, one executed group per non-absorbed division group
-    Rat proposed{0, 1};
+template <class T>
+__device__ __forceinline__ void put_rec(ds_entity_rec& e, int origin, int gen, int part, bool launched, int group,
+                                        int m, RatT<T> load, RatT<T> exec, RatT<T> res, bool& ovf) {
+    e.origin = (unsigned short)origin;
+    e.generation = (unsigned short)gen;
+    e.part = (unsigned char)part;
+    e.launched = launched ? 1 : 0;
+    e.group = (unsigned short)group;
+    e.parallelism = m;
+    e.reserved = 0;
+    ovf |= !fits_i64(load.n) || !fits_i64(load.d) || !fits_i64(exec.n) || !fits_i64(exec.d) ||
+           !fits_i64(res.n) || !fits_i64(res.d);
+    e.load_num = (long long)load.n;
+    e.load_den = (long long)load.d;
+    e.exec_num = (long long)exec.n;
+    e.exec_den = (long long)exec.d;
+    e.res_num = (long long)res.n;
+    e.res_den = (long long)res.d;
+}
+
+// ----------------------------------------------------------- phase: schedule
+// scheduler.cpp:214-359, one executed group per non-absorbed division group.
+// Returns status | (n_groups << 8) | (n_entities << 20).
+template <int W, class T, bool DETAIL>
+__device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane, const int n, const int n_div,
+                                             const PlatT<T> P, DetailOut det) {
+    bool ovf = false;
+    Mask<W> V;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int lo = k * 64;
+        V.w[k] = n >= lo + 64 ? ~0ull : (n <= lo ? 0ull : ((1ull << (n - lo)) - 1));
+    }
+    RatT<T> proposed{0, 1};
     int gidx = 0, n_ent = 0;
-    Mask<W> done_mask;
-    done_mask.clear();
+    Mask<W> done;
+    done.clear();
+#pragma unroll 1
     for (int g = 0; g < n_div; ++g) {
         const Mask<W> G = load_mask<W>(S.divg[g]);
         Mask<W> org;
 #pragma unroll
-        for (int k = 0; k < W; ++k) org.w[k] = G.w[k] & ~done_mask.w[k];
+        for (int k = 0; k < W; ++k) org.w[k] = G.w[k] & ~done.w[k];
         if (!org.any()) continue;  // fully absorbed by earlier launches
 
-        // -- apportion (scheduler.cpp:35-95) over pending loads
-        Rat Wt{0, 1};
-        for_bits<W>(org, [&](int v) { Wt = rat_add(Wt, Rat{S.pn[v], S.pd[v]}, ovf); });
+        // -- apportion (scheduler.cpp:35-95) over the pending loads
+        RatT<T> Wt{0, 1};
+        for_bits<W>(org, [&](int v) { Wt = n_add(Wt, RatT<T>{S.pn[v], S.pd[v]}); });
+        ovf |= Wt.d == 0;
         int tot = 0, capsum = 0;
+#pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             if (!org.test(v)) continue;
-            const Rat l{S.pn[v], S.pd[v]};
-            const int cp = min(max_par(l, P), P.M);
-            // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n)
-            unsigned __int128 qn = (unsigned __int128)mulc(l.n, u64(P.M), ovf) * Wt.d;
-            unsigned __int128 qd = (unsigned __int128)l.d * Wt.n;
-            u64 fl, rem_n, rem_d;
-            if (((qn | qd) >> 64) == 0) {
-                const u64 a = u64(qn), c = u64(qd);
-                fl = div64(a, c);
-                rem_n = a - fl * c;
-                rem_d = c;
-            } else {
-                const unsigned __int128 f = qn / qd;
-                const unsigned __int128 r = qn - f * qd;
-                if ((f >> 63) || (r >> 64) || (qd >> 64)) ovf = true;
-                fl = u64(f);
-                rem_n = u64(r);
-                rem_d = u64(qd);
+            const RatT<T> l{S.pn[v], S.pd[v]};
+            int cp = n_max_par(l, P);
+            if (cp < 0) {
+                ovf = true;
+                cp = 1;
             }
-            const long long base = max(1ll, min((long long)min(fl, u64(0x7fffffffffffll)), (long long)cp));
+            cp = min(cp, P.M);
+            // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n); floor and remainder
+            const T qn = mulc(mulc(l.n, T(P.M), ovf), Wt.d, ovf);
+            const T qd = mulc(l.d, Wt.n, ovf);
+            const T fl = divw(qn, qd);
+            const long long flc = fl > T(0x7fffffff) ? 0x7fffffffll : (long long)fl;
+            const long long base = max(1ll, min(flc, (long long)cp));
             S.mq[v] = int(base);
             S.cap[v] = cp;
-            S.rn[v] = rem_n;
-            S.rd[v] = rem_d;
+            S.rn[v] = qn - fl * qd;
+            S.rd[v] = qd;
             tot += int(base);
             capsum += cp;
         }
         tot = __reduce_add_sync(FULL, tot);
         capsum = __reduce_add_sync(FULL, capsum);
         __syncwarp();
+#pragma unroll 1
         while (tot > P.M) {  // shed: smallest slowdown, first index wins ties
             int pick = -1;
-            Rat best{0, 1};
+            RatT<T> best{0, 1};
             for_bits<W>(org, [&](int v) {
                 const int m = S.mq[v];
                 if (m <= 1) return;
-                const Rat s = exec_raw(Rat{S.pn[v], S.pd[v]}, m - 1, P, ovf);
-                if (pick < 0 || rat_cmp(s, best) < 0) {
+                const RatT<T> s = n_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m - 1, P);
+                ovf |= s.d == 0;
+                if (pick < 0 || n_cmp(s, best) < 0) {
                     pick = v;
                     best = s;
                 }
@@ -546,18 +633,20 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
             --tot;
         }
         const int target = min(P.M, capsum);
+#pragma unroll 1
         while (tot < target) {  // fill: largest exec, then larger remainder, then first index
             int pick = -1;
-            Rat be{0, 1}, br{0, 1};
+            RatT<T> be{0, 1}, br{0, 1};
             for_bits<W>(org, [&](int v) {
                 const int m = S.mq[v];
                 if (m >= S.cap[v]) return;
-                const Rat cur = exec_raw(Rat{S.pn[v], S.pd[v]}, m, P, ovf);
-                const Rat rm{S.rn[v], S.rd[v]};
+                const RatT<T> cur = n_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m, P);
+                ovf |= cur.d == 0;
+                const RatT<T> rm{S.rn[v], S.rd[v]};
                 int c = 1;
                 if (pick >= 0) {
-                    c = rat_cmp(cur, be);
-                    if (c == 0) c = rat_cmp(rm, br);
+                    c = n_cmp(cur, be);
+                    if (c == 0) c = n_cmp(rm, br);
                 }
                 if (c > 0) {
                     pick = v;
@@ -572,18 +661,20 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
         }
 
         // -- members: exec, response (first strict max), bottleneck
+#pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             if (!org.test(v)) continue;
-            const Rat e = exec_time(Rat{S.pn[v], S.pd[v]}, S.mq[v], P, ovf);
+            const RatT<T> e = n_exec(RatT<T>{S.pn[v], S.pd[v]}, S.mq[v], P);
+            ovf |= e.d == 0;
             S.xn[v] = e.n;
             S.xd[v] = e.d;
         }
         __syncwarp();
-        Rat R{0, 1};
+        RatT<T> R{0, 1};
         int bott = -1, used = 0, n_mem = 0, bott_pos = 0;
         for_bits<W>(org, [&](int v) {
-            const Rat e{S.xn[v], S.xd[v]};
-            if (bott < 0 || rat_cmp(e, R) > 0) {
+            const RatT<T> e{S.xn[v], S.xd[v]};
+            if (bott < 0 || n_cmp(e, R) > 0) {
                 R = e;
                 bott = v;
                 bott_pos = n_mem;
@@ -607,12 +698,12 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
             return hit != 0;
         });
         const Mask<W> cands = ballot_nodes<W>(lane, [&](int c) {
-            if (c >= n || !pool.test(c) || done_mask.test(c)) return false;
+            if (c >= n || !pool.test(c) || done.test(c)) return false;
             bool ok = true;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                ok &= (S.pred[c][k] & pool.w[k]) == 0;       // source of the pool
-                ok &= (S.pred[c][k] & ~done_mask.w[k]) == 0; // released (preds done earlier)
+                ok &= (S.pred[c][k] & pool.w[k]) == 0;   // a source of the pool
+                ok &= (S.pred[c][k] & ~done.w[k]) == 0;  // released: preds done earlier
             }
             return ok;
         });
@@ -626,6 +717,7 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
 #pragma unroll
             for (int k = 0; k < W; ++k) S.rmask[k] = 0;
             __syncwarp();
+#pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 if (cands.test(v)) atomicOr(&S.rmask[S.rank[v] >> 6], 1ull << (S.rank[v] & 63));
             }
@@ -639,50 +731,31 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
                     return;
                 }
                 const int c = S.order[r];
-                const Rat l{S.pn[c], S.pd[c]};
-                const int mc = min(max_par(l, P), spare);
-                const Rat dur = exec_time(l, mc, P, ovf);
-                if (rat_cmp(dur, R) <= 0) {
+                const RatT<T> l{S.pn[c], S.pd[c]};
+                int mp = n_max_par(l, P);
+                if (mp < 0) {
+                    ovf = true;
+                    mp = 1;
+                }
+                const int mc = min(mp, spare);
+                const RatT<T> dur = n_exec(l, mc, P);
+                ovf |= dur.d == 0;
+                if (n_cmp(dur, R) <= 0) {
                     if (DETAIL && lane == 0) {
-                        ds_entity_rec& e = det.ent[n_ent];
-                        e.origin = (unsigned short)c;
-                        e.generation = S.gen[c];
-                        e.part = S.ppart[c];
-                        e.launched = 1;
-                        e.group = (unsigned short)gidx;
-                        e.parallelism = mc;
-                        e.load_num = (long long)l.n;
-                        e.load_den = (long long)l.d;
-                        e.exec_num = (long long)dur.n;
-                        e.exec_den = (long long)dur.d;
-                        e.res_num = 0;
-                        e.res_den = 0;
+                        put_rec(det.ent[n_ent], c, S.gen[c], S.ppart[c], true, gidx, mc, l, dur, RatT<T>{0, 0},
+                                ovf);
                     }
                     whole.set(c);
-                    if (lane == 0) S.done[c] = short(gidx);
                     spare -= mc;
                 } else {
-                    const Rat pl = rat_mul_int(R, u64(mc), ovf);
-                    const Rat rl = rat_sub(l, pl, ovf);
-                    const unsigned short gn = (unsigned short)(S.gen[c] + 1);
-                    if (DETAIL && lane == 0) {
-                        ds_entity_rec& e = det.ent[n_ent];
-                        e.origin = (unsigned short)c;
-                        e.generation = gn;
-                        e.part = 1;
-                        e.launched = 1;
-                        e.group = (unsigned short)gidx;
-                        e.parallelism = mc;
-                        e.load_num = (long long)pl.n;
-                        e.load_den = (long long)pl.d;
-                        e.exec_num = (long long)R.n;
-                        e.exec_den = (long long)R.d;
-                        e.res_num = (long long)rl.n;
-                        e.res_den = (long long)rl.d;
-                    }
+                    const RatT<T> pl = n_mul_int(R, T(mc));
+                    const RatT<T> rl = n_sub(l, pl);
+                    ovf |= pl.d == 0 || rl.d == 0;
+                    const int gn = S.gen[c] + 1;
+                    if (DETAIL && lane == 0) put_rec(det.ent[n_ent], c, gn, 1, true, gidx, mc, pl, R, rl, ovf);
                     __syncwarp();
                     if (lane == 0) {
-                        S.gen[c] = gn;
+                        S.gen[c] = (unsigned short)gn;
                         S.ppart[c] = 2;
                         S.pn[c] = rl.n;
                         S.pd[c] = rl.d;
@@ -701,24 +774,14 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
             int pos = 0;
             for_bits<W>(org, [&](int v) {
                 if (lane == 0) {
-                    ds_entity_rec& e = det.ent[n_ent + pos];
-                    e.origin = (unsigned short)v;
-                    e.generation = S.gen[v];
-                    e.part = S.ppart[v];
-                    e.launched = 0;
-                    e.group = (unsigned short)gidx;
-                    e.parallelism = S.mq[v];
-                    e.load_num = (long long)S.pn[v];
-                    e.load_den = (long long)S.pd[v];
-                    e.exec_num = (long long)S.xn[v];
-                    e.exec_den = (long long)S.xd[v];
-                    e.res_num = 0;
-                    e.res_den = 0;
+                    put_rec(det.ent[n_ent + pos], v, S.gen[v], S.ppart[v], false, gidx, S.mq[v],
+                            RatT<T>{S.pn[v], S.pd[v]}, RatT<T>{S.xn[v], S.xd[v]}, RatT<T>{0, 0}, ovf);
                 }
                 ++pos;
             });
             if (lane == 0) {
                 ds_group_rec& gr = det.grp[gidx];
+                ovf |= !fits_i64(R.n) || !fits_i64(R.d);
                 gr.resp_num = (long long)R.n;
                 gr.resp_den = (long long)R.d;
                 gr.spare_sms = spare0;
@@ -732,26 +795,63 @@ __device__ int analyse_dag(WarpState<W>& S, const int lane, const int n, const u
                 for (int k = 0; k < 4; ++k) gr.unlaunched[k] = k < W ? (cands.w[k] & ~whole.w[k]) : 0;
             }
         }
-        for (int v = lane; v < n; v += 32) {
-            if (org.test(v)) S.done[v] = short(gidx);
-        }
 #pragma unroll
-        for (int k = 0; k < W; ++k) done_mask.w[k] |= org.w[k] | whole.w[k];
+        for (int k = 0; k < W; ++k) done.w[k] |= org.w[k] | whole.w[k];
         n_ent += n_mem;
-        proposed = rat_add(proposed, R, ovf);
+        proposed = n_add(proposed, R);
+        ovf |= proposed.d == 0;
         ++gidx;
         __syncwarp();
     }
-    {
-        bool all = true;
-#pragma unroll
-        for (int k = 0; k < W; ++k) all &= done_mask.w[k] == V.w[k];
-        if (!all) return DS_EINVARIANT;  // "scheduling finished with unplaced kernels"
+    if (!done.eq(V)) return DS_EINVARIANT;  // "scheduling finished with unplaced kernels"
+    if (lane == 0) {
+        S.bn[DS_BOUND_PROPOSED] = proposed.n;
+        S.bd[DS_BOUND_PROPOSED] = proposed.d;
     }
-    bound[DS_BOUND_PROPOSED] = proposed;
-    n_groups_out = gidx;
-    n_ent_out = n_ent;
-    return __any_sync(FULL, ovf) ? DS_EOVERFLOW : DS_OK;
+    __syncwarp();
+    const int st = __any_sync(FULL, ovf) ? DS_EOVERFLOW : DS_OK;
+    return (long long)st | ((long long)gidx << 8) | ((long long)n_ent << 20);
+}
+
+// -------------------------------------------------------------- one DAG
+// Returns status; fills S.bn/S.bd and the out-params.
+template <int W, class T, bool DETAIL>
+__device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, const int n,
+                                           const u64* __restrict__ lnum, const u64* __restrict__ lden,
+                                           const u32* __restrict__ edges, const int n_edges, const PlatT<T> P,
+                                           const u32 mask, int& n_groups, DetailOut det, int& n_ent, int& n_div) {
+    constexpr int N = WarpState<W, T>::N;
+    n_groups = 0;
+    n_ent = 0;
+    n_div = 0;
+    if (lane < DS_N_BOUNDS) {
+        S.bn[lane] = 0;
+        S.bd[lane] = 0;
+    }
+    if (n <= 0) return DS_E_EMPTY;
+    if (n > N) return DS_ETOOBIG;
+    int st = p_load<W, T>(S, lane, n, lnum, lden, P);
+    if ((st & 0xff) != DS_OK) return st & 0xff;
+    const bool integer = (st >> 8) & 1;
+    __syncwarp();
+    if ((st = p_edges<W, T>(S, lane, n, edges, n_edges)) != DS_OK) return st;
+    const bool lower = mask & DS_M_LOWER;
+    const int rounds = p_closure<W, T, true>(S, lane, n, lower, P);
+    if (rounds == -1) return DS_E_CYCLE;
+    if (rounds == -2) return DS_EOVERFLOW;
+    if ((st = p_ends<W, T>(S, lane, n)) != DS_OK) return st;
+    p_closure<W, T, false>(S, lane, n, false, P);
+    if (mask & (DS_M_GREEDY | DS_M_GREEDY_UNAWARE | DS_M_GRAHAM_PARA | DS_M_LOWER)) {
+        if ((st = p_bounds<W, T>(S, lane, n, rounds, P, mask)) != DS_OK) return st;
+    }
+    if (!((mask & DS_M_PROPOSED) || DETAIL)) return DS_OK;
+    const int n_joins = p_rank<W, T>(S, lane, n, integer);
+    if (n_joins < 0) return DS_EOVERFLOW;
+    n_div = p_division<W, T, DETAIL>(S, lane, n, n_joins, P.M, det);
+    const long long r = p_schedule<W, T, DETAIL>(S, lane, n, n_div, P, det);
+    n_groups = int((r >> 8) & 0xfff);
+    n_ent = int(r >> 20);
+    return int(r & 0xff);
 }
 
 struct K1Args {
@@ -761,69 +861,94 @@ struct K1Args {
     const u64* load_num;
     const u64* load_den;
     const u32* edges;
-    Plat plat;
+    PlatT<u64> plat;
     u32 mask;
     int32_t* status;
     int64_t* bounds;
     uint16_t* n_groups;
-    // detail mode
-    ds_scheme_out det;
+    ds_scheme_out det;     // detail mode
+    u32* retry;            // DAG indices whose u64 pass overflowed
+    u32* retry_count;
 };
 
+template <int W, class T, bool DETAIL>
+__device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, const K1Args& a, const u64 d,
+                                        const u32 nbase, const u32 ebase, const PlatT<T> P) {
+    const u32 n0 = a.node_off[d] - nbase, n1 = a.node_off[d + 1] - nbase;
+    const u32 e0 = a.edge_off[d] - ebase, e1 = a.edge_off[d + 1] - ebase;
+    const int n = int(n1 - n0);
+    int ng = 0, nent = 0, ndiv = 0;
+    DetailOut det{};
+    if (DETAIL) {
+        det.ent = a.det.entities + 2ull * n0;
+        det.grp = a.det.groups + n0;
+        det.node_block = a.det.node_block + n0;
+        det.node_div_group = a.det.node_div_group + n0;
+    }
+    int st = analyse_dag<W, T, DETAIL>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
+                                       a.edges + e0, int(e1 - e0), P, a.mask, ng, det, nent, ndiv);
+    if (st == DS_EOVERFLOW && sizeof(T) == 8 && a.retry) {
+        // re-run in 128-bit words (k1_analyse_retry); nothing is written now
+        if (lane == 0) a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+        __syncwarp();
+        return;
+    }
+    // canonical results must fit the ABI's int64 slots
+    if (st == DS_OK) {
+        bool fit = true;
+        if (lane < DS_N_BOUNDS) fit = fits_i64(S.bn[lane]) && fits_i64(S.bd[lane]);
+        if (!__all_sync(FULL, fit)) st = DS_EOVERFLOW;
+    }
+    int64_t* b = (DETAIL ? a.det.bounds : a.bounds) + 10 * d;
+    if (lane < 10) {
+        const int k = lane >> 1;
+        b[lane] = st == DS_OK ? (long long)((lane & 1) ? S.bd[k] : S.bn[k]) : 0;
+    }
+    if (lane == 0) {
+        if (DETAIL) {
+            a.det.status[d] = st;
+            a.det.n_groups[d] = (unsigned short)ng;
+            a.det.n_entities[d] = (unsigned short)nent;
+            a.det.n_div_groups[d] = (unsigned short)ndiv;
+        } else {
+            a.status[d] = st;
+            if (a.n_groups) a.n_groups[d] = (unsigned short)ng;
+        }
+    }
+    __syncwarp();
+}
+
+// Main pass: every DAG of its size class (W=1: n <= 64; W=4: 64 < n <= 256),
+// persistent warps striding over the batch.
 template <int W, bool DETAIL>
 __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    WarpState<W>& S = reinterpret_cast<WarpState<W>*>(smem_raw)[wib];
+    WarpState<W, u64>& S = reinterpret_cast<WarpState<W, u64>*>(smem_raw)[wib];
     const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];  // offsets are relative to element 0
+#pragma unroll 1
     for (u64 d = u64(blockIdx.x) * (blockDim.x >> 5) + wib; d < a.n_dags; d += warps) {
-        const u32 n0 = a.node_off[d] - nbase, n1 = a.node_off[d + 1] - nbase;
-        const u32 e0 = a.edge_off[d] - ebase, e1 = a.edge_off[d + 1] - ebase;
-        const int n = int(n1 - n0);
-        // size classes: the W-word kernel takes 64*(W/4)... < n <= 64*W (W=1: n <= 64)
+        const int n = int(a.node_off[d + 1] - a.node_off[d]);
         if (W > 1 && n <= 64) continue;
         if (W == 1 && n > 64 && n <= DS_MAX_NODES) continue;
-        Rat bound[DS_N_BOUNDS];
-#pragma unroll
-        for (int k = 0; k < DS_N_BOUNDS; ++k) bound[k] = Rat{0, 0};
-        int ng = 0, nent = 0, ndiv = 0;
-        DetailOut det{};
-        if (DETAIL) {
-            det.ent = a.det.entities + 2ull * n0;
-            det.grp = a.det.groups + n0;
-            det.node_block = a.det.node_block + n0;
-            det.node_div_group = a.det.node_div_group + n0;
-        }
-        int st = analyse_dag<W, DETAIL>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
-                                        a.edges + e0, int(e1 - e0), a.plat, a.mask, bound, ng, det, nent,
-                                        ndiv);
-        // canonical results must fit the ABI's int64 slots
-        if (st == DS_OK) {
-#pragma unroll
-            for (int k = 0; k < DS_N_BOUNDS; ++k) {
-                if (((bound[k].n | bound[k].d) >> 63) != 0) st = DS_EOVERFLOW;
-            }
-        }
-        int64_t* b = (DETAIL ? a.det.bounds : a.bounds) + 10 * d;
-        if (lane < 10) {
-            const int k = lane >> 1;
-            const u64 v = st == DS_OK ? ((lane & 1) ? bound[k].d : bound[k].n) : 0;
-            b[lane] = (long long)v;
-        }
-        if (lane == 0) {
-            if (DETAIL) {
-                a.det.status[d] = st;
-                a.det.n_groups[d] = (unsigned short)ng;
-                a.det.n_entities[d] = (unsigned short)nent;
-                a.det.n_div_groups[d] = (unsigned short)ndiv;
-            } else {
-                a.status[d] = st;
-                if (a.n_groups) a.n_groups[d] = (unsigned short)ng;
-            }
-        }
-        __syncwarp();
+        run_one<W, u64, DETAIL>(S, lane, a, d, nbase, ebase, a.plat);
+    }
+}
+
+// Retry pass: the DAGs listed by the main pass, in 128-bit words.
+template <bool DETAIL>
+__global__ void __launch_bounds__(32) k1_analyse_retry(const K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    WarpState<4, u128>& S = *reinterpret_cast<WarpState<4, u128>*>(smem_raw);
+    const PlatT<u128> P{a.plat.M, RatT<u128>{a.plat.tmin.n, a.plat.tmin.d}};
+    const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
+    const u32 count = *a.retry_count;
+#pragma unroll 1
+    for (u32 i = blockIdx.x; i < count; i += gridDim.x) {
+        run_one<4, u128, DETAIL>(S, lane, a, a.retry[i], nbase, ebase, P);
     }
 }
 
