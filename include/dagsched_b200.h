@@ -155,6 +155,54 @@ typedef struct ds_scheme_out {
     int64_t* bounds;          /* [n_dags * 10] as in ds_results                  */
 } ds_scheme_out;
 
+/* ------------------------------------------------------ executor (K2/K3) */
+/* Node workloads (K2). Every entity of a schedule is one launch of one of
+ * these memory-bound kernels over its element range of its node's buffers;
+ * per-CTA start/end are stamped with %globaltimer and %smid. */
+#define DS_WL_MIX32 0   /* y[i] = mix(x[i]), uint32, LDG.128/STG.128: 8 B/elem   */
+#define DS_WL_AXPY32 1  /* y[i] = a*x[i] + y[i], fp32 (no FMA contraction): 12 B  */
+#define DS_WL_MIX32_BULK 2 /* DS_WL_MIX32 staged through shared memory with
+                              cp.async.bulk (TMA engine) + mbarrier: 8 B/elem   */
+
+/* One schedulable entity (EntityRecord, scheduler.hpp:31-39) as executed:
+ * grid = parallelism CTAs, one CTA per SM enforced by the kernel's shared
+ * memory footprint; elements [elem_lo, elem_hi) of node `node`'s buffers. */
+typedef struct ds_exec_entity {
+    int32_t group;        /* executed group, -1 when the plan has no groups    */
+    int32_t parallelism;  /* CTAs = SMs held                                   */
+    int32_t node;         /* origin node (buffer)                              */
+    uint32_t pred_off;    /* preds[pred_off .. pred_off + n_preds)             */
+    uint32_t n_preds;
+    uint32_t reserved;
+    uint64_t elem_lo, elem_hi;
+} ds_exec_entity;
+
+typedef struct ds_exec_plan {
+    int32_t n_entities;
+    int32_t n_nodes;
+    const ds_exec_entity* entities;
+    const uint32_t* preds;       /* entity indices (graph edges pred -> entity)  */
+    const uint64_t* node_elems;  /* [n_nodes] buffer length per node             */
+    int32_t barrier_groups;      /* 1: group g+1 starts after all of group g
+                                    (simulate_scheme semantics, simulator.cpp:44-94) */
+    int32_t reserved;
+} ds_exec_plan;
+
+typedef struct ds_exec_cfg {
+    int32_t workload;       /* DS_WL_*                                           */
+    int32_t block_threads;  /* threads per CTA (<= 1024)                         */
+    uint32_t seed;          /* input initialisation                              */
+    int32_t reserved;
+} ds_exec_cfg;
+
+/* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
+typedef struct ds_exec_trace {
+    uint64_t* span;    /* [replays * 2] min CTA start, max CTA end (ns, %globaltimer) */
+    uint64_t* stamps;  /* [replays * total_ctas * 2] start, end per CTA (optional)   */
+    uint32_t* smids;   /* [replays * total_ctas] (optional)                          */
+    float* launch_ms;  /* [replays] host-side graph launch -> completion, CUDA events */
+} ds_exec_trace;
+
 /* ------------------------------------------------------------- functions */
 #if defined(__GNUC__)
 #pragma GCC visibility push(default)
@@ -201,6 +249,27 @@ int ds_session_run(void* session, float* kernel_ms);
 /* Copies results of the last run back to host buffers. */
 int ds_session_results(void* session, ds_results* out);
 int ds_session_free(void* session);
+
+/* Executor (K3) — replaces simulate_scheme (simulator.cpp:44-94) with real
+ * execution: builds device buffers (inputs initialised from cfg->seed) and a
+ * CUDA Graph with one kernel node per entity (grid = quota) and an edge per
+ * entry of preds (plus group barriers when plan->barrier_groups). */
+int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device, void** exec);
+/* Replays the graph `replays` times (after `warmup` untimed replays that are
+ * not recorded); fills the trace arrays for the recorded replays. */
+int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace);
+/* Total CTAs of one replay (sum of parallelism) — sizes the stamp arrays. */
+int ds_exec_total_ctas(void* exec, uint64_t* total);
+/* Copies node `node`'s output buffer (uint32 / fp32 words) to host memory. */
+int ds_exec_read_output(void* exec, int node, void* host, uint64_t n_elems);
+int ds_exec_free(void* exec);
+
+/* Node-kernel roofline probe: one launch of `workload` over ctas CTAs x
+ * elems_per_cta elements (1 CTA per SM), timed with CUDA events over `reps`
+ * launches after warm-up; returns the mean ms per launch and the per-CTA
+ * globaltimer span of the last launch. */
+int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int block_threads, int reps,
+                         float* ms_per_launch, uint64_t* span_ns, int device);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -1,0 +1,394 @@
+// K3 — balanced-group executor: a schedule becomes one CUDA Graph.
+//
+// Replaces the reference's idealised executor simulate_scheme
+// (simulator.cpp:44-94) with real sm_100a execution:
+//   * one kernel node per entity (EntityRecord, scheduler.hpp:31-39), grid =
+//     its SM quota; K2's shared-memory footprint forces one CTA per SM, so
+//     concurrently running entities land on disjoint SMs;
+//   * an edge per augmented-graph predecessor (EntityRecord::preds: original
+//     edges resolved to segment chains + extra dependencies + segment
+//     rewiring), and with barrier_groups an empty node between consecutive
+//     executed groups (simulate_scheme's "group j+1 starts when everything of
+//     group j has finished");
+//   * a 1-thread tail node advancing the replay counter, so every replay's
+//     %globaltimer stamps land in their own slot.
+// The same entry point executes the baselines: a serial chain (one stream,
+// topological order) and naive multi-stream launch (original DAG edges only,
+// every kernel at min(m^max, M) — the Greedy of PAPER.md:533 and
+// simulate_greedy semantics, simulator.cpp:96-190).
+#include "../../include/dagsched_b200.h"
+#include "k2_workload.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+namespace ds {
+int fail(int code, const std::string& msg);
+}
+
+using namespace ds;
+
+#define DS_CUDA(call)                                                                                   \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) return fail(DS_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+namespace {
+
+struct Exec {
+    int device = 0;
+    int workload = DS_WL_MIX32;
+    int threads = 1024;
+    cudaStream_t s = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint32_t*> x, y;
+    std::vector<uint64_t> elems;
+    std::vector<ds_exec_entity> ents;
+    uint32_t total_ctas = 0;
+    int* replay = nullptr;
+    unsigned long long* span = nullptr;
+    unsigned long long* stamps = nullptr;
+    uint32_t* smids = nullptr;
+    int cap = 0;
+    std::vector<NodeArgs> args;  // kernel-node parameters (stable storage)
+};
+
+void* kernel_of(int wl) {
+    switch (wl) {
+        case DS_WL_AXPY32: return reinterpret_cast<void*>(k2_axpy);
+        case DS_WL_MIX32_BULK: return reinterpret_cast<void*>(k2_mix_bulk);
+        default: return reinterpret_cast<void*>(k2_mix);
+    }
+}
+
+int smem_of(int wl) { return wl == DS_WL_MIX32_BULK ? kBulkStages * kBulkChunk : kNodeSmem; }
+
+int set_attrs(int wl) {
+    DS_CUDA(cudaFuncSetAttribute(kernel_of(wl), cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem));
+    return DS_OK;
+}
+
+void destroy(Exec* E) {
+    if (!E) return;
+    cudaSetDevice(E->device);
+    if (E->s) cudaStreamSynchronize(E->s);
+    if (E->exec) cudaGraphExecDestroy(E->exec);
+    if (E->graph) cudaGraphDestroy(E->graph);
+    for (auto* p : E->x) cudaFree(p);
+    for (auto* p : E->y) cudaFree(p);
+    if (E->replay) cudaFree(E->replay);
+    if (E->span) cudaFree(E->span);
+    if (E->stamps) cudaFree(E->stamps);
+    if (E->smids) cudaFree(E->smids);
+    if (E->s) cudaStreamDestroy(E->s);
+    delete E;
+}
+
+// (Re)build the graph; the recording buffers are baked into the node params.
+int build_graph(Exec* E, const ds_exec_plan* plan) {
+    if (E->exec) cudaGraphExecDestroy(E->exec);
+    if (E->graph) cudaGraphDestroy(E->graph);
+    E->exec = nullptr;
+    E->graph = nullptr;
+    DS_CUDA(cudaGraphCreate(&E->graph, 0));
+    const int n = plan->n_entities;
+    std::vector<cudaGraphNode_t> node(n);
+    E->args.assign(n, NodeArgs{});
+    // group barriers (simulate_scheme: group g+1 starts after all of group g)
+    int max_group = -1;
+    for (int i = 0; i < n; ++i) max_group = std::max(max_group, int(plan->entities[i].group));
+    const bool barriers = plan->barrier_groups && max_group > 0;
+    std::vector<std::vector<int>> members(max_group + 1);
+    for (int i = 0; i < n; ++i) {
+        if (plan->entities[i].group >= 0) members[plan->entities[i].group].push_back(i);
+    }
+    std::vector<cudaGraphNode_t> barrier(max_group + 1, nullptr);
+    uint32_t slot = 0;
+    std::vector<uint32_t> slots(n);
+    for (int i = 0; i < n; ++i) {
+        slots[i] = slot;
+        slot += uint32_t(plan->entities[i].parallelism);
+    }
+    // create nodes group by group so barrier nodes can take their inputs
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return plan->entities[a].group < plan->entities[b].group; });
+    int cur_group = -2;
+    for (int idx = 0; idx < n; ++idx) {
+        const int i = order[idx];
+        const ds_exec_entity& e = plan->entities[i];
+        if (barriers && e.group != cur_group) {
+            cur_group = e.group;
+            if (e.group > 0) {
+                std::vector<cudaGraphNode_t> deps;
+                for (int j : members[e.group - 1]) deps.push_back(node[j]);
+                DS_CUDA(cudaGraphAddEmptyNode(&barrier[e.group], E->graph, deps.data(), deps.size()));
+            }
+        }
+        std::vector<cudaGraphNode_t> deps;
+        for (uint32_t k = 0; k < e.n_preds; ++k) {
+            const uint32_t p = plan->preds[e.pred_off + k];
+            // entities arrive in a topological order of the augmented graph
+            // (group order for schedules): a predecessor node already exists
+            if (!node[p]) return fail(DS_EINVAL, "plan is not topologically ordered");
+            deps.push_back(node[p]);
+        }
+        if (barriers && e.group > 0) deps.push_back(barrier[e.group]);
+        NodeArgs& a = E->args[i];
+        a.x = E->x[e.node];
+        a.y = E->y[e.node];
+        a.lo = e.elem_lo;
+        a.hi = e.elem_hi;
+        a.stamps = E->stamps;
+        a.smids = E->smids;
+        a.span = E->span;
+        a.replay = E->replay;
+        a.slot = slots[i];
+        a.total = E->total_ctas;
+        a.a = 0.75f;
+        a.cap = E->cap;
+        void* params[] = {&E->args[i]};
+        cudaKernelNodeParams kp{};
+        kp.func = kernel_of(E->workload);
+        kp.gridDim = dim3(unsigned(e.parallelism));
+        kp.blockDim = dim3(unsigned(E->threads));
+        kp.sharedMemBytes = unsigned(smem_of(E->workload) > kNodeSmem ? smem_of(E->workload) : kNodeSmem);
+        kp.kernelParams = params;
+        DS_CUDA(cudaGraphAddKernelNode(&node[i], E->graph, deps.data(), deps.size(), &kp));
+    }
+    // tail: advance the replay counter after every sink entity
+    std::vector<char> has_succ(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const ds_exec_entity& e = plan->entities[i];
+        for (uint32_t k = 0; k < e.n_preds; ++k) has_succ[plan->preds[e.pred_off + k]] = 1;
+        if (barriers && e.group >= 0 && e.group < max_group) has_succ[i] = 1;
+    }
+    std::vector<cudaGraphNode_t> sinks;
+    for (int i = 0; i < n; ++i) {
+        if (!has_succ[i]) sinks.push_back(node[i]);
+    }
+    cudaGraphNode_t tail;
+    void* tparams[] = {&E->replay};
+    cudaKernelNodeParams tp{};
+    tp.func = reinterpret_cast<void*>(k2_tick);
+    tp.gridDim = dim3(1);
+    tp.blockDim = dim3(1);
+    tp.kernelParams = tparams;
+    DS_CUDA(cudaGraphAddKernelNode(&tail, E->graph, sinks.data(), sinks.size(), &tp));
+    DS_CUDA(cudaGraphInstantiate(&E->exec, E->graph, 0));
+    return DS_OK;
+}
+
+struct PlanCopy {  // the plan must outlive ds_exec_create for graph rebuilds
+    std::vector<ds_exec_entity> ents;
+    std::vector<uint32_t> preds;
+    std::vector<uint64_t> elems;
+    ds_exec_plan plan{};
+};
+
+}  // namespace
+
+struct ExecHandle {
+    Exec* E;
+    PlanCopy P;
+};
+
+extern "C" {
+
+int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device, void** exec) {
+    if (!plan || !cfg || !exec || plan->n_entities < 1 || plan->n_nodes < 1) return fail(DS_EINVAL, "bad plan");
+    if (cfg->workload < DS_WL_MIX32 || cfg->workload > DS_WL_MIX32_BULK) return fail(DS_EINVAL, "bad workload");
+    const int threads = cfg->block_threads > 0 ? cfg->block_threads : 1024;
+    if (threads > 1024 || threads % 32) return fail(DS_EINVAL, "block_threads must be a multiple of 32 <= 1024");
+    auto* H = new ExecHandle();
+    Exec* E = H->E = new Exec();
+    E->device = device;
+    E->workload = cfg->workload;
+    E->threads = threads;
+    auto bail = [&](int rc) {
+        destroy(E);
+        delete H;
+        return rc;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DS_ECUDA, "cudaSetDevice"));
+    if (int rc = set_attrs(E->workload)) return bail(rc);
+    H->P.ents.assign(plan->entities, plan->entities + plan->n_entities);
+    uint64_t npreds = 0;
+    for (const auto& e : H->P.ents) {
+        if (e.parallelism < 1 || e.node < 0 || e.node >= plan->n_nodes || e.elem_hi < e.elem_lo ||
+            e.elem_hi > plan->node_elems[e.node])
+            return bail(fail(DS_EINVAL, "bad entity"));
+        npreds = std::max<uint64_t>(npreds, uint64_t(e.pred_off) + e.n_preds);
+        E->total_ctas += uint32_t(e.parallelism);
+    }
+    H->P.preds.assign(plan->preds, plan->preds + npreds);
+    for (uint32_t p : H->P.preds) {
+        if (p >= uint32_t(plan->n_entities)) return bail(fail(DS_EINVAL, "bad pred index"));
+    }
+    H->P.elems.assign(plan->node_elems, plan->node_elems + plan->n_nodes);
+    H->P.plan = *plan;
+    H->P.plan.entities = H->P.ents.data();
+    H->P.plan.preds = H->P.preds.data();
+    H->P.plan.node_elems = H->P.elems.data();
+    if (cudaStreamCreateWithFlags(&E->s, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(DS_ECUDA, "stream"));
+    for (int v = 0; v < plan->n_nodes; ++v) {
+        const uint64_t ne = std::max<uint64_t>(plan->node_elems[v], 4);
+        uint32_t *x = nullptr, *y = nullptr;
+        if (cudaMalloc(&x, ne * 4) != cudaSuccess || cudaMalloc(&y, ne * 4) != cudaSuccess)
+            return bail(fail(DS_ENOMEM, "node buffers"));
+        E->x.push_back(x);
+        E->y.push_back(y);
+        E->elems.push_back(plan->node_elems[v]);
+        k2_init<<<296, 512, 0, E->s>>>(x, ne, cfg->seed * 0x9e3779b9u + uint32_t(v),
+                                        cfg->workload == DS_WL_AXPY32, y);
+    }
+    if (cudaMalloc(&E->replay, sizeof(int)) != cudaSuccess) return bail(fail(DS_ENOMEM, "replay"));
+    if (cudaStreamSynchronize(E->s) != cudaSuccess) return bail(fail(DS_ECUDA, "init"));
+    *exec = H;
+    return DS_OK;
+}
+
+int ds_exec_total_ctas(void* exec, uint64_t* total) {
+    *total = static_cast<ExecHandle*>(exec)->E->total_ctas;
+    return DS_OK;
+}
+
+int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
+    auto* H = static_cast<ExecHandle*>(exec);
+    Exec* E = H->E;
+    if (replays < 1 || warmup < 0 || !trace || !trace->span) return fail(DS_EINVAL, "bad run arguments");
+    DS_CUDA(cudaSetDevice(E->device));
+    const bool want_stamps = trace->stamps || trace->smids;
+    if (replays > E->cap || !E->exec || (want_stamps && !E->stamps)) {
+        if (E->span) cudaFree(E->span);
+        if (E->stamps) cudaFree(E->stamps);
+        if (E->smids) cudaFree(E->smids);
+        E->span = nullptr;
+        E->stamps = nullptr;
+        E->smids = nullptr;
+        E->cap = std::max(replays, E->cap);
+        DS_CUDA(cudaMalloc(&E->span, size_t(E->cap) * 16));
+        if (want_stamps) {
+            DS_CUDA(cudaMalloc(&E->stamps, size_t(E->cap) * E->total_ctas * 16));
+            DS_CUDA(cudaMalloc(&E->smids, size_t(E->cap) * E->total_ctas * 4));
+        }
+        if (int rc = build_graph(E, &H->P.plan)) return rc;
+    }
+    // span[r] = {~0, 0}
+    std::vector<unsigned long long> init(size_t(E->cap) * 2);
+    for (int r = 0; r < E->cap; ++r) {
+        init[2 * r] = ~0ull;
+        init[2 * r + 1] = 0;
+    }
+    DS_CUDA(cudaMemcpyAsync(E->span, init.data(), init.size() * 8, cudaMemcpyHostToDevice, E->s));
+    const int start = -warmup;
+    DS_CUDA(cudaMemcpyAsync(E->replay, &start, sizeof(int), cudaMemcpyHostToDevice, E->s));
+    DS_CUDA(cudaStreamSynchronize(E->s));
+    std::vector<cudaEvent_t> ev(2 * size_t(replays));
+    for (auto& e : ev) DS_CUDA(cudaEventCreate(&e));
+    for (int r = -warmup; r < replays; ++r) {
+        if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
+        DS_CUDA(cudaGraphLaunch(E->exec, E->s));
+        if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r + 1], E->s));
+    }
+    DS_CUDA(cudaStreamSynchronize(E->s));
+    if (trace->launch_ms) {
+        for (int r = 0; r < replays; ++r) DS_CUDA(cudaEventElapsedTime(&trace->launch_ms[r], ev[2 * r], ev[2 * r + 1]));
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    DS_CUDA(cudaMemcpy(trace->span, E->span, size_t(replays) * 16, cudaMemcpyDeviceToHost));
+    if (trace->stamps && E->stamps)
+        DS_CUDA(cudaMemcpy(trace->stamps, E->stamps, size_t(replays) * E->total_ctas * 16, cudaMemcpyDeviceToHost));
+    if (trace->smids && E->smids)
+        DS_CUDA(cudaMemcpy(trace->smids, E->smids, size_t(replays) * E->total_ctas * 4, cudaMemcpyDeviceToHost));
+    return DS_OK;
+}
+
+int ds_exec_read_output(void* exec, int node, void* host, uint64_t n_elems) {
+    Exec* E = static_cast<ExecHandle*>(exec)->E;
+    if (node < 0 || node >= int(E->y.size()) || n_elems > E->elems[node]) return fail(DS_EINVAL, "bad node");
+    DS_CUDA(cudaSetDevice(E->device));
+    DS_CUDA(cudaMemcpy(host, E->y[node], n_elems * 4, cudaMemcpyDeviceToHost));
+    return DS_OK;
+}
+
+int ds_exec_free(void* exec) {
+    auto* H = static_cast<ExecHandle*>(exec);
+    if (!H) return DS_OK;
+    destroy(H->E);
+    delete H;
+    return DS_OK;
+}
+
+int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int block_threads, int reps,
+                         float* ms_per_launch, uint64_t* span_ns, int device) {
+    if (ctas < 1 || reps < 1 || elems_per_cta < 4) return fail(DS_EINVAL, "bad bench arguments");
+    if (workload < DS_WL_MIX32 || workload > DS_WL_MIX32_BULK) return fail(DS_EINVAL, "bad workload");
+    const int threads = block_threads > 0 ? block_threads : 1024;
+    DS_CUDA(cudaSetDevice(device));
+    if (int rc = set_attrs(workload)) return rc;
+    const uint64_t n = uint64_t(ctas) * elems_per_cta;
+    uint32_t *x = nullptr, *y = nullptr;
+    int* replay = nullptr;
+    unsigned long long* span = nullptr;
+    DS_CUDA(cudaMalloc(&x, n * 4));
+    DS_CUDA(cudaMalloc(&y, n * 4));
+    DS_CUDA(cudaMalloc(&replay, sizeof(int)));
+    DS_CUDA(cudaMalloc(&span, 16));
+    k2_init<<<592, 512>>>(x, n, 7u, workload == DS_WL_AXPY32, y);
+    const int zero = 0;
+    const unsigned long long sinit[2] = {~0ull, 0};
+    DS_CUDA(cudaMemcpy(replay, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    NodeArgs a{};
+    a.x = x;
+    a.y = y;
+    a.lo = 0;
+    a.hi = n;
+    a.span = span;
+    a.replay = replay;
+    a.total = uint32_t(ctas);
+    a.a = 0.75f;
+    a.cap = 1;
+    const size_t sm = size_t(smem_of(workload) > kNodeSmem ? smem_of(workload) : kNodeSmem);
+    auto launch = [&]() {
+        switch (workload) {
+            case DS_WL_AXPY32: k2_axpy<<<ctas, threads, sm>>>(a); break;
+            case DS_WL_MIX32_BULK: k2_mix_bulk<<<ctas, threads, sm>>>(a); break;
+            default: k2_mix<<<ctas, threads, sm>>>(a);
+        }
+    };
+    for (int i = 0; i < 3; ++i) launch();  // warm-up
+    cudaEvent_t e0, e1;
+    DS_CUDA(cudaEventCreate(&e0));
+    DS_CUDA(cudaEventCreate(&e1));
+    DS_CUDA(cudaDeviceSynchronize());
+    DS_CUDA(cudaEventRecord(e0));
+    for (int i = 0; i < reps; ++i) launch();
+    DS_CUDA(cudaEventRecord(e1));
+    DS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    DS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    DS_CUDA(cudaMemcpy(span, sinit, 16, cudaMemcpyHostToDevice));
+    launch();  // one stamped launch for the globaltimer span
+    unsigned long long s[2];
+    DS_CUDA(cudaMemcpy(s, span, 16, cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaGetLastError());
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(x);
+    cudaFree(y);
+    cudaFree(replay);
+    cudaFree(span);
+    if (ms_per_launch) *ms_per_launch = ms / reps;
+    if (span_ns) *span_ns = s[1] - s[0];
+    return DS_OK;
+}
+
+}  // extern "C"

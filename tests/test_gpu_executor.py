@@ -1,0 +1,111 @@
+"""GPU suite for the executor (K3) and node workloads (K2).
+
+* node-kernel outputs are bit-exact against host twins (integer mix: exact;
+  fp32 axpy: computed without FMA contraction, so numpy float32 is exact);
+* measured traces satisfy the reference's executor contracts on every
+  replay: check_precedence (simulator.cpp:209-224) on %globaltimer stamps,
+  SM exclusivity (check_capacity, :192-207, at SM granularity) on %smid, and
+  group order (simulate_scheme, :44-94) with barrier_groups.
+"""
+import numpy as np
+import pytest
+
+from paper_2602_20826_b200 import executor as X
+from paper_2602_20826_b200 import scheme, workloads, _lib
+from paper_2602_20826_b200.batch import pack
+
+pytestmark = pytest.mark.gpu
+UNIT = 4096  # small unit for tests
+
+
+def _scheme_and_loads(dag, M):
+    b = pack([dag])
+    schemes, st = scheme.schedule_batch(b, M)
+    assert st[0] == 0
+    nodes = sorted(dag[0], key=lambda t: t[0]) if isinstance(dag[0][0], tuple) else list(enumerate(dag[0]))
+    loads = [l for _, l in nodes]
+    ids = [i for i, _ in nodes]
+    idx = {i: k for k, i in enumerate(ids)}
+    edges = [(idx[u], idx[v]) for u, v in dag[1]]
+    return schemes[0], loads, edges
+
+
+@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_BULK])
+@pytest.mark.parametrize("name,dag,M", [("fig2_M8_split", workloads.make_example_task(), 8),
+                                        ("c1_fan", workloads.c1_fork_join(), 148),
+                                        ("c4", workloads.oversized_dag(1, 148), 148)])
+def test_outputs_bit_exact(workload, name, dag, M):
+    s, loads, edges = _scheme_and_loads(dag, M)
+    plan = X.plan_from_scheme(s, loads, UNIT + 3)  # odd unit: ragged slices
+    ex = X.Executor(plan, workload=workload, seed=5)
+    ex.run(1, warmup=0, stamps=False)
+    for v in range(len(loads)):
+        want = X.mix32(X.node_input(5, v, plan.node_elems[v]))
+        assert np.array_equal(ex.output(v), want), (name, v)
+    ex.close()
+
+
+def test_axpy_matches_numpy_fp32():
+    s, loads, edges = _scheme_and_loads(workloads.make_example_task(), 8)
+    plan = X.plan_from_scheme(s, loads, UNIT + 1)
+    ex = X.Executor(plan, workload=X.WL_AXPY32, seed=9)
+    ex.run(1, warmup=0, stamps=False)
+    for v in range(len(loads)):
+        x, y = X.node_inputs_fp(9, v, plan.node_elems[v])
+        want = (np.float32(0.75) * x) + y
+        got = ex.output(v).view(np.float32)
+        assert np.array_equal(got, want), v  # tolerance 0 ulp: no FMA contraction
+    ex.close()
+
+
+def test_segments_cover_each_node_once():
+    s, loads, edges = _scheme_and_loads(workloads.make_example_task(), 8)
+    assert s.segmentations, "Fig. 2 at M=8 splits node 2 (Appendix A.2)"
+    plan = X.plan_from_scheme(s, loads, 1000)
+    for v in range(len(loads)):
+        rng = sorted((e.lo, e.hi) for e in plan.entities if e.node == v)
+        assert rng[0][0] == 0 and rng[-1][1] == plan.node_elems[v]
+        assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+
+
+@pytest.mark.parametrize("barrier", [True, False])
+def test_trace_contracts_hold(barrier):
+    corpus = _lib.Corpus(40, seed=1)
+    b = corpus.batch()
+    schemes, st = scheme.schedule_batch(b, 148)
+    for d in range(0, 40, 8):
+        n0, n1 = int(b.node_off[d]), int(b.node_off[d + 1])
+        loads = [int(x) for x in b.load_num[n0:n1]]
+        plan = X.plan_from_scheme(schemes[d], loads, 8192, barrier_groups=barrier)
+        ex = X.Executor(plan)
+        res = ex.run(20, warmup=2)
+        for r in range(20):
+            assert X.check_precedence(plan, res, r) == []
+            assert X.check_sm_exclusive(plan, res, r) == 0
+            if barrier:
+                assert X.group_overlap_violations(plan, res, r) == 0
+        assert (res.makespan_us > 0).all()
+        ex.close()
+
+
+@pytest.mark.parametrize("kind", ["serial", "multistream"])
+def test_baselines_run_and_respect_edges(kind):
+    dag = workloads.inception_dag()
+    loads = [l for _, l in dag[0]]
+    plan = X.plan_baseline(kind, loads, dag[1], 148, 4096)
+    ex = X.Executor(plan)
+    res = ex.run(10, warmup=2)
+    for r in range(10):
+        assert X.check_precedence(plan, res, r) == []
+        assert X.check_sm_exclusive(plan, res, r) == 0
+    for v in (0, 5, len(loads) - 1):
+        assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+    ex.close()
+
+
+def test_node_kernel_bench_sane():
+    for wl in (X.WL_MIX32, X.WL_MIX32_BULK, X.WL_AXPY32):
+        ms, span = X.node_kernel_bench(wl, 148, 1 << 20, reps=5)
+        gbs = 148 * (1 << 20) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
+        assert 500 < gbs < 9000, (wl, gbs)
+        assert span > 0
