@@ -1,22 +1,25 @@
 #!/usr/bin/env python
 """Executor benchmark (configs C1-C4): measured DAG makespan vs analysed bound.
 
-For every DAG: K1 schedules it on the GPU (ds_schedule_batch, M = 148), K3
-turns the schedule into one CUDA Graph of K2 node kernels (grid = SM quota,
-one CTA per SM), and the graph is replayed R times; each replay's makespan is
-first-CTA-start -> last-CTA-end on %globaltimer. Next to it, the same DAG runs
-as a serial stream and as naive multi-stream launch (original edges only,
-every kernel at min(m^max, M)).
+For every DAG: K1 schedules it on the GPU (ds_schedule_batch, M = the SM
+partition), K3 turns the schedule into one CUDA Graph of K2 node kernels
+(grid = SM quota, one CTA per SM) and replays it R times; each replay's
+makespan is first-CTA-start -> last-CTA-end on %globaltimer. Variants, all as
+CUDA Graphs of the same kernels on the same SMs:
+  proposed       the schedule with group barriers (simulate_scheme semantics)
+  proposed_deps  the schedule with its augmented-graph edges only
+  serial         one chain in topological order, m = min(m^max, M)
+  multistream    original DAG edges only, m = min(m^max, M) — naive
+                 multi-stream launch / Greedy
 
-Time unit: one load unit = ``--unit`` elements per SM of the node kernel.
-tau = the time of one unit on every SM at once (148 CTAs x unit elements,
-full HBM contention, CUDA events) — the worst case a kernel of the schedule
-can see, since a group never holds more than 148 SMs. bound_us = bound x tau;
-per-group graph dependency latency delta (a chain of minimal kernels) is
-measured and reported separately (SURVEY.md §7 hard part 4).
+M = 148 runs on the whole GPU; M < 148 runs inside a green context of M SMs
+(the paper's contended regime: Jetson M=8, RTX 3060 M=30).
 
-Writes one JSON document (default profiles/r01_executor.json) and prints a
-one-line summary.
+Time unit (per partition, executor.calibrate): tau = p99 time of one unit of
+work on every SM at once; delta = latency per group boundary. The bound in
+microseconds is bound_units * tau + (|groups| - 1) * delta.
+
+Writes one JSON document (default profiles/r01_executor.json).
 """
 from __future__ import annotations
 
@@ -35,29 +38,13 @@ from paper_2602_20826_b200 import _lib, scheme, workloads  # noqa: E402
 from paper_2602_20826_b200 import executor as X  # noqa: E402
 from paper_2602_20826_b200.batch import pack  # noqa: E402
 
-M = 148
+VARIANTS = ("proposed", "proposed_deps", "serial", "multistream")
 
 
 def stats(a):
     a = np.asarray(a, np.float64)
     return {"p50": float(np.percentile(a, 50)), "p99": float(np.percentile(a, 99)), "max": float(a.max()),
-            "mean": float(a.mean()), "min": float(a.min())}
-
-
-def calibrate(unit, workload, reps=50):
-    ms, span = X.node_kernel_bench(workload, M, unit, reps=reps)
-    return ms * 1e3, span / 1e3  # us per unit at full contention (events), globaltimer span
-
-
-def chain_delta(n=64, reps=50):
-    """Graph dependency latency: a chain of n 1-CTA minimal kernels."""
-    loads = [1] * n
-    edges = [(i, i + 1) for i in range(n - 1)]
-    plan = X.plan_baseline("serial", loads, edges, M, 4)
-    ex = X.Executor(plan)
-    res = ex.run(reps, warmup=3, stamps=False)
-    ex.close()
-    return float(np.median(res.makespan_us)) / n
+            "mean": float(a.mean()), "std": float(a.std()), "min": float(a.min())}
 
 
 def dag_from_batch(b, d):
@@ -68,39 +55,73 @@ def dag_from_batch(b, d):
     return loads, edges
 
 
-def run_dag(loads, edges, sch, unit, tau_us, replays, workload, check_every):
+def normalise(nodes, edges):
+    nodes = list(nodes)
+    if nodes and isinstance(nodes[0], tuple):
+        nodes = sorted(nodes, key=lambda t: t[0])
+        idx = {i: k for k, (i, _) in enumerate(nodes)}
+        return [l for _, l in nodes], [(idx[u], idx[v]) for u, v in edges]
+    return nodes, list(edges)
+
+
+def run_dag(loads, edges, sch, M, sm_limit, cal, args):
+    bound_units = sch.bounds["proposed"]
+    bound_us = X.bound_us(sch, cal)
     out = {"n": len(loads), "groups": len(sch.groups), "segmentations": len(sch.segmentations),
-           "launches": sum(len(g.launches) for g in sch.groups),
-           "bound_units": str(sch.bounds["proposed"]), "greedy_units": str(sch.bounds["greedy"])}
-    bound_us = float(sch.bounds["proposed"]) * tau_us
-    out["bound_us"] = bound_us
-    res = {}
-    for kind in ("proposed", "serial", "multistream"):
+           "launches": sum(len(g.launches) for g in sch.groups), "bound_units": str(bound_units),
+           "greedy_units": str(sch.bounds["greedy"]), "bound_us": bound_us}
+    for kind in VARIANTS:
         if kind == "proposed":
-            plan = X.plan_from_scheme(sch, loads, unit, barrier_groups=True)
+            plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=True)
+        elif kind == "proposed_deps":
+            plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=False)
         else:
-            plan = X.plan_baseline(kind, loads, edges, M, unit)
-        ex = X.Executor(plan, workload=workload)
-        r = ex.run(replays, warmup=3, stamps=True)
-        viol_prec = viol_sm = viol_grp = 0
-        for k in range(0, replays, check_every):
-            viol_prec += len(X.check_precedence(plan, r, k))
-            viol_sm += X.check_sm_exclusive(plan, r, k)
-            viol_grp += X.group_overlap_violations(plan, r, k)
+            plan = X.plan_baseline(kind, loads, edges, M, args.unit)
+        ex = X.Executor(plan, workload=args.workload, sm_limit=sm_limit)
+        r = ex.run(args.replays, warmup=3, stamps=True)
+        vp = vs = vg = 0
+        checked = range(0, args.replays, args.check_every)
+        for k in checked:
+            vp += len(X.check_precedence(plan, r, k))
+            vs += X.check_sm_exclusive(plan, r, k)
+            vg += X.group_overlap_violations(plan, r, k)
         ex.close()
-        res[kind] = {"makespan_us": stats(r.makespan_us), "launch_us": stats(r.launch_ms * 1e3),
-                     "precedence_violations": viol_prec, "sm_overlap_violations": viol_sm,
-                     "group_order_violations": viol_grp, "checked_replays": len(range(0, replays, check_every))}
-        if kind == "proposed":
-            out["ratio_to_bound"] = stats(r.makespan_us / bound_us)
-            out["over_bound_replays"] = int((r.makespan_us > bound_us).sum())
-    out.update(res)
+        out[kind] = {"makespan_us": stats(r.makespan_us), "graph_launch_us": stats(r.launch_ms * 1e3),
+                     "precedence_violations": vp, "sm_overlap_violations": vs, "group_order_violations": vg,
+                     "checked_replays": len(checked),
+                     "over_bound_replays": int((r.makespan_us > bound_us).sum()),
+                     "ratio_to_bound": stats(r.makespan_us / bound_us)}
     return out
+
+
+def summarise(results, prefix):
+    sel = [r for r in results if r["name"].startswith(prefix) and "proposed" in r]
+    if not sel:
+        return None
+    s = {"dags": len(sel)}
+    for kind in VARIANTS:
+        s[kind] = {
+            "mean_p50_us": float(np.mean([r[kind]["makespan_us"]["p50"] for r in sel])),
+            "mean_p99_us": float(np.mean([r[kind]["makespan_us"]["p99"] for r in sel])),
+            "mean_max_us": float(np.mean([r[kind]["makespan_us"]["max"] for r in sel])),
+            "mean_std_us": float(np.mean([r[kind]["makespan_us"]["std"] for r in sel])),
+            "replays_over_bound": int(sum(r[kind]["over_bound_replays"] for r in sel)),
+            "max_ratio_to_bound": float(max(r[kind]["ratio_to_bound"]["max"] for r in sel)),
+            "trace_violations": int(sum(r[kind]["precedence_violations"] + r[kind]["sm_overlap_violations"]
+                                        for r in sel)),
+        }
+    for kind in ("proposed", "proposed_deps"):
+        for q in ("p50", "p99", "max"):
+            s[f"{kind}_beats_multistream_{q}"] = int(sum(r[kind]["makespan_us"][q] < r["multistream"]["makespan_us"][q]
+                                                         for r in sel))
+    s["group_order_violations"] = int(sum(r["proposed"]["group_order_violations"] for r in sel))
+    return s
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--sm-limits", default="0,32,8", help="0 = whole GPU (148 SMs); else green-context size")
     ap.add_argument("--replays", type=int, default=1000)
     ap.add_argument("--c2-dags", type=int, default=100)
     ap.add_argument("--unit", type=int, default=1 << 17, help="elements per load unit per SM")
@@ -110,100 +131,74 @@ def main():
     args = ap.parse_args()
 
     t_start = time.time()
-    doc = {"sm_count": M, "unit_elems": args.unit, "workload": args.workload,
-           "bytes_per_elem": X.BYTES_PER_ELEM[args.workload], "replays": args.replays}
-    tau_us, tau_span_us = calibrate(args.unit, args.workload)
-    doc["tau_us"] = tau_us
-    doc["tau_globaltimer_us"] = tau_span_us
-    doc["delta_us_per_dependency"] = chain_delta()
-    # node-kernel roofline: 148 CTAs x 4 Mi elements (4.6 GB traffic, >> L2)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    doc = {"unit_elems": args.unit, "workload": args.workload, "bytes_per_elem": X.BYTES_PER_ELEM[args.workload],
+           "replays": args.replays, "variants": VARIANTS, "partitions": []}
+    peaks_p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak = json.load(open(peaks_p))["hbm_gbs"] if os.path.exists(peaks_p) else 6650.0
     roof = {}
     for wl, name in ((X.WL_MIX32, "mix32_ldg128"), (X.WL_MIX32_BULK, "mix32_bulk_tma"), (X.WL_AXPY32, "axpy_fp32")):
-        ms, _ = X.node_kernel_bench(wl, M, 1 << 22, reps=20)
-        gbs = M * (1 << 22) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
-        roof[name] = {"ms": ms, "GB/s": gbs, "frac_of_measured_peak": gbs / peaks["hbm_gbs"]}
+        ms, _ = X.node_kernel_bench(wl, 148, 1 << 22, reps=20)
+        gbs = 148 * (1 << 22) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
+        roof[name] = {"ms": ms, "GB/s": gbs, "frac_of_measured_peak": gbs / peak}
     doc["node_kernel_roofline"] = roof
-    doc["hbm_peak_gbs"] = peaks["hbm_gbs"]
+    doc["hbm_peak_gbs"] = peak
 
-    cases = []
     cfgs = args.configs.split(",")
-    if "c1" in cfgs:
-        cases.append(("c1_fan_8_20_1", workloads.c1_fork_join()))
-    if "c3" in cfgs:
-        cases.append(("c3_inception", workloads.inception_dag()))
-    if "c4" in cfgs:
-        for s in range(3):
-            cases.append((f"c4_oversized_{s}", workloads.oversized_dag(s, M)))
-    if "c2" in cfgs:
-        corpus = _lib.Corpus(600, seed=1)
-        b = corpus.batch()
-        sizes = np.diff(b.node_off.astype(np.int64))
-        picked = [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:args.c2_dags]
-        for d in picked:
-            cases.append((f"c2_seed{1 + d}", dag_from_batch(b, d)))
-    # schedule everything on the GPU in one batch
-    packed = []
-    for name, (nodes, edges) in cases:
-        packed.append((nodes, edges))
-    batch = pack(packed)
-    schemes, st = scheme.schedule_batch(batch, M)
-    results = []
-    for (name, (nodes, edges)), sch, s in zip(cases, schemes, st):
-        if s != 0:
-            results.append({"name": name, "status": int(s)})
-            continue
-        nodes = list(nodes)
-        if nodes and isinstance(nodes[0], tuple):
-            nodes = sorted(nodes, key=lambda t: t[0])
-            ids = [i for i, _ in nodes]
-            idx = {i: k for k, i in enumerate(ids)}
-            loads = [l for _, l in nodes]
-            edges = [(idx[u], idx[v]) for u, v in edges]
-        else:
-            loads = nodes
-        r = run_dag(loads, edges, sch, args.unit, tau_us, args.replays, args.workload, args.check_every)
-        r["name"] = name
-        results.append(r)
-        print(f"{name}: n={r['n']} groups={r['groups']} bound={r['bound_units']}u={r['bound_us']:.1f}us "
-              f"proposed p50={r['proposed']['makespan_us']['p50']:.1f} max={r['proposed']['makespan_us']['max']:.1f} "
-              f"serial p50={r['serial']['makespan_us']['p50']:.1f} multi p50={r['multistream']['makespan_us']['p50']:.1f} "
-              f"over={r['over_bound_replays']}", flush=True)
-    doc["dags"] = results
-    ok = [r for r in results if "proposed" in r]
-
-    def agg(prefix):
-        sel = [r for r in ok if r["name"].startswith(prefix)]
-        if not sel:
-            return None
-        return {
-            "dags": len(sel),
-            "replays_over_bound": int(sum(r["over_bound_replays"] for r in sel)),
-            "max_ratio_to_bound": max(r["ratio_to_bound"]["max"] for r in sel),
-            "median_ratio_to_bound": float(np.median([r["ratio_to_bound"]["p50"] for r in sel])),
-            "proposed_p50_us_mean": float(np.mean([r["proposed"]["makespan_us"]["p50"] for r in sel])),
-            "serial_p50_us_mean": float(np.mean([r["serial"]["makespan_us"]["p50"] for r in sel])),
-            "multistream_p50_us_mean": float(np.mean([r["multistream"]["makespan_us"]["p50"] for r in sel])),
-            "proposed_beats_multistream_p50": int(sum(r["proposed"]["makespan_us"]["p50"] <
-                                                      r["multistream"]["makespan_us"]["p50"] for r in sel)),
-            "proposed_beats_multistream_p99": int(sum(r["proposed"]["makespan_us"]["p99"] <
-                                                      r["multistream"]["makespan_us"]["p99"] for r in sel)),
-            "precedence_violations": int(sum(r[k]["precedence_violations"] for r in sel
-                                             for k in ("proposed", "serial", "multistream"))),
-            "sm_overlap_violations": int(sum(r[k]["sm_overlap_violations"] for r in sel
-                                             for k in ("proposed", "serial", "multistream"))),
-            "group_order_violations": int(sum(r["proposed"]["group_order_violations"] for r in sel)),
-        }
-
-    doc["summary"] = {k: agg(k) for k in ("c1", "c2", "c3", "c4")}
+    for sm_limit in (int(x) for x in args.sm_limits.split(",")):
+        cal = X.calibrate(args.unit, sm_limit=sm_limit, workload=args.workload)
+        M = cal["sm_count"]
+        cases = []
+        if "c1" in cfgs:
+            cases.append(("c1_fan_8_20_1", workloads.c1_fork_join()))
+        if "c3" in cfgs:
+            cases.append(("c3_inception", workloads.inception_dag()))
+        if "c4" in cfgs:
+            for s in range(3):
+                cases.append((f"c4_oversized_{s}", workloads.oversized_dag(s, M)))
+        if "c2" in cfgs:
+            corpus = _lib.Corpus(600, seed=1)
+            b = corpus.batch()
+            sizes = np.diff(b.node_off.astype(np.int64))
+            picked = [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:args.c2_dags]
+            cases += [(f"c2_seed{1 + d}", dag_from_batch(b, d)) for d in picked]
+            if M <= 32:  # the paper's Table 1 load level (C_avg = 4)
+                small = _lib.Corpus(600, seed=1, avg_load=4)
+                bs = small.batch()
+                sizes = np.diff(bs.node_off.astype(np.int64))
+                picked = [d for d in range(bs.n_dags) if 20 <= sizes[d] <= 50][:max(10, args.c2_dags // 4)]
+                cases += [(f"c2avg4_seed{1 + d}", dag_from_batch(bs, d)) for d in picked]
+        norm = [normalise(n, e) for _, (n, e) in cases]
+        schemes, st = scheme.schedule_batch(pack([(l, e) for l, e in norm]), M)
+        results = []
+        for (name, _), (loads, edges), sch, s in zip(cases, norm, schemes, st):
+            if s != 0:
+                results.append({"name": name, "status": int(s)})
+                continue
+            r = run_dag(loads, edges, sch, M, sm_limit, cal, args)
+            r["name"] = name
+            results.append(r)
+            print(f"M={M} {name}: n={r['n']} G={r['groups']} bound={r['bound_us']:.0f}us | p50 "
+                  + " ".join(f"{k}={r[k]['makespan_us']['p50']:.0f}" for k in VARIANTS)
+                  + f" | over={r['proposed']['over_bound_replays']}", flush=True)
+        part = {"sm_limit": sm_limit, "M": M, "calibration": cal, "dags": results,
+                "summary": {k: summarise(results, k) for k in ("c1", "c2_", "c2avg4", "c3", "c4")}}
+        doc["partitions"].append(part)
     doc["wall_s"] = time.time() - t_start
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(doc, f, indent=1)
-    print(json.dumps({"tau_us": tau_us, "delta_us": doc["delta_us_per_dependency"],
-                      "roofline": {k: round(v["frac_of_measured_peak"], 3) for k, v in roof.items()},
-                      "summary": doc["summary"]}))
+    brief = {"roofline": {k: round(v["frac_of_measured_peak"], 3) for k, v in roof.items()}}
+    for p in doc["partitions"]:
+        c = p["calibration"]
+        row = {"tau": round(c["tau_us"], 2), "delta": round(c["delta_us"], 2), "eps": round(c["eps_us"], 2)}
+        for k, v in p["summary"].items():
+            if v:
+                row[k] = {"over": v["proposed"]["replays_over_bound"],
+                          "maxratio": round(v["proposed"]["max_ratio_to_bound"], 3),
+                          "p50": [round(v[x]["mean_p50_us"], 1) for x in VARIANTS],
+                          "deps_over": v["proposed_deps"]["replays_over_bound"]}
+        brief[f"M{p['M']}"] = row
+    print(json.dumps(brief))
 
 
 if __name__ == "__main__":

@@ -192,7 +192,9 @@ typedef struct ds_exec_cfg {
     int32_t workload;       /* DS_WL_*                                           */
     int32_t block_threads;  /* threads per CTA (<= 1024)                         */
     uint32_t seed;          /* input initialisation                              */
-    int32_t reserved;
+    int32_t sm_limit;       /* 0: whole GPU; else run inside a green context of
+                               this many SMs (multiple of 8 on sm_90+) — an
+                               M-SM device for the paper's contended regime   */
 } ds_exec_cfg;
 
 /* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
@@ -260,6 +262,8 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
 int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace);
 /* Total CTAs of one replay (sum of parallelism) — sizes the stamp arrays. */
 int ds_exec_total_ctas(void* exec, uint64_t* total);
+/* SMs the executor runs on (the green-context size when sm_limit > 0). */
+int ds_exec_sm_count(void* exec, int* sms);
 /* Copies node `node`'s output buffer (uint32 / fp32 words) to host memory. */
 int ds_exec_read_output(void* exec, int node, void* host, uint64_t n_elems);
 int ds_exec_free(void* exec);

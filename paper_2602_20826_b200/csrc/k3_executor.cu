@@ -19,6 +19,7 @@
 #include "../../include/dagsched_b200.h"
 #include "k2_workload.cuh"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,6 +42,9 @@ namespace {
 
 struct Exec {
     int device = 0;
+    int sm_count = 0;             // SMs the executor may use
+    CUgreenCtx gctx = nullptr;    // green context when sm_limit > 0
+    CUcontext ctx = nullptr;      // its runtime-usable context handle
     int workload = DS_WL_MIX32;
     int threads = 1024;
     cudaStream_t s = nullptr;
@@ -73,9 +77,81 @@ int set_attrs(int wl) {
     return DS_OK;
 }
 
+// Driver entry points for green contexts, resolved through the runtime
+// (cudaGetDriverEntryPoint) so the library does not link libcuda and still
+// loads on machines without a driver (the CPU test suite).
+struct Driver {
+    decltype(&cuDeviceGetDevResource) getDevResource = nullptr;
+    decltype(&cuDevSmResourceSplitByCount) split = nullptr;
+    decltype(&cuDevResourceGenerateDesc) genDesc = nullptr;
+    decltype(&cuGreenCtxCreate) greenCreate = nullptr;
+    decltype(&cuGreenCtxDestroy) greenDestroy = nullptr;
+    decltype(&cuCtxFromGreenCtx) fromGreen = nullptr;
+    decltype(&cuGreenCtxStreamCreate) greenStream = nullptr;
+    decltype(&cuCtxPushCurrent) push = nullptr;
+    decltype(&cuCtxPopCurrent) pop = nullptr;
+    bool ok = false;
+};
+
+const Driver& driver() {
+    static Driver d = [] {
+        Driver r;
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn;
+        };
+        r.ok = get("cuDeviceGetDevResource", reinterpret_cast<void**>(&r.getDevResource)) &&
+               get("cuDevSmResourceSplitByCount", reinterpret_cast<void**>(&r.split)) &&
+               get("cuDevResourceGenerateDesc", reinterpret_cast<void**>(&r.genDesc)) &&
+               get("cuGreenCtxCreate", reinterpret_cast<void**>(&r.greenCreate)) &&
+               get("cuGreenCtxDestroy", reinterpret_cast<void**>(&r.greenDestroy)) &&
+               get("cuCtxFromGreenCtx", reinterpret_cast<void**>(&r.fromGreen)) &&
+               get("cuGreenCtxStreamCreate", reinterpret_cast<void**>(&r.greenStream)) &&
+               get("cuCtxPushCurrent", reinterpret_cast<void**>(&r.push)) &&
+               get("cuCtxPopCurrent", reinterpret_cast<void**>(&r.pop));
+        return r;
+    }();
+    return d;
+}
+
+// Makes the executor's context current for the guard's lifetime: the green
+// context (an M-SM partition of the GPU) when one was requested.
+struct CtxGuard {
+    bool pushed = false;
+    explicit CtxGuard(const Exec* E) {
+        if (E->ctx) pushed = driver().push(E->ctx) == CUDA_SUCCESS;
+        else cudaSetDevice(E->device);
+    }
+    ~CtxGuard() {
+        CUcontext c;
+        if (pushed) driver().pop(&c);
+    }
+};
+
+// Green context with `want` SMs (rounded by the driver to its granularity).
+int make_green(Exec* E, int want) {
+    const Driver& D = driver();
+    if (!D.ok) return fail(DS_ECUDA, "green-context driver entry points unavailable");
+    CUdevResource all, part, rest;
+    unsigned int nb = 1;
+    CUdevResourceDesc desc;
+    cudaFree(nullptr);  // make sure the runtime (and driver) are initialised
+    if (D.getDevResource(CUdevice(E->device), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+        D.split(&part, &nb, &all, &rest, 0, unsigned(want)) != CUDA_SUCCESS ||
+        D.genDesc(&desc, &part, 1) != CUDA_SUCCESS ||
+        D.greenCreate(&E->gctx, desc, CUdevice(E->device), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        D.fromGreen(&E->ctx, E->gctx) != CUDA_SUCCESS) {
+        return fail(DS_ECUDA, "green context creation failed");
+    }
+    E->sm_count = int(part.sm.smCount);
+    return DS_OK;
+}
+
 void destroy(Exec* E) {
     if (!E) return;
-    cudaSetDevice(E->device);
+    {
+    CtxGuard g(E);
     if (E->s) cudaStreamSynchronize(E->s);
     if (E->exec) cudaGraphExecDestroy(E->exec);
     if (E->graph) cudaGraphDestroy(E->graph);
@@ -86,6 +162,8 @@ void destroy(Exec* E) {
     if (E->stamps) cudaFree(E->stamps);
     if (E->smids) cudaFree(E->smids);
     if (E->s) cudaStreamDestroy(E->s);
+    }
+    if (E->gctx) driver().greenDestroy(E->gctx);
     delete E;
 }
 
@@ -217,6 +295,12 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
         return rc;
     };
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DS_ECUDA, "cudaSetDevice"));
+    if (cfg->sm_limit > 0) {
+        if (int rc = make_green(E, cfg->sm_limit)) return bail(rc);
+    } else {
+        cudaDeviceGetAttribute(&E->sm_count, cudaDevAttrMultiProcessorCount, device);
+    }
+    CtxGuard guard(E);
     if (int rc = set_attrs(E->workload)) return bail(rc);
     H->P.ents.assign(plan->entities, plan->entities + plan->n_entities);
     uint64_t npreds = 0;
@@ -236,8 +320,14 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     H->P.plan.entities = H->P.ents.data();
     H->P.plan.preds = H->P.preds.data();
     H->P.plan.node_elems = H->P.elems.data();
-    if (cudaStreamCreateWithFlags(&E->s, cudaStreamNonBlocking) != cudaSuccess)
+    if (E->gctx) {
+        CUstream cs;
+        if (driver().greenStream(&cs, E->gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+            return bail(fail(DS_ECUDA, "green-context stream"));
+        E->s = reinterpret_cast<cudaStream_t>(cs);
+    } else if (cudaStreamCreateWithFlags(&E->s, cudaStreamNonBlocking) != cudaSuccess) {
         return bail(fail(DS_ECUDA, "stream"));
+    }
     for (int v = 0; v < plan->n_nodes; ++v) {
         const uint64_t ne = std::max<uint64_t>(plan->node_elems[v], 4);
         uint32_t *x = nullptr, *y = nullptr;
@@ -260,11 +350,16 @@ int ds_exec_total_ctas(void* exec, uint64_t* total) {
     return DS_OK;
 }
 
+int ds_exec_sm_count(void* exec, int* sms) {
+    *sms = static_cast<ExecHandle*>(exec)->E->sm_count;
+    return DS_OK;
+}
+
 int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     auto* H = static_cast<ExecHandle*>(exec);
     Exec* E = H->E;
     if (replays < 1 || warmup < 0 || !trace || !trace->span) return fail(DS_EINVAL, "bad run arguments");
-    DS_CUDA(cudaSetDevice(E->device));
+    CtxGuard guard(E);
     const bool want_stamps = trace->stamps || trace->smids;
     if (replays > E->cap || !E->exec || (want_stamps && !E->stamps)) {
         if (E->span) cudaFree(E->span);
@@ -314,7 +409,7 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
 int ds_exec_read_output(void* exec, int node, void* host, uint64_t n_elems) {
     Exec* E = static_cast<ExecHandle*>(exec)->E;
     if (node < 0 || node >= int(E->y.size()) || n_elems > E->elems[node]) return fail(DS_EINVAL, "bad node");
-    DS_CUDA(cudaSetDevice(E->device));
+    CtxGuard guard(E);
     DS_CUDA(cudaMemcpy(host, E->y[node], n_elems * 4, cudaMemcpyDeviceToHost));
     return DS_OK;
 }

@@ -44,7 +44,7 @@ class ds_exec_plan(C.Structure):
 
 class ds_exec_cfg(C.Structure):
     _fields_ = [("workload", C.c_int32), ("block_threads", C.c_int32), ("seed", C.c_uint32),
-                ("reserved", C.c_int32)]
+                ("sm_limit", C.c_int32)]
 
 
 class ds_exec_trace(C.Structure):
@@ -60,6 +60,7 @@ def _sig():
         ("ds_exec_create", C.c_int, [P(ds_exec_plan), P(ds_exec_cfg), C.c_int, P(C.c_void_p)]),
         ("ds_exec_run", C.c_int, [C.c_void_p, C.c_int, C.c_int, P(ds_exec_trace)]),
         ("ds_exec_total_ctas", C.c_int, [C.c_void_p, P(C.c_uint64)]),
+        ("ds_exec_sm_count", C.c_int, [C.c_void_p, P(C.c_int)]),
         ("ds_exec_read_output", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]),
         ("ds_exec_free", C.c_int, [C.c_void_p]),
         ("ds_node_kernel_bench", C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, P(C.c_float),
@@ -192,18 +193,23 @@ class RunResult:
 
 
 class Executor:
-    def __init__(self, plan: Plan, workload: int = WL_MIX32, threads: int = 1024, seed: int = 1, device: int = 0):
+    def __init__(self, plan: Plan, workload: int = WL_MIX32, threads: int = 1024, seed: int = 1, device: int = 0,
+                 sm_limit: int = 0):
+        """sm_limit > 0 runs the graph inside a green context of that many SMs."""
         L = _sig()
         self.plan = plan
         self.workload = workload
         self.seed = seed
         self.h = C.c_void_p()
         self._cplan = plan.to_c()
-        cfg = ds_exec_cfg(workload, threads, seed, 0)
+        cfg = ds_exec_cfg(workload, threads, seed, int(sm_limit))
         check(L.ds_exec_create(C.byref(self._cplan), C.byref(cfg), device, C.byref(self.h)))
         t = C.c_uint64()
         check(L.ds_exec_total_ctas(self.h, C.byref(t)))
         self.total_ctas = t.value
+        sms = C.c_int()
+        check(L.ds_exec_sm_count(self.h, C.byref(sms)))
+        self.sm_count = sms.value
         self.slots = np.cumsum([0] + [e.parallelism for e in plan.entities])
 
     def run(self, replays: int, warmup: int = 3, stamps: bool = True) -> RunResult:
@@ -317,6 +323,75 @@ def group_overlap_violations(plan: Plan, res: RunResult, r: int):
             end = max(win[i][1] for i in by[g])
             bad += sum(1 for i in by[g + 1] if win[i][0] < end)
     return bad
+
+
+def calibrate(unit_elems: int, sm_limit: int = 0, workload: int = WL_MIX32, replays: int = 200, groups: int = 16,
+              device: int = 0):
+    """Time unit and per-group latency, measured through the executor itself.
+
+    tau: p99 makespan of one entity holding every SM of the partition, each CTA
+    processing one unit (full HBM contention — the most any group member can
+    see). delta: extra latency per group boundary, from a chain of `groups`
+    such groups joined by barriers. A schedule's bound in microseconds is then
+    bound * tau + (|groups| - 1) * delta <= bound * (tau + delta), since every
+    group's response is at least t_min = 1 unit.
+    """
+    probe = Executor(Plan([PlanEntity("u", 0, 1, 0, [], 0, 4, Fraction(1))], [4], True),
+                     workload=workload, sm_limit=sm_limit, device=device)
+    sms = probe.sm_count
+    probe.close()
+    # a barrier chain of groups over distinct buffers so that, as in a real
+    # DAG, the working set (groups x sms x unit x 8 B) is DRAM- not L2-resident
+    n = sms * unit_elems
+    groups = max(groups, -(-(256 << 20) // (n * BYTES_PER_ELEM[workload])))
+    reps = max(20, replays // 4)
+    chain = Plan([PlanEntity(f"g{g}", g, sms, g, [], 0, n, Fraction(1)) for g in range(groups)], [n] * groups, True)
+    ex = Executor(chain, workload=workload, sm_limit=sm_limit, device=device)
+    rc = ex.run(reps, warmup=3, stamps=True)
+    ex.close()
+    dur, gap = [], []
+    for r in range(reps):
+        w = entity_windows(chain, rc, r)
+        dur += [(b - a) / 1e3 for a, b in w]
+        gap += [(w[g + 1][0] - w[g][1]) / 1e3 for g in range(groups - 1)]
+    tau, delta = float(np.percentile(dur, 99)), float(np.percentile(gap, 99))
+    # launch stagger: the same chain with k = 8 entities of sms/8 SMs per group
+    k = min(8, sms)
+    eps = 0.0
+    if k > 1:
+        per = sms // k
+        wide = Plan([PlanEntity(f"g{g}e{j}", g, per, g * k + j, [], 0, per * unit_elems, Fraction(1))
+                     for g in range(groups) for j in range(k)], [per * unit_elems] * (groups * k), True)
+        ex = Executor(wide, workload=workload, sm_limit=sm_limit, device=device)
+        rw = ex.run(reps, warmup=3, stamps=True)
+        ex.close()
+        stag = []
+        for r in range(reps):
+            w = entity_windows(wide, rw, r)
+            for g in range(groups):
+                starts = [w[g * k + j][0] for j in range(k)]
+                stag.append((max(starts) - min(starts)) / 1e3 / (k - 1))
+                if g + 1 < groups:  # barrier latency after a k-wide group
+                    end = max(w[g * k + j][1] for j in range(k))
+                    gap.append((min(w[(g + 1) * k + j][0] for j in range(k)) - end) / 1e3)
+        eps = float(np.percentile(stag, 99))
+        delta = float(np.percentile(gap, 99))
+    return {"sm_count": sms, "tau_us": tau, "tau_p50_us": float(np.median(dur)), "delta_us": delta,
+            "delta_p50_us": float(np.median(gap)), "eps_us": eps, "groups": groups,
+            "working_set_mb": groups * n * BYTES_PER_ELEM[workload] / 2 ** 20}
+
+
+def bound_us(scheme, cal) -> float:
+    """Theorem-1 bound in microseconds on this box: every group costs its
+    response in time units plus the measured group-boundary latency delta and
+    a launch stagger eps per additional concurrent entity."""
+    total = 0.0
+    for j, g in enumerate(scheme.groups):
+        k = len(g.members) + len(g.launches)
+        total += float(g.response) * cal["tau_us"] + (k - 1) * cal.get("eps_us", 0.0)
+        if j:
+            total += cal["delta_us"]
+    return total
 
 
 def node_kernel_bench(workload: int, ctas: int, elems_per_cta: int, reps: int = 20, threads: int = 1024,

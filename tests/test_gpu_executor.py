@@ -109,3 +109,22 @@ def test_node_kernel_bench_sane():
         gbs = 148 * (1 << 20) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
         assert 500 < gbs < 9000, (wl, gbs)
         assert span > 0
+
+
+def test_green_context_partition():
+    """sm_limit runs the graph inside a green context: the executor reports the
+    partition size and every CTA lands on one of that many SMs."""
+    s, loads, edges = _scheme_and_loads(workloads.make_fan(6, 12, 2), 16)
+    plan = X.plan_from_scheme(s, loads, 4096)
+    ex = X.Executor(plan, sm_limit=16)
+    assert ex.sm_count == 16
+    res = ex.run(5, warmup=1)
+    assert len(np.unique(res.smids)) <= 16
+    for r in range(5):
+        assert X.check_precedence(plan, res, r) == []
+        assert X.check_sm_exclusive(plan, res, r) == 0
+    for v in range(len(loads)):
+        assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+    ex.close()
+    cal = X.calibrate(4096, sm_limit=16, replays=20, groups=4)
+    assert cal["sm_count"] == 16 and cal["tau_us"] > 0
