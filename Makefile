@@ -18,7 +18,7 @@ CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/
 CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/dagsched_b200.h
 
 .PHONY: all product oracle ref clean
-all: product oracle ref
+all: product cppapi oracle ref
 
 product: $(LIBDIR)/libdagsched_b200.so
 
@@ -42,3 +42,26 @@ ref:
 clean:
 	rm -rf $(LIBDIR)
 	$(MAKE) -C oracle clean
+
+# ---------------------------------------------------------------- C++ API
+CPP_SRCS := $(wildcard $(PKG)/cpp/*.cpp)
+CPP_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(LIBDIR)/cpp_%.o,$(CPP_SRCS))
+API_INC  := -Iinclude -I$(PKG)/cpp
+REFPROJ  ?= /root/reference/proj
+
+cppapi: $(LIBDIR)/libdagsched_cpp.so $(LIBDIR)/api_parity $(if $(wildcard $(REFPROJ)/tests),$(LIBDIR)/api_test_dag_model $(LIBDIR)/api_test_exec_model)
+
+$(LIBDIR)/cpp_%.o: $(PKG)/cpp/%.cpp $(wildcard include/dagsched/*.hpp) $(PKG)/cpp/device.hpp include/dagsched_b200.h
+	@mkdir -p $(LIBDIR)
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Wno-comment $(API_INC) -c $< -o $@
+
+$(LIBDIR)/libdagsched_cpp.so: $(CPP_OBJS) $(LIBDIR)/libdagsched_b200.so
+	$(CXX) -shared -o $@ $(CPP_OBJS) -L$(LIBDIR) -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
+
+$(LIBDIR)/api_parity: tests/cpp/api_parity.cpp $(LIBDIR)/libdagsched_cpp.so
+	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
+
+# the reference's own unit tests (proj/tests, read in place) against this API
+$(LIBDIR)/api_test_%: $(REFPROJ)/tests/test_%.cpp $(LIBDIR)/libdagsched_cpp.so
+	$(CXX) -std=c++20 -O2 $(API_INC) -Ioracle/shim -I$(REFPROJ)/tests -DDOCTEST_CONFIG_IMPLEMENT_WITH_MAIN \
+	    -include oracle/shim/doctest.h $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
