@@ -146,6 +146,60 @@ def cpu_baseline_run(batch, kind_pref="ref", target_s=8.0, min_dags=4000, max_da
                       else "oracle/src restatement"}
 
 
+def makespan_summary(device, replays, n_c2=8, unit=1 << 17):
+    """First half of the BASELINE metric, small: measured DAG makespan vs the
+    analysed bound on this B200 (C1 fork-join + the first n_c2 C2 DAGs, M=148),
+    next to serial-stream and naive multi-stream launch. The full C1-C4 study
+    (1000 replays, 100 C2 DAGs, green-context partitions) is bench_executor.py
+    -> profiles/r01_executor.json."""
+    from paper_2602_20826_b200 import _lib, executor as X, scheme, workloads
+    from paper_2602_20826_b200.batch import pack
+
+    cal = X.calibrate(unit, device=device)
+    M = cal["sm_count"]
+    corpus = _lib.Corpus(200, seed=1)
+    b = corpus.batch()
+    sizes = np.diff(b.node_off.astype(np.int64))
+    dags = [workloads.c1_fork_join()]
+    names = ["c1"]
+    for d in [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:n_c2]:
+        n0, n1, e0, e1 = (int(b.node_off[d]), int(b.node_off[d + 1]), int(b.edge_off[d]), int(b.edge_off[d + 1]))
+        dags.append(([int(x) for x in b.load_num[n0:n1]],
+                     [(int(w) >> 16, int(w) & 0xFFFF) for w in b.edges[e0:e1]]))
+        names.append(f"c2_seed{1 + d}")
+    norm = []
+    for nodes, edges in dags:
+        if isinstance(nodes[0], tuple):
+            idx = {i: k for k, (i, _) in enumerate(sorted(nodes))}
+            norm.append(([l for _, l in sorted(nodes)], [(idx[u], idx[v]) for u, v in edges]))
+        else:
+            norm.append((nodes, edges))
+    schemes, st = scheme.schedule_batch(pack(norm), M, device=device)
+    ratio, over, launches = [], 0, 0
+    p50 = {"proposed": [], "serial": [], "multistream": []}
+    for (loads, edges), sch in zip(norm, schemes):
+        bus = X.bound_us(sch, cal)
+        for kind in p50:
+            plan = (X.plan_from_scheme(sch, loads, unit) if kind == "proposed"
+                    else X.plan_baseline(kind, loads, edges, M, unit))
+            ex = X.Executor(plan, device=device)
+            r = ex.run(replays, warmup=3, stamps=False)
+            ex.close()
+            p50[kind].append(float(np.median(r.makespan_us)))
+            if kind == "proposed":
+                ratio.extend((r.makespan_us / bus).tolist())
+                over += int((r.makespan_us > bus).sum())
+                launches += len(plan.entities) * replays
+    ratio = np.asarray(ratio)
+    return {"dags": names, "replays_per_dag": replays, "sm_count": M,
+            "tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
+            "measured_over_bound": {"p50": float(np.percentile(ratio, 50)), "p99": float(np.percentile(ratio, 99)),
+                                    "max": float(ratio.max())},
+            "replays_over_bound": over,
+            "mean_p50_us": {k: float(np.mean(v)) for k, v in p50.items()},
+            "executor_kernel_launches": launches}
+
+
 def run_reference(args):
     rank, _, world = env_rank()
     if rank != 0:
@@ -186,6 +240,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-makespan", action="store_true")
+    ap.add_argument("--makespan-replays", type=int, default=200)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -235,7 +291,9 @@ def main():
     st, bounds, ng = sess.results()
     ok = int((st == 0).sum())
     value = world * n * args.steps / (dev_ms / 1e3)
-    launches_per_step = 1 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
+    # per step: the n<=64 kernel, the n<=256 kernel when such DAGs exist, and the
+    # 128-bit retry kernel (exits at once when no DAG overflowed u64)
+    launches_per_step = 2 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
 
     # ---------------------------------------------------------------- e2e leg
     res_status = np.zeros(n, np.int32)
@@ -266,6 +324,13 @@ def main():
     traffic_per_dag, ncu = ncu_traffic()
     traffic = traffic_per_dag * n if traffic_per_dag else None
 
+    makespan = None
+    if rank == 0 and not args.no_makespan:
+        try:
+            makespan = makespan_summary(local_rank, args.makespan_replays)
+        except Exception as e:  # reported, never required for the headline line
+            makespan = {"error": str(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -289,6 +354,7 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "note": "integer-latency bound (serial greedy per DAG); HBM is not the limiter"},
             "cpu_baseline": cpu,
+            "makespan": makespan,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
             "e2e_gpu_launches": chunks * args.e2e_steps,

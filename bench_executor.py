@@ -38,7 +38,7 @@ from paper_2602_20826_b200 import _lib, scheme, workloads  # noqa: E402
 from paper_2602_20826_b200 import executor as X  # noqa: E402
 from paper_2602_20826_b200.batch import pack  # noqa: E402
 
-VARIANTS = ("proposed", "proposed_deps", "serial", "multistream")
+VARIANTS = ("proposed", "proposed_deps", "persistent", "persistent_deps", "serial", "multistream")
 
 
 def stats(a):
@@ -71,13 +71,14 @@ def run_dag(loads, edges, sch, M, sm_limit, cal, args):
            "launches": sum(len(g.launches) for g in sch.groups), "bound_units": str(bound_units),
            "greedy_units": str(sch.bounds["greedy"]), "bound_us": bound_us}
     for kind in VARIANTS:
-        if kind == "proposed":
+        engine = X.ENGINE_PERSISTENT if kind.startswith("persistent") else X.ENGINE_GRAPH
+        if kind in ("proposed", "persistent"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=True)
-        elif kind == "proposed_deps":
+        elif kind in ("proposed_deps", "persistent_deps"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=False)
         else:
             plan = X.plan_baseline(kind, loads, edges, M, args.unit)
-        ex = X.Executor(plan, workload=args.workload, sm_limit=sm_limit)
+        ex = X.Executor(plan, workload=args.workload, sm_limit=sm_limit, engine=engine)
         r = ex.run(args.replays, warmup=3, stamps=True)
         vp = vs = vg = 0
         checked = range(0, args.replays, args.check_every)
@@ -110,7 +111,7 @@ def summarise(results, prefix):
             "trace_violations": int(sum(r[kind]["precedence_violations"] + r[kind]["sm_overlap_violations"]
                                         for r in sel)),
         }
-    for kind in ("proposed", "proposed_deps"):
+    for kind in ("proposed", "proposed_deps", "persistent", "persistent_deps"):
         for q in ("p50", "p99", "max"):
             s[f"{kind}_beats_multistream_{q}"] = int(sum(r[kind]["makespan_us"][q] < r["multistream"]["makespan_us"][q]
                                                          for r in sel))

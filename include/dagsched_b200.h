@@ -195,7 +195,18 @@ typedef struct ds_exec_cfg {
     int32_t sm_limit;       /* 0: whole GPU; else run inside a green context of
                                this many SMs (multiple of 8 on sm_90+) — an
                                M-SM device for the paper's contended regime   */
+    int32_t engine;         /* DS_ENGINE_*                                       */
+    int32_t reserved;
 } ds_exec_cfg;
+
+/* Executor engines. GRAPH: one CUDA Graph kernel node per entity (any plan).
+ * PERSISTENT: one resident CTA per SM for the whole DAG; each CTA walks its
+ * list of (entity, slice) items in group order and waits on per-entity
+ * completion counters instead of kernel boundaries (no launch latency).
+ * Needs a group-structured plan (every entity's group >= 0, sum of
+ * parallelism per group <= SMs): the proposed schedule. */
+#define DS_ENGINE_GRAPH 0
+#define DS_ENGINE_PERSISTENT 1
 
 /* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
 typedef struct ds_exec_trace {

@@ -153,8 +153,8 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         if (int rc = sl.status.ensure(nd * 4)) return rc;
         if (int rc = sl.bounds.ensure(nd * 80)) return rc;
         if (int rc = sl.ngroups.ensure(nd * 2)) return rc;
-        if (int rc = sl.retry.ensure(nd * 4)) return rc;
-        if (int rc = sl.retry_count.ensure(4)) return rc;
+        if (int rc = sl.retry.ensure(2 * nd * 4)) return rc;  // two retry lists
+        if (int rc = sl.retry_count.ensure(8)) return rc;
         DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
@@ -176,6 +176,8 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         a.n_groups = out->n_groups ? sl.ngroups.as<uint16_t>() : nullptr;
         a.retry = sl.retry.as<u32>();
         a.retry_count = sl.retry_count.as<u32>();
+        a.retry2 = a.retry + nd;
+        a.retry2_count = a.retry_count + 1;
         DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, lo, hi), false, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, sl.s));
@@ -260,8 +262,8 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     if (int rc = configure(device, false, occ)) return rc;
     DeviceCtx& ctx = device_ctx(device);
     std::lock_guard<std::mutex> lock(ctx.mu);
-    if (int rc = ctx.retry.ensure(batch->n_dags * 4)) return rc;
-    if (int rc = ctx.retry_count.ensure(4)) return rc;
+    if (int rc = ctx.retry.ensure(2 * batch->n_dags * 4)) return rc;
+    if (int rc = ctx.retry_count.ensure(8)) return rc;
     K1Args a{};
     a.n_dags = batch->n_dags;
     a.node_off = batch->node_off;
@@ -276,6 +278,8 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     a.n_groups = out->n_groups;
     a.retry = ctx.retry.as<u32>();
     a.retry_count = ctx.retry_count.as<u32>();
+    a.retry2 = a.retry + batch->n_dags;
+    a.retry2_count = a.retry_count + 1;
     // device pointers: size classes are unknown on the host, so the n <= 256
     // kernel always runs (it skips DAGs with n <= 64 after two offset loads)
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -340,8 +344,8 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     if (int rc = B.ent.ensure(2 * N * sizeof(ds_entity_rec))) return rc;
     if (int rc = B.grp.ensure(N * sizeof(ds_group_rec))) return rc;
     if (int rc = B.bounds.ensure(n * 80)) return rc;
-    if (int rc = B.retry.ensure(n * 4)) return rc;
-    if (int rc = B.retry_count.ensure(4)) return rc;
+    if (int rc = B.retry.ensure(2 * n * 4)) return rc;
+    if (int rc = B.retry_count.ensure(8)) return rc;
     DS_CUDA(cudaMemset(B.nb.p, 0xff, N * 2));
     DS_CUDA(cudaMemset(B.ndg.p, 0xff, N * 2));
     DS_CUDA(cudaMemset(B.ent.p, 0, 2 * N * sizeof(ds_entity_rec)));
@@ -366,6 +370,8 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     a.det.bounds = B.bounds.as<int64_t>();
     a.retry = B.retry.as<u32>();
     a.retry_count = B.retry_count.as<u32>();
+    a.retry2 = a.retry + n;
+    a.retry2_count = a.retry_count + 1;
     DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, 0, n), true, s));
     DS_CUDA(cudaDeviceSynchronize());
     if (out->status) DS_CUDA(cudaMemcpy(out->status, B.status.p, n * 4, cudaMemcpyDeviceToHost));
@@ -406,8 +412,8 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     rc = rc ? rc : S->status.ensure(n * 4);
     rc = rc ? rc : S->bounds.ensure(n * 80);
     rc = rc ? rc : S->ngroups.ensure(n * 2);
-    rc = rc ? rc : S->retry.ensure(n * 4);
-    rc = rc ? rc : S->retry_count.ensure(4);
+    rc = rc ? rc : S->retry.ensure(2 * n * 4);
+    rc = rc ? rc : S->retry_count.ensure(8);
     if (rc) return bail(rc);
     K1Args& a = S->args;
     a.n_dags = n;
@@ -423,6 +429,8 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     a.n_groups = S->ngroups.as<uint16_t>();
     a.retry = S->retry.as<u32>();
     a.retry_count = S->retry_count.as<u32>();
+    a.retry2 = a.retry + n;
+    a.retry2_count = a.retry_count + 1;
     *session = S;
     return DS_OK;
 }

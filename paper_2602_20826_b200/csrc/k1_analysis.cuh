@@ -128,7 +128,8 @@ __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
 
 template <class T>
 __device__ __forceinline__ bool fits_i64(T v) {
-    return (v >> 63) == 0;
+    if constexpr (sizeof(T) <= 4) return true;
+    else return (v >> 63) == 0;
 }
 
 struct DetailOut {
@@ -155,8 +156,14 @@ __device__ __noinline__ int p_load(WarpState<W, T>& S, const int lane, const int
             b = -b;
         }
         RatT<T> l{0, 1};
-        if (a > 0 && b > 0) l = n_reduce<T>(T(u64(a)), T(u64(b)));
-        if (a <= 0 || n_cmp(l, P.tmin) < 0) bad_load = true;
+        const bool too_wide = sizeof(T) == 4 && a > 0 && b > 0 && ((u64(a) | u64(b)) >> 32) != 0;
+        if (too_wide) {
+            ovf = true;  // handled by a wider tier
+            l = P.tmin;
+        } else if (a > 0 && b > 0) {
+            l = n_reduce<T>(T(u64(a)), T(u64(b)));
+        }
+        if (a <= 0 || (!too_wide && n_cmp(l, P.tmin) < 0)) bad_load = true;
         frac |= l.d != 1;
         S.ln[v] = l.n;
         S.ld[v] = l.d;
@@ -282,6 +289,23 @@ __device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const 
     }
     if (__any_sync(FULL, ovf)) return -2;
     return done.popc() == n ? rounds : -1;
+}
+
+// Descendants for n <= 64 as the transpose of the ancestor matrix:
+// desc[v] = { u : v in anc[u] }. One broadcast shared-memory read per node and
+// two bit tests per lane replace the reverse Kahn rounds (dag.cpp:119-124).
+template <class T>
+__device__ __noinline__ void p_desc_transpose(WarpState<1, T>& S, const int lane, const int n) {
+    u64 lo = 0, hi = 0;  // desc of nodes lane and lane + 32
+#pragma unroll 4
+    for (int u = 0; u < n; ++u) {
+        const u64 a = S.anc[u][0];
+        lo |= ((a >> lane) & 1ull) << u;
+        hi |= ((a >> (lane + 32)) & 1ull) << u;
+    }
+    if (lane < n) S.desc[lane][0] = lo;
+    if (lane + 32 < n) S.desc[lane + 32][0] = hi;
+    __syncwarp();
 }
 
 // dag.cpp:97-108: exactly one source and one sink.
@@ -840,7 +864,8 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     if (rounds == -1) return DS_E_CYCLE;
     if (rounds == -2) return DS_EOVERFLOW;
     if ((st = p_ends<W, T>(S, lane, n)) != DS_OK) return st;
-    p_closure<W, T, false>(S, lane, n, false, P);
+    if constexpr (W == 1) p_desc_transpose<T>(S, lane, n);
+    else p_closure<W, T, false>(S, lane, n, false, P);
     if (mask & (DS_M_GREEDY | DS_M_GREEDY_UNAWARE | DS_M_GRAHAM_PARA | DS_M_LOWER)) {
         if ((st = p_bounds<W, T>(S, lane, n, rounds, P, mask)) != DS_OK) return st;
     }
@@ -867,13 +892,16 @@ struct K1Args {
     int64_t* bounds;
     uint16_t* n_groups;
     ds_scheme_out det;     // detail mode
-    u32* retry;            // DAG indices whose u64 pass overflowed
+    u32* retry;            // DAG indices whose 32-bit pass overflowed
     u32* retry_count;
+    u32* retry2;           // ... and whose 64-bit pass overflowed
+    u32* retry2_count;
 };
 
 template <int W, class T, bool DETAIL>
 __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, const K1Args& a, const u64 d,
-                                        const u32 nbase, const u32 ebase, const PlatT<T> P) {
+                                        const u32 nbase, const u32 ebase, const PlatT<T> P, u32* next,
+                                        u32* next_count) {
     const u32 n0 = a.node_off[d] - nbase, n1 = a.node_off[d + 1] - nbase;
     const u32 e0 = a.edge_off[d] - ebase, e1 = a.edge_off[d + 1] - ebase;
     const int n = int(n1 - n0);
@@ -887,9 +915,9 @@ __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, cons
     }
     int st = analyse_dag<W, T, DETAIL>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
                                        a.edges + e0, int(e1 - e0), P, a.mask, ng, det, nent, ndiv);
-    if (st == DS_EOVERFLOW && sizeof(T) == 8 && a.retry) {
-        // re-run in 128-bit words (k1_analyse_retry); nothing is written now
-        if (lane == 0) a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+    if (st == DS_EOVERFLOW && next) {
+        // re-run in wider words (k1_analyse_retry); nothing is written now
+        if (lane == 0) next[atomicAdd(next_count, 1u)] = u32(d);
         __syncwarp();
         return;
     }
@@ -919,36 +947,50 @@ __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, cons
 }
 
 // Main pass: every DAG of its size class (W=1: n <= 64; W=4: 64 < n <= 256),
-// persistent warps striding over the batch.
+// persistent warps striding over the batch, in 32-bit words. A DAG whose
+// 32-bit pass overflows is queued for the 64-bit retry, and from there for
+// the 128-bit one (k1_analyse_retry).
 template <int W, bool DETAIL>
 __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    WarpState<W, u64>& S = reinterpret_cast<WarpState<W, u64>*>(smem_raw)[wib];
+    WarpState<W, u32>& S = reinterpret_cast<WarpState<W, u32>*>(smem_raw)[wib];
     const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];  // offsets are relative to element 0
+    // a t_min that needs more than 32 bits sends every DAG to the wider tiers
+    const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
 #pragma unroll 1
     for (u64 d = u64(blockIdx.x) * (blockDim.x >> 5) + wib; d < a.n_dags; d += warps) {
         const int n = int(a.node_off[d + 1] - a.node_off[d]);
         if (W > 1 && n <= 64) continue;
         if (W == 1 && n > 64 && n <= DS_MAX_NODES) continue;
-        run_one<W, u64, DETAIL>(S, lane, a, d, nbase, ebase, a.plat);
+        if (!narrow) {
+            if (lane == 0) a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+            __syncwarp();
+            continue;
+        }
+        run_one<W, u32, DETAIL>(S, lane, a, d, nbase, ebase, P, a.retry, a.retry_count);
     }
 }
 
-// Retry pass: the DAGs listed by the main pass, in 128-bit words.
-template <bool DETAIL>
+// Retry passes over the DAGs queued by the narrower tier: T = u64 reads
+// retry/retry_count and queues its own overflows in retry2; T = u128 is final.
+template <bool DETAIL, class T>
 __global__ void __launch_bounds__(32) k1_analyse_retry(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
-    WarpState<4, u128>& S = *reinterpret_cast<WarpState<4, u128>*>(smem_raw);
-    const PlatT<u128> P{a.plat.M, RatT<u128>{a.plat.tmin.n, a.plat.tmin.d}};
+    WarpState<4, T>& S = *reinterpret_cast<WarpState<4, T>*>(smem_raw);
+    const PlatT<T> P{a.plat.M, RatT<T>{T(a.plat.tmin.n), T(a.plat.tmin.d)}};
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
-    const u32 count = *a.retry_count;
+    constexpr bool wide = sizeof(T) == 16;
+    const u32* list = wide ? a.retry2 : a.retry;
+    const u32 count = *(wide ? a.retry2_count : a.retry_count);
 #pragma unroll 1
     for (u32 i = blockIdx.x; i < count; i += gridDim.x) {
-        run_one<4, u128, DETAIL>(S, lane, a, a.retry[i], nbase, ebase, P);
+        run_one<4, T, DETAIL>(S, lane, a, list[i], nbase, ebase, P, wide ? nullptr : a.retry2,
+                              wide ? nullptr : a.retry2_count);
     }
 }
 

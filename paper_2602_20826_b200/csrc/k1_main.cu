@@ -1,27 +1,38 @@
-// K1 kernel instantiations: bounds mode (evaluate_corpus path).
+// K1 kernel instantiations and launchers. Compiled twice: bounds mode (this
+// file) and schedule-detail mode (k1_detail.cu defines K1_DETAIL_TU).
 #include "k1_launch.h"
 
 namespace ds {
+
+namespace {
+constexpr size_t kSmemSmall = sizeof(WarpState<1, u32>) * kWarpsSmall;
+constexpr size_t kSmemBig = sizeof(WarpState<4, u32>) * kWarpsBig;
+constexpr size_t kSmemR64 = sizeof(WarpState<4, u64>);
+constexpr size_t kSmemR128 = sizeof(WarpState<4, u128>);
+}  // namespace
 
 template <bool DETAIL>
 cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    const size_t s1 = sizeof(WarpState<1, u64>) * kWarpsSmall, s4 = sizeof(WarpState<4, u64>) * kWarpsBig;
-    const size_t sr = sizeof(WarpState<4, u128>);
-    if ((e = cudaFuncSetAttribute(k1_analyse<1, DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s1))))
+    if ((e = cudaFuncSetAttribute(k1_analyse<1, DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
         return e;
-    if ((e = cudaFuncSetAttribute(k1_analyse<4, DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s4))))
+    if ((e = cudaFuncSetAttribute(k1_analyse<4, DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBig))))
         return e;
-    if ((e = cudaFuncSetAttribute(k1_analyse_retry<DETAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sr))))
+    if ((e = cudaFuncSetAttribute(k1_analyse_retry<DETAIL, u64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemR64))))
+        return e;
+    if ((e = cudaFuncSetAttribute(k1_analyse_retry<DETAIL, u128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemR128))))
         return e;
     int o1 = 0, o4 = 0, orr = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k1_analyse<1, DETAIL>, 32 * kWarpsSmall, s1)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k1_analyse<1, DETAIL>, 32 * kWarpsSmall, kSmemSmall)))
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k1_analyse<4, DETAIL>, 32 * kWarpsBig, s4)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k1_analyse<4, DETAIL>, 32 * kWarpsBig, kSmemBig)))
         return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, k1_analyse_retry<DETAIL>, 32, sr))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, k1_analyse_retry<DETAIL, u128>, 32, kSmemR128)))
+        return e;
     if (o1 < 1 || o4 < 1 || orr < 1) return cudaErrorInvalidConfiguration;
     occ.grid_small = sms * o1;  // one full wave; warps stride over the DAGs
     occ.grid_big = sms * o4;
@@ -33,26 +44,27 @@ template <bool DETAIL>
 cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
     if (a.n_dags == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(a.retry_count, 0, sizeof(u32), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.retry2_count, 0, sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     const int gs = int(need_small < u64(occ.grid_small) ? need_small : u64(occ.grid_small));
-    k1_analyse<1, DETAIL><<<gs, 32 * kWarpsSmall, sizeof(WarpState<1, u64>) * kWarpsSmall, s>>>(a);
+    k1_analyse<1, DETAIL><<<gs, 32 * kWarpsSmall, kSmemSmall, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (any_big) {
         const int gb = int(a.n_dags < u64(occ.grid_big) ? a.n_dags : u64(occ.grid_big));
-        k1_analyse<4, DETAIL><<<gb, 32 * kWarpsBig, sizeof(WarpState<4, u64>) * kWarpsBig, s>>>(a);
+        k1_analyse<4, DETAIL><<<gb, 32 * kWarpsBig, kSmemBig, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    // 128-bit retry of the DAGs that overflowed u64 (usually none: the kernel
-    // reads the count and exits)
+    // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
+    // nothing queued each kernel reads the count and exits
     const int gr = int(a.n_dags < u64(occ.grid_retry) ? a.n_dags : u64(occ.grid_retry));
-    k1_analyse_retry<DETAIL><<<gr, 32, sizeof(WarpState<4, u128>), s>>>(a);
+    k1_analyse_retry<DETAIL, u64><<<gr, 32, kSmemR64, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k1_analyse_retry<DETAIL, u128><<<gr, 32, kSmemR128, s>>>(a);
     return cudaGetLastError();
 }
 
 #ifndef K1_DETAIL_TU
-cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ);
-cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s);
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ);
 cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s);
 

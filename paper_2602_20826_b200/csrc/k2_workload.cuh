@@ -285,4 +285,108 @@ __global__ void k2_init(uint32_t* x, unsigned long long n, uint32_t seed, int fp
 
 __global__ void k2_tick(int* replay) { *replay += 1; }
 
+// ------------------------------------------------ persistent engine (K3)
+// One CTA per SM for the whole DAG. CTA b walks items[item_off[b] ..
+// item_off[b+1]) — (entity, rank) pairs in group order — waits until every
+// predecessor entity has all of its CTAs done for this epoch (counters only
+// grow: entity p is complete in epoch k when done[p] >= m_p * (k+1)), runs its
+// slice of the entity's element range with the k2_mix body, then publishes
+// completion (fence + atomicAdd). Deadlock-free: predecessors always sit in
+// strictly earlier groups, and every CTA walks its items in group order.
+struct PEnt {
+    const uint32_t* x;
+    uint32_t* y;
+    unsigned long long lo, hi;
+    uint32_t m, slot, pred_off, n_preds;
+};
+struct PItem {
+    uint32_t ent, rank;
+};
+struct PArgs {
+    const PEnt* ents;
+    const uint32_t* preds;
+    const uint32_t* item_off;
+    const PItem* items;
+    unsigned int* done;
+    unsigned int epoch;
+    int rec;  // recorded replay slot, < 0: not recorded
+    unsigned long long* stamps;
+    uint32_t* smids;
+    unsigned long long* span;
+    uint32_t total;
+};
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(1024, 1) k3_persistent(const PArgs a) {
+    __shared__ unsigned long long t0s;
+    const uint32_t b = blockIdx.x;
+#pragma unroll 1
+    for (uint32_t it = a.item_off[b]; it < a.item_off[b + 1]; ++it) {
+        const PItem w = a.items[it];
+        const PEnt e = a.ents[w.ent];
+        if (threadIdx.x == 0) {
+            for (uint32_t k = 0; k < e.n_preds; ++k) {
+                const uint32_t p = a.preds[e.pred_off + k];
+                const unsigned int need = a.ents[p].m * (a.epoch + 1);
+                while (ld_acquire(a.done + p) < need) __nanosleep(32);
+            }
+            t0s = gtimer();
+        }
+        __syncthreads();
+        const unsigned long long len = e.hi - e.lo;
+        const unsigned long long s0 = e.lo + len * w.rank / e.m, s1 = e.lo + len * (w.rank + 1) / e.m;
+        const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
+        if (v0 >= v1) {
+            for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
+        } else {
+            for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
+            for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
+            const uint4* x4 = reinterpret_cast<const uint4*>(e.x);
+            uint4* y4 = reinterpret_cast<uint4*>(e.y);
+            const unsigned long long step = blockDim.x;
+            unsigned long long i = v0 + threadIdx.x;
+            for (; i + 3 * step < v1; i += 4 * step) {
+                uint4 r0 = __ldcs(x4 + i), r1 = __ldcs(x4 + i + step), r2 = __ldcs(x4 + i + 2 * step),
+                      r3 = __ldcs(x4 + i + 3 * step);
+#define DS_MIX4(r) r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w)
+                DS_MIX4(r0);
+                DS_MIX4(r1);
+                DS_MIX4(r2);
+                DS_MIX4(r3);
+                __stcs(y4 + i, r0);
+                __stcs(y4 + i + step, r1);
+                __stcs(y4 + i + 2 * step, r2);
+                __stcs(y4 + i + 3 * step, r3);
+            }
+            for (; i < v1; i += step) {
+                uint4 r = __ldcs(x4 + i);
+                DS_MIX4(r);
+                __stcs(y4 + i, r);
+            }
+#undef DS_MIX4
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long t1 = gtimer();
+            if (a.rec >= 0) {
+                const unsigned long long idx = (unsigned long long)a.rec * a.total + e.slot + w.rank;
+                if (a.stamps) {
+                    a.stamps[2 * idx] = t0s;
+                    a.stamps[2 * idx + 1] = t1;
+                }
+                if (a.smids) a.smids[idx] = smid();
+                atomicMin(&a.span[2 * a.rec], t0s);
+                atomicMax(&a.span[2 * a.rec + 1], t1);
+            }
+            __threadfence();
+            atomicAdd(a.done + w.ent, 1u);
+        }
+    }
+}
+
 }  // namespace ds

@@ -60,7 +60,85 @@ struct Exec {
     uint32_t* smids = nullptr;
     int cap = 0;
     std::vector<NodeArgs> args;  // kernel-node parameters (stable storage)
+    // persistent engine
+    int engine = DS_ENGINE_GRAPH;
+    PEnt* d_ents = nullptr;
+    uint32_t* d_preds = nullptr;
+    uint32_t* d_item_off = nullptr;
+    PItem* d_items = nullptr;
+    unsigned int* d_done = nullptr;
+    unsigned int epoch = 0;
+    uint32_t grid = 0;
 };
+
+// Persistent engine tables: per group, entities take consecutive CTA slots
+// (the scheduler guarantees sum of parallelism <= M per group); each CTA's
+// work list is its slots' (entity, rank) items in group order.
+int build_persistent(Exec* E, const ds_exec_plan* plan) {
+    const int n = plan->n_entities;
+    std::vector<uint32_t> cta0(n);
+    int max_group = -1;
+    for (int i = 0; i < n; ++i) {
+        if (plan->entities[i].group < 0) return fail(DS_EINVAL, "persistent engine needs a group-structured plan");
+        if (i && plan->entities[i].group < plan->entities[i - 1].group)
+            return fail(DS_EINVAL, "persistent engine needs entities in group order");
+        max_group = std::max(max_group, int(plan->entities[i].group));
+    }
+    std::vector<std::vector<int>> members(max_group + 1);
+    uint32_t grid = 0;
+    for (int i = 0; i < n; ++i) members[plan->entities[i].group].push_back(i);
+    for (auto& g : members) {
+        uint32_t cur = 0;
+        for (int i : g) {
+            cta0[i] = cur;
+            cur += uint32_t(plan->entities[i].parallelism);
+        }
+        if (cur > uint32_t(E->sm_count)) return fail(DS_EINVAL, "group holds more SMs than the device has");
+        grid = std::max(grid, cur);
+    }
+    std::vector<std::vector<PItem>> per(grid);
+    for (int i = 0; i < n; ++i)  // plan order = group order
+        for (int r = 0; r < plan->entities[i].parallelism; ++r) per[cta0[i] + r].push_back(PItem{uint32_t(i), uint32_t(r)});
+    std::vector<uint32_t> item_off{0};
+    std::vector<PItem> items;
+    for (auto& v : per) {
+        items.insert(items.end(), v.begin(), v.end());
+        item_off.push_back(uint32_t(items.size()));
+    }
+    std::vector<PEnt> ents(n);
+    std::vector<uint32_t> preds;
+    uint32_t slot = 0;
+    for (int i = 0; i < n; ++i) {
+        const ds_exec_entity& e = plan->entities[i];
+        PEnt& p = ents[i];
+        p.x = E->x[e.node];
+        p.y = E->y[e.node];
+        p.lo = e.elem_lo;
+        p.hi = e.elem_hi;
+        p.m = uint32_t(e.parallelism);
+        p.slot = slot;
+        slot += p.m;
+        p.pred_off = uint32_t(preds.size());
+        for (uint32_t k = 0; k < e.n_preds; ++k) preds.push_back(plan->preds[e.pred_off + k]);
+        if (plan->barrier_groups && e.group > 0)  // simulate_scheme's group windows
+            for (int j : members[e.group - 1]) preds.push_back(uint32_t(j));
+        p.n_preds = uint32_t(preds.size()) - p.pred_off;
+    }
+    DS_CUDA(cudaMalloc(&E->d_ents, ents.size() * sizeof(PEnt)));
+    DS_CUDA(cudaMalloc(&E->d_preds, std::max<size_t>(preds.size(), 1) * 4));
+    DS_CUDA(cudaMalloc(&E->d_item_off, item_off.size() * 4));
+    DS_CUDA(cudaMalloc(&E->d_items, std::max<size_t>(items.size(), 1) * sizeof(PItem)));
+    DS_CUDA(cudaMalloc(&E->d_done, size_t(n) * 4));
+    DS_CUDA(cudaMemcpy(E->d_ents, ents.data(), ents.size() * sizeof(PEnt), cudaMemcpyHostToDevice));
+    if (!preds.empty()) DS_CUDA(cudaMemcpy(E->d_preds, preds.data(), preds.size() * 4, cudaMemcpyHostToDevice));
+    DS_CUDA(cudaMemcpy(E->d_item_off, item_off.data(), item_off.size() * 4, cudaMemcpyHostToDevice));
+    DS_CUDA(cudaMemcpy(E->d_items, items.data(), items.size() * sizeof(PItem), cudaMemcpyHostToDevice));
+    DS_CUDA(cudaMemset(E->d_done, 0, size_t(n) * 4));
+    DS_CUDA(cudaFuncSetAttribute(k3_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem));
+    E->grid = grid;
+    E->epoch = 0;
+    return DS_OK;
+}
 
 void* kernel_of(int wl) {
     switch (wl) {
@@ -161,6 +239,11 @@ void destroy(Exec* E) {
     if (E->span) cudaFree(E->span);
     if (E->stamps) cudaFree(E->stamps);
     if (E->smids) cudaFree(E->smids);
+    if (E->d_ents) cudaFree(E->d_ents);
+    if (E->d_preds) cudaFree(E->d_preds);
+    if (E->d_item_off) cudaFree(E->d_item_off);
+    if (E->d_items) cudaFree(E->d_items);
+    if (E->d_done) cudaFree(E->d_done);
     if (E->s) cudaStreamDestroy(E->s);
     }
     if (E->gctx) driver().greenDestroy(E->gctx);
@@ -341,6 +424,13 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     }
     if (cudaMalloc(&E->replay, sizeof(int)) != cudaSuccess) return bail(fail(DS_ENOMEM, "replay"));
     if (cudaStreamSynchronize(E->s) != cudaSuccess) return bail(fail(DS_ECUDA, "init"));
+    E->engine = cfg->engine;
+    if (E->engine == DS_ENGINE_PERSISTENT) {
+        if (E->workload != DS_WL_MIX32) return bail(fail(DS_EINVAL, "persistent engine runs the mix32 workload"));
+        if (int rc = build_persistent(E, &H->P.plan)) return bail(rc);
+    } else if (E->engine != DS_ENGINE_GRAPH) {
+        return bail(fail(DS_EINVAL, "unknown engine"));
+    }
     *exec = H;
     return DS_OK;
 }
@@ -361,7 +451,8 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     if (replays < 1 || warmup < 0 || !trace || !trace->span) return fail(DS_EINVAL, "bad run arguments");
     CtxGuard guard(E);
     const bool want_stamps = trace->stamps || trace->smids;
-    if (replays > E->cap || !E->exec || (want_stamps && !E->stamps)) {
+    const bool persistent = E->engine == DS_ENGINE_PERSISTENT;
+    if (replays > E->cap || (!persistent && !E->exec) || (want_stamps && !E->stamps)) {
         if (E->span) cudaFree(E->span);
         if (E->stamps) cudaFree(E->stamps);
         if (E->smids) cudaFree(E->smids);
@@ -374,7 +465,9 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
             DS_CUDA(cudaMalloc(&E->stamps, size_t(E->cap) * E->total_ctas * 16));
             DS_CUDA(cudaMalloc(&E->smids, size_t(E->cap) * E->total_ctas * 4));
         }
-        if (int rc = build_graph(E, &H->P.plan)) return rc;
+        if (!persistent) {
+            if (int rc = build_graph(E, &H->P.plan)) return rc;
+        }
     }
     // span[r] = {~0, 0}
     std::vector<unsigned long long> init(size_t(E->cap) * 2);
@@ -390,7 +483,17 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     for (auto& e : ev) DS_CUDA(cudaEventCreate(&e));
     for (int r = -warmup; r < replays; ++r) {
         if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
-        DS_CUDA(cudaGraphLaunch(E->exec, E->s));
+        if (persistent) {
+            PArgs pa{E->d_ents, E->d_preds, E->d_item_off, E->d_items, E->d_done, E->epoch++, r,
+                     E->stamps, E->smids, E->span, E->total_ctas};
+            void* kargs[] = {&pa};
+            // cooperative: all CTAs (one per SM) must be resident together,
+            // they wait on each other's completion counters
+            DS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k3_persistent), dim3(E->grid),
+                                                dim3(unsigned(E->threads)), kargs, size_t(kNodeSmem), E->s));
+        } else {
+            DS_CUDA(cudaGraphLaunch(E->exec, E->s));
+        }
         if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r + 1], E->s));
     }
     DS_CUDA(cudaStreamSynchronize(E->s));

@@ -47,6 +47,20 @@ __device__ __forceinline__ u32 gcd32(u32 a, u32 b) {
     return a << s;
 }
 
+// 32-bit words: the tier every DAG takes first (all C5 values fit).
+__device__ __forceinline__ u32 gcdw(u32 a, u32 b) { return gcd32(a, b); }
+__device__ __forceinline__ u32 divw(u32 a, u32 b) { return a / b; }
+__device__ __forceinline__ u32 mulc(u32 a, u32 b, bool& ovf) {
+    const u64 p = u64(a) * b;
+    if (p >> 32) ovf = true;
+    return u32(p);
+}
+__device__ __forceinline__ int cmp_prod(u32 a, u32 b, u32 c, u32 d) {
+    const u64 l = u64(a) * b, r = u64(c) * d;
+    return l < r ? -1 : (l > r ? 1 : 0);
+}
+__device__ __forceinline__ u32 shfl_xor_w(u32 v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
 __device__ __forceinline__ u64 gcdw(u64 a, u64 b) {
     if (((a | b) >> 32) == 0) return gcd32(u32(a), u32(b));
     if (a == 0) return b;

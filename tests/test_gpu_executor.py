@@ -128,3 +128,23 @@ def test_green_context_partition():
     ex.close()
     cal = X.calibrate(4096, sm_limit=16, replays=20, groups=4)
     assert cal["sm_count"] == 16 and cal["tau_us"] > 0
+
+
+@pytest.mark.parametrize("barrier", [True, False])
+def test_persistent_engine(barrier):
+    """DS_ENGINE_PERSISTENT: one resident CTA per SM walking (entity, slice)
+    items with completion counters — outputs bit-exact, contracts hold."""
+    for dag, M in ((workloads.make_example_task(), 8), (workloads.oversized_dag(2, 148), 148),
+                   (workloads.inception_dag(), 148)):
+        s, loads, edges = _scheme_and_loads(dag, M)
+        plan = X.plan_from_scheme(s, loads, UNIT + 5, barrier_groups=barrier)
+        ex = X.Executor(plan, engine=X.ENGINE_PERSISTENT, sm_limit=0 if M == 148 else 8)
+        res = ex.run(8, warmup=2)
+        for r in range(8):
+            assert X.check_precedence(plan, res, r) == []
+            assert X.check_sm_exclusive(plan, res, r) == 0
+            if barrier:
+                assert X.group_overlap_violations(plan, res, r) == 0
+        for v in range(len(loads)):
+            assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+        ex.close()
