@@ -296,9 +296,10 @@ def main():
     launches_per_step = 2 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
 
     # ---------------------------------------------------------------- e2e leg
-    res_status = np.zeros(n, np.int32)
-    res_bounds = np.zeros((n, 10), np.int64)
-    res_groups = np.zeros(n, np.uint16)
+    # pinned result buffers (the inputs are pinned too: Corpus(pinned=True))
+    res_status = torch.zeros(n, dtype=torch.int32, pin_memory=True).numpy()
+    res_bounds = torch.zeros((n, 10), dtype=torch.int64, pin_memory=True).numpy()
+    res_groups = torch.zeros(n, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)
     import ctypes as C
     r = _abi.ds_results(res_status.ctypes.data, res_bounds.ctypes.data, res_groups.ctypes.data)
     cb = batch.as_c()

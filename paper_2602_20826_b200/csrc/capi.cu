@@ -135,8 +135,11 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         ctx.init = true;
     }
     const u64 n = b->n_dags;
-    for (u64 lo = 0, c = 0; lo < n; lo += kChunk, ++c) {
-        const u64 hi = std::min(n, lo + kChunk), nd = hi - lo;
+    // ~4 chunks: enough to hide the copies behind the analysis, few enough
+    // that the per-launch tail (uneven per-DAG cost) is paid rarely
+    const u64 chunk = std::max<u64>(kChunk, (n + 3) / 4);
+    for (u64 lo = 0, c = 0; lo < n; lo += chunk, ++c) {
+        const u64 hi = std::min(n, lo + chunk), nd = hi - lo;
         Slot& sl = ctx.slot[c % 3];
         // indices are relative to node_off[0] / edge_off[0] (header contract)
         const u64 n0 = b->node_off[lo] - b->node_off[0], n1 = b->node_off[hi] - b->node_off[0];

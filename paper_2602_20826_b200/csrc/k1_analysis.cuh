@@ -961,8 +961,19 @@ __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
     // a t_min that needs more than 32 bits sends every DAG to the wider tiers
     const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
     const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    // W=1 takes DAGs dynamically (one atomic per DAG) so the per-DAG cost
+    // spread does not leave a tail of idle SMs; W=4 only picks out the rare
+    // big DAGs, statically.
+    u32* const next = a.retry_count + 2;
+    u64 d = W == 1 ? 0 : u64(blockIdx.x) * (blockDim.x >> 5) + wib;
 #pragma unroll 1
-    for (u64 d = u64(blockIdx.x) * (blockDim.x >> 5) + wib; d < a.n_dags; d += warps) {
+    for (;; d += warps) {
+        if (W == 1) {
+            u32 t = 0;
+            if (lane == 0) t = atomicAdd(next, 1u);
+            d = __shfl_sync(FULL, t, 0);
+        }
+        if (d >= a.n_dags) break;
         const int n = int(a.node_off[d + 1] - a.node_off[d]);
         if (W > 1 && n <= 64) continue;
         if (W == 1 && n > 64 && n <= DS_MAX_NODES) continue;

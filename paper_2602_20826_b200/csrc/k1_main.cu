@@ -43,8 +43,8 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
 template <bool DETAIL>
 cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
     if (a.n_dags == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(a.retry_count, 0, sizeof(u32), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.retry2_count, 0, sizeof(u32), s);
+    // counters, contiguous: [retry, retry2, next DAG for the W=1 kernel, spare]
+    cudaError_t e = cudaMemsetAsync(a.retry_count, 0, 4 * sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     const int gs = int(need_small < u64(occ.grid_small) ? need_small : u64(occ.grid_small));

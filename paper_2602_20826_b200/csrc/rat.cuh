@@ -288,7 +288,8 @@ __device__ __forceinline__ int max_par(RatT<T> load, const PlatT<T>& p, bool& ov
 // comparisons only.
 template <class T>
 __device__ __forceinline__ RatT<T> exec_raw(RatT<T> load, long long m, const PlatT<T>& p, bool& ovf) {
-    const T passes = T((m + p.M - 1) / p.M);
+    // ceil(m / M); m <= M (one pass) is the common case and skips the 64-bit divide
+    const T passes = m <= p.M ? T(1) : T((m + p.M - 1) / p.M);
     RatT<T> c{passes == 1 ? load.n : mulc(load.n, passes, ovf), mulc(load.d, T(m), ovf)};
     return rat_cmp(c, p.tmin) < 0 ? p.tmin : c;
 }
@@ -298,7 +299,8 @@ __device__ __forceinline__ RatT<T> exec_raw(RatT<T> load, long long m, const Pla
 // is the common case at M = 148, and then no gcd/division is needed at all.
 template <class T>
 __device__ __forceinline__ RatT<T> exec_time(RatT<T> load, long long m, const PlatT<T>& p, bool& ovf) {
-    const T passes = T((m + p.M - 1) / p.M);
+    // ceil(m / M); m <= M (one pass) is the common case and skips the 64-bit divide
+    const T passes = m <= p.M ? T(1) : T((m + p.M - 1) / p.M);
     bool o = false;
     const RatT<T> raw{passes == 1 ? load.n : mulc(load.n, passes, o), mulc(load.d, T(m), o)};
     if (!o && rat_cmp(raw, p.tmin) <= 0) return p.tmin;

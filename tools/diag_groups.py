@@ -6,6 +6,7 @@ from paper_2602_20826_b200 import _lib, scheme, executor as X
 from paper_2602_20826_b200.batch import pack
 
 sm_limit = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+engine = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 avg = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 cal = X.calibrate(1 << 17, sm_limit=sm_limit)
 M = cal["sm_count"]
@@ -20,7 +21,7 @@ e0, e1 = int(b.edge_off[d]), int(b.edge_off[d + 1])
 edges = [(int(w) >> 16, int(w) & 0xFFFF) for w in b.edges[e0:e1]]
 sch = scheme.schedule_batch(pack([(loads, edges)]), M)[0][0]
 plan = X.plan_from_scheme(sch, loads, 1 << 17)
-ex = X.Executor(plan, sm_limit=sm_limit)
+ex = X.Executor(plan, sm_limit=sm_limit, engine=engine)
 res = ex.run(20, warmup=3)
 r = 5
 win = X.entity_windows(plan, res, r)
