@@ -291,9 +291,10 @@ def main():
     st, bounds, ng = sess.results()
     ok = int((st == 0).sum())
     value = world * n * args.steps / (dev_ms / 1e3)
-    # per step: the n<=64 kernel, the n<=256 kernel when such DAGs exist, and the
-    # 128-bit retry kernel (exits at once when no DAG overflowed u64)
-    launches_per_step = 2 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
+    # per step: the n<=64 kernel, the n<=256 kernel when such DAGs exist, and
+    # the 64- and 128-bit retry kernels (each exits at once when nothing was
+    # queued) — the launch list in profiles/r01_launches.csv shows the same
+    launches_per_step = 3 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
 
     # ---------------------------------------------------------------- e2e leg
     # pinned result buffers (the inputs are pinned too: Corpus(pinned=True))
