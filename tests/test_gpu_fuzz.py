@@ -1,0 +1,70 @@
+"""GPU fuzz parity: random general DAGs (shuffled ids, n up to 200, fractional
+loads, oversized kernels, small M so Rule 1 truncates and nodes are split and
+re-split) through K1 vs the restated oracle and, where built, the reference
+itself (oracle/_ref); schedules vs the reference's write_scheme JSON."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import bindings
+from paper_2602_20826_b200 import _lib, scheme
+from paper_2602_20826_b200.batch import pack
+from tests import fuzz_dags, helpers
+
+pytestmark = pytest.mark.gpu
+
+
+def _checkers():
+    out = [bindings.Checker("oracle")]
+    if bindings.available("ref"):
+        out.append(bindings.Checker("ref"))
+    return out
+
+
+@pytest.mark.parametrize("seed,tmin,max_n", [(1, 1, 96), (2, Fraction(1, 2), 96), (3, 1, 200),
+                                             (4, Fraction(3, 2), 60)])
+def test_fuzz_bounds(seed, tmin, max_n):
+    dags = fuzz_dags.corpus(seed, 600, max_n=max_n, tmin=Fraction(tmin))
+    b = pack(dags)
+    for M in (1, 2, 3, 5, 8, 16, 37, 148, 1000):
+        st, bounds, _ = _lib.analyze(b, M, tmin)
+        for chk in _checkers():
+            c = chk.corpus(helpers_raw(b), min_load=tmin)
+            st_o, b_o, _ = c.evaluate(M, tmin)
+            assert np.array_equal(st, st_o), (chk.kind, M, np.nonzero(st != st_o)[0][:5])
+            bad = np.nonzero((bounds != b_o).any(1))[0]
+            assert len(bad) == 0, (chk.kind, M, bad[:5])
+
+
+def test_fuzz_invalid_statuses():
+    dags = fuzz_dags.broken(7, 200)
+    b = pack(dags)
+    st, bounds, _ = _lib.analyze(b, 8)
+    ref =bindings.Checker("ref" if bindings.available("ref") else "oracle")
+    for i, (nodes, edges) in enumerate(dags):
+        one = helpers.fixture_raw_batch({"nodes": [[v, str(Fraction(l))] for v, l in nodes], "edges": edges})
+        c = ref.corpus(one)
+        s_ref, _, _ = c.evaluate(8)
+        assert int(st[i]) == int(s_ref[0]), (i, int(st[i]), int(s_ref[0]))
+    assert (st != 0).sum() >= 150
+
+
+@pytest.mark.skipif(not bindings.available("ref"), reason="needs oracle/_ref")
+@pytest.mark.parametrize("M", [3, 8, 148])
+def test_fuzz_schemes_vs_reference(M):
+    dags = fuzz_dags.corpus(11, 150, max_n=80)
+    b = pack(dags)
+    schemes, st = scheme.schedule_batch(b, M)
+    ref = bindings.Checker("ref").corpus(helpers_raw(b))
+    for d in range(len(dags)):
+        if st[d] != 0:
+            continue
+        got = scheme.to_reference_json(schemes[d])
+        assert helpers.normalise_scheme(got) == helpers.normalise_scheme(ref.scheme(d, M)), d
+
+
+def helpers_raw(b):
+    """The packed batch as the checkers take it (same arrays, id-free)."""
+    from paper_2602_20826_b200.batch import from_arrays
+    return from_arrays(b.node_off, b.edge_off, b.load_num, b.load_den, b.edges)

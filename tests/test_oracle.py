@@ -102,3 +102,23 @@ def test_reference_unit_tests(binary):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed: 0" in r.stdout
+
+
+@pytest.mark.skipif(not bindings.available("ref"), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("seed,tmin", [(1, 1), (2, "1/2"), (3, "3/2")])
+def test_restatement_vs_reference_on_random_general_dags(orc, seed, tmin):
+    """Fuzz: non-layered DAGs, shuffled ids, fractional and oversized loads."""
+    from fractions import Fraction
+    from paper_2602_20826_b200.batch import from_arrays, pack
+    from tests import fuzz_dags
+    b = pack(fuzz_dags.corpus(seed, 300, max_n=120, tmin=Fraction(tmin)))
+    raw = from_arrays(b.node_off, b.edge_off, b.load_num, b.load_den, b.edges)
+    ref = bindings.Checker("ref")
+    a, o = ref.corpus(raw, min_load=Fraction(tmin)), orc.corpus(raw, min_load=Fraction(tmin))
+    for M in (1, 3, 8, 37, 148):
+        sa, ba, _ = a.evaluate(M, tmin)
+        so, bo, _ = o.evaluate(M, tmin)
+        assert np.array_equal(sa, so) and np.array_equal(ba, bo), M
+        for d in range(0, 300, 15):
+            if sa[d] == 0:
+                assert a.scheme(d, M, tmin) == o.scheme(d, M, tmin), (M, d)
