@@ -39,6 +39,7 @@
 namespace ds {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kFlatPath = 1 << 16;  // p_closure flag: every lower-bound weight is t_min
 
 template <int W, class T>
 struct WarpState {
@@ -227,19 +228,23 @@ __device__ __noinline__ int p_edges(WarpState<W, T>& S, const int lane, const in
 // lower_bound (analysis.cpp:11-24, 72-81). Returns rounds, or -1 on a cycle,
 // or -2 on overflow.
 template <int W, class T, bool FWD>
-__device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const int n, const bool lower,
+__device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const int n, bool lower,
                                       const PlatT<T> P) {
     bool ovf = false;
+    bool flat = FWD && lower;  // every weight is t_min: the path is (hop length) x t_min
     if (FWD && lower) {
 #pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             const RatT<T> w = n_exec(RatT<T>{S.ln[v], S.ld[v]}, min(S.mmax[v], P.M), P);
             ovf |= w.d == 0;
+            flat &= w.n == P.tmin.n && w.d == P.tmin.d;
             S.cn[v] = w.n;  // weight; replaced by the path prefix below
             S.cd[v] = w.d;
         }
         __syncwarp();
     }
+    flat = __all_sync(FULL, flat);
+    lower = lower && !flat;  // the weighted prefix is only needed when weights differ
     Mask<W> done;
     done.clear();
     int rounds = 0;
@@ -288,7 +293,7 @@ __device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const 
         __syncwarp();
     }
     if (__any_sync(FULL, ovf)) return -2;
-    return done.popc() == n ? rounds : -1;
+    return done.popc() == n ? (rounds | (flat ? kFlatPath : 0)) : -1;
 }
 
 // Descendants for n <= 64 as the transpose of the ancestor matrix:
@@ -333,16 +338,27 @@ __device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int
 // ------------------------------------------------------------- phase: bounds
 // analysis.cpp:40-81 — greedy, greedy_unaware, graham_para, lower_bound.
 template <int W, class T>
-__device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const int n, const int rounds,
+__device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const int n, const int closure,
                                      const PlatT<T> P, const u32 mask) {
+    const int rounds = closure & (kFlatPath - 1);
+    const bool flat = closure & kFlatPath;
     RatT<T> g{0, 1}, gu{0, 1}, tot{0, 1}, cp{0, 1};
     T units = 0;
     bool ovf = false;
+    // integer operands add inline; only a fractional operand takes the call
+    auto acc = [&](RatT<T>& s, const RatT<T> x) {
+        if (s.d == 1 && x.d == 1) s.n = addc(s.n, x.n, ovf);
+        else s = n_add(s, x);
+    };
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         const RatT<T> l{S.ln[v], S.ld[v]};
-        if (mask & DS_M_GREEDY) g = n_add(g, n_exec(l, min(S.mmax[v], P.M), P));
-        if (mask & DS_M_GREEDY_UNAWARE) gu = n_add(gu, n_exec(l, S.mmax[v], P));
+        // greedy's per-node time exec(l, min(m^max, M)) is the lower-bound
+        // weight: when every one is t_min (flat) greedy is n * t_min
+        if ((mask & DS_M_GREEDY) && !flat) acc(g, n_exec(l, min(S.mmax[v], P.M), P));
+        if (mask & DS_M_GREEDY_UNAWARE) {
+            acc(gu, S.mmax[v] <= P.M && flat ? P.tmin : n_exec(l, S.mmax[v], P));
+        }
         if (mask & DS_M_GRAHAM_PARA) {  // ceil(load / t_min) unit nodes
             T u;
             if (P.tmin.n == 1 && P.tmin.d == 1 && l.d == 1) {
@@ -355,21 +371,26 @@ __device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const i
             units = addc(units, u, ovf);
         }
         if (mask & DS_M_LOWER) {
-            tot = n_add(tot, l);
-            const RatT<T> c{S.cn[v], S.cd[v]};
-            if (n_cmp(c, cp) > 0) cp = c;
+            acc(tot, l);
+            if (!flat) {
+                const RatT<T> c{S.cn[v], S.cd[v]};
+                if (n_cmp(c, cp) > 0) cp = c;
+            }
         }
     }
     ovf |= g.d == 0 || gu.d == 0 || tot.d == 0;
 #pragma unroll 1
     for (int o = 16; o; o >>= 1) {
-        g = n_add(g, RatT<T>{shfl_xor_w(g.n, o), shfl_xor_w(g.d, o)});
-        gu = n_add(gu, RatT<T>{shfl_xor_w(gu.n, o), shfl_xor_w(gu.d, o)});
-        tot = n_add(tot, RatT<T>{shfl_xor_w(tot.n, o), shfl_xor_w(tot.d, o)});
+        if ((mask & DS_M_GREEDY) && !flat) acc(g, RatT<T>{shfl_xor_w(g.n, o), shfl_xor_w(g.d, o)});
+        if (mask & DS_M_GREEDY_UNAWARE) acc(gu, RatT<T>{shfl_xor_w(gu.n, o), shfl_xor_w(gu.d, o)});
+        if (mask & DS_M_LOWER) acc(tot, RatT<T>{shfl_xor_w(tot.n, o), shfl_xor_w(tot.d, o)});
         units = addc(units, shfl_xor_w(units, o), ovf);
-        const RatT<T> c{shfl_xor_w(cp.n, o), shfl_xor_w(cp.d, o)};
-        if (n_cmp(c, cp) > 0) cp = c;
+        if (!flat) {
+            const RatT<T> c{shfl_xor_w(cp.n, o), shfl_xor_w(cp.d, o)};
+            if (n_cmp(c, cp) > 0) cp = c;
+        }
     }
+    if ((mask & DS_M_GREEDY) && flat) g = n_mul_int(P.tmin, T(n));
     ovf |= g.d == 0 || gu.d == 0 || tot.d == 0;
     if (lane == 0) {
         if (mask & DS_M_GREEDY) {
@@ -392,6 +413,10 @@ __device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const i
         if (mask & DS_M_LOWER) {
             const RatT<T> wf = n_div_int(tot, T(P.M));
             ovf |= wf.d == 0;
+            if (flat) {  // all weights t_min: critical path = hop length x t_min
+                cp = n_mul_int(P.tmin, T(rounds));
+                ovf |= cp.d == 0;
+            }
             const RatT<T> r = n_cmp(wf, cp) < 0 ? cp : wf;
             S.bn[DS_BOUND_LOWER] = r.n;
             S.bd[DS_BOUND_LOWER] = r.d;
@@ -490,7 +515,7 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
         Mask<W> grouped;
         grouped.clear();
 #pragma unroll 1
-        for (;;) {
+        while (!grouped.eq(B)) {  // empty blocks are skipped (division.cpp:73)
             // heads: ungrouped members whose in-block predecessor is grouped or absent
             const Mask<W> H = ballot_nodes<W>(lane, [&](int v) {
                 if (v >= n || !B.test(v) || grouped.test(v)) return false;
@@ -860,9 +885,10 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     __syncwarp();
     if ((st = p_edges<W, T>(S, lane, n, edges, n_edges)) != DS_OK) return st;
     const bool lower = mask & DS_M_LOWER;
-    const int rounds = p_closure<W, T, true>(S, lane, n, lower, P);
-    if (rounds == -1) return DS_E_CYCLE;
-    if (rounds == -2) return DS_EOVERFLOW;
+    const int closure = p_closure<W, T, true>(S, lane, n, lower, P);
+    if (closure == -1) return DS_E_CYCLE;
+    if (closure == -2) return DS_EOVERFLOW;
+    const int rounds = closure;  // hop count | kFlatPath, decoded by p_bounds
     if ((st = p_ends<W, T>(S, lane, n)) != DS_OK) return st;
     if constexpr (W == 1) p_desc_transpose<T>(S, lane, n);
     else p_closure<W, T, false>(S, lane, n, false, P);
