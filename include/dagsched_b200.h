@@ -207,6 +207,13 @@ typedef struct ds_exec_cfg {
  * parallelism per group <= SMs): the proposed schedule. */
 #define DS_ENGINE_GRAPH 0
 #define DS_ENGINE_PERSISTENT 1
+/* GRAPH_FREE: the graph engine with the launch shape a developer would use
+ * without quota control — 4 x parallelism CTAs of 256 threads, no shared
+ * memory — so concurrent kernels share SMs and interfere (the naive
+ * multi-stream baseline of PAPER.md:533 on real hardware). Stamps then hold
+ * 4 x parallelism CTAs per entity. */
+#define DS_ENGINE_GRAPH_FREE 2
+#define DS_FREE_CTA_FACTOR 4
 
 /* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
 typedef struct ds_exec_trace {

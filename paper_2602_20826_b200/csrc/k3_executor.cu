@@ -76,29 +76,42 @@ struct Exec {
 // work list is its slots' (entity, rank) items in group order.
 int build_persistent(Exec* E, const ds_exec_plan* plan) {
     const int n = plan->n_entities;
-    std::vector<uint32_t> cta0(n);
     int max_group = -1;
     for (int i = 0; i < n; ++i) {
         if (plan->entities[i].group < 0) return fail(DS_EINVAL, "persistent engine needs a group-structured plan");
         if (i && plan->entities[i].group < plan->entities[i - 1].group)
             return fail(DS_EINVAL, "persistent engine needs entities in group order");
+        if (plan->entities[i].parallelism > E->sm_count) return fail(DS_EINVAL, "entity wider than the device");
         max_group = std::max(max_group, int(plan->entities[i].group));
     }
     std::vector<std::vector<int>> members(max_group + 1);
-    uint32_t grid = 0;
     for (int i = 0; i < n; ++i) members[plan->entities[i].group].push_back(i);
-    for (auto& g : members) {
-        uint32_t cur = 0;
-        for (int i : g) {
-            cta0[i] = cur;
-            cur += uint32_t(plan->entities[i].parallelism);
-        }
-        if (cur > uint32_t(E->sm_count)) return fail(DS_EINVAL, "group holds more SMs than the device has");
-        grid = std::max(grid, cur);
-    }
+    // Place every entity's CTAs on the SM slots that free up first (list
+    // scheduling over the model durations, entities in group order = a
+    // topological order of the augmented graph), so that without barriers a
+    // later group's entity is not queued behind an unrelated earlier item.
+    // Each slot's items stay in that topological order: deadlock-free.
+    const uint32_t grid = uint32_t(E->sm_count);
+    std::vector<double> slot_free(grid, 0.0), finish(n, 0.0);
     std::vector<std::vector<PItem>> per(grid);
-    for (int i = 0; i < n; ++i)  // plan order = group order
-        for (int r = 0; r < plan->entities[i].parallelism; ++r) per[cta0[i] + r].push_back(PItem{uint32_t(i), uint32_t(r)});
+    std::vector<uint32_t> order(grid);
+    for (int i = 0; i < n; ++i) {
+        const ds_exec_entity& e = plan->entities[i];
+        double ready = 0.0;
+        for (uint32_t k = 0; k < e.n_preds; ++k) ready = std::max(ready, finish[plan->preds[e.pred_off + k]]);
+        if (plan->barrier_groups && e.group > 0)
+            for (int j : members[e.group - 1]) ready = std::max(ready, finish[j]);
+        for (uint32_t c = 0; c < grid; ++c) order[c] = c;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return slot_free[a] < slot_free[b]; });
+        const double dur = double(e.elem_hi - e.elem_lo) / double(e.parallelism);
+        for (int r = 0; r < e.parallelism; ++r) {
+            const uint32_t c = order[r];
+            const double end = std::max(ready, slot_free[c]) + dur;
+            slot_free[c] = end;
+            finish[i] = std::max(finish[i], end);
+            per[c].push_back(PItem{uint32_t(i), uint32_t(r)});
+        }
+    }
     std::vector<uint32_t> item_off{0};
     std::vector<PItem> items;
     for (auto& v : per) {
@@ -273,7 +286,7 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
     std::vector<uint32_t> slots(n);
     for (int i = 0; i < n; ++i) {
         slots[i] = slot;
-        slot += uint32_t(plan->entities[i].parallelism);
+        slot += uint32_t(plan->entities[i].parallelism) * (E->engine == DS_ENGINE_GRAPH_FREE ? DS_FREE_CTA_FACTOR : 1);
     }
     // create nodes group by group so barrier nodes can take their inputs
     std::vector<int> order(n);
@@ -317,9 +330,15 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
         void* params[] = {&E->args[i]};
         cudaKernelNodeParams kp{};
         kp.func = kernel_of(E->workload);
-        kp.gridDim = dim3(unsigned(e.parallelism));
-        kp.blockDim = dim3(unsigned(E->threads));
-        kp.sharedMemBytes = unsigned(smem_of(E->workload) > kNodeSmem ? smem_of(E->workload) : kNodeSmem);
+        if (E->engine == DS_ENGINE_GRAPH_FREE) {  // unconstrained launch shape: CTAs share SMs
+            kp.gridDim = dim3(unsigned(e.parallelism) * DS_FREE_CTA_FACTOR);
+            kp.blockDim = dim3(256u);
+            kp.sharedMemBytes = 0;
+        } else {
+            kp.gridDim = dim3(unsigned(e.parallelism));
+            kp.blockDim = dim3(unsigned(E->threads));
+            kp.sharedMemBytes = unsigned(smem_of(E->workload) > kNodeSmem ? smem_of(E->workload) : kNodeSmem);
+        }
         kp.kernelParams = params;
         DS_CUDA(cudaGraphAddKernelNode(&node[i], E->graph, deps.data(), deps.size(), &kp));
     }
@@ -371,6 +390,7 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     Exec* E = H->E = new Exec();
     E->device = device;
     E->workload = cfg->workload;
+    E->engine = cfg->engine;
     E->threads = threads;
     auto bail = [&](int rc) {
         destroy(E);
@@ -392,7 +412,7 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
             e.elem_hi > plan->node_elems[e.node])
             return bail(fail(DS_EINVAL, "bad entity"));
         npreds = std::max<uint64_t>(npreds, uint64_t(e.pred_off) + e.n_preds);
-        E->total_ctas += uint32_t(e.parallelism);
+        E->total_ctas += uint32_t(e.parallelism) * (cfg->engine == DS_ENGINE_GRAPH_FREE ? DS_FREE_CTA_FACTOR : 1);
     }
     H->P.preds.assign(plan->preds, plan->preds + npreds);
     for (uint32_t p : H->P.preds) {
@@ -428,7 +448,7 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     if (E->engine == DS_ENGINE_PERSISTENT) {
         if (E->workload != DS_WL_MIX32) return bail(fail(DS_EINVAL, "persistent engine runs the mix32 workload"));
         if (int rc = build_persistent(E, &H->P.plan)) return bail(rc);
-    } else if (E->engine != DS_ENGINE_GRAPH) {
+    } else if (E->engine != DS_ENGINE_GRAPH && E->engine != DS_ENGINE_GRAPH_FREE) {
         return bail(fail(DS_EINVAL, "unknown engine"));
     }
     *exec = H;

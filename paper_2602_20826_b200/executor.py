@@ -47,7 +47,8 @@ class ds_exec_cfg(C.Structure):
                 ("sm_limit", C.c_int32), ("engine", C.c_int32), ("reserved", C.c_int32)]
 
 
-ENGINE_GRAPH, ENGINE_PERSISTENT = 0, 1
+ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE = 0, 1, 2
+FREE_CTA_FACTOR = 4  # DS_FREE_CTA_FACTOR
 
 
 class ds_exec_trace(C.Structure):
@@ -215,7 +216,10 @@ class Executor:
         sms = C.c_int()
         check(L.ds_exec_sm_count(self.h, C.byref(sms)))
         self.sm_count = sms.value
-        self.slots = np.cumsum([0] + [e.parallelism for e in plan.entities])
+        # stamp slots per entity (GRAPH_FREE launches FREE_CTA_FACTOR x parallelism CTAs)
+        factor = FREE_CTA_FACTOR if engine == ENGINE_GRAPH_FREE else 1
+        self.slots = np.cumsum([0] + [factor * e.parallelism for e in plan.entities])
+        plan._slots = self.slots
 
     def run(self, replays: int, warmup: int = 3, stamps: bool = True) -> RunResult:
         span = np.zeros((replays, 2), np.uint64)
