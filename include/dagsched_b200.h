@@ -270,6 +270,21 @@ int ds_session_run(void* session, float* kernel_ms);
 int ds_session_results(void* session, ds_results* out);
 int ds_session_free(void* session);
 
+/* Theorem-1 validation — replaces run_validation (experiment.cpp:163-240)
+ * over a given batch: per DAG the proposed schedule (K1) is simulated at
+ * worst case and `samples` times with durations scaled by factors k/1024,
+ * k ~ uniform_int_distribution<long long>(ceil(smin*1024), floor(smax*1024))
+ * over std::mt19937_64(seed + 7919*d + s) — bit-exact with the reference
+ * (simulator.cpp:14-94). Per-DAG arrays are optional (NULL to skip). */
+typedef struct ds_validation {
+    int64_t tasks, runs, violations;
+    double mean_tightness_worst, mean_tightness_scaled;
+} ds_validation;
+int ds_validate_batch(const ds_dag_batch* batch, const ds_platform* platform, int samples, int64_t smin_num,
+                      int64_t smin_den, int64_t smax_num, int64_t smax_den, uint64_t seed, int32_t* status,
+                      int32_t* violations, double* tight_worst, double* tight_scaled, ds_validation* summary,
+                      int device);
+
 /* Executor (K3) — replaces simulate_scheme (simulator.cpp:44-94) with real
  * execution: builds device buffers (inputs initialised from cfg->seed) and a
  * CUDA Graph with one kernel node per entity (grid = quota) and an edge per

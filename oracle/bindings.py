@@ -140,3 +140,24 @@ class Corpus:
 
     def analyze(self, d: int, sm_count: int, t_min=1) -> dict:
         return self._json("analyze_json", d, sm_count, t_min)
+
+
+def ref_run_validation(corpus_size: int, sm_count: int, samples: int, scale_min, scale_max, t_min=1,
+                       parallel=True, **cfg) -> dict:
+    """The reference's run_validation on generate_corpus(cfg, corpus_size)."""
+    chk = Checker("ref")
+    f = chk.lib.ref_run_validation
+    f.restype = C.c_int
+    f.argtypes = [C.POINTER(_abi.ds_gen_config), C.c_int, C.POINTER(_abi.ds_platform), C.c_int, C.c_int64,
+                  C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+    g = gen_config(t_min=t_min, **cfg)
+    pl = platform(sm_count, t_min)
+    smin, smax = Fraction(scale_min), Fraction(scale_max)
+    out = np.zeros(3, np.int64)
+    dbl = np.zeros(2, np.float64)
+    rc = f(C.byref(g), corpus_size, C.byref(pl), samples, smin.numerator, smin.denominator, smax.numerator,
+           smax.denominator, int(parallel), out.ctypes.data, dbl.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(chk.error())
+    return {"tasks": int(out[0]), "runs": int(out[1]), "violations": int(out[2]),
+            "mean_tightness_worst": float(dbl[0]), "mean_tightness_scaled": float(dbl[1])}

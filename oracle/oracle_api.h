@@ -48,6 +48,13 @@ extern "C" {
 ORACLE_DECLARE(ref_)
 ORACLE_DECLARE(orc_)
 
+/* The reference's run_validation (experiment.cpp:163-240) on
+ * generate_corpus(cfg, corpus_size); ref_ only. out = {tasks, runs,
+ * violations} and dbl = {mean_tightness_worst, mean_tightness_scaled}. */
+int ref_run_validation(const ds_gen_config* cfg, int corpus_size, const ds_platform* plat, int samples,
+                       int64_t smin_num, int64_t smin_den, int64_t smax_num, int64_t smax_den, int parallel,
+                       int64_t* out, double* dbl);
+
 #undef ORACLE_DECLARE
 
 #ifdef __cplusplus

@@ -294,3 +294,29 @@ char* ref_analyze_json(void* h, uint64_t d, const ds_platform* p) {
 }
 
 }  // extern "C"
+
+extern "C" int ref_run_validation(const ds_gen_config* g, int corpus_size, const ds_platform* p, int samples,
+                                  int64_t smin_num, int64_t smin_den, int64_t smax_num, int64_t smax_den,
+                                  int parallel, int64_t* out, double* dbl) {
+    return guarded([&] {
+        GenConfig cfg;
+        cfg.depth_min = g->depth_min;
+        cfg.depth_max = g->depth_max;
+        cfg.max_width = g->max_width;
+        cfg.avg_load = rat(g->avg_load_num, g->avg_load_den);
+        cfg.load_jitter = g->load_jitter;
+        cfg.edge_density = g->edge_density;
+        cfg.seed = g->seed;
+        cfg.integer_loads = g->integer_loads != 0;
+        cfg.exact_mean = g->exact_mean != 0;
+        cfg.t_min = rat(g->tmin_num, g->tmin_den);
+        // the reference's own Theorem-1 check (experiment.cpp:163-240)
+        ValidationSummary s = run_validation(cfg, corpus_size, platform_of(p), samples, rat(smin_num, smin_den),
+                                             rat(smax_num, smax_den), parallel != 0);
+        out[0] = s.tasks;
+        out[1] = s.runs;
+        out[2] = s.violations;
+        dbl[0] = s.mean_tightness_worst;
+        dbl[1] = s.mean_tightness_scaled;
+    });
+}

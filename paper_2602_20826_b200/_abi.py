@@ -92,3 +92,8 @@ class ds_scheme_out(C.Structure):
                 ("node_block", C.c_void_p), ("node_div_group", C.c_void_p),
                 ("entities", C.c_void_p), ("groups", C.c_void_p),
                 ("bounds", C.c_void_p)]
+
+
+class ds_validation(C.Structure):
+    _fields_ = [("tasks", C.c_int64), ("runs", C.c_int64), ("violations", C.c_int64),
+                ("mean_tightness_worst", C.c_double), ("mean_tightness_scaled", C.c_double)]

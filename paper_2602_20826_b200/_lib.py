@@ -204,3 +204,35 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+def validate(batch: DagBatch, sm_count: int, samples: int, scale_min, scale_max, seed: int, t_min=1,
+             device: int = 0):
+    """Batched Theorem-1 check (run_validation, experiment.cpp:163-240) on GPU.
+
+    Returns (summary dict, per-DAG status, violations, tight_worst, tight_scaled).
+    `seed` is the GenConfig seed the corpus came from (sample seeds are
+    seed + 7919 * d + s as in the reference)."""
+    from fractions import Fraction
+    L = lib()
+    f = L.ds_validate_batch
+    P = C.POINTER
+    f.restype = C.c_int
+    f.argtypes = [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                  C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(_abi.ds_validation), C.c_int]
+    n = batch.n_dags
+    st = np.zeros(n, np.int32)
+    viol = np.zeros(n, np.int32)
+    tw = np.zeros(n, np.float64)
+    ts = np.zeros(n, np.float64)
+    summ = _abi.ds_validation()
+    smin, smax = Fraction(scale_min), Fraction(scale_max)
+    cb = batch.as_c()
+    pl = platform(sm_count, t_min)
+    check(f(C.byref(cb), C.byref(pl), int(samples), smin.numerator, smin.denominator, smax.numerator,
+            smax.denominator, int(seed), st.ctypes.data, viol.ctypes.data, tw.ctypes.data, ts.ctypes.data,
+            C.byref(summ), device))
+    summary = {"tasks": summ.tasks, "runs": summ.runs, "violations": summ.violations,
+               "mean_tightness_worst": summ.mean_tightness_worst,
+               "mean_tightness_scaled": summ.mean_tightness_scaled}
+    return summary, combine_status(batch.pack_status, st), viol, tw, ts

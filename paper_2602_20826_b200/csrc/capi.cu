@@ -22,6 +22,11 @@
 
 namespace ds {
 
+// k4_validate.cu
+void k4_launch(u64 n_dags, const u32* node_off, const int32_t* status, const uint16_t* n_groups,
+               const ds_group_rec* groups, const ds_entity_rec* ents, const int64_t* bounds, int samples,
+               long long lo, long long hi, u64 seed, unsigned char* over, double* ratio, int32_t* st);
+
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -325,16 +330,15 @@ int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platfor
     return DS_OK;
 }
 
-int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_scheme_out* out, int device) {
-    if (!b || !out) return fail(DS_EINVAL, "NULL batch or output");
-    PlatT<u64> P;
-    if (int rc = check_platform(platform, P)) return rc;
+}  // extern "C"
+
+namespace ds {
+// K1 in detail mode over a host batch; results stay in B (device).
+int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DetailBufs& B) {
     const u64 n = b->n_dags;
-    if (n == 0) return DS_OK;
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
     if (int rc = configure(device, true, occ)) return rc;
-    DetailBufs B;
     cudaStream_t s = nullptr;
     if (int rc = upload(b, B, s)) return rc;
     const u64 N = b->node_off[n] - b->node_off[0];
@@ -377,6 +381,21 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     a.retry2_count = a.retry_count + 1;
     DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, 0, n), true, s));
     DS_CUDA(cudaDeviceSynchronize());
+    return DS_OK;
+}
+}  // namespace ds
+
+extern "C" {
+
+int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_scheme_out* out, int device) {
+    if (!b || !out) return fail(DS_EINVAL, "NULL batch or output");
+    PlatT<u64> P;
+    if (int rc = check_platform(platform, P)) return rc;
+    const u64 n = b->n_dags;
+    if (n == 0) return DS_OK;
+    DetailBufs B;
+    if (int rc = run_detail(b, P, device, B)) return rc;
+    const u64 N = b->node_off[n] - b->node_off[0];
     if (out->status) DS_CUDA(cudaMemcpy(out->status, B.status.p, n * 4, cudaMemcpyDeviceToHost));
     if (out->n_entities) DS_CUDA(cudaMemcpy(out->n_entities, B.ne.p, n * 2, cudaMemcpyDeviceToHost));
     if (out->n_groups) DS_CUDA(cudaMemcpy(out->n_groups, B.ng.p, n * 2, cudaMemcpyDeviceToHost));
@@ -387,6 +406,70 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
         DS_CUDA(cudaMemcpy(out->entities, B.ent.p, 2 * N * sizeof(ds_entity_rec), cudaMemcpyDeviceToHost));
     if (out->groups) DS_CUDA(cudaMemcpy(out->groups, B.grp.p, N * sizeof(ds_group_rec), cudaMemcpyDeviceToHost));
     if (out->bounds) DS_CUDA(cudaMemcpy(out->bounds, B.bounds.p, n * 80, cudaMemcpyDeviceToHost));
+    return DS_OK;
+}
+
+int ds_validate_batch(const ds_dag_batch* b, const ds_platform* platform, int samples, int64_t smin_num,
+                      int64_t smin_den, int64_t smax_num, int64_t smax_den, uint64_t seed, int32_t* status,
+                      int32_t* violations, double* tight_worst, double* tight_scaled, ds_validation* summary,
+                      int device) {
+    if (!b || samples < 0) return fail(DS_EINVAL, "bad arguments");
+    PlatT<u64> P;
+    if (int rc = check_platform(platform, P)) return rc;
+    // FactorSource (simulator.cpp:18-30): 0 < min <= max <= 1 on a 1/1024 grid
+    long long lo = 1024, hi = 1024;
+    if (samples > 0) {
+        if (smin_den <= 0 || smax_den <= 0 || smin_num <= 0 || smax_num > smax_den ||
+            (__int128)smin_num * smax_den > (__int128)smax_num * smin_den)
+            return fail(DS_EINVAL, "scale factors must satisfy 0 < min <= max <= 1");
+        lo = std::max(1LL, (long long)((smin_num * 1024 + smin_den - 1) / smin_den));  // ceil
+        hi = std::max(lo, (long long)(smax_num * 1024 / smax_den));                  // floor
+    }
+    const u64 n = b->n_dags;
+    if (n == 0) return DS_OK;
+    DetailBufs B;
+    if (int rc = run_detail(b, P, device, B)) return rc;
+    const u64 per = u64(samples) + 1, T = n * per;
+    DevBuf over, ratio, st;
+    if (int rc = over.ensure(T)) return rc;
+    if (int rc = ratio.ensure(T * 8)) return rc;
+    if (int rc = st.ensure(T * 4)) return rc;
+    k4_launch(n, B.node_off.as<const u32>(), B.status.as<int32_t>(), B.ng.as<uint16_t>(), B.grp.as<ds_group_rec>(),
+              B.ent.as<ds_entity_rec>(), B.bounds.as<int64_t>(), samples, lo, hi, seed, over.as<unsigned char>(),
+              ratio.as<double>(), st.as<int32_t>());
+    DS_CUDA(cudaGetLastError());
+    std::vector<unsigned char> h_over(T);
+    std::vector<double> h_ratio(T);
+    std::vector<int32_t> h_st(T);
+    DS_CUDA(cudaMemcpy(h_over.data(), over.p, T, cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaMemcpy(h_ratio.data(), ratio.p, T * 8, cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaMemcpy(h_st.data(), st.p, T * 4, cudaMemcpyDeviceToHost));
+    // experiment.cpp:179-239 reductions, in the same order (samples, then tasks)
+    ds_validation sum{int64_t(n), int64_t(n * per), 0, 0.0, 0.0};
+    double worst_sum = 0.0, scaled_total = 0.0;
+    for (u64 d = 0; d < n; ++d) {
+        int sd = DS_OK;
+        for (u64 k = 0; k < per; ++k) sd = sd != DS_OK ? sd : h_st[d * per + k];
+        int viol = 0;
+        double scaled = 0.0;
+        for (int s = 0; s < samples; ++s) {
+            viol += h_over[d * per + s];
+            scaled += h_ratio[d * per + s];
+        }
+        viol += h_over[d * per + samples];
+        const double tw = h_ratio[d * per + samples];
+        const double ts = samples > 0 ? scaled / samples : 0.0;
+        if (status) status[d] = sd;
+        if (violations) violations[d] = viol;
+        if (tight_worst) tight_worst[d] = tw;
+        if (tight_scaled) tight_scaled[d] = ts;
+        sum.violations += viol;
+        worst_sum += tw;
+        scaled_total += ts;
+    }
+    sum.mean_tightness_worst = worst_sum / double(n);
+    sum.mean_tightness_scaled = scaled_total / double(n);
+    if (summary) *summary = sum;
     return DS_OK;
 }
 

@@ -141,6 +141,20 @@ def main():
             for d in range(120):
                 f.write(json.dumps({"dag": d, "sm_count": M, "scheme": corp.scheme(d, M)},
                                    sort_keys=True) + "\n")
+    # run_validation (experiment.cpp:163-240): the reference's own summary
+    from oracle.bindings import ref_run_validation
+    vals = []
+    for cfg, n, M, S, smin, smax in ((dict(seed=1), 300, 32, 10, "1/2", "1"),
+                                     (dict(seed=5, avg_load=4), 200, 8, 10, "1/4", "3/4"),
+                                     (dict(seed=9), 300, 148, 5, "9/10", "1"),
+                                     (dict(seed=13, avg_load=200, max_width=12), 100, 148, 8, "1/3", "1"),
+                                     (dict(seed=17, integer_loads=False, avg_load=5), 150, 16, 10, "1/2", "1")):
+        r = ref_run_validation(n, M, S, smin, smax, **cfg)
+        vals.append({"config": cfg, "corpus_size": n, "sm_count": M, "samples": S, "scale_min": smin,
+                     "scale_max": smax, "summary": {k: (v.hex() if isinstance(v, float) else v)
+                                                    for k, v in r.items()}})
+    with open(os.path.join(OUT, "validation.json"), "w") as f:
+        json.dump(vals, f, indent=1)
     print("golden fixtures written to", OUT)
 
 
