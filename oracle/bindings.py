@@ -161,3 +161,29 @@ def ref_run_validation(corpus_size: int, sm_count: int, samples: int, scale_min,
         raise RuntimeError(chk.error())
     return {"tasks": int(out[0]), "runs": int(out[1]), "violations": int(out[2]),
             "mean_tightness_worst": float(dbl[0]), "mean_tightness_scaled": float(dbl[1])}
+
+
+def ref_run_experiment(sweep: str, values, sm_count: int, corpus_size: int,
+                       methods=("proposed", "greedy", "greedy_unaware", "graham_para"),
+                       normalize_to="greedy_unaware", t_min=1, **cfg) -> str:
+    """The reference's run_experiment + write_csv -> CSV text."""
+    names = ("proposed", "greedy", "greedy_unaware", "graham_para")
+    chk = Checker("ref")
+    f = chk.lib.ref_run_experiment
+    f.restype = C.c_void_p
+    f.argtypes = [C.c_char, C.c_void_p, C.c_int, C.POINTER(_abi.ds_gen_config), C.POINTER(_abi.ds_platform),
+                  C.c_int, C.c_uint32, C.c_int]
+    vals = np.asarray(list(values), np.int64)
+    g = gen_config(t_min=t_min, **cfg)
+    pl = platform(sm_count, t_min)
+    mask = 0
+    for m in methods:
+        mask |= 1 << names.index(m)
+    ptr = f(sweep.encode(), vals.ctypes.data, len(vals), C.byref(g), C.byref(pl), corpus_size, mask,
+            names.index(normalize_to))
+    if not ptr:
+        raise RuntimeError(chk.error())
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        chk._f["free"](ptr)

@@ -55,6 +55,13 @@ int ref_run_validation(const ds_gen_config* cfg, int corpus_size, const ds_platf
                        int64_t smin_num, int64_t smin_den, int64_t smax_num, int64_t smax_den, int parallel,
                        int64_t* out, double* dbl);
 
+/* The reference's run_experiment + write_csv (experiment.cpp:81-161): sweep
+ * 'M', 'P' or 'V' over values[n_values]; methods as a DS_M_* mask (bits 0-3),
+ * normalised to method index `normalize_to`. Returns malloc'd CSV (ref_free)
+ * or NULL (ref_last_error). */
+char* ref_run_experiment(char sweep, const long long* values, int n_values, const ds_gen_config* base,
+                         const ds_platform* plat, int corpus_size, uint32_t methods, int normalize_to);
+
 #undef ORACLE_DECLARE
 
 #ifdef __cplusplus

@@ -320,3 +320,37 @@ extern "C" int ref_run_validation(const ds_gen_config* g, int corpus_size, const
         dbl[1] = s.mean_tightness_scaled;
     });
 }
+
+extern "C" char* ref_run_experiment(char sweep, const long long* values, int n_values, const ds_gen_config* g,
+                                    const ds_platform* p, int corpus_size, uint32_t methods, int normalize_to) {
+    std::string text;
+    int st = guarded([&] {
+        ExperimentSpec spec;
+        spec.sweep = sweep == 'M' ? ExperimentSpec::SweepVar::sm_count
+                     : sweep == 'P' ? ExperimentSpec::SweepVar::max_width
+                                    : ExperimentSpec::SweepVar::depth;
+        spec.values.assign(values, values + n_values);
+        spec.base.depth_min = g->depth_min;
+        spec.base.depth_max = g->depth_max;
+        spec.base.max_width = g->max_width;
+        spec.base.avg_load = rat(g->avg_load_num, g->avg_load_den);
+        spec.base.load_jitter = g->load_jitter;
+        spec.base.edge_density = g->edge_density;
+        spec.base.seed = g->seed;
+        spec.base.integer_loads = g->integer_loads != 0;
+        spec.base.exact_mean = g->exact_mean != 0;
+        spec.base.t_min = rat(g->tmin_num, g->tmin_den);
+        spec.platform = platform_of(p);
+        spec.corpus_size = corpus_size;
+        const Method all[4] = {Method::proposed, Method::greedy, Method::greedy_unaware, Method::graham_para};
+        spec.methods.clear();
+        for (int k = 0; k < 4; ++k)
+            if (methods & (1u << k)) spec.methods.push_back(all[k]);
+        spec.normalize_to = all[normalize_to];
+        // the reference's own sweep driver and CSV writer (experiment.cpp:81-161)
+        std::ostringstream out;
+        write_csv(run_experiment(spec), out);
+        text = out.str();
+    });
+    return st == DS_OK ? dup(text) : nullptr;
+}

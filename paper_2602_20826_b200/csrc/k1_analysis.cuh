@@ -103,13 +103,14 @@ __device__ __forceinline__ Mask<W> load_mask(const u64 (&m)[W]) {
 // Uniform mask from a per-node predicate evaluated by the owning lanes. The
 // predicate body is instantiated once per mask word.
 template <int W, class Pred>
-__device__ __forceinline__ Mask<W> ballot_nodes(int lane, Pred pred) {
+__device__ __forceinline__ Mask<W> ballot_nodes(int lane, int n, Pred pred) {
     Mask<W> r;
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         u64 acc = 0;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
+            if (k * 64 + h * 32 >= n) break;  // uniform: most DAGs fit one 32-node half
             acc |= u64(__ballot_sync(FULL, pred(k * 64 + h * 32 + lane))) << (32 * h);
         }
         r.w[k] = acc;
@@ -124,6 +125,29 @@ __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
     for (int k = 0; k < W; ++k) {
 #pragma unroll 1
         for (u64 x = m.w[k]; x; x &= x - 1) f(k * 64 + __ffsll(x) - 1);
+    }
+}
+
+// Ascending bitonic sort of 64 keys held as (a: element lane, b: element
+// lane + 32); afterwards element e of the sorted order is in lane e % 32.
+__device__ __forceinline__ void bitonic64(u64& a, u64& b, const int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // partners are the two registers of one lane (k == 64: ascending)
+                const u64 lo = min(a, b), hi = max(a, b);
+                a = lo;
+                b = hi;
+                continue;
+            }
+            const u64 pa = __shfl_xor_sync(FULL, a, j), pb = __shfl_xor_sync(FULL, b, j);
+            const bool lower = (lane & j) == 0;          // this element has the smaller index
+            const bool up_a = (lane & k) == 0;           // element lane: ascending run?
+            const bool up_b = ((lane + 32) & k) == 0;    // element lane + 32
+            a = (lower == up_a) ? min(a, pa) : max(a, pa);
+            b = (lower == up_b) ? min(b, pb) : max(b, pb);
+        }
     }
 }
 
@@ -250,7 +274,7 @@ __device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const 
     int rounds = 0;
 #pragma unroll 1
     for (;;) {
-        const Mask<W> R = ballot_nodes<W>(lane, [&](int v) {
+        const Mask<W> R = ballot_nodes<W>(lane, n, [&](int v) {
             if (v >= n || done.test(v)) return false;
             bool ok = true;
 #pragma unroll
@@ -273,7 +297,7 @@ __device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const 
                 a[p >> 6] |= 1ull << (p & 63);
                 if (FWD && lower) {
                     const RatT<T> c{S.cn[p], S.cd[p]};
-                    if (n_cmp(c, best) > 0) best = c;
+                    if (q_cmp(c, best) > 0) best = c;
                 }
             });
 #pragma unroll
@@ -316,7 +340,7 @@ __device__ __noinline__ void p_desc_transpose(WarpState<1, T>& S, const int lane
 // dag.cpp:97-108: exactly one source and one sink.
 template <int W, class T>
 __device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int n) {
-    const Mask<W> src = ballot_nodes<W>(lane, [&](int v) {
+    const Mask<W> src = ballot_nodes<W>(lane, n, [&](int v) {
         if (v >= n) return false;
         u64 a = 0;
 #pragma unroll
@@ -324,7 +348,7 @@ __device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int
         return a == 0;
     });
     if (src.popc() != 1) return DS_E_SOURCES;
-    const Mask<W> snk = ballot_nodes<W>(lane, [&](int v) {
+    const Mask<W> snk = ballot_nodes<W>(lane, n, [&](int v) {
         if (v >= n) return false;
         u64 a = 0;
 #pragma unroll
@@ -451,13 +475,43 @@ __device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int
         }
     }
     __syncwarp();
-    const Mask<W> J = ballot_nodes<W>(lane, [&](int v) {
+    const Mask<W> J = ballot_nodes<W>(lane, n, [&](int v) {
         if (v >= n) return false;
         int c = 0;
 #pragma unroll
         for (int k = 0; k < W; ++k) c += __popcll(S.pred[v][k]);
         return c >= 2;
     });
+    if constexpr (W == 1) {
+        // Integer W^anc (the common case): two warp bitonic sorts of 64 keys
+        // (2 per lane) replace the O(n) compare loop per node. Key for the
+        // rank: (W^anc desc, id asc) = ((~W) << 8 | id); for the joins:
+        // (W^anc asc, id asc) = (W << 8 | id), non-joins pushed to the end.
+        bool small = true;
+        for (int v = lane; v < n; v += 32) small &= u64(S.xn[v]) < (1ull << 48);
+        if (integer && __all_sync(FULL, small)) {
+            const u64 mask48 = (1ull << 48) - 1;
+            u64 a = lane < n ? ((mask48 - u64(S.xn[lane])) << 8) | u64(lane) : ~0ull;
+            u64 b = lane + 32 < n ? ((mask48 - u64(S.xn[lane + 32])) << 8) | u64(lane + 32) : ~0ull;
+            u64 ja = lane < n && J.test(lane) ? (u64(S.xn[lane]) << 8) | u64(lane) : ~0ull;
+            u64 jb = lane + 32 < n && J.test(lane + 32) ? (u64(S.xn[lane + 32]) << 8) | u64(lane + 32) : ~0ull;
+            bitonic64(a, b, lane);
+            bitonic64(ja, jb, lane);
+            if (a != ~0ull) {
+                S.order[lane] = short(a & 0xff);
+                S.rank[a & 0xff] = short(lane);
+            }
+            if (b != ~0ull) {
+                S.order[lane + 32] = short(b & 0xff);
+                S.rank[b & 0xff] = short(lane + 32);
+            }
+            if (ja != ~0ull) S.jorder[lane] = short(ja & 0xff);
+            if (jb != ~0ull) S.jorder[lane + 32] = short(jb & 0xff);
+            __syncwarp();
+            if (__any_sync(FULL, ovf)) return -1;
+            return J.popc();
+        }
+    }
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         const RatT<T> wv{S.xn[v], S.xd[v]};
@@ -467,7 +521,7 @@ __device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int
         for (int u = 0; u < n; ++u) {
             int c;
             if (integer) c = S.xn[u] < wv.n ? -1 : (S.xn[u] > wv.n ? 1 : 0);
-            else c = n_cmp(RatT<T>{S.xn[u], S.xd[u]}, wv);
+            else c = q_cmp(RatT<T>{S.xn[u], S.xd[u]}, wv);
             r += (c > 0) || (c == 0 && u < v);
             jr += isj && J.test(u) && ((c < 0) || (c == 0 && u < v));
         }
@@ -517,7 +571,7 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
 #pragma unroll 1
         while (!grouped.eq(B)) {  // empty blocks are skipped (division.cpp:73)
             // heads: ungrouped members whose in-block predecessor is grouped or absent
-            const Mask<W> H = ballot_nodes<W>(lane, [&](int v) {
+            const Mask<W> H = ballot_nodes<W>(lane, n, [&](int v) {
                 if (v >= n || !B.test(v) || grouped.test(v)) return false;
                 bool ok = true;
 #pragma unroll
@@ -535,7 +589,7 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
                     if (H.test(v)) atomicOr(&S.rmask[S.rank[v] >> 6], 1ull << (S.rank[v] & 63));
                 }
                 __syncwarp();
-                sel = ballot_nodes<W>(lane, [&](int v) {
+                sel = ballot_nodes<W>(lane, n, [&](int v) {
                     if (v >= n || !H.test(v)) return false;
                     const int r = S.rank[v];
                     int below = 0;
@@ -557,7 +611,7 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
             }
             mx = __reduce_max_sync(FULL, mx);
             if (mx >= M) {
-                const Mask<W> top = ballot_nodes<W>(lane, [&](int v) {
+                const Mask<W> top = ballot_nodes<W>(lane, n, [&](int v) {
                     return v < n && sel.test(v) && S.mmax[v] == mx;
                 });
                 int pick = -1;
@@ -633,7 +687,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
 
         // -- apportion (scheduler.cpp:35-95) over the pending loads
         RatT<T> Wt{0, 1};
-        for_bits<W>(org, [&](int v) { Wt = n_add(Wt, RatT<T>{S.pn[v], S.pd[v]}); });
+        for_bits<W>(org, [&](int v) { Wt = q_add(Wt, RatT<T>{S.pn[v], S.pd[v]}); });
         ovf |= Wt.d == 0;
         int tot = 0, capsum = 0;
 #pragma unroll 1
@@ -669,9 +723,9 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
             for_bits<W>(org, [&](int v) {
                 const int m = S.mq[v];
                 if (m <= 1) return;
-                const RatT<T> s = n_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m - 1, P);
+                const RatT<T> s = q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m - 1, P);
                 ovf |= s.d == 0;
-                if (pick < 0 || n_cmp(s, best) < 0) {
+                if (pick < 0 || q_cmp(s, best) < 0) {
                     pick = v;
                     best = s;
                 }
@@ -689,13 +743,13 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
             for_bits<W>(org, [&](int v) {
                 const int m = S.mq[v];
                 if (m >= S.cap[v]) return;
-                const RatT<T> cur = n_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m, P);
+                const RatT<T> cur = q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m, P);
                 ovf |= cur.d == 0;
                 const RatT<T> rm{S.rn[v], S.rd[v]};
                 int c = 1;
                 if (pick >= 0) {
-                    c = n_cmp(cur, be);
-                    if (c == 0) c = n_cmp(rm, br);
+                    c = q_cmp(cur, be);
+                    if (c == 0) c = q_cmp(rm, br);
                 }
                 if (c > 0) {
                     pick = v;
@@ -723,7 +777,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
         int bott = -1, used = 0, n_mem = 0, bott_pos = 0;
         for_bits<W>(org, [&](int v) {
             const RatT<T> e{S.xn[v], S.xd[v]};
-            if (bott < 0 || n_cmp(e, R) > 0) {
+            if (bott < 0 || q_cmp(e, R) > 0) {
                 R = e;
                 bott = v;
                 bott_pos = n_mem;
@@ -735,7 +789,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
 
         // -- candidates (scheduler.cpp:253-280). Concurrency is symmetric, so
         // c is in the pool iff some pending member is concurrent with c.
-        const Mask<W> pool = ballot_nodes<W>(lane, [&](int c) {
+        const Mask<W> pool = ballot_nodes<W>(lane, n, [&](int c) {
             if (c >= n || G.test(c)) return false;
             u64 hit = 0;
 #pragma unroll
@@ -746,7 +800,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
             }
             return hit != 0;
         });
-        const Mask<W> cands = ballot_nodes<W>(lane, [&](int c) {
+        const Mask<W> cands = ballot_nodes<W>(lane, n, [&](int c) {
             if (c >= n || !pool.test(c) || done.test(c)) return false;
             bool ok = true;
 #pragma unroll
@@ -789,7 +843,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
                 const int mc = min(mp, spare);
                 const RatT<T> dur = n_exec(l, mc, P);
                 ovf |= dur.d == 0;
-                if (n_cmp(dur, R) <= 0) {
+                if (q_cmp(dur, R) <= 0) {
                     if (DETAIL && lane == 0) {
                         put_rec(det.ent[n_ent], c, S.gen[c], S.ppart[c], true, gidx, mc, l, dur, RatT<T>{0, 0},
                                 ovf);
@@ -847,7 +901,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
 #pragma unroll
         for (int k = 0; k < W; ++k) done.w[k] |= org.w[k] | whole.w[k];
         n_ent += n_mem;
-        proposed = n_add(proposed, R);
+        proposed = q_add(proposed, R);
         ovf |= proposed.d == 0;
         ++gidx;
         __syncwarp();

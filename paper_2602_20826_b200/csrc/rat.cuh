@@ -414,3 +414,33 @@ __device__ __noinline__ T n_ceil(RatT<T> a) {
     return rat_ceil(a);
 }
 }  // namespace ds
+
+namespace ds {
+// Hot-loop helpers: the 32-bit tier's compare / unreduced exec_time are a few
+// instructions, cheaper inline than a call; wider tiers keep the single
+// out-of-line copy. Integer sums add inline at every width.
+template <class T>
+__device__ __forceinline__ int q_cmp(RatT<T> a, RatT<T> b) {
+    if constexpr (sizeof(T) == 4) return rat_cmp(a, b);
+    else return n_cmp(a, b);
+}
+template <class T>
+__device__ __forceinline__ RatT<T> q_exec_raw(RatT<T> load, long long m, const PlatT<T>& p) {
+    if constexpr (sizeof(T) == 4) {
+        bool o = false;
+        RatT<T> r = exec_raw(load, m, p, o);
+        if (o) r.d = 0;
+        return r;
+    } else {
+        return n_exec_raw(load, m, p);
+    }
+}
+template <class T>
+__device__ __forceinline__ RatT<T> q_add(RatT<T> a, RatT<T> b) {
+    if (a.d == 1 && b.d == 1) {
+        const T s = a.n + b.n;
+        return RatT<T>{s, T(s < a.n ? 0 : 1)};  // den 0 flags overflow
+    }
+    return n_add(a, b);
+}
+}  // namespace ds

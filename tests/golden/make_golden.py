@@ -155,6 +155,17 @@ def main():
                                                     for k, v in r.items()}})
     with open(os.path.join(OUT, "validation.json"), "w") as f:
         json.dump(vals, f, indent=1)
+    # run_experiment + write_csv (experiment.cpp:81-161), at sizes where the
+    # reference's 128-bit exact mean does not overflow
+    from oracle.bindings import ref_run_experiment
+    exps = []
+    for sweep, values, M, n, cfg in (("M", [148], 148, 20, dict(seed=3)), ("M", [4, 8], 8, 20, dict(seed=3)),
+                                     ("M", [148, 256], 148, 30, dict(seed=3)), ("P", [4, 6], 148, 15, dict(seed=3)),
+                                     ("V", [3, 4], 148, 15, dict(seed=3, max_width=4))):
+        exps.append({"sweep": sweep, "values": values, "sm_count": M, "corpus_size": n, "config": cfg,
+                     "csv": ref_run_experiment(sweep, values, M, n, **cfg)})
+    with open(os.path.join(OUT, "experiments.json"), "w") as f:
+        json.dump(exps, f, indent=1)
     print("golden fixtures written to", OUT)
 
 
