@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden
 CXXFLAGS:= -std=c++17 -O3 -fPIC -fopenmp -fvisibility=hidden -I/usr/local/cuda/include -Wall -Wno-comment
 LDOMP   := -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp -lpthread
 
-CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o
+CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o $(LIBDIR)/k5_generate.o
 CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/dagsched_b200.h
 
 .PHONY: all product oracle ref clean
@@ -26,7 +26,7 @@ $(LIBDIR)/%.o: $(PKG)/csrc/%.cu $(CU_DEPS) $(PKG)/csrc/k1_main.cu
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(LIBDIR)/ptxas_$*.txt || (cat $(LIBDIR)/ptxas_$*.txt; false)
 
-$(LIBDIR)/host_gen.o: $(PKG)/csrc/host_gen.cpp include/dagsched_b200.h
+$(LIBDIR)/host_gen.o: $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/k5_generate_host.h include/dagsched_b200.h
 	@mkdir -p $(LIBDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 

@@ -64,6 +64,8 @@ extern "C" {
 /* Flags for the batch entry points. */
 #define DS_F_DEVICE_PTRS 1u /* batch and result pointers are device memory on `device` */
 #define DS_F_PINNED 2u      /* (corpus generation) allocate host arrays pinned         */
+#define DS_F_GPU_GENERATE 4u /* (corpus generation) generate on the calling thread's
+                              * current CUDA device (K5), copy into the host arrays  */
 
 /* --------------------------------------------------------------- inputs */
 /* Platform (exec_model.hpp:11-19): M identical SMs and the time floor t_min. */
@@ -251,12 +253,16 @@ int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platfor
 int ds_schedule_batch(const ds_dag_batch* batch, const ds_platform* platform,
                       ds_scheme_out* out, int device);
 
-/* Corpus generation on the host — replaces generate_corpus (generator.cpp:98-108)
- * with identical RNG call order; parallel over seeds. The handle owns packed
- * arrays (pinned when DS_F_PINNED) exposed through ds_corpus_view. */
+/* Corpus generation — replaces generate_corpus (generator.cpp:98-108) with
+ * identical RNG call order: on the host, parallel over seeds, or with
+ * DS_F_GPU_GENERATE on the device (one thread per DAG, K5). The handle owns
+ * packed host arrays (pinned when DS_F_PINNED) exposed through ds_corpus_view. */
 int ds_corpus_generate(const ds_gen_config* cfg, int64_t count, uint32_t flags,
                        void** handle);
 int ds_corpus_view(void* handle, ds_dag_batch* view);
+/* Device milliseconds of a DS_F_GPU_GENERATE generation (kernels + scans; 0
+ * for host generation). */
+float ds_corpus_gen_ms(void* handle);
 void ds_corpus_free(void* handle);
 
 /* Timed-analysis session: uploads a batch once and replays the kernel on it

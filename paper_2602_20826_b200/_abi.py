@@ -32,6 +32,7 @@ BOUND_NAMES = ("proposed", "greedy", "greedy_unaware", "graham_para", "lower")
 DS_M_ALL = 0x1F
 DS_F_DEVICE_PTRS = 1
 DS_F_PINNED = 2
+DS_F_GPU_GENERATE = 4
 
 STATUS_NAMES = {
     DS_OK: "ok", DS_EINVAL: "invalid_argument", DS_EOVERFLOW: "overflow", DS_ECUDA: "cuda",

@@ -42,6 +42,7 @@ def _sig(lib):
         "ds_corpus_generate": (C.c_int, [P(_abi.ds_gen_config), C.c_int64, C.c_uint32, P(C.c_void_p)]),
         "ds_corpus_view": (C.c_int, [C.c_void_p, P(_abi.ds_dag_batch)]),
         "ds_corpus_free": (None, [C.c_void_p]),
+        "ds_corpus_gen_ms": (C.c_float, [C.c_void_p]),
         "ds_session_create": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                         C.c_int, P(C.c_void_p)]),
         "ds_session_run": (C.c_int, [C.c_void_p, P(C.c_float)]),
@@ -130,13 +131,15 @@ def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = 
 
 
 class Corpus:
-    """Host-generated corpus (product generator, generator.cpp semantics)."""
+    """Generated corpus (product generator, generator.cpp semantics): on the
+    host, or on the current CUDA device with ``gpu=True`` (K5)."""
 
-    def __init__(self, count: int, pinned: bool = False, **cfg):
+    def __init__(self, count: int, pinned: bool = False, gpu: bool = False, **cfg):
         self.h = C.c_void_p()
         g = gen_config(**cfg)
-        check(lib().ds_corpus_generate(C.byref(g), int(count), _abi.DS_F_PINNED if pinned else 0,
-                                       C.byref(self.h)))
+        flags = (_abi.DS_F_PINNED if pinned else 0) | (_abi.DS_F_GPU_GENERATE if gpu else 0)
+        check(lib().ds_corpus_generate(C.byref(g), int(count), flags, C.byref(self.h)))
+        self.gen_ms = float(lib().ds_corpus_gen_ms(self.h))
         self.view = _abi.ds_dag_batch()
         check(lib().ds_corpus_view(self.h, C.byref(self.view)))
         v = self.view

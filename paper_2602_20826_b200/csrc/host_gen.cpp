@@ -21,6 +21,7 @@
 namespace ds {
 int fail(int code, const std::string& msg);
 }
+#include "k5_generate_host.h"
 
 namespace {
 
@@ -124,6 +125,7 @@ void generate_one(const Cfg& c, uint64_t seed, Dag& out) {
 
 struct Corpus {
     bool pinned = false;
+    float gen_ms = 0.f;  // device generation (DS_F_GPU_GENERATE): kernels + scans
     uint64_t n = 0, nn = 0, ne = 0;
     uint32_t *node_off = nullptr, *edge_off = nullptr, *edges = nullptr;
     int64_t *load_num = nullptr, *load_den = nullptr;
@@ -186,6 +188,51 @@ int ds_corpus_generate(const ds_gen_config* g, int64_t count, uint32_t flags, vo
     c.tmin_d = double(g->tmin_num) / double(g->tmin_den);
     if (2 + int64_t(c.dmax - 2) * c.width > DS_MAX_NODES)
         return fail(DS_ETOOBIG, "generated DAGs could exceed DS_MAX_NODES nodes");
+    if (flags & DS_F_GPU_GENERATE) {
+        ds::K5Params p;
+        p.count = uint64_t(count);
+        p.seed = g->seed;
+        p.dmin = c.dmin;
+        p.dmax = c.dmax;
+        p.width = c.width;
+        p.integer_loads = c.integer_loads;
+        p.exact_mean = c.exact_mean;
+        p.lo = c.avg_d * (1.0 - c.jitter);  // the load distribution's bounds (generator.cpp:62-63)
+        p.hi = c.avg_d * (1.0 + c.jitter);
+        p.tmin_f = c.tmin_d;
+        p.density = c.density;
+        p.tmin_n = uint64_t(c.tmin.n);
+        p.tmin_d = uint64_t(c.tmin.d);
+        p.avg_n = uint64_t(c.avg.n);
+        p.avg_d = uint64_t(c.avg.d);
+        auto* cp = new Corpus();
+        cp->pinned = flags & DS_F_PINNED;
+        cp->n = uint64_t(count);
+        int device = 0;
+        if (cudaGetDevice(&device) != cudaSuccess) device = 0;
+        auto alloc = [](uint64_t nn, uint64_t ne, void* user, ds::K5Host* h) -> int {
+            auto* cp = static_cast<Corpus*>(user);
+            cp->nn = nn;
+            cp->ne = ne;
+            cp->node_off = static_cast<uint32_t*>(host_alloc((cp->n + 1) * 4, cp->pinned));
+            cp->edge_off = static_cast<uint32_t*>(host_alloc((cp->n + 1) * 4, cp->pinned));
+            cp->edges = static_cast<uint32_t*>(host_alloc(ne * 4, cp->pinned));
+            cp->load_num = static_cast<int64_t*>(host_alloc(nn * 8, cp->pinned));
+            cp->load_den = static_cast<int64_t*>(host_alloc(nn * 8, cp->pinned));
+            if (!cp->node_off || !cp->edge_off || !cp->edges || !cp->load_num || !cp->load_den)
+                return ds::fail(DS_ENOMEM, "host allocation failed");
+            *h = ds::K5Host{cp->node_off, cp->edge_off, cp->edges, cp->load_num, cp->load_den};
+            return DS_OK;
+        };
+        const int words = 2 + int64_t(c.dmax - 2) * c.width <= 64 ? 1 : 4;
+        const int rc = ds::k5_generate_host(p, words, device, alloc, cp, &cp->gen_ms);
+        if (rc != DS_OK) {
+            corpus_free(cp);
+            return rc;
+        }
+        *handle = cp;
+        return DS_OK;
+    }
 
     // pass 1: generate in parallel into per-thread buffers (chunked by seed)
     const int nt = std::max(1, omp_get_max_threads());
@@ -274,6 +321,11 @@ int ds_corpus_view(void* handle, ds_dag_batch* view) {
     view->load_den = c->load_den;
     view->edges = c->edges;
     return DS_OK;
+}
+
+float ds_corpus_gen_ms(void* handle) {
+    auto* c = static_cast<Corpus*>(handle);
+    return c ? c->gen_ms : 0.f;
 }
 
 void ds_corpus_free(void* handle) { corpus_free(static_cast<Corpus*>(handle)); }
