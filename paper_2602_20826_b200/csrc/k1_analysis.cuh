@@ -128,25 +128,33 @@ __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
     }
 }
 
-// Ascending bitonic sort of 64 keys held as (a: element lane, b: element
-// lane + 32); afterwards element e of the sorted order is in lane e % 32.
-__device__ __forceinline__ void bitonic64(u64& a, u64& b, const int lane) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
+// Ascending bitonic sorts of two independent key sets of up to 64 keys each,
+// held as (a: element lane, b: element lane + 32) and (c, d) likewise;
+// afterwards element e of each sorted order is in lane e % 32. The network
+// runs as a loop (not unrolled: the kernel is instruction-fetch bound) up to
+// size K (32 when every key fits the a/c halves, else 64).
+__device__ __forceinline__ void bitonic64x2(u64& a, u64& b, u64& c, u64& d, const int lane, const int K) {
+#pragma unroll 1
+    for (int k = 2; k <= K; k <<= 1) {
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j == 32) {  // partners are the two registers of one lane (k == 64: ascending)
-                const u64 lo = min(a, b), hi = max(a, b);
+                const u64 lo = min(a, b), hi = max(a, b), lo2 = min(c, d), hi2 = max(c, d);
                 a = lo;
                 b = hi;
+                c = lo2;
+                d = hi2;
                 continue;
             }
             const u64 pa = __shfl_xor_sync(FULL, a, j), pb = __shfl_xor_sync(FULL, b, j);
+            const u64 pc = __shfl_xor_sync(FULL, c, j), pd = __shfl_xor_sync(FULL, d, j);
             const bool lower = (lane & j) == 0;          // this element has the smaller index
             const bool up_a = (lane & k) == 0;           // element lane: ascending run?
             const bool up_b = ((lane + 32) & k) == 0;    // element lane + 32
             a = (lower == up_a) ? min(a, pa) : max(a, pa);
             b = (lower == up_b) ? min(b, pb) : max(b, pb);
+            c = (lower == up_a) ? min(c, pc) : max(c, pc);
+            d = (lower == up_b) ? min(d, pd) : max(d, pd);
         }
     }
 }
@@ -495,8 +503,7 @@ __device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int
             u64 b = lane + 32 < n ? ((mask48 - u64(S.xn[lane + 32])) << 8) | u64(lane + 32) : ~0ull;
             u64 ja = lane < n && J.test(lane) ? (u64(S.xn[lane]) << 8) | u64(lane) : ~0ull;
             u64 jb = lane + 32 < n && J.test(lane + 32) ? (u64(S.xn[lane + 32]) << 8) | u64(lane + 32) : ~0ull;
-            bitonic64(a, b, lane);
-            bitonic64(ja, jb, lane);
+            bitonic64x2(a, b, ja, jb, lane, n <= 32 ? 32 : 64);
             if (a != ~0ull) {
                 S.order[lane] = short(a & 0xff);
                 S.rank[a & 0xff] = short(lane);
