@@ -667,6 +667,23 @@ __device__ __forceinline__ void put_rec(ds_entity_rec& e, int origin, int gen, i
     e.res_den = (long long)res.d;
 }
 
+// ------------------------------------------------- apportion member selection
+// shed: min k1, ties smaller index (scheduler.cpp:60-72); fill: max k1, then
+// max k2, ties smaller index (:74-93).
+template <class T>
+struct Pick {
+    RatT<T> k1, k2;
+    int idx;
+};
+template <class T>
+__device__ __forceinline__ bool pick_better(const Pick<T>& a, const Pick<T>& b, const bool shed) {
+    if (a.idx < 0) return false;
+    if (b.idx < 0) return true;
+    int c = q_cmp(a.k1, b.k1);
+    if (shed) c = -c;
+    if (c == 0) c = q_cmp(a.k2, b.k2);  // shed: k2 is constant
+    return c > 0 || (c == 0 && a.idx < b.idx);
+}
 // ----------------------------------------------------------- phase: schedule
 // scheduler.cpp:214-359, one executed group per non-absorbed division group.
 // Returns status | (n_groups << 8) | (n_entities << 20).
@@ -723,51 +740,27 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
         tot = __reduce_add_sync(FULL, tot);
         capsum = __reduce_add_sync(FULL, capsum);
         __syncwarp();
-#pragma unroll 1
-        while (tot > P.M) {  // shed: smallest slowdown, first index wins ties
-            int pick = -1;
-            RatT<T> best{0, 1};
-            for_bits<W>(org, [&](int v) {
-                const int m = S.mq[v];
-                if (m <= 1) return;
-                const RatT<T> s = q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m - 1, P);
-                ovf |= s.d == 0;
-                if (pick < 0 || q_cmp(s, best) < 0) {
-                    pick = v;
-                    best = s;
-                }
-            });
-            if (pick < 0) return DS_EINVARIANT;
-            if (lane == 0) S.mq[pick] -= 1;
-            __syncwarp();
-            --tot;
-        }
+        // shed while over M (smallest slowdown exec(m-1), first index wins
+        // ties), else fill up to target (largest exec(m), then larger remainder,
+        // then first index); shedding ends at M >= target, so at most one runs
         const int target = min(P.M, capsum);
 #pragma unroll 1
-        while (tot < target) {  // fill: largest exec, then larger remainder, then first index
-            int pick = -1;
-            RatT<T> be{0, 1}, br{0, 1};
+        while (tot > P.M || tot < target) {
+            const bool shed = tot > P.M;
+            Pick<T> c{{0, 1}, {0, 1}, -1};
             for_bits<W>(org, [&](int v) {
                 const int m = S.mq[v];
-                if (m >= S.cap[v]) return;
-                const RatT<T> cur = q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, m, P);
-                ovf |= cur.d == 0;
-                const RatT<T> rm{S.rn[v], S.rd[v]};
-                int c = 1;
-                if (pick >= 0) {
-                    c = q_cmp(cur, be);
-                    if (c == 0) c = q_cmp(rm, br);
-                }
-                if (c > 0) {
-                    pick = v;
-                    be = cur;
-                    br = rm;
-                }
+                if (shed ? m <= 1 : m >= S.cap[v]) return;
+                const Pick<T> x{q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, shed ? m - 1 : m, P),
+                                shed ? RatT<T>{0, 1} : RatT<T>{S.rn[v], S.rd[v]}, v};
+                ovf |= x.k1.d == 0;
+                if (pick_better<T>(x, c, shed)) c = x;
             });
-            if (pick < 0) return DS_EINVARIANT;
-            if (lane == 0) S.mq[pick] += 1;
+            if (c.idx < 0) return DS_EINVARIANT;
+            const int step = shed ? -1 : 1;
+            if (lane == 0) S.mq[c.idx] += step;
             __syncwarp();
-            ++tot;
+            tot += step;
         }
 
         // -- members: exec, response (first strict max), bottleneck
