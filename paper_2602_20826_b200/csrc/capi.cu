@@ -10,6 +10,8 @@
 #include "../../include/dagsched_b200.h"
 #include "k1_launch.h"
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -112,15 +114,33 @@ struct DevBuf {
 // ------------------------------------------------------ chunked host path
 struct Slot {
     cudaStream_t s = nullptr;
-    DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count;
+    DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
 };
 
 struct DeviceCtx {
     std::mutex mu;
     bool init = false;
     Slot slot[3];
-    DevBuf retry, retry_count;  // scratch for the device-pointer entry point
+    DevBuf retry, retry_count, handoff;  // scratch for the device-pointer entry point
 };
+
+// The bounds pass runs as k1_front + k1_back (K1Handoff) unless DS_K1_SPLIT=0
+// selects the single-kernel variant (kept for A/B measurement and tests).
+bool k1_split_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("DS_K1_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+int attach_handoff(K1Args& a, DevBuf& buf, u64 n_dags, u64 n_nodes) {
+    a.h = K1Handoff{};
+    if (!k1_split_enabled() || !(a.mask & DS_M_PROPOSED)) return DS_OK;
+    if (int rc = buf.ensure(k1_handoff_bytes(n_dags, n_nodes))) return rc;
+    a.h = k1_handoff_carve(buf.p, n_dags, n_nodes);
+    return DS_OK;
+}
 
 DeviceCtx& device_ctx(int dev) {
     static DeviceCtx ctx[64];
@@ -162,7 +182,7 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         if (int rc = sl.bounds.ensure(nd * 80)) return rc;
         if (int rc = sl.ngroups.ensure(nd * 2)) return rc;
         if (int rc = sl.retry.ensure(2 * nd * 4)) return rc;  // two retry lists
-        if (int rc = sl.retry_count.ensure(8)) return rc;
+        if (int rc = sl.retry_count.ensure(16)) return rc;
         DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
@@ -186,6 +206,7 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         a.retry_count = sl.retry_count.as<u32>();
         a.retry2 = a.retry + nd;
         a.retry2_count = a.retry_count + 1;
+        if (int rc = attach_handoff(a, sl.handoff, nd, nn)) return rc;
         DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, lo, hi), false, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, sl.s));
@@ -202,7 +223,7 @@ struct Session {
     int device = 0;
     cudaStream_t s = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count;
+    DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
     K1Args args{};
     K1Occupancy occ;
     bool any_big = false;
@@ -271,7 +292,12 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     DeviceCtx& ctx = device_ctx(device);
     std::lock_guard<std::mutex> lock(ctx.mu);
     if (int rc = ctx.retry.ensure(2 * batch->n_dags * 4)) return rc;
-    if (int rc = ctx.retry_count.ensure(8)) return rc;
+    if (int rc = ctx.retry_count.ensure(16)) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    u32 ends[2];  // node_off[0], node_off[n]: sizes the split pass's scratch
+    DS_CUDA(cudaMemcpyAsync(&ends[0], batch->node_off, 4, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaMemcpyAsync(&ends[1], batch->node_off + batch->n_dags, 4, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaStreamSynchronize(s));
     K1Args a{};
     a.n_dags = batch->n_dags;
     a.node_off = batch->node_off;
@@ -288,9 +314,9 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     a.retry_count = ctx.retry_count.as<u32>();
     a.retry2 = a.retry + batch->n_dags;
     a.retry2_count = a.retry_count + 1;
+    if (int rc = attach_handoff(a, ctx.handoff, batch->n_dags, u64(ends[1] - ends[0]))) return rc;
     // device pointers: size classes are unknown on the host, so the n <= 256
     // kernel always runs (it skips DAGs with n <= 64 after two offset loads)
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     DS_CUDA(k1_launch(a, occ, true, false, s));
     // the scratch is reused by the next call: finish before releasing it
     DS_CUDA(cudaStreamSynchronize(s));
@@ -499,7 +525,7 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     rc = rc ? rc : S->bounds.ensure(n * 80);
     rc = rc ? rc : S->ngroups.ensure(n * 2);
     rc = rc ? rc : S->retry.ensure(2 * n * 4);
-    rc = rc ? rc : S->retry_count.ensure(8);
+    rc = rc ? rc : S->retry_count.ensure(16);
     if (rc) return bail(rc);
     K1Args& a = S->args;
     a.n_dags = n;
@@ -517,6 +543,7 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     a.retry_count = S->retry_count.as<u32>();
     a.retry2 = a.retry + n;
     a.retry2_count = a.retry_count + 1;
+    if (int rc2 = attach_handoff(a, S->handoff, n, u64(b->node_off[n] - b->node_off[0]))) return bail(rc2);
     *session = S;
     return DS_OK;
 }

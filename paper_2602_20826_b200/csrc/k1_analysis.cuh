@@ -44,13 +44,33 @@ constexpr int kFlatPath = 1 << 16;  // p_closure flag: every lower-bound weight 
 template <int W, class T>
 struct WarpState {
     static constexpr int N = 64 * W;
-    u64 pred[N][W], succ[N][W], anc[N][W], desc[N][W];
-    u64 divg[N][W];   // division groups, in order
-    T ln[N], ld[N];   // original load
-    T pn[N], pd[N];   // pending load (residual after a split)
-    T xn[N], xd[N];   // W^anc, later per-member exec
-    T rn[N], rd[N];   // apportion remainder (unreduced)
-    T cn[N], cd[N];   // critical-path prefix (lower bound)
+    // Phase-disjoint fields share storage (shared memory decides how many
+    // warps fit on an SM): successors die with p_ends / the backward closure
+    // before the division groups are formed; the original loads die with
+    // p_rank, after which the same words hold the pending loads; the
+    // critical-path prefix dies with p_bounds before apportion remainders.
+    u64 pred[N][W], anc[N][W], desc[N][W];
+    union {
+        u64 succ[N][W];
+        u64 divg[N][W];  // division groups, in order
+    };
+    union {
+        T ln[N];  // original load
+        T pn[N];  // pending load (residual after a split)
+    };
+    union {
+        T ld[N];
+        T pd[N];
+    };
+    T xn[N], xd[N];  // W^anc, later per-member exec
+    union {
+        T cn[N];  // critical-path prefix (lower bound)
+        T rn[N];  // apportion remainder (unreduced)
+    };
+    union {
+        T cd[N];
+        T rd[N];
+    };
     int mmax[N];      // max_parallelism(original load)
     int mq[N];        // apportioned parallelism
     int cap[N];       // min(max_parallelism(pending load), M)
@@ -200,8 +220,6 @@ __device__ __noinline__ int p_load(WarpState<W, T>& S, const int lane, const int
         frac |= l.d != 1;
         S.ln[v] = l.n;
         S.ld[v] = l.d;
-        S.pn[v] = l.n;
-        S.pd[v] = l.d;
         int mp = 1;
         if (a > 0 && b > 0) {
             mp = n_max_par(l, P);
@@ -710,13 +728,17 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
         if (!org.any()) continue;  // fully absorbed by earlier launches
 
         // -- apportion (scheduler.cpp:35-95) over the pending loads
-        RatT<T> Wt{0, 1};
-        for_bits<W>(org, [&](int v) { Wt = q_add(Wt, RatT<T>{S.pn[v], S.pd[v]}); });
-        ovf |= Wt.d == 0;
-        int tot = 0, capsum = 0;
-#pragma unroll 1
-        for (int v = lane; v < n; v += 32) {
-            if (!org.test(v)) continue;
+        RatT<T> R{0, 1};
+        int used = 0, n_mem = 0, bott_pos = 0;
+        const bool single = sizeof(T) < 16 && org.popc() == 1;
+        if (single) {
+            // one pending member (70% of C5 groups): quota = l*M/l = M, so
+            // m = cap = min(m^max, M), no shed/fill, and it is the response
+            int v = 0;
+#pragma unroll
+            for (int k = W - 1; k >= 0; --k) {
+                if (org.w[k]) v = k * 64 + __ffsll(org.w[k]) - 1;
+            }
             const RatT<T> l{S.pn[v], S.pd[v]};
             int cp = n_max_par(l, P);
             if (cp < 0) {
@@ -724,92 +746,125 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
                 cp = 1;
             }
             cp = min(cp, P.M);
-            // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n); floor and remainder
-            const T qn = mulc(mulc(l.n, T(P.M), ovf), Wt.d, ovf);
-            const T qd = mulc(l.d, Wt.n, ovf);
-            const T fl = divw(qn, qd);
-            const long long flc = fl > T(0x7fffffff) ? 0x7fffffffll : (long long)fl;
-            const long long base = max(1ll, min(flc, (long long)cp));
-            S.mq[v] = int(base);
-            S.cap[v] = cp;
-            S.rn[v] = qn - fl * qd;
-            S.rd[v] = qd;
-            tot += int(base);
-            capsum += cp;
-        }
-        tot = __reduce_add_sync(FULL, tot);
-        capsum = __reduce_add_sync(FULL, capsum);
-        __syncwarp();
-        // shed while over M (smallest slowdown exec(m-1), first index wins
-        // ties), else fill up to target (largest exec(m), then larger remainder,
-        // then first index); shedding ends at M >= target, so at most one runs
-        const int target = min(P.M, capsum);
-#pragma unroll 1
-        while (tot > P.M || tot < target) {
-            const bool shed = tot > P.M;
-            Pick<T> c{{0, 1}, {0, 1}, -1};
-            for_bits<W>(org, [&](int v) {
-                const int m = S.mq[v];
-                if (shed ? m <= 1 : m >= S.cap[v]) return;
-                const Pick<T> x{q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, shed ? m - 1 : m, P),
-                                shed ? RatT<T>{0, 1} : RatT<T>{S.rn[v], S.rd[v]}, v};
-                ovf |= x.k1.d == 0;
-                if (pick_better<T>(x, c, shed)) c = x;
-            });
-            if (c.idx < 0) return DS_EINVARIANT;
-            const int step = shed ? -1 : 1;
-            if (lane == 0) S.mq[c.idx] += step;
-            __syncwarp();
-            tot += step;
-        }
-
-        // -- members: exec, response (first strict max), bottleneck
-#pragma unroll 1
-        for (int v = lane; v < n; v += 32) {
-            if (!org.test(v)) continue;
-            const RatT<T> e = n_exec(RatT<T>{S.pn[v], S.pd[v]}, S.mq[v], P);
-            ovf |= e.d == 0;
-            S.xn[v] = e.n;
-            S.xd[v] = e.d;
-        }
-        __syncwarp();
-        RatT<T> R{0, 1};
-        int bott = -1, used = 0, n_mem = 0, bott_pos = 0;
-        for_bits<W>(org, [&](int v) {
-            const RatT<T> e{S.xn[v], S.xd[v]};
-            if (bott < 0 || q_cmp(e, R) > 0) {
-                R = e;
-                bott = v;
-                bott_pos = n_mem;
+            R = n_exec(l, cp, P);
+            ovf |= R.d == 0;
+            used = cp;
+            n_mem = 1;
+            if (DETAIL) {
+                if (lane == 0) {
+                    S.mq[v] = cp;
+                    S.xn[v] = R.n;
+                    S.xd[v] = R.d;
+                }
+                __syncwarp();
             }
-            used += S.mq[v];
-            ++n_mem;
-        });
+        } else {
+            RatT<T> Wt{0, 1};
+            for_bits<W>(org, [&](int v) { Wt = q_add(Wt, RatT<T>{S.pn[v], S.pd[v]}); });
+            ovf |= Wt.d == 0;
+            int tot = 0, capsum = 0;
+#pragma unroll 1
+            for (int v = lane; v < n; v += 32) {
+                if (!org.test(v)) continue;
+                const RatT<T> l{S.pn[v], S.pd[v]};
+                int cp = n_max_par(l, P);
+                if (cp < 0) {
+                    ovf = true;
+                    cp = 1;
+                }
+                cp = min(cp, P.M);
+                // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n); floor and remainder
+                const T qn = mulc(mulc(l.n, T(P.M), ovf), Wt.d, ovf);
+                const T qd = mulc(l.d, Wt.n, ovf);
+                const T fl = divw(qn, qd);
+                const long long flc = fl > T(0x7fffffff) ? 0x7fffffffll : (long long)fl;
+                const long long base = max(1ll, min(flc, (long long)cp));
+                S.mq[v] = int(base);
+                S.cap[v] = cp;
+                S.rn[v] = qn - fl * qd;
+                S.rd[v] = qd;
+                tot += int(base);
+                capsum += cp;
+            }
+            tot = __reduce_add_sync(FULL, tot);
+            capsum = __reduce_add_sync(FULL, capsum);
+            __syncwarp();
+            // shed while over M (smallest slowdown exec(m-1), first index wins
+            // ties), else fill up to target (largest exec(m), then larger remainder,
+            // then first index); shedding ends at M >= target, so at most one runs
+            const int target = min(P.M, capsum);
+#pragma unroll 1
+            while (tot > P.M || tot < target) {
+                const bool shed = tot > P.M;
+                Pick<T> c{{0, 1}, {0, 1}, -1};
+                for_bits<W>(org, [&](int v) {
+                    const int m = S.mq[v];
+                    if (shed ? m <= 1 : m >= S.cap[v]) return;
+                    const Pick<T> x{q_exec_raw(RatT<T>{S.pn[v], S.pd[v]}, shed ? m - 1 : m, P),
+                                    shed ? RatT<T>{0, 1} : RatT<T>{S.rn[v], S.rd[v]}, v};
+                    ovf |= x.k1.d == 0;
+                    if (pick_better<T>(x, c, shed)) c = x;
+                });
+                if (c.idx < 0) return DS_EINVARIANT;
+                const int step = shed ? -1 : 1;
+                if (lane == 0) S.mq[c.idx] += step;
+                __syncwarp();
+                tot += step;
+            }
+
+            // -- members: exec, response (first strict max), bottleneck
+#pragma unroll 1
+            for (int v = lane; v < n; v += 32) {
+                if (!org.test(v)) continue;
+                const RatT<T> e = n_exec(RatT<T>{S.pn[v], S.pd[v]}, S.mq[v], P);
+                ovf |= e.d == 0;
+                S.xn[v] = e.n;
+                S.xd[v] = e.d;
+            }
+            __syncwarp();
+            int bott = -1;
+            for_bits<W>(org, [&](int v) {
+                const RatT<T> e{S.xn[v], S.xd[v]};
+                if (bott < 0 || q_cmp(e, R) > 0) {
+                    R = e;
+                    bott = v;
+                    bott_pos = n_mem;
+                }
+                used += S.mq[v];
+                ++n_mem;
+            });
+        }
         const int spare0 = P.M - used;
 
         // -- candidates (scheduler.cpp:253-280). Concurrency is symmetric, so
-        // c is in the pool iff some pending member is concurrent with c.
-        const Mask<W> pool = ballot_nodes<W>(lane, n, [&](int c) {
-            if (c >= n || G.test(c)) return false;
-            u64 hit = 0;
+        // the pool is the union of the members' concurrent sets minus the
+        // division group (which also removes each member itself).
+        Mask<W> pool;
+        pool.clear();
+        for_bits<W>(org, [&](int v) {
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                u64 con = V.w[k] & ~(S.anc[c][k] | S.desc[c][k]);
-                if ((c >> 6) == k) con &= ~(1ull << (c & 63));
-                hit |= con & org.w[k];
-            }
-            return hit != 0;
+            for (int k = 0; k < W; ++k) pool.w[k] |= V.w[k] & ~(S.anc[v][k] | S.desc[v][k]);
         });
-        const Mask<W> cands = ballot_nodes<W>(lane, n, [&](int c) {
-            if (c >= n || !pool.test(c) || done.test(c)) return false;
-            bool ok = true;
+        Mask<W> avail;
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                ok &= (S.pred[c][k] & pool.w[k]) == 0;   // a source of the pool
-                ok &= (S.pred[c][k] & ~done.w[k]) == 0;  // released: preds done earlier
-            }
-            return ok;
-        });
+        for (int k = 0; k < W; ++k) {
+            pool.w[k] &= ~G.w[k];
+            avail.w[k] = pool.w[k] & ~done.w[k];
+        }
+        Mask<W> cands;
+        cands.clear();
+        if (avail.any() && (DETAIL || spare0 >= 1)) {
+            cands = ballot_nodes<W>(lane, n, [&](int c) {
+                if (c >= n || !avail.test(c)) return false;
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    ok &= (S.pred[c][k] & pool.w[k]) == 0;   // a source of the pool
+                    ok &= (S.pred[c][k] & ~done.w[k]) == 0;  // released: preds done earlier
+                }
+                return ok;
+            });
+        }
 
         // -- launches in rank order (scheduler.cpp:286-330)
         Mask<W> whole;
@@ -918,7 +973,7 @@ __device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane,
 
 // -------------------------------------------------------------- one DAG
 // Returns status; fills S.bn/S.bd and the out-params.
-template <int W, class T, bool DETAIL>
+template <int W, class T, bool DETAIL, bool FRONT = false>
 __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, const int n,
                                            const u64* __restrict__ lnum, const u64* __restrict__ lden,
                                            const u32* __restrict__ edges, const int n_edges, const PlatT<T> P,
@@ -953,11 +1008,30 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     const int n_joins = p_rank<W, T>(S, lane, n, integer);
     if (n_joins < 0) return DS_EOVERFLOW;
     n_div = p_division<W, T, DETAIL>(S, lane, n, n_joins, P.M, det);
+    if (FRONT) return DS_OK;  // p_schedule runs in k1_back
     const long long r = p_schedule<W, T, DETAIL>(S, lane, n, n_div, P, det);
     n_groups = int((r >> 8) & 0xfff);
     n_ent = int(r >> 20);
     return int(r & 0xff);
 }
+
+// Front/back split of the 32-bit W=1 bounds pass. The kernel is instruction-
+// fetch bound (its hot code exceeds the SM's 32 KB L1.5 instruction cache), so
+// the schedule phase runs as its own kernel: k1_front (load .. division)
+// leaves per-node state in HBM (~42 B per node, re-read once), k1_back runs
+// p_schedule over it. Status codes mark the hand-over.
+constexpr int32_t kStPending = -1000;  // front done, schedule pending
+constexpr int32_t kStRetried = -1001;  // queued for a wider tier
+struct K1Handoff {  // SoA over the batch's node index (node_off[d] - node_off[0] + v)
+    u64* pred;
+    u64* anc;
+    u64* desc;
+    u64* divg;       // division group g of DAG d at node slot g
+    u32* ln;         // canonical loads
+    u32* ld;
+    uint16_t* ro;    // rank[v] | order[v] << 8
+    uint16_t* ndiv;  // per DAG
+};
 
 struct K1Args {
     u64 n_dags;
@@ -976,6 +1050,7 @@ struct K1Args {
     u32* retry_count;
     u32* retry2;           // ... and whose 64-bit pass overflowed
     u32* retry2_count;
+    K1Handoff h;           // split mode when h.pred != nullptr (bounds mode only)
 };
 
 template <int W, class T, bool DETAIL>
@@ -1063,6 +1138,125 @@ __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
             continue;
         }
         run_one<W, u32, DETAIL>(S, lane, a, d, nbase, ebase, P, a.retry, a.retry_count);
+    }
+}
+
+// k1_front: the W=1 main pass up to the division, 32-bit words.
+template <bool UNUSED = false>  // a template so both K1 translation units may include it
+__global__ void __launch_bounds__(128) k1_front(const K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
+    const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
+    const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const bool proposed = a.mask & DS_M_PROPOSED;
+#pragma unroll 1
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(a.retry_count + 2, 1u);
+        const u64 d = __shfl_sync(FULL, t, 0);
+        if (d >= a.n_dags) break;
+        const u32 n0 = a.node_off[d] - nbase, e0 = a.edge_off[d] - ebase;
+        const int n = int(a.node_off[d + 1] - nbase - n0);
+        if (n > 64 && n <= DS_MAX_NODES) continue;  // k1_analyse<4>
+        int st = DS_EOVERFLOW, ng = 0, nent = 0, ndiv = 0;
+        if (narrow) {
+            st = analyse_dag<1, u32, false, true>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
+                                                  a.edges + e0, int(a.edge_off[d + 1] - ebase - e0), P, a.mask, ng,
+                                                  DetailOut{}, nent, ndiv);
+        }
+        if (st == DS_EOVERFLOW) {
+            if (lane == 0) {
+                a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+                a.status[d] = kStRetried;
+            }
+            __syncwarp();
+            continue;
+        }
+        const bool pending = st == DS_OK && proposed;
+        int64_t* b = a.bounds + 10 * d;
+        if (lane < 10 && !(pending && lane < 2)) {
+            const int k = lane >> 1;
+            b[lane] = st == DS_OK ? (long long)((lane & 1) ? S.bd[k] : S.bn[k]) : 0;
+        }
+        if (pending) {
+#pragma unroll 1
+            for (int v = lane; v < n; v += 32) {
+                const u32 i = n0 + v;
+                a.h.pred[i] = S.pred[v][0];
+                a.h.anc[i] = S.anc[v][0];
+                a.h.desc[i] = S.desc[v][0];
+                a.h.ln[i] = S.ln[v];
+                a.h.ld[i] = S.ld[v];
+                a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
+                if (v < ndiv) a.h.divg[i] = S.divg[v][0];
+            }
+        }
+        if (lane == 0) {
+            a.status[d] = pending ? kStPending : st;
+            if (pending) a.h.ndiv[d] = uint16_t(ndiv);
+            else if (a.n_groups) a.n_groups[d] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+// k1_back: p_schedule over the state k1_front left behind.
+template <bool UNUSED = false>
+__global__ void __launch_bounds__(128) k1_back(const K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
+    const u32 nbase = a.node_off[0];
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+#pragma unroll 1
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(a.retry_count + 3, 1u);
+        const u64 d = __shfl_sync(FULL, t, 0);
+        if (d >= a.n_dags) break;
+        if (a.status[d] != kStPending) continue;
+        const u32 n0 = a.node_off[d] - nbase;
+        const int n = int(a.node_off[d + 1] - nbase - n0);
+        const int ndiv = a.h.ndiv[d];
+#pragma unroll 1
+        for (int v = lane; v < n; v += 32) {
+            const u32 i = n0 + v;
+            S.pred[v][0] = a.h.pred[i];
+            S.anc[v][0] = a.h.anc[i];
+            S.desc[v][0] = a.h.desc[i];
+            S.pn[v] = a.h.ln[i];
+            S.pd[v] = a.h.ld[i];
+            const uint16_t ro = a.h.ro[i];
+            S.rank[v] = short(ro & 0xff);
+            S.order[v] = short(ro >> 8);
+            S.gen[v] = 0;
+            S.ppart[v] = 0;
+            if (v < ndiv) S.divg[v][0] = a.h.divg[i];
+        }
+        __syncwarp();
+        const long long r = p_schedule<1, u32, false>(S, lane, n, ndiv, P, DetailOut{});
+        const int st = int(r & 0xff);
+        if (st == DS_EOVERFLOW) {
+            if (lane == 0) {
+                a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+                a.status[d] = kStRetried;
+            }
+            __syncwarp();
+            continue;
+        }
+        int64_t* b = a.bounds + 10 * d;
+        if (st == DS_OK) {
+            if (lane < 2) b[lane] = (long long)(lane ? S.bd[DS_BOUND_PROPOSED] : S.bn[DS_BOUND_PROPOSED]);
+        } else if (lane < 10) {
+            b[lane] = 0;
+        }
+        if (lane == 0) {
+            a.status[d] = st;
+            if (a.n_groups) a.n_groups[d] = (unsigned short)((r >> 8) & 0xfff);
+        }
+        __syncwarp();
     }
 }
 

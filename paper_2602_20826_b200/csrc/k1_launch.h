@@ -12,10 +12,31 @@ struct K1Occupancy {
     int grid_small = 0;  // persistent grid of the n <= 64 kernel (CTAs)
     int grid_big = 0;    // n <= 256 kernel
     int grid_retry = 0;  // 128-bit retry kernel
+    int grid_front = 0;  // split bounds pass (k1_front / k1_back)
+    int grid_back = 0;
 };
 
 constexpr int kWarpsSmall = 4;  // WarpState<1,u64> per warp, 4 warps per CTA
 constexpr int kWarpsBig = 1;    // WarpState<4,u64> (~50 KB) per CTA
+
+// Scratch for the front/back split (K1Handoff), carved from one buffer.
+inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
+    return size_t(n_nodes) * (4 * 8 + 2 * 4 + 2) + size_t(n_dags) * 2 + 64;
+}
+inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
+    K1Handoff h;
+    u64* m = static_cast<u64*>(base);
+    h.pred = m;
+    h.anc = m + n_nodes;
+    h.desc = m + 2 * n_nodes;
+    h.divg = m + 3 * n_nodes;
+    h.ln = reinterpret_cast<u32*>(m + 4 * n_nodes);
+    h.ld = h.ln + n_nodes;
+    h.ro = reinterpret_cast<uint16_t*>(h.ld + n_nodes);
+    h.ndiv = h.ro + n_nodes;
+    (void)n_dags;
+    return h;
+}
 
 // Query occupancy once per device and set the dynamic shared-memory limits.
 cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ);

@@ -2,6 +2,8 @@
 // file) and schedule-detail mode (k1_detail.cu defines K1_DETAIL_TU).
 #include "k1_launch.h"
 
+#include <cstdlib>
+
 namespace ds {
 
 namespace {
@@ -34,7 +36,27 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, k1_analyse_retry<DETAIL, u128>, 32, kSmemR128)))
         return e;
     if (o1 < 1 || o4 < 1 || orr < 1) return cudaErrorInvalidConfiguration;
-    occ.grid_small = sms * o1;  // one full wave; warps stride over the DAGs
+    if (!DETAIL) {
+        if ((e = cudaFuncSetAttribute(k1_front<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
+            return e;
+        if ((e = cudaFuncSetAttribute(k1_back<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
+            return e;
+        int of = 0, ob = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k1_front<>, 32 * kWarpsSmall, kSmemSmall)))
+            return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k1_back<>, 32 * kWarpsSmall, kSmemSmall)))
+            return e;
+        if (of < 1 || ob < 1) return cudaErrorInvalidConfiguration;
+        occ.grid_front = sms * of;
+        occ.grid_back = sms * ob;
+    }
+    // one full wave; warps stride over the DAGs. DS_K1_CTAS_PER_SM (tuning
+    // knob) caps the resident CTAs per SM below the occupancy limit.
+    if (const char* env = getenv("DS_K1_CTAS_PER_SM")) {
+        const int c = atoi(env);
+        if (c >= 1 && c < o1) o1 = c;
+    }
+    occ.grid_small = sms * o1;
     occ.grid_big = sms * o4;
     occ.grid_retry = sms * orr;
     return cudaSuccess;
@@ -43,16 +65,22 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
 template <bool DETAIL>
 cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
     if (a.n_dags == 0) return cudaSuccess;
-    // counters, contiguous: [retry, retry2, next DAG for the W=1 kernel, spare]
+    // counters, contiguous: [retry, retry2, next DAG for the W=1 kernel / k1_front<>, k1_back]
     cudaError_t e = cudaMemsetAsync(a.retry_count, 0, 4 * sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
-    const int gs = int(need_small < u64(occ.grid_small) ? need_small : u64(occ.grid_small));
-    k1_analyse<1, DETAIL><<<gs, 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+    auto cap = [&](int g) { return int(need_small < u64(g) ? need_small : u64(g)); };
+    const bool split = !DETAIL && a.h.pred != nullptr;
+    if (split) k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+    else k1_analyse<1, DETAIL><<<cap(occ.grid_small), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (any_big) {
         const int gb = int(a.n_dags < u64(occ.grid_big) ? a.n_dags : u64(occ.grid_big));
         k1_analyse<4, DETAIL><<<gb, 32 * kWarpsBig, kSmemBig, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (split && (a.mask & DS_M_PROPOSED)) {
+        k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
