@@ -182,7 +182,7 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         if (int rc = sl.bounds.ensure(nd * 80)) return rc;
         if (int rc = sl.ngroups.ensure(nd * 2)) return rc;
         if (int rc = sl.retry.ensure(2 * nd * 4)) return rc;  // two retry lists
-        if (int rc = sl.retry_count.ensure(16)) return rc;
+        if (int rc = sl.retry_count.ensure(kK1Counters * 4)) return rc;
         DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
@@ -292,7 +292,7 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     DeviceCtx& ctx = device_ctx(device);
     std::lock_guard<std::mutex> lock(ctx.mu);
     if (int rc = ctx.retry.ensure(2 * batch->n_dags * 4)) return rc;
-    if (int rc = ctx.retry_count.ensure(16)) return rc;
+    if (int rc = ctx.retry_count.ensure(kK1Counters * 4)) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     u32 ends[2];  // node_off[0], node_off[n]: sizes the split pass's scratch
     DS_CUDA(cudaMemcpyAsync(&ends[0], batch->node_off, 4, cudaMemcpyDeviceToHost, s));
@@ -378,7 +378,7 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DetailBuf
     if (int rc = B.grp.ensure(N * sizeof(ds_group_rec))) return rc;
     if (int rc = B.bounds.ensure(n * 80)) return rc;
     if (int rc = B.retry.ensure(2 * n * 4)) return rc;
-    if (int rc = B.retry_count.ensure(8)) return rc;
+    if (int rc = B.retry_count.ensure(kK1Counters * 4)) return rc;
     DS_CUDA(cudaMemset(B.nb.p, 0xff, N * 2));
     DS_CUDA(cudaMemset(B.ndg.p, 0xff, N * 2));
     DS_CUDA(cudaMemset(B.ent.p, 0, 2 * N * sizeof(ds_entity_rec)));
@@ -525,7 +525,7 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     rc = rc ? rc : S->bounds.ensure(n * 80);
     rc = rc ? rc : S->ngroups.ensure(n * 2);
     rc = rc ? rc : S->retry.ensure(2 * n * 4);
-    rc = rc ? rc : S->retry_count.ensure(16);
+    rc = rc ? rc : S->retry_count.ensure(kK1Counters * 4);
     if (rc) return bail(rc);
     K1Args& a = S->args;
     a.n_dags = n;

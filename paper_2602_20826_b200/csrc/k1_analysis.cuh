@@ -571,6 +571,7 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
         V.w[k] = n >= lo + 64 ? ~0ull : (n <= lo ? 0ull : ((1ull << (n - lo)) - 1));
     }
     assigned.clear();
+    const Mask<W> big = ballot_nodes<W>(lane, n, [&](int v) { return v < n && S.mmax[v] >= M; });
     int n_div = 0;
 #pragma unroll 1
     for (int b = 0; b <= n_joins; ++b) {
@@ -628,16 +629,20 @@ __device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const
                 });
                 __syncwarp();
             }
-            // Rule 2: any selected head with m^max >= M -> the max-m^max head alone
-            int mx = 0;
+            // Rule 2: any selected head with m^max >= M -> the max-m^max head
+            // alone (only a question when several heads and an oversized one)
+            Mask<W> sb;
+#pragma unroll
+            for (int k = 0; k < W; ++k) sb.w[k] = sel.w[k] & big.w[k];
+            if (sb.any() && sel.popc() > 1) {
+                int mx = 0;
 #pragma unroll 1
-            for (int v = lane; v < n; v += 32) {
-                if (sel.test(v)) mx = max(mx, S.mmax[v]);
-            }
-            mx = __reduce_max_sync(FULL, mx);
-            if (mx >= M) {
+                for (int v = lane; v < n; v += 32) {
+                    if (sb.test(v)) mx = max(mx, S.mmax[v]);
+                }
+                mx = __reduce_max_sync(FULL, mx);
                 const Mask<W> top = ballot_nodes<W>(lane, n, [&](int v) {
-                    return v < n && sel.test(v) && S.mmax[v] == mx;
+                    return v < n && sb.test(v) && S.mmax[v] == mx;
                 });
                 int pick = -1;
 #pragma unroll
@@ -1004,23 +1009,25 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     if (mask & (DS_M_GREEDY | DS_M_GREEDY_UNAWARE | DS_M_GRAHAM_PARA | DS_M_LOWER)) {
         if ((st = p_bounds<W, T>(S, lane, n, rounds, P, mask)) != DS_OK) return st;
     }
-    if (!((mask & DS_M_PROPOSED) || DETAIL)) return DS_OK;
+    if (FRONT || !((mask & DS_M_PROPOSED) || DETAIL)) return DS_OK;  // FRONT: k1_mid, k1_back go on
     const int n_joins = p_rank<W, T>(S, lane, n, integer);
     if (n_joins < 0) return DS_EOVERFLOW;
     n_div = p_division<W, T, DETAIL>(S, lane, n, n_joins, P.M, det);
-    if (FRONT) return DS_OK;  // p_schedule runs in k1_back
     const long long r = p_schedule<W, T, DETAIL>(S, lane, n, n_div, P, det);
     n_groups = int((r >> 8) & 0xfff);
     n_ent = int(r >> 20);
     return int(r & 0xff);
 }
 
-// Front/back split of the 32-bit W=1 bounds pass. The kernel is instruction-
-// fetch bound (its hot code exceeds the SM's 32 KB L1.5 instruction cache), so
-// the schedule phase runs as its own kernel: k1_front (load .. division)
-// leaves per-node state in HBM (~42 B per node, re-read once), k1_back runs
-// p_schedule over it. Status codes mark the hand-over.
-constexpr int32_t kStPending = -1000;  // front done, schedule pending
+// Three-kernel split of the 32-bit W=1 bounds pass. As one kernel it is
+// instruction-fetch bound (its hot code exceeds the SM's 32 KB L1.5
+// instruction cache; ncu: ~60% of stall samples "no_instructions"), so it runs
+// as k1_front (load, edges, closure, ends, descendants, bounds), k1_mid (ranks,
+// division) and k1_back (schedule), each with a hot loop that fits, over
+// per-node state left in HBM (~42 B per node, written and re-read once).
+// Status codes mark the hand-over.
+constexpr int32_t kStMid = -999;       // k1_front done, k1_mid pending
+constexpr int32_t kStPending = -1000;  // k1_mid done, k1_back pending
 constexpr int32_t kStRetried = -1001;  // queued for a wider tier
 struct K1Handoff {  // SoA over the batch's node index (node_off[d] - node_off[0] + v)
     u64* pred;
@@ -1189,14 +1196,66 @@ __global__ void __launch_bounds__(128) k1_front(const K1Args a) {
                 a.h.desc[i] = S.desc[v][0];
                 a.h.ln[i] = S.ln[v];
                 a.h.ld[i] = S.ld[v];
-                a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
-                if (v < ndiv) a.h.divg[i] = S.divg[v][0];
             }
         }
         if (lane == 0) {
-            a.status[d] = pending ? kStPending : st;
-            if (pending) a.h.ndiv[d] = uint16_t(ndiv);
-            else if (a.n_groups) a.n_groups[d] = 0;
+            a.status[d] = pending ? kStMid : st;
+            if (!pending && a.n_groups) a.n_groups[d] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+// k1_mid: ranks and division over k1_front's state.
+template <bool UNUSED = false>
+__global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
+    const u32 nbase = a.node_off[0];
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+#pragma unroll 1
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(a.retry_count + 3, 1u);
+        const u64 d = __shfl_sync(FULL, t, 0);
+        if (d >= a.n_dags) break;
+        if (a.status[d] != kStMid) continue;
+        const u32 n0 = a.node_off[d] - nbase;
+        const int n = int(a.node_off[d + 1] - nbase - n0);
+        bool integer = true;
+#pragma unroll 1
+        for (int v = lane; v < n; v += 32) {
+            const u32 i = n0 + v;
+            S.pred[v][0] = a.h.pred[i];
+            S.anc[v][0] = a.h.anc[i];
+            const RatT<u32> l{a.h.ln[i], a.h.ld[i]};
+            S.ln[v] = l.n;
+            S.ld[v] = l.d;
+            integer &= l.d == 1;
+            S.mmax[v] = n_max_par(l, P);  // fits: k1_front computed it already
+        }
+        integer = __all_sync(FULL, integer);
+        __syncwarp();
+        const int n_joins = p_rank<1, u32>(S, lane, n, integer);
+        if (n_joins < 0) {
+            if (lane == 0) {
+                a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+                a.status[d] = kStRetried;
+            }
+            __syncwarp();
+            continue;
+        }
+        const int ndiv = p_division<1, u32, false>(S, lane, n, n_joins, P.M, DetailOut{});
+#pragma unroll 1
+        for (int v = lane; v < n; v += 32) {
+            const u32 i = n0 + v;
+            a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
+            if (v < ndiv) a.h.divg[i] = S.divg[v][0];
+        }
+        if (lane == 0) {
+            a.h.ndiv[d] = uint16_t(ndiv);
+            a.status[d] = kStPending;
         }
         __syncwarp();
     }
@@ -1213,7 +1272,7 @@ __global__ void __launch_bounds__(128) k1_back(const K1Args a) {
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
-        if (lane == 0) t = atomicAdd(a.retry_count + 3, 1u);
+        if (lane == 0) t = atomicAdd(a.retry_count + 4, 1u);
         const u64 d = __shfl_sync(FULL, t, 0);
         if (d >= a.n_dags) break;
         if (a.status[d] != kStPending) continue;

@@ -12,12 +12,14 @@ struct K1Occupancy {
     int grid_small = 0;  // persistent grid of the n <= 64 kernel (CTAs)
     int grid_big = 0;    // n <= 256 kernel
     int grid_retry = 0;  // 128-bit retry kernel
-    int grid_front = 0;  // split bounds pass (k1_front / k1_back)
+    int grid_front = 0;  // split bounds pass (k1_front / k1_mid / k1_back)
+    int grid_mid = 0;
     int grid_back = 0;
 };
 
 constexpr int kWarpsSmall = 4;  // WarpState<1,u64> per warp, 4 warps per CTA
 constexpr int kWarpsBig = 1;    // WarpState<4,u64> (~50 KB) per CTA
+constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 bytes)
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {

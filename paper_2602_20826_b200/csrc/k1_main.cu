@@ -39,15 +39,20 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
     if (!DETAIL) {
         if ((e = cudaFuncSetAttribute(k1_front<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
             return e;
+        if ((e = cudaFuncSetAttribute(k1_mid<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
+            return e;
         if ((e = cudaFuncSetAttribute(k1_back<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
             return e;
-        int of = 0, ob = 0;
+        int of = 0, om = 0, ob = 0;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k1_front<>, 32 * kWarpsSmall, kSmemSmall)))
+            return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k1_mid<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k1_back<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
-        if (of < 1 || ob < 1) return cudaErrorInvalidConfiguration;
+        if (of < 1 || om < 1 || ob < 1) return cudaErrorInvalidConfiguration;
         occ.grid_front = sms * of;
+        occ.grid_mid = sms * om;
         occ.grid_back = sms * ob;
     }
     // one full wave; warps stride over the DAGs. DS_K1_CTAS_PER_SM (tuning
@@ -66,7 +71,7 @@ template <bool DETAIL>
 cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
     if (a.n_dags == 0) return cudaSuccess;
     // counters, contiguous: [retry, retry2, next DAG for the W=1 kernel / k1_front<>, k1_back]
-    cudaError_t e = cudaMemsetAsync(a.retry_count, 0, 4 * sizeof(u32), s);
+    cudaError_t e = cudaMemsetAsync(a.retry_count, 0, kK1Counters * sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     auto cap = [&](int g) { return int(need_small < u64(g) ? need_small : u64(g)); };
@@ -80,6 +85,8 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (split && (a.mask & DS_M_PROPOSED)) {
+        k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
         k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
