@@ -115,13 +115,30 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
+def ncu_summary():
+    """profiles/k1_ncu_summary.json: per-kernel figures of the latest
+    `ncu --set full` capture of this command (dram bytes, instructions)."""
     p = os.path.join(ROOT, "profiles", "k1_ncu_summary.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch_per_dag"), d
-    return None, None
+            return json.load(f)
+    return {}
+
+
+def kernel_alg_bytes(name, n, N, E, integer, n_div):
+    """Algorithmic bytes one launch of K1 kernel `name` must move: its inputs
+    read once and its outputs written once. N nodes, E edges,
+    n DAGs, n_div division groups in the batch."""
+    loads = N * (8 if integer else 16)
+    offs = 8 * (n + 1)
+    handoff_masks, handoff_loads = 24 * N, 8 * N
+    if name == "k1_front":   # packed DAGs in; bounds 2..9 + status + the hand-off out
+        return offs + loads + 4 * E + 68 * n + handoff_masks + handoff_loads
+    if name == "k1_mid":     # status + pred/anc + loads in; ranks, division groups, status out
+        return 4 * n + 4 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 2 * n + 4 * n
+    if name == "k1_back":    # status + hand-off in; proposed bound, status, groups out
+        return 4 * n + 4 * n + 2 * n + handoff_masks + handoff_loads + 2 * N + 8 * n_div + 16 * n + 4 * n + 2 * n
+    return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
 
 
 def cpu_baseline_run(batch, kind_pref="ref", target_s=8.0, min_dags=4000, max_dags=200_000):
@@ -283,18 +300,24 @@ def main():
     for _ in range(args.warmup):
         sess.run()
     barrier()
+    per_kernel = {}
     with Clocks(local_rank) as clk:
         barrier()
-        kms = [sess.run() for _ in range(args.steps)]
+        kms = []
+        for _ in range(args.steps):
+            kms.append(sess.run())
+            for k, v in sess.kernel_times().items():  # events between the step's launches
+                per_kernel.setdefault(k, []).append(v)
         barrier()
     dev_ms = max_over_ranks(sum(kms))
     st, bounds, ng = sess.results()
     ok = int((st == 0).sum())
     value = world * n * args.steps / (dev_ms / 1e3)
-    # per step: the n<=64 kernel, the n<=256 kernel when such DAGs exist, and
-    # the 64- and 128-bit retry kernels (each exits at once when nothing was
-    # queued) — the launch list in profiles/r01_launches.csv shows the same
-    launches_per_step = 3 + int(np.any(np.diff(batch.node_off.astype(np.int64)) > 64))
+    # per step: k1_front, k1_mid, k1_back, the n<=256 kernel when such DAGs
+    # exist, and the 64- and 128-bit retry kernels (each exits at once when
+    # nothing was queued) — one event per launch; the ncu launch list in
+    # profiles/ shows the same
+    launches_per_step = len(per_kernel)
 
     # ---------------------------------------------------------------- e2e leg
     # pinned result buffers (the inputs are pinned too: Corpus(pinned=True))
@@ -317,15 +340,28 @@ def main():
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
     h2d = batch.nbytes(with_den=not integer)
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
-    chunks = (n + (1 << 16) - 1) >> 16
+    chunks = -(-n // max(1 << 16, (n + 3) // 4))  # analyze_host's chunking (capi.cu)
 
     # ---------------------------------------------------------------- roofline
+    # dominant kernel of the step, timed live with CUDA events on its stream
     peak, peak_kind = measured_peak()
-    alg_bytes = h2d + d2h  # per launch: read the packed DAGs once, write results once
-    achieved = alg_bytes / (statistics.mean(kms) / 1e3) / 1e9
-    traffic_per_dag, ncu = ncu_traffic()
-    traffic = traffic_per_dag * n if traffic_per_dag else None
-
+    kmean = {k: statistics.mean(v) for k, v in per_kernel.items()}
+    dom = max(kmean, key=kmean.get)
+    N = int(batch.node_off[-1] - batch.node_off[0])
+    E = int(batch.edge_off[-1] - batch.edge_off[0])
+    ncu = ncu_summary()
+    n_div = int(round(ncu.get("division_groups_per_dag", 0) * n))
+    alg_bytes = kernel_alg_bytes(dom, n, N, E, integer, n_div)
+    achieved = alg_bytes / (kmean[dom] / 1e3) / 1e9
+    kn = ncu.get("kernels", {}).get(dom, {})
+    traffic = kn["dram_bytes_per_dag"] * n if kn.get("dram_bytes_per_dag") else None
+    issue = None
+    if kn.get("warp_instructions_per_dag") and ncu.get("sm_clock_mhz"):
+        peak_ips = 4 * ncu["sm_count"] * ncu["sm_clock_mhz"] * 1e6  # 4 schedulers x 1 warp-instr / clk
+        ips = kn["warp_instructions_per_dag"] * n / (kmean[dom] / 1e3)
+        issue = {"achieved": ips, "peak": peak_ips, "unit": "warp-instr/s", "frac": ips / peak_ips,
+                 "source": "instruction count per DAG from the ncu capture in profiles/, time live"}
+    pass_bytes = h2d + d2h
     makespan = None
     if rank == 0 and not args.no_makespan:
         try:
@@ -352,14 +388,18 @@ def main():
                     "matches_device_leg": same},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "k1_analyse<1,false>",
+                         "kernel": dom, "kernel_ms": kmean[dom],
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "note": "integer-latency bound (serial greedy per DAG); HBM is not the limiter"},
+                         "issue": issue,
+                         "pass": {"kernels_ms": kmean, "algorithmic_bytes": pass_bytes,
+                                  "achieved_gbs": pass_bytes / (statistics.mean(kms) / 1e3) / 1e9},
+                         "note": "integer issue-bound (exact-rational greedy per DAG, one warp per DAG); "
+                                 "HBM is not the limiter"},
             "cpu_baseline": cpu,
             "makespan": makespan,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
-            "e2e_gpu_launches": chunks * args.e2e_steps,
+            "e2e_gpu_launches": chunks * launches_per_step * args.e2e_steps,
             "dags_ok": ok, "generation_s": gen_s,
             "kernel_ms": {"mean": statistics.mean(kms), "min": min(kms), "max": max(kms)},
         }

@@ -272,6 +272,10 @@ int ds_session_create(const ds_dag_batch* batch, const ds_platform* platform,
 /* Launches the analysis kernel on the session's stream; returns the kernel's
  * duration in ms measured with CUDA events on that stream. */
 int ds_session_run(void* session, float* kernel_ms);
+/* Per-kernel device times of the last run (CUDA events between consecutive
+ * launches on the session's stream): fills up to `max` entries of ms[] and
+ * names[] (static strings), returns the count, or -status on error. */
+int ds_session_kernel_times(void* session, float* ms, const char** names, int max);
 /* Copies results of the last run back to host buffers. */
 int ds_session_results(void* session, ds_results* out);
 int ds_session_free(void* session);

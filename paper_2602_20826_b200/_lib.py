@@ -43,6 +43,7 @@ def _sig(lib):
         "ds_corpus_view": (C.c_int, [C.c_void_p, P(_abi.ds_dag_batch)]),
         "ds_corpus_free": (None, [C.c_void_p]),
         "ds_corpus_gen_ms": (C.c_float, [C.c_void_p]),
+        "ds_session_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_char_p), C.c_int]),
         "ds_session_create": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                         C.c_int, P(C.c_void_p)]),
         "ds_session_run": (C.c_int, [C.c_void_p, P(C.c_float)]),
@@ -191,6 +192,15 @@ class Session:
         ms = C.c_float(0)
         check(lib().ds_session_run(self.h, C.byref(ms)))
         return ms.value
+
+    def kernel_times(self) -> dict:
+        """{kernel name: ms} of the last run (events between launches)."""
+        ms = (C.c_float * 8)()
+        names = (C.c_char_p * 8)()
+        k = lib().ds_session_kernel_times(self.h, ms, names, 8)
+        if k < 0:
+            check(-k)
+        return {names[i].decode(): float(ms[i]) for i in range(k)}
 
     def results(self):
         st, b, ng, r = _results(self.n)

@@ -226,8 +226,16 @@ struct Session {
     DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
     K1Args args{};
     K1Occupancy occ;
+    K1Marks marks;
     bool any_big = false;
     u64 n_dags = 0;
+    ~Session() {
+        for (int i = 0; i < K1Marks::kMax; ++i)
+            if (marks.ev[i]) cudaEventDestroy(marks.ev[i]);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (s) cudaStreamDestroy(s);
+    }
 };
 
 // Upload a whole batch (rebased offsets) into fresh device buffers.
@@ -513,9 +521,13 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     };
     if (cudaSetDevice(device) != cudaSuccess) return bail(fail(DS_ECUDA, "cudaSetDevice"));
     if (int rc = configure(device, false, S->occ)) return bail(rc);
+    for (int i = 0; i < K1Marks::kMax; ++i) S->marks.ev[i] = nullptr;
     if (cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&S->e0) != cudaSuccess || cudaEventCreate(&S->e1) != cudaSuccess) {
         return bail(fail(DS_ECUDA, "stream/event creation failed"));
+    }
+    for (int i = 0; i < K1Marks::kMax; ++i) {
+        if (cudaEventCreate(&S->marks.ev[i]) != cudaSuccess) return bail(fail(DS_ECUDA, "event creation failed"));
     }
     if (int rc = upload(b, *S, S->s)) return bail(rc);
     const u64 n = b->n_dags;
@@ -552,11 +564,26 @@ int ds_session_run(void* session, float* kernel_ms) {
     auto* S = static_cast<Session*>(session);
     DS_CUDA(cudaSetDevice(S->device));
     DS_CUDA(cudaEventRecord(S->e0, S->s));
-    DS_CUDA(k1_launch(S->args, S->occ, S->any_big, false, S->s));
+    DS_CUDA(k1_launch(S->args, S->occ, S->any_big, false, S->s, &S->marks));
     DS_CUDA(cudaEventRecord(S->e1, S->s));
     DS_CUDA(cudaEventSynchronize(S->e1));
     if (kernel_ms) DS_CUDA(cudaEventElapsedTime(kernel_ms, S->e0, S->e1));
     return DS_OK;
+}
+
+int ds_session_kernel_times(void* session, float* ms, const char** names, int max) {
+    auto* S = static_cast<Session*>(session);
+    if (!S || max < 0) return -fail(DS_EINVAL, "bad argument");
+    const K1Marks& m = S->marks;
+    int k = 0;
+    for (int i = 0; i < m.n && k < max; ++i, ++k) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, i == 0 ? S->e0 : m.ev[i - 1], m.ev[i]) != cudaSuccess)
+            return -fail(DS_ECUDA, "cudaEventElapsedTime");
+        if (ms) ms[k] = t;
+        if (names) names[k] = m.name[i];
+    }
+    return k;
 }
 
 int ds_session_results(void* session, ds_results* out) {
@@ -575,10 +602,7 @@ int ds_session_free(void* session) {
     if (!S) return DS_OK;
     cudaSetDevice(S->device);
     if (S->s) cudaStreamSynchronize(S->s);
-    if (S->e0) cudaEventDestroy(S->e0);
-    if (S->e1) cudaEventDestroy(S->e1);
-    if (S->s) cudaStreamDestroy(S->s);
-    delete S;
+    delete S;  // ~Session releases the stream and events
     return DS_OK;
 }
 

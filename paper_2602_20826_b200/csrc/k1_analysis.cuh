@@ -39,6 +39,12 @@
 namespace ds {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Phases are inlined into their kernel: each kernel calls each phase once, and
+// inlined the compiler sees that WarpState lives in shared memory (direct
+// LDS/STS addressing instead of generic loads through a pointer argument).
+// The rational primitives stay out of line (rat.cuh) — they have many sites.
+#define K1_PHASE __device__ __forceinline__
 constexpr int kFlatPath = 1 << 16;  // p_closure flag: every lower-bound weight is t_min
 
 template <int W, class T>
@@ -196,7 +202,7 @@ struct DetailOut {
 // dag.cpp:35-41 (load >= min_load; min_load = t_min on this path).
 // Returns status | (integer_loads << 8).
 template <int W, class T>
-__device__ __noinline__ int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* __restrict__ lnum,
+K1_PHASE int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* __restrict__ lnum,
                                    const u64* __restrict__ lden, const PlatT<T> P) {
     bool bad_load = false, bad_arg = false, frac = false, ovf = false;
 #pragma unroll 1
@@ -245,7 +251,7 @@ __device__ __noinline__ int p_load(WarpState<W, T>& S, const int lane, const int
 // --------------------------------------------------------------- phase: edges
 // dag.cpp:48-67: checked in sorted (from, to) order; the first failure wins.
 template <int W, class T>
-__device__ __noinline__ int p_edges(WarpState<W, T>& S, const int lane, const int n, const u32* __restrict__ edges,
+K1_PHASE int p_edges(WarpState<W, T>& S, const int lane, const int n, const u32* __restrict__ edges,
                                     const int n_edges) {
     u32 first_bad = 0xffffffffu;
     int bad_kind = 0;
@@ -278,7 +284,7 @@ __device__ __noinline__ int p_edges(WarpState<W, T>& S, const int lane, const in
 // lower_bound (analysis.cpp:11-24, 72-81). Returns rounds, or -1 on a cycle,
 // or -2 on overflow.
 template <int W, class T, bool FWD>
-__device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const int n, bool lower,
+K1_PHASE int p_closure(WarpState<W, T>& S, const int lane, const int n, bool lower,
                                       const PlatT<T> P) {
     bool ovf = false;
     bool flat = FWD && lower;  // every weight is t_min: the path is (hop length) x t_min
@@ -350,7 +356,7 @@ __device__ __noinline__ int p_closure(WarpState<W, T>& S, const int lane, const 
 // desc[v] = { u : v in anc[u] }. One broadcast shared-memory read per node and
 // two bit tests per lane replace the reverse Kahn rounds (dag.cpp:119-124).
 template <class T>
-__device__ __noinline__ void p_desc_transpose(WarpState<1, T>& S, const int lane, const int n) {
+K1_PHASE void p_desc_transpose(WarpState<1, T>& S, const int lane, const int n) {
     u64 lo = 0, hi = 0;  // desc of nodes lane and lane + 32
 #pragma unroll 4
     for (int u = 0; u < n; ++u) {
@@ -365,7 +371,7 @@ __device__ __noinline__ void p_desc_transpose(WarpState<1, T>& S, const int lane
 
 // dag.cpp:97-108: exactly one source and one sink.
 template <int W, class T>
-__device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int n) {
+K1_PHASE int p_ends(WarpState<W, T>& S, const int lane, const int n) {
     const Mask<W> src = ballot_nodes<W>(lane, n, [&](int v) {
         if (v >= n) return false;
         u64 a = 0;
@@ -388,7 +394,7 @@ __device__ __noinline__ int p_ends(WarpState<W, T>& S, const int lane, const int
 // ------------------------------------------------------------- phase: bounds
 // analysis.cpp:40-81 — greedy, greedy_unaware, graham_para, lower_bound.
 template <int W, class T>
-__device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const int n, const int closure,
+K1_PHASE int p_bounds(WarpState<W, T>& S, const int lane, const int n, const int closure,
                                      const PlatT<T> P, const u32 mask) {
     const int rounds = closure & (kFlatPath - 1);
     const bool flat = closure & kFlatPath;
@@ -482,7 +488,7 @@ __device__ __noinline__ int p_bounds(WarpState<W, T>& S, const int lane, const i
 // (scheduler.cpp:275-280); joins in (W^anc asc, id asc) (dag.cpp:218-230).
 // Returns the join count, or -1 on overflow.
 template <int W, class T>
-__device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int n, const bool integer) {
+K1_PHASE int p_rank(WarpState<W, T>& S, const int lane, const int n, const bool integer) {
     bool ovf = false;
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) {
@@ -562,7 +568,7 @@ __device__ __noinline__ int p_rank(WarpState<W, T>& S, const int lane, const int
 // ----------------------------------------------------------- phase: division
 // division.cpp:10-30 blocks in join order + residual; :67-126 groups.
 template <int W, class T, bool DETAIL>
-__device__ __noinline__ int p_division(WarpState<W, T>& S, const int lane, const int n, const int n_joins,
+K1_PHASE int p_division(WarpState<W, T>& S, const int lane, const int n, const int n_joins,
                                        const int M, DetailOut det) {
     Mask<W> V, assigned;
 #pragma unroll
@@ -711,7 +717,7 @@ __device__ __forceinline__ bool pick_better(const Pick<T>& a, const Pick<T>& b, 
 // scheduler.cpp:214-359, one executed group per non-absorbed division group.
 // Returns status | (n_groups << 8) | (n_entities << 20).
 template <int W, class T, bool DETAIL>
-__device__ __noinline__ long long p_schedule(WarpState<W, T>& S, const int lane, const int n, const int n_div,
+K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, const int n_div,
                                              const PlatT<T> P, DetailOut det) {
     bool ovf = false;
     Mask<W> V;

@@ -43,8 +43,18 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
 // Query occupancy once per device and set the dynamic shared-memory limits.
 cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ);
 
+// Optional per-launch markers: an event recorded after each kernel launch
+// (bench.py times the kernels one by one inside the timed region).
+struct K1Marks {
+    static constexpr int kMax = 8;
+    cudaEvent_t ev[kMax];
+    const char* name[kMax];
+    int n = 0;
+};
+
 // Launch the main pass(es) and the 128-bit retry pass on `s`. `a.retry` and
 // `a.retry_count` must point to device scratch (count zeroed here).
-cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s);
+cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s,
+                      K1Marks* marks = nullptr);
 
 }  // namespace ds

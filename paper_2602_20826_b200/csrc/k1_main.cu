@@ -68,51 +68,67 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
 }
 
 template <bool DETAIL>
-cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
+cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* marks) {
+    if (marks) marks->n = 0;
     if (a.n_dags == 0) return cudaSuccess;
+    int mark_i = 0;
+    auto mark = [&](const char* name) -> cudaError_t {
+        cudaError_t err = cudaGetLastError();
+        if (err != cudaSuccess || !marks || mark_i >= K1Marks::kMax) return err;
+        marks->name[mark_i] = name;
+        err = cudaEventRecord(marks->ev[mark_i++], s);
+        marks->n = mark_i;
+        return err;
+    };
     // counters, contiguous: [retry, retry2, next DAG for the W=1 kernel / k1_front<>, k1_back]
     cudaError_t e = cudaMemsetAsync(a.retry_count, 0, kK1Counters * sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     auto cap = [&](int g) { return int(need_small < u64(g) ? need_small : u64(g)); };
     const bool split = !DETAIL && a.h.pred != nullptr;
-    if (split) k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
-    else k1_analyse<1, DETAIL><<<cap(occ.grid_small), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (split) {
+        k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        if ((e = mark("k1_front")) != cudaSuccess) return e;
+    } else {
+        k1_analyse<1, DETAIL><<<cap(occ.grid_small), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        if ((e = mark("k1_analyse<1>")) != cudaSuccess) return e;
+    }
     if (any_big) {
         const int gb = int(a.n_dags < u64(occ.grid_big) ? a.n_dags : u64(occ.grid_big));
         k1_analyse<4, DETAIL><<<gb, 32 * kWarpsBig, kSmemBig, s>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = mark("k1_analyse<4>")) != cudaSuccess) return e;
     }
     if (split && (a.mask & DS_M_PROPOSED)) {
         k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = mark("k1_mid")) != cudaSuccess) return e;
         k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = mark("k1_back")) != cudaSuccess) return e;
     }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
     // nothing queued each kernel reads the count and exits
     const int gr = int(a.n_dags < u64(occ.grid_retry) ? a.n_dags : u64(occ.grid_retry));
     k1_analyse_retry<DETAIL, u64><<<gr, 32, kSmemR64, s>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = mark("k1_analyse_retry<u64>")) != cudaSuccess) return e;
     k1_analyse_retry<DETAIL, u128><<<gr, 32, kSmemR128, s>>>(a);
-    return cudaGetLastError();
+    if ((e = mark("k1_analyse_retry<u128>")) != cudaSuccess) return e;
+    return cudaSuccess;
 }
 
 #ifndef K1_DETAIL_TU
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ);
-cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s);
+cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* m);
 
 cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ) {
     return detail ? k1_configure_detail(device, occ) : k1_configure_t<false>(device, occ);
 }
-cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s) {
-    return detail ? k1_launch_detail(a, occ, any_big, s) : k1_launch_t<false>(a, occ, any_big, s);
+cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s,
+                      K1Marks* marks) {
+    return detail ? k1_launch_detail(a, occ, any_big, s, marks) : k1_launch_t<false>(a, occ, any_big, s, marks);
 }
 #else
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ) { return k1_configure_t<true>(device, occ); }
-cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s) {
-    return k1_launch_t<true>(a, occ, any_big, s);
+cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* m) {
+    return k1_launch_t<true>(a, occ, any_big, s, m);
 }
 #endif
 

@@ -12,7 +12,8 @@ s = _lib.Session(c.batch(), 148)
 for _ in range(3): s.run()
 t = sorted(s.run() for _ in range(5))
 st, b, ng = s.results()
-print(f"{t[2]:.3f} ms  ok={(st == 0).mean():.4f} bsum={int(b[:, 0].sum())}")
+kt = {k: round(v, 3) for k, v in s.kernel_times().items()}
+print(f"{t[2]:.3f} ms  ok={(st == 0).mean():.4f} bsum={int(b[:, 0].sum())} {kt}")
 '''
 for setting in sys.argv[1:]:
     env = dict(os.environ)
