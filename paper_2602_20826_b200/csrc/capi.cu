@@ -148,6 +148,7 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 16;  // >= one wave of warps, small enough to pipeline
+constexpr u64 kDefaultChunks = 8;   // DS_CHUNKS overrides (tuning knob)
 
 int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
     DS_CUDA(cudaSetDevice(device));
@@ -160,9 +161,14 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         ctx.init = true;
     }
     const u64 n = b->n_dags;
-    // ~4 chunks: enough to hide the copies behind the analysis, few enough
+    // a few chunks: enough to hide the copies behind the analysis, few enough
     // that the per-launch tail (uneven per-DAG cost) is paid rarely
-    const u64 chunk = std::max<u64>(kChunk, (n + 3) / 4);
+    static const u64 n_chunks = [] {
+        const char* e = getenv("DS_CHUNKS");
+        const long v = e ? atol(e) : 0;
+        return u64(v >= 1 && v <= 64 ? v : kDefaultChunks);
+    }();
+    const u64 chunk = std::max<u64>(kChunk, (n + n_chunks - 1) / n_chunks);
     for (u64 lo = 0, c = 0; lo < n; lo += chunk, ++c) {
         const u64 hi = std::min(n, lo + chunk), nd = hi - lo;
         Slot& sl = ctx.slot[c % 3];

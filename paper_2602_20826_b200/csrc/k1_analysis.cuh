@@ -144,13 +144,28 @@ __device__ __forceinline__ Mask<W> ballot_nodes(int lane, int n, Pred pred) {
     return r;
 }
 
-// Set bits of a uniform mask, ascending.
+// Set bits of a uniform mask, ascending. Walks each word as two 32-bit
+// halves (one body instantiation): 32-bit find-first-set and clear-lowest
+// take half the instructions of their 64-bit forms, and most DAGs have their
+// nodes in the low half.
 template <int W, class F>
 __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
+        u32 lo = u32(m.w[k]), hi = u32(m.w[k] >> 32);
+        int base = k * 64;
 #pragma unroll 1
-        for (u64 x = m.w[k]; x; x &= x - 1) f(k * 64 + __ffsll(x) - 1);
+        for (;;) {
+            if (!lo) {
+                if (!hi) break;
+                lo = hi;
+                hi = 0;
+                base = k * 64 + 32;
+            }
+            const int b = base + __ffs(lo) - 1;
+            lo &= lo - 1;
+            f(b);
+        }
     }
 }
 
