@@ -1171,7 +1171,7 @@ __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
 
 // k1_front: the W=1 main pass up to the division, 32-bit words.
 template <bool UNUSED = false>  // a template so both K1 translation units may include it
-__global__ void __launch_bounds__(128) k1_front(const K1Args a) {
+__global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
 
 // k1_back: p_schedule over the state k1_front left behind.
 template <bool UNUSED = false>
-__global__ void __launch_bounds__(128) k1_back(const K1Args a) {
+__global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
