@@ -141,7 +141,7 @@ def kernel_alg_bytes(name, n, N, E, integer, n_div):
     return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
 
 
-def cpu_baseline_run(batch, kind_pref="ref", target_s=8.0, min_dags=4000, max_dags=200_000):
+def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_dags=1_000_000):
     """Time the reference CPU path on a bounded sample of the same workload."""
     from oracle import bindings
     from paper_2602_20826_b200 import _abi
@@ -340,7 +340,8 @@ def main():
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
     h2d = batch.nbytes(with_den=not integer)
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
-    chunks = -(-n // max(1 << 16, (n + 3) // 4))  # analyze_host's chunking (capi.cu)
+    n_chunks = int(os.environ.get("DS_CHUNKS", "8"))  # analyze_host's chunking (capi.cu)
+    chunks = -(-n // max(1 << 16, -(-n // n_chunks)))
 
     # ---------------------------------------------------------------- roofline
     # dominant kernel of the step, timed live with CUDA events on its stream
