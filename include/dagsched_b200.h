@@ -253,6 +253,33 @@ int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platfor
 int ds_schedule_batch(const ds_dag_batch* batch, const ds_platform* platform,
                       ds_scheme_out* out, int device);
 
+/* ------------------------------------------------ greedy simulation (K6) */
+/* simulate_greedy (simulator.cpp:96-190) for every DAG of a batch, `runs`
+ * times each: run r dispatches with DispatchPolicy `policy` (0 fifo, 1 random)
+ * seeded policy_seed + r (run_benchmarks' convention, experiment.cpp:271-276);
+ * durations are exec_time(load, min(m^max, M)) times the TimeModel factor
+ * (scaled: uniform on the 1/1024 grid of [scale_min, scale_max], generator
+ * seeded time_seed, identical for every run). */
+typedef struct ds_greedy_cfg {
+    int32_t policy;
+    int32_t runs;
+    uint64_t policy_seed;
+    int32_t scaled;   /* TimeModel::Kind: 0 worst_case, 1 scaled */
+    int32_t reserved;
+    uint64_t time_seed;
+    int64_t scale_min_num, scale_min_den, scale_max_num, scale_max_den;
+} ds_greedy_cfg;
+
+/* Host pointers. status[n*runs], makespan[n*runs*2] (num, den); events
+ * (optional, NULL to skip) [N*runs*4]: per node and run start num/den, finish
+ * num/den (index (node_off[d] - node_off[0] + v) * runs + r). Exact rationals
+ * (64-bit words, 128-bit redo on overflow); DS_EOVERFLOW where a value leaves
+ * int64. DAGs must satisfy DagTask::make (one source; edges as in the batch
+ * format, duplicates collapse). */
+int ds_simulate_greedy_batch(const ds_dag_batch* batch, const ds_platform* platform,
+                             const ds_greedy_cfg* cfg, int32_t* status, int64_t* makespan,
+                             int64_t* events, int device);
+
 /* Corpus generation — replaces generate_corpus (generator.cpp:98-108) with
  * identical RNG call order: on the host, parallel over seeds, or with
  * DS_F_GPU_GENERATE on the device (one thread per DAG, K5). The handle owns

@@ -187,3 +187,84 @@ def ref_run_experiment(sweep: str, values, sm_count: int, corpus_size: int,
         return C.string_at(ptr).decode()
     finally:
         chk._f["free"](ptr)
+
+
+def _text(chk, ptr) -> str:
+    if not ptr:
+        raise RuntimeError(chk.error())
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        chk._f["free"](ptr)
+
+
+def _tm(scaled, smin, smax):
+    smin, smax = Fraction(smin), Fraction(smax)
+    return (int(bool(scaled)), smin.numerator, smin.denominator, smax.numerator, smax.denominator)
+
+
+def ref_sim_greedy(corpus: Corpus, sm_count: int, runs: int, policy: str = "random", policy_seed: int = 0,
+                   scaled: bool = False, time_seed: int = 0, scale_min=1, scale_max=1, t_min=1):
+    """simulate_greedy per DAG x run (policy seed policy_seed + r) -> (status[n, runs], makespan[n, runs, 2])."""
+    chk = corpus.chk
+    f = chk.lib.ref_sim_greedy
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.POINTER(_abi.ds_platform), C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_uint64,
+                  C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+    st = np.zeros((corpus.n_dags, runs), np.int32)
+    mk = np.zeros((corpus.n_dags, runs, 2), np.int64)
+    sc, a, b, c, d = _tm(scaled, scale_min, scale_max)
+    pl = platform(sm_count, t_min)
+    f(corpus.h, C.byref(pl), int(policy == "random"), policy_seed, runs, sc, time_seed, a, b, c, d,
+      st.ctypes.data, mk.ctypes.data)
+    return st, mk
+
+
+def ref_sim_greedy_trace(corpus: Corpus, d: int, sm_count: int, policy: str = "random", policy_seed: int = 0,
+                         scaled: bool = False, time_seed: int = 0, scale_min=1, scale_max=1, t_min=1) -> str:
+    chk = corpus.chk
+    f = chk.lib.ref_sim_greedy_trace
+    f.restype = C.c_void_p
+    f.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(_abi.ds_platform), C.c_int, C.c_uint64, C.c_int, C.c_uint64,
+                  C.c_int64, C.c_int64, C.c_int64, C.c_int64]
+    sc, a, b, c, e = _tm(scaled, scale_min, scale_max)
+    pl = platform(sm_count, t_min)
+    return _text(chk, f(corpus.h, d, C.byref(pl), int(policy == "random"), policy_seed, sc, time_seed, a, b, c, e))
+
+
+def ref_sim_scheme_trace(corpus: Corpus, d: int, sm_count: int, scaled: bool = False, time_seed: int = 0,
+                         scale_min=1, scale_max=1, t_min=1) -> str:
+    chk = corpus.chk
+    f = chk.lib.ref_sim_scheme_trace
+    f.restype = C.c_void_p
+    f.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(_abi.ds_platform), C.c_int, C.c_uint64, C.c_int64, C.c_int64,
+                  C.c_int64, C.c_int64]
+    sc, a, b, c, e = _tm(scaled, scale_min, scale_max)
+    pl = platform(sm_count, t_min)
+    return _text(chk, f(corpus.h, d, C.byref(pl), sc, time_seed, a, b, c, e))
+
+
+def ref_task_roundtrip(text: str, min_load=1, seed=None):
+    """write_task(read_task(text, min_load)) -> (status, text or None)."""
+    chk = Checker("ref")
+    f = chk.lib.ref_task_roundtrip
+    f.restype = C.c_void_p
+    f.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int, C.c_uint64, C.POINTER(C.c_int32)]
+    m = Fraction(min_load)
+    st = C.c_int32(0)
+    p = f(text.encode(), m.numerator, m.denominator, int(seed is not None), int(seed or 0), C.byref(st))
+    if not p:
+        return int(st.value), None
+    return int(st.value), _text(chk, p)
+
+
+def ref_run_benchmarks(paths, sm_counts, avg_loads, greedy_runs: int, seed: int) -> str:
+    """write_bench_table(run_benchmarks(...)) -> CSV text."""
+    chk = Checker("ref")
+    f = chk.lib.ref_run_benchmarks
+    f.restype = C.c_void_p
+    f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint64]
+    arr = (C.c_char_p * len(paths))(*[p.encode() for p in paths])
+    sms = np.asarray(sm_counts, np.int32)
+    avg = np.asarray(avg_loads, np.int64)
+    return _text(chk, f(arr, len(paths), sms.ctypes.data, len(sms), avg.ctypes.data, len(avg), greedy_runs, seed))

@@ -62,6 +62,23 @@ int ref_run_validation(const ds_gen_config* cfg, int corpus_size, const ds_platf
 char* ref_run_experiment(char sweep, const long long* values, int n_values, const ds_gen_config* base,
                          const ds_platform* plat, int corpus_size, uint32_t methods, int normalize_to);
 
+/* simulate_greedy (simulator.cpp:96-190) per DAG of the handle, `runs` times
+ * with policy seed policy_seed + r: status[n*runs], makespan[n*runs*2]. */
+int ref_sim_greedy(void* h, const ds_platform* p, int policy, uint64_t policy_seed, int runs, int scaled,
+                   uint64_t time_seed, int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d,
+                   int32_t* status, int64_t* makespan);
+/* write_trace(simulate_greedy(...)) / write_trace(simulate_scheme(schedule(...))) for DAG d. */
+char* ref_sim_greedy_trace(void* h, uint64_t d, const ds_platform* p, int policy, uint64_t policy_seed, int scaled,
+                           uint64_t time_seed, int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d);
+char* ref_sim_scheme_trace(void* h, uint64_t d, const ds_platform* p, int scaled, uint64_t time_seed,
+                           int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d);
+/* write_task(read_task(json, min_load)) (task_io.cpp:40-91); NULL + *status on failure. */
+char* ref_task_roundtrip(const char* json, int64_t min_n, int64_t min_d, int has_seed, uint64_t seed,
+                         int32_t* status);
+/* write_bench_table(run_benchmarks(...)) (experiment.cpp:242-307). */
+char* ref_run_benchmarks(const char* const* paths, int n_paths, const int* sms, int n_sms, const long long* avgs,
+                         int n_avgs, int greedy_runs, uint64_t seed);
+
 #undef ORACLE_DECLARE
 
 #ifdef __cplusplus

@@ -354,3 +354,122 @@ extern "C" char* ref_run_experiment(char sweep, const long long* values, int n_v
     });
     return st == DS_OK ? dup(text) : nullptr;
 }
+
+// ---------------------------------------------------------------------------
+// Simulator, task I/O and run_benchmarks (simulator.cpp, task_io.cpp,
+// experiment.cpp:242-307), through the reference's own functions.
+#include "dagsched/simulator.hpp"
+
+#include <fstream>
+
+namespace {
+TimeModel time_model(int scaled, uint64_t seed, int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d) {
+    TimeModel t;
+    t.kind = scaled ? TimeModel::Kind::scaled : TimeModel::Kind::worst_case;
+    t.seed = seed;
+    if (scaled) {
+        t.scale_min = rat(smin_n, smin_d);
+        t.scale_max = rat(smax_n, smax_d);
+    }
+    return t;
+}
+}  // namespace
+
+extern "C" int ref_sim_greedy(void* h, const ds_platform* p, int policy, uint64_t policy_seed, int runs, int scaled,
+                              uint64_t time_seed, int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d,
+                              int32_t* status, int64_t* makespan) {
+    auto* c = static_cast<Corpus*>(h);
+    for (uint64_t d = 0; d < c->n_dags; ++d) {
+        for (int r = 0; r < runs; ++r) {
+            status[d * runs + r] = DS_EINVAL;
+            makespan[2 * (d * runs + r)] = makespan[2 * (d * runs + r) + 1] = 0;
+        }
+    }
+    for (std::size_t i = 0; i < c->tasks.size(); ++i) {
+        const uint64_t d = c->index[i];
+        for (int r = 0; r < runs; ++r) {
+            SimTrace tr;
+            int st = guarded([&] {
+                SimConfig cfg;
+                cfg.platform = platform_of(p);
+                cfg.mode = SimMode::greedy;
+                cfg.policy = policy ? DispatchPolicy::random : DispatchPolicy::fifo;
+                cfg.policy_seed = policy_seed + uint64_t(r);
+                cfg.time_model = time_model(scaled, time_seed, smin_n, smin_d, smax_n, smax_d);
+                tr = simulate_greedy(c->tasks[i], cfg);
+            });
+            if (st == DS_OK && !put(tr.makespan, makespan + 2 * (d * runs + r))) st = DS_EOVERFLOW;
+            status[d * runs + r] = st;
+        }
+    }
+    return DS_OK;
+}
+
+extern "C" char* ref_sim_greedy_trace(void* h, uint64_t d, const ds_platform* p, int policy, uint64_t policy_seed,
+                                      int scaled, uint64_t time_seed, int64_t smin_n, int64_t smin_d, int64_t smax_n,
+                                      int64_t smax_d) {
+    auto* c = static_cast<Corpus*>(h);
+    std::string text;
+    int st = guarded([&] {
+        SimConfig cfg;
+        cfg.platform = platform_of(p);
+        cfg.mode = SimMode::greedy;
+        cfg.policy = policy ? DispatchPolicy::random : DispatchPolicy::fifo;
+        cfg.policy_seed = policy_seed;
+        cfg.time_model = time_model(scaled, time_seed, smin_n, smin_d, smax_n, smax_d);
+        std::ostringstream out;
+        write_trace(simulate_greedy(c->tasks.at(d), cfg), out);
+        text = out.str();
+    });
+    return st == DS_OK ? dup(text) : nullptr;
+}
+
+extern "C" char* ref_sim_scheme_trace(void* h, uint64_t d, const ds_platform* p, int scaled, uint64_t time_seed,
+                                      int64_t smin_n, int64_t smin_d, int64_t smax_n, int64_t smax_d) {
+    auto* c = static_cast<Corpus*>(h);
+    std::string text;
+    int st = guarded([&] {
+        SimConfig cfg;
+        cfg.platform = platform_of(p);
+        cfg.mode = SimMode::scheme;
+        cfg.time_model = time_model(scaled, time_seed, smin_n, smin_d, smax_n, smax_d);
+        const DagTask& t = c->tasks.at(d);
+        const ScheduleScheme sch = schedule(t, cfg.platform);
+        SimTrace tr = simulate_scheme(t, sch, cfg);
+        check_precedence(tr, sch);
+        std::ostringstream out;
+        write_trace(tr, out);
+        text = out.str();
+    });
+    return st == DS_OK ? dup(text) : nullptr;
+}
+
+// read_task + write_task round trip; *status gets the DS code of read_task's failure
+extern "C" char* ref_task_roundtrip(const char* json, int64_t min_n, int64_t min_d, int has_seed, uint64_t seed,
+                                    int32_t* status) {
+    std::string text;
+    int st = guarded([&] {
+        std::istringstream in(json);
+        DagTask t = read_task(in, rat(min_n, min_d));
+        std::ostringstream out;
+        if (has_seed) write_task(t, out, seed);
+        else write_task(t, out);
+        text = out.str();
+    });
+    if (status) *status = st;
+    return st == DS_OK ? dup(text) : nullptr;
+}
+
+extern "C" char* ref_run_benchmarks(const char* const* paths, int n_paths, const int* sms, int n_sms,
+                                    const long long* avgs, int n_avgs, int greedy_runs, uint64_t seed) {
+    std::string text;
+    int st = guarded([&] {
+        std::vector<std::string> ps(paths, paths + n_paths);
+        std::vector<int> ms(sms, sms + n_sms);
+        std::vector<long long> as(avgs, avgs + n_avgs);
+        std::ostringstream out;
+        write_bench_table(run_benchmarks(ps, ms, as, greedy_runs, seed), out);
+        text = out.str();
+    });
+    return st == DS_OK ? dup(text) : nullptr;
+}

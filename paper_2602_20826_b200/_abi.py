@@ -29,6 +29,7 @@ DS_MAX_NODES = 256
 
 DS_BOUND_PROPOSED, DS_BOUND_GREEDY, DS_BOUND_GREEDY_UNAWARE, DS_BOUND_GRAHAM_PARA, DS_BOUND_LOWER = range(5)
 BOUND_NAMES = ("proposed", "greedy", "greedy_unaware", "graham_para", "lower")
+DS_M_PROPOSED, DS_M_GREEDY, DS_M_GREEDY_UNAWARE, DS_M_GRAHAM_PARA, DS_M_LOWER = 1, 2, 4, 8, 16
 DS_M_ALL = 0x1F
 DS_F_DEVICE_PTRS = 1
 DS_F_PINNED = 2
@@ -98,3 +99,9 @@ class ds_scheme_out(C.Structure):
 class ds_validation(C.Structure):
     _fields_ = [("tasks", C.c_int64), ("runs", C.c_int64), ("violations", C.c_int64),
                 ("mean_tightness_worst", C.c_double), ("mean_tightness_scaled", C.c_double)]
+
+
+class ds_greedy_cfg(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("runs", C.c_int32), ("policy_seed", C.c_uint64), ("scaled", C.c_int32),
+                ("reserved", C.c_int32), ("time_seed", C.c_uint64), ("scale_min_num", C.c_int64),
+                ("scale_min_den", C.c_int64), ("scale_max_num", C.c_int64), ("scale_max_den", C.c_int64)]

@@ -43,6 +43,8 @@ def _sig(lib):
         "ds_corpus_view": (C.c_int, [C.c_void_p, P(_abi.ds_dag_batch)]),
         "ds_corpus_free": (None, [C.c_void_p]),
         "ds_corpus_gen_ms": (C.c_float, [C.c_void_p]),
+        "ds_simulate_greedy_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), P(_abi.ds_greedy_cfg),
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
         "ds_session_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_char_p), C.c_int]),
         "ds_session_create": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                         C.c_int, P(C.c_void_p)]),
