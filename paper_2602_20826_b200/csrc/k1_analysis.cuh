@@ -243,7 +243,7 @@ K1_PHASE int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* 
         S.ld[v] = l.d;
         int mp = 1;
         if (a > 0 && b > 0) {
-            mp = n_max_par(l, P);
+            mp = q_max_par(l, P);
             if (mp < 0) ovf = true;
         }
         S.mmax[v] = mp;
@@ -766,13 +766,13 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
                 if (org.w[k]) v = k * 64 + __ffsll(org.w[k]) - 1;
             }
             const RatT<T> l{S.pn[v], S.pd[v]};
-            int cp = n_max_par(l, P);
+            int cp = q_max_par(l, P);
             if (cp < 0) {
                 ovf = true;
                 cp = 1;
             }
             cp = min(cp, P.M);
-            R = n_exec(l, cp, P);
+            R = q_exec(l, cp, P);
             ovf |= R.d == 0;
             used = cp;
             n_mem = 1;
@@ -793,7 +793,7 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
             for (int v = lane; v < n; v += 32) {
                 if (!org.test(v)) continue;
                 const RatT<T> l{S.pn[v], S.pd[v]};
-                int cp = n_max_par(l, P);
+                int cp = q_max_par(l, P);
                 if (cp < 0) {
                     ovf = true;
                     cp = 1;
@@ -842,7 +842,7 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
 #pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 if (!org.test(v)) continue;
-                const RatT<T> e = n_exec(RatT<T>{S.pn[v], S.pd[v]}, S.mq[v], P);
+                const RatT<T> e = q_exec(RatT<T>{S.pn[v], S.pd[v]}, S.mq[v], P);
                 ovf |= e.d == 0;
                 S.xn[v] = e.n;
                 S.xd[v] = e.d;
@@ -916,13 +916,13 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
                 }
                 const int c = S.order[r];
                 const RatT<T> l{S.pn[c], S.pd[c]};
-                int mp = n_max_par(l, P);
+                int mp = q_max_par(l, P);
                 if (mp < 0) {
                     ovf = true;
                     mp = 1;
                 }
                 const int mc = min(mp, spare);
-                const RatT<T> dur = n_exec(l, mc, P);
+                const RatT<T> dur = q_exec(l, mc, P);
                 ovf |= dur.d == 0;
                 if (q_cmp(dur, R) <= 0) {
                     if (DETAIL && lane == 0) {
@@ -1254,7 +1254,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
             S.ln[v] = l.n;
             S.ld[v] = l.d;
             integer &= l.d == 1;
-            S.mmax[v] = n_max_par(l, P);  // fits: k1_front computed it already
+            S.mmax[v] = q_max_par(l, P);  // fits: k1_front computed it already
         }
         integer = __all_sync(FULL, integer);
         __syncwarp();

@@ -435,6 +435,24 @@ __device__ __forceinline__ RatT<T> q_exec_raw(RatT<T> load, long long m, const P
         return n_exec_raw(load, m, p);
     }
 }
+// t_min = 1 and an integer load (every C5 node): max_parallelism is the load
+// itself, and exec_time(load, m) is t_min whenever m >= load (one pass, raw
+// value <= 1) — decided inline; anything else goes to the out-of-line copies.
+template <class T>
+__device__ __forceinline__ bool unit_tmin(const PlatT<T>& p) {
+    return p.tmin.n == 1 && p.tmin.d == 1;
+}
+template <class T>
+__device__ __forceinline__ int q_max_par(RatT<T> load, const PlatT<T>& p) {
+    if (unit_tmin(p) && load.d == 1 && load.n >= T(1) && load.n <= T(0x7fffffff)) return int(load.n);
+    return n_max_par(load, p);
+}
+template <class T>
+__device__ __forceinline__ RatT<T> q_exec(RatT<T> load, int m, const PlatT<T>& p) {
+    if (unit_tmin(p) && load.d == 1 && m <= p.M && load.n <= T(m)) return p.tmin;
+    return n_exec(load, m, p);
+}
+
 template <class T>
 __device__ __forceinline__ RatT<T> q_add(RatT<T> a, RatT<T> b) {
     if (a.d == 1 && b.d == 1) {
