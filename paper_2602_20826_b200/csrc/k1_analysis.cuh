@@ -134,7 +134,7 @@ __device__ __forceinline__ Mask<W> ballot_nodes(int lane, int n, Pred pred) {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         u64 acc = 0;
-#pragma unroll 1
+#pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (k * 64 + h * 32 >= n) break;  // uniform: most DAGs fit one 32-node half
             acc |= u64(__ballot_sync(FULL, pred(k * 64 + h * 32 + lane))) << (32 * h);
@@ -174,21 +174,22 @@ __device__ __forceinline__ void for_bits(const Mask<W>& m, F f) {
 // afterwards element e of each sorted order is in lane e % 32. The network
 // runs as a loop (not unrolled: the kernel is instruction-fetch bound) up to
 // size K (32 when every key fits the a/c halves, else 64).
-__device__ __forceinline__ void bitonic64x2(u64& a, u64& b, u64& c, u64& d, const int lane, const int K) {
+template <class K_t>
+__device__ __forceinline__ void bitonic64x2(K_t& a, K_t& b, K_t& c, K_t& d, const int lane, const int K) {
 #pragma unroll 1
     for (int k = 2; k <= K; k <<= 1) {
 #pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j == 32) {  // partners are the two registers of one lane (k == 64: ascending)
-                const u64 lo = min(a, b), hi = max(a, b), lo2 = min(c, d), hi2 = max(c, d);
+                const K_t lo = min(a, b), hi = max(a, b), lo2 = min(c, d), hi2 = max(c, d);
                 a = lo;
                 b = hi;
                 c = lo2;
                 d = hi2;
                 continue;
             }
-            const u64 pa = __shfl_xor_sync(FULL, a, j), pb = __shfl_xor_sync(FULL, b, j);
-            const u64 pc = __shfl_xor_sync(FULL, c, j), pd = __shfl_xor_sync(FULL, d, j);
+            const K_t pa = __shfl_xor_sync(FULL, a, j), pb = __shfl_xor_sync(FULL, b, j);
+            const K_t pc = __shfl_xor_sync(FULL, c, j), pd = __shfl_xor_sync(FULL, d, j);
             const bool lower = (lane & j) == 0;          // this element has the smaller index
             const bool up_a = (lane & k) == 0;           // element lane: ascending run?
             const bool up_b = ((lane + 32) & k) == 0;    // element lane + 32
@@ -534,25 +535,34 @@ K1_PHASE int p_rank(WarpState<W, T>& S, const int lane, const int n, const bool 
         // (2 per lane) replace the O(n) compare loop per node. Key for the
         // rank: (W^anc desc, id asc) = ((~W) << 8 | id); for the joins:
         // (W^anc asc, id asc) = (W << 8 | id), non-joins pushed to the end.
-        bool small = true;
-        for (int v = lane; v < n; v += 32) small &= u64(S.xn[v]) < (1ull << 48);
-        if (integer && __all_sync(FULL, small)) {
-            const u64 mask48 = (1ull << 48) - 1;
-            u64 a = lane < n ? ((mask48 - u64(S.xn[lane])) << 8) | u64(lane) : ~0ull;
-            u64 b = lane + 32 < n ? ((mask48 - u64(S.xn[lane + 32])) << 8) | u64(lane + 32) : ~0ull;
-            u64 ja = lane < n && J.test(lane) ? (u64(S.xn[lane]) << 8) | u64(lane) : ~0ull;
-            u64 jb = lane + 32 < n && J.test(lane + 32) ? (u64(S.xn[lane + 32]) << 8) | u64(lane + 32) : ~0ull;
-            bitonic64x2(a, b, ja, jb, lane, n <= 32 ? 32 : 64);
-            if (a != ~0ull) {
-                S.order[lane] = short(a & 0xff);
-                S.rank[a & 0xff] = short(lane);
-            }
-            if (b != ~0ull) {
-                S.order[lane + 32] = short(b & 0xff);
-                S.rank[b & 0xff] = short(lane + 32);
-            }
-            if (ja != ~0ull) S.jorder[lane] = short(ja & 0xff);
-            if (jb != ~0ull) S.jorder[lane + 32] = short(jb & 0xff);
+        // Keys fit 32 bits (W^anc < 2^24, the C5 case) or 64 (W^anc < 2^48).
+        u64 wmax = 0;
+        for (int v = lane; v < n; v += 32) wmax = max(wmax, u64(S.xn[v]));
+        const u32 whi = __reduce_max_sync(FULL, u32(wmax >> 32)), wlo = __reduce_max_sync(FULL, u32(wmax));
+        wmax = whi ? (u64(whi) << 32 | 0xffffffffull) : u64(wlo);  // an upper bound is enough
+        if (integer && wmax < (1ull << 48)) {
+            const bool k32 = wmax < (1ull << 24);
+            auto sort_keys = [&](auto kz) {
+                using K_t = decltype(kz);
+                const K_t top = k32 ? K_t((1u << 24) - 1) : K_t((1ull << 48) - 1), none = ~K_t(0);
+                K_t a = lane < n ? ((top - K_t(S.xn[lane])) << 8) | K_t(lane) : none;
+                K_t b = lane + 32 < n ? ((top - K_t(S.xn[lane + 32])) << 8) | K_t(lane + 32) : none;
+                K_t ja = lane < n && J.test(lane) ? (K_t(S.xn[lane]) << 8) | K_t(lane) : none;
+                K_t jb = lane + 32 < n && J.test(lane + 32) ? (K_t(S.xn[lane + 32]) << 8) | K_t(lane + 32) : none;
+                bitonic64x2<K_t>(a, b, ja, jb, lane, n <= 32 ? 32 : 64);
+                if (a != none) {
+                    S.order[lane] = short(a & 0xff);
+                    S.rank[a & 0xff] = short(lane);
+                }
+                if (b != none) {
+                    S.order[lane + 32] = short(b & 0xff);
+                    S.rank[b & 0xff] = short(lane + 32);
+                }
+                if (ja != none) S.jorder[lane] = short(ja & 0xff);
+                if (jb != none) S.jorder[lane + 32] = short(jb & 0xff);
+            };
+            if (k32) sort_keys(u32(0));
+            else sort_keys(u64(0));
             __syncwarp();
             if (__any_sync(FULL, ovf)) return -1;
             return J.popc();
