@@ -144,6 +144,13 @@ __device__ __forceinline__ Mask<W> ballot_nodes(int lane, int n, Pred pred) {
     return r;
 }
 
+// Sets bit i of a 64-bit word in shared memory with a native 32-bit atomicOr
+// on the half that holds it (a 64-bit atomicOr on shared memory compiles to a
+// CAS spin loop, ATOMS.CAST.SPIN.64).
+__device__ __forceinline__ void smem_set_bit(u64* words, int i) {
+    atomicOr(reinterpret_cast<unsigned int*>(words) + (i >> 5), 1u << (i & 31));
+}
+
 // Set bits of a uniform mask, ascending. Walks each word as two 32-bit
 // halves (one body instantiation): 32-bit find-first-set and clear-lowest
 // take half the instructions of their 64-bit forms, and most DAGs have their
@@ -281,8 +288,8 @@ K1_PHASE int p_edges(WarpState<W, T>& S, const int lane, const int n, const u32*
                 bad_kind = (u >= n || v >= n) ? DS_E_EDGE : DS_E_SELFLOOP;
             }
         } else {
-            atomicOr(&S.succ[u][v >> 6], 1ull << (v & 63));
-            atomicOr(&S.pred[v][u >> 6], 1ull << (u & 63));
+            smem_set_bit(S.succ[u], v);
+            smem_set_bit(S.pred[v], u);
         }
     }
     const u32 m = __reduce_min_sync(FULL, first_bad);
@@ -369,19 +376,27 @@ K1_PHASE int p_closure(WarpState<W, T>& S, const int lane, const int n, bool low
 }
 
 // Descendants for n <= 64 as the transpose of the ancestor matrix:
-// desc[v] = { u : v in anc[u] }. One broadcast shared-memory read per node and
-// two bit tests per lane replace the reverse Kahn rounds (dag.cpp:119-124).
+// desc[v] = { u : v in anc[u] }. Lane u holds anc[u] (and anc[u + 32]); one
+// ballot per column v (two when n > 32) yields desc[v] warp-uniformly, and
+// lane v % 32 keeps it. Replaces the reverse Kahn rounds (dag.cpp:119-124).
 template <class T>
 K1_PHASE void p_desc_transpose(WarpState<1, T>& S, const int lane, const int n) {
-    u64 lo = 0, hi = 0;  // desc of nodes lane and lane + 32
+    const u64 a0 = lane < n ? S.anc[lane][0] : 0ull;
+    const u64 a1 = lane + 32 < n ? S.anc[lane + 32][0] : 0ull;
+    u64 d0 = 0, d1 = 0;  // desc of nodes lane and lane + 32
+    const bool two = n > 32;
 #pragma unroll 4
-    for (int u = 0; u < n; ++u) {
-        const u64 a = S.anc[u][0];
-        lo |= ((a >> lane) & 1ull) << u;
-        hi |= ((a >> (lane + 32)) & 1ull) << u;
+    for (int v = 0; v < n; ++v) {
+        const u32 lo = __ballot_sync(FULL, (a0 >> v) & 1ull);
+        const u32 hi = two ? __ballot_sync(FULL, (a1 >> v) & 1ull) : 0u;
+        const u64 d = (u64(hi) << 32) | lo;
+        if (lane == (v & 31)) {
+            if (v < 32) d0 = d;
+            else d1 = d;
+        }
     }
-    if (lane < n) S.desc[lane][0] = lo;
-    if (lane + 32 < n) S.desc[lane + 32][0] = hi;
+    if (lane < n) S.desc[lane][0] = d0;
+    if (lane + 32 < n) S.desc[lane + 32][0] = d1;
     __syncwarp();
 }
 
@@ -643,7 +658,7 @@ K1_PHASE int p_division(WarpState<W, T>& S, const int lane, const int n, const i
                 __syncwarp();
 #pragma unroll 1
                 for (int v = lane; v < n; v += 32) {
-                    if (H.test(v)) atomicOr(&S.rmask[S.rank[v] >> 6], 1ull << (S.rank[v] & 63));
+                    if (H.test(v)) smem_set_bit(S.rmask, S.rank[v]);
                 }
                 __syncwarp();
                 sel = ballot_nodes<W>(lane, n, [&](int v) {
@@ -913,7 +928,7 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
             __syncwarp();
 #pragma unroll 1
             for (int v = lane; v < n; v += 32) {
-                if (cands.test(v)) atomicOr(&S.rmask[S.rank[v] >> 6], 1ull << (S.rank[v] & 63));
+                if (cands.test(v)) smem_set_bit(S.rmask, S.rank[v]);
             }
             __syncwarp();
             const Mask<W> rm = load_mask<W>(S.rmask);
