@@ -891,11 +891,19 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
         // the pool is the union of the members' concurrent sets minus the
         // division group (which also removes each member itself).
         Mask<W> pool;
-        pool.clear();
-        for_bits<W>(org, [&](int v) {
+        if constexpr (W == 1) {
+            // lanes OR their members' concurrent sets, the warp reduces (REDUX)
+            u64 c = 0;
+            if (org.test(lane)) c = ~(S.anc[lane][0] | S.desc[lane][0]);
+            if (lane + 32 < n && org.test(lane + 32)) c |= ~(S.anc[lane + 32][0] | S.desc[lane + 32][0]);
+            pool.w[0] = V.w[0] & ((u64(__reduce_or_sync(FULL, u32(c >> 32))) << 32) | __reduce_or_sync(FULL, u32(c)));
+        } else {
+            pool.clear();
+            for_bits<W>(org, [&](int v) {
 #pragma unroll
-            for (int k = 0; k < W; ++k) pool.w[k] |= V.w[k] & ~(S.anc[v][k] | S.desc[v][k]);
-        });
+                for (int k = 0; k < W; ++k) pool.w[k] |= V.w[k] & ~(S.anc[v][k] | S.desc[v][k]);
+            });
+        }
         Mask<W> avail;
 #pragma unroll
         for (int k = 0; k < W; ++k) {
