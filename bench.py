@@ -340,7 +340,7 @@ def main():
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
     h2d = batch.nbytes(with_den=not integer)
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
-    n_chunks = int(os.environ.get("DS_CHUNKS", "8"))  # analyze_host's chunking (capi.cu)
+    n_chunks = int(os.environ.get("DS_CHUNKS", "12"))  # analyze_host's chunking (capi.cu)
     chunks = -(-n // max(1 << 16, -(-n // n_chunks)))
 
     # ---------------------------------------------------------------- roofline

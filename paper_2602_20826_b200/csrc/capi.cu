@@ -148,7 +148,7 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 16;  // >= one wave of warps, small enough to pipeline
-constexpr u64 kDefaultChunks = 8;   // DS_CHUNKS overrides (tuning knob)
+constexpr u64 kDefaultChunks = 12;  // DS_CHUNKS overrides (tuning knob)
 
 int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
     DS_CUDA(cudaSetDevice(device));

@@ -375,28 +375,36 @@ K1_PHASE int p_closure(WarpState<W, T>& S, const int lane, const int n, bool low
     return done.popc() == n ? (rounds | (flat ? kFlatPath : 0)) : -1;
 }
 
+// 32x32 bit-matrix transpose across a warp: lane i holds row i (bit c =
+// element (i, c)); afterwards lane j holds column j. Five butterfly steps, each
+// swapping the off-diagonal j x j blocks between lanes i and i ^ j.
+__device__ __forceinline__ u32 warp_transpose32(u32 x, const int lane) {
+    constexpr u32 m0[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const u32 y = __shfl_xor_sync(FULL, x, j);
+        x = (lane & j) ? ((x & ~m0[s]) | ((y >> j) & m0[s])) : ((x & m0[s]) | ((y << j) & ~m0[s]));
+    }
+    return x;
+}
+
 // Descendants for n <= 64 as the transpose of the ancestor matrix:
-// desc[v] = { u : v in anc[u] }. Lane u holds anc[u] (and anc[u + 32]); one
-// ballot per column v (two when n > 32) yields desc[v] warp-uniformly, and
-// lane v % 32 keeps it. Replaces the reverse Kahn rounds (dag.cpp:119-124).
+// desc[v] = { u : v in anc[u] } — one to four 32x32 warp transposes replace the
+// reverse Kahn rounds (dag.cpp:119-124).
 template <class T>
 K1_PHASE void p_desc_transpose(WarpState<1, T>& S, const int lane, const int n) {
     const u64 a0 = lane < n ? S.anc[lane][0] : 0ull;
-    const u64 a1 = lane + 32 < n ? S.anc[lane + 32][0] : 0ull;
-    u64 d0 = 0, d1 = 0;  // desc of nodes lane and lane + 32
-    const bool two = n > 32;
-#pragma unroll 4
-    for (int v = 0; v < n; ++v) {
-        const u32 lo = __ballot_sync(FULL, (a0 >> v) & 1ull);
-        const u32 hi = two ? __ballot_sync(FULL, (a1 >> v) & 1ull) : 0u;
-        const u64 d = (u64(hi) << 32) | lo;
-        if (lane == (v & 31)) {
-            if (v < 32) d0 = d;
-            else d1 = d;
-        }
+    if (n <= 32) {
+        const u32 t = warp_transpose32(u32(a0), lane);
+        if (lane < n) S.desc[lane][0] = t;
+    } else {
+        const u64 a1 = lane + 32 < n ? S.anc[lane + 32][0] : 0ull;
+        const u32 t00 = warp_transpose32(u32(a0), lane), t10 = warp_transpose32(u32(a1), lane);
+        const u32 t01 = warp_transpose32(u32(a0 >> 32), lane), t11 = warp_transpose32(u32(a1 >> 32), lane);
+        S.desc[lane][0] = (u64(t10) << 32) | t00;
+        if (lane + 32 < n) S.desc[lane + 32][0] = (u64(t11) << 32) | t01;
     }
-    if (lane < n) S.desc[lane][0] = d0;
-    if (lane + 32 < n) S.desc[lane + 32][0] = d1;
     __syncwarp();
 }
 
