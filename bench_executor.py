@@ -4,13 +4,18 @@
 For every DAG: K1 schedules it on the GPU (ds_schedule_batch, M = the SM
 partition), K3 turns the schedule into one CUDA Graph of K2 node kernels
 (grid = SM quota, one CTA per SM) and replays it R times; each replay's
-makespan is first-CTA-start -> last-CTA-end on %globaltimer. Variants, all as
-CUDA Graphs of the same kernels on the same SMs:
-  proposed       the schedule with group barriers (simulate_scheme semantics)
-  proposed_deps  the schedule with its augmented-graph edges only
+makespan is first-CTA-start -> last-CTA-end on %globaltimer. Variants, all running the same node kernel (default k2_mix_tma) on the same
+SMs:
+  proposed       the schedule with group barriers (simulate_scheme semantics),
+                 CUDA graph
+  proposed_deps  the schedule with its augmented-graph edges only, CUDA graph
+  dynamic        = proposed on the dynamic persistent engine (one resident CTA
+                 per SM, device-side claiming of quota-capped entity ranks)
+  dynamic_deps   = proposed_deps on the dynamic engine
   serial         one chain in topological order, m = min(m^max, M)
   multistream    original DAG edges only, m = min(m^max, M) — naive
                  multi-stream launch / Greedy
+  multistream_free  the same with 4 m unconstrained 256-thread CTAs
 
 M = 148 runs on the whole GPU; M < 148 runs inside a green context of M SMs
 (the paper's contended regime: Jetson M=8, RTX 3060 M=30).
@@ -38,8 +43,7 @@ from paper_2602_20826_b200 import _lib, scheme, workloads  # noqa: E402
 from paper_2602_20826_b200 import executor as X  # noqa: E402
 from paper_2602_20826_b200.batch import pack  # noqa: E402
 
-VARIANTS = ("proposed", "proposed_deps", "persistent", "persistent_deps", "serial", "multistream",
-            "multistream_free")
+VARIANTS = ("proposed", "proposed_deps", "dynamic", "dynamic_deps", "serial", "multistream", "multistream_free")
 
 
 def stats(a):
@@ -72,11 +76,11 @@ def run_dag(loads, edges, sch, M, sm_limit, cal, args):
            "launches": sum(len(g.launches) for g in sch.groups), "bound_units": str(bound_units),
            "greedy_units": str(sch.bounds["greedy"]), "bound_us": bound_us}
     for kind in VARIANTS:
-        engine = (X.ENGINE_PERSISTENT if kind.startswith("persistent") else
+        engine = (X.ENGINE_DYNAMIC if kind.startswith("dynamic") else
                   X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
-        if kind in ("proposed", "persistent"):
+        if kind in ("proposed", "dynamic"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=True)
-        elif kind in ("proposed_deps", "persistent_deps"):
+        elif kind in ("proposed_deps", "dynamic_deps"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=False)
         else:
             plan = X.plan_baseline(kind.replace("_free", ""), loads, edges, M, args.unit)
@@ -114,7 +118,7 @@ def summarise(results, prefix):
             "trace_violations": int(sum(r[kind]["precedence_violations"] + r[kind]["sm_overlap_violations"]
                                         for r in sel)),
         }
-    for kind in ("proposed", "proposed_deps", "persistent", "persistent_deps"):
+    for kind in ("proposed", "proposed_deps", "dynamic", "dynamic_deps"):
         for q in ("p50", "p99", "max"):
             s[f"{kind}_beats_multistream_{q}"] = int(sum(r[kind]["makespan_us"][q] < r["multistream"]["makespan_us"][q]
                                                          for r in sel))
@@ -129,7 +133,7 @@ def main():
     ap.add_argument("--replays", type=int, default=1000)
     ap.add_argument("--c2-dags", type=int, default=100)
     ap.add_argument("--unit", type=int, default=1 << 17, help="elements per load unit per SM")
-    ap.add_argument("--workload", type=int, default=X.WL_MIX32)
+    ap.add_argument("--workload", type=int, default=X.WL_MIX32_TMA)
     ap.add_argument("--check-every", type=int, default=25)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_executor.json"))
     args = ap.parse_args()

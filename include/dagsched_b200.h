@@ -165,6 +165,11 @@ typedef struct ds_scheme_out {
 #define DS_WL_AXPY32 1  /* y[i] = a*x[i] + y[i], fp32 (no FMA contraction): 12 B  */
 #define DS_WL_MIX32_BULK 2 /* DS_WL_MIX32 staged through shared memory with
                               cp.async.bulk (TMA engine) + mbarrier: 8 B/elem   */
+#define DS_WL_MIX32_TMA 3  /* DS_WL_MIX32 through a warp-specialised 6 x 32 KB
+                              cp.async.bulk ring (1 producer + 16 consumer
+                              warps, 544 threads per CTA): 8 B/elem            */
+#define DS_WL_MIX32_LDG8 4 /* DS_WL_MIX32 with 8 LDG.128 in flight per thread  */
+#define DS_WL_LAST 4
 
 /* One schedulable entity (EntityRecord, scheduler.hpp:31-39) as executed:
  * grid = parallelism CTAs, one CTA per SM enforced by the kernel's shared
@@ -216,6 +221,18 @@ typedef struct ds_exec_cfg {
  * 4 x parallelism CTAs per entity. */
 #define DS_ENGINE_GRAPH_FREE 2
 #define DS_FREE_CTA_FACTOR 4
+/* DYNAMIC: one resident CTA per SM, work-conserving: an entity enters a
+ * device-side ready queue (plan order = schedule priority) when its last
+ * augmented-graph predecessor completes, and idle CTAs claim its m ranks, so
+ * it never holds more than its quota of SMs. Any topologically ordered plan;
+ * workloads DS_WL_MIX32 and DS_WL_MIX32_TMA. */
+#define DS_ENGINE_DYNAMIC 3
+/* STREAM: DYNAMIC's claiming with one TMA ring per SM kept streaming across
+ * items — under contention the producer warp claims the next startable item
+ * while the ring drains the current one, so an SM moves between entities
+ * without a launch/drain bubble. Runs the DS_WL_MIX32 computation through
+ * DS_WL_MIX32_TMA's ring (544 threads per CTA). */
+#define DS_ENGINE_STREAM 4
 
 /* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
 typedef struct ds_exec_trace {
@@ -344,6 +361,10 @@ int ds_exec_free(void* exec);
  * globaltimer span of the last launch. */
 int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int block_threads, int reps,
                          float* ms_per_launch, uint64_t* span_ns, int device);
+/* Placement probe (diagnostic): one CTA per SM; the SMs whose %smid bit is set
+ * in mask8 (8 x 32 bits) each stream `elems` uint32 through the mix kernel;
+ * *avg_span_ns = mean device span over `reps` launches (HBM-resident data). */
+int ds_node_placement_bench(const uint32_t* mask8, uint64_t elems, int reps, double* avg_span_ns, int device);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

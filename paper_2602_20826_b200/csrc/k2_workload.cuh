@@ -83,42 +83,49 @@ __device__ __forceinline__ void stamp_exit(const NodeArgs& a, unsigned long long
     atomicMax(&a.span[2 * r + 1], t1);
 }
 
+// y[s0, s1) = mix(x[s0, s1)) with LDG.128/STG.128, U independent 16-B loads
+// in flight per thread per iteration (1024 threads: U x 16 KB per SM).
+template <int U>
+__device__ __forceinline__ void mix_ldg_slice(const uint32_t* x, uint32_t* y, unsigned long long s0,
+                                              unsigned long long s1) {
+    // scalar head/tail, 16-byte vectors in between (buffers are 256-B aligned)
+    const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
+    if (v0 >= v1) {
+        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) y[i] = mix32(__ldg(x + i));
+        return;
+    }
+    for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) y[i] = mix32(__ldg(x + i));
+    for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) y[i] = mix32(__ldg(x + i));
+    const uint4* x4 = reinterpret_cast<const uint4*>(x);
+    uint4* y4 = reinterpret_cast<uint4*>(y);
+    const unsigned long long step = blockDim.x;
+    unsigned long long i = v0 + threadIdx.x;
+#define DS_MIX4(r) r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w)
+    for (; i + (U - 1) * step < v1; i += U * step) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = __ldcs(x4 + i + u * step);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            DS_MIX4(r[u]);
+            __stcs(y4 + i + u * step, r[u]);
+        }
+    }
+    for (; i < v1; i += step) {
+        uint4 r = __ldcs(x4 + i);
+        DS_MIX4(r);
+        __stcs(y4 + i, r);
+    }
+#undef DS_MIX4
+}
+
+template <int U>
 __global__ void __launch_bounds__(1024, 1) k2_mix(const NodeArgs a) {
     __shared__ unsigned long long t0s;
     if (threadIdx.x == 0) t0s = gtimer();
     unsigned long long s0, s1;
     cta_slice(a, s0, s1);
-    // scalar head/tail, 16-byte vectors in between (buffers are 256-B aligned)
-    const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
-    if (v0 >= v1) {
-        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-    } else {
-        for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-        for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-        const uint4* x4 = reinterpret_cast<const uint4*>(a.x);
-        uint4* y4 = reinterpret_cast<uint4*>(a.y);
-        const unsigned long long step = blockDim.x;
-        unsigned long long i = v0 + threadIdx.x;
-        for (; i + 3 * step < v1; i += 4 * step) {
-            uint4 r0 = __ldcs(x4 + i), r1 = __ldcs(x4 + i + step), r2 = __ldcs(x4 + i + 2 * step),
-                  r3 = __ldcs(x4 + i + 3 * step);
-#define DS_MIX4(r) r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w)
-            DS_MIX4(r0);
-            DS_MIX4(r1);
-            DS_MIX4(r2);
-            DS_MIX4(r3);
-            __stcs(y4 + i, r0);
-            __stcs(y4 + i + step, r1);
-            __stcs(y4 + i + 2 * step, r2);
-            __stcs(y4 + i + 3 * step, r3);
-        }
-        for (; i < v1; i += step) {
-            uint4 r = __ldcs(x4 + i);
-            DS_MIX4(r);
-            __stcs(y4 + i, r);
-        }
-#undef DS_MIX4
-    }
+    mix_ldg_slice<U>(a.x, a.y, s0, s1);
     __syncthreads();
     stamp_exit(a, t0s);
 }
@@ -269,6 +276,106 @@ __global__ void __launch_bounds__(1024, 1) k2_mix_bulk(const NodeArgs a) {
     stamp_exit(a, t0s);
 }
 
+// ------------------------------------ warp-specialised TMA streaming variant
+// One producer warp (one elected lane) streams the CTA's slice through a
+// ring of kTmaStages x kTmaChunk shared-memory stages with cp.async.bulk
+// (TMA engine, completion on the stage's `full` mbarrier); kTmaConsumerWarps
+// consumer warps transform each stage (LDS.128 -> mix -> STG.128 streaming
+// stores) and release it on its `empty` mbarrier (one arrival per warp). No
+// CTA-wide barrier in the steady state, and up to kTmaStages x 32 KB of reads
+// in flight per SM without holding registers — what a lone node (a few SMs
+// busy, the critical path of a DAG) needs to go beyond the ~64 KB an LDG loop
+// keeps in flight. The 192 KB ring also forces one CTA per SM.
+constexpr int kTmaStages = 6;
+constexpr int kTmaChunk = 32 * 1024;
+constexpr int kTmaConsumerWarps = 16;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaSmem = kTmaStages * kTmaChunk;
+
+struct TmaRing {
+    uint64_t full[kTmaStages];
+    uint64_t empty[kTmaStages];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_ring_init(TmaRing* r) {  // one thread, then a CTA barrier
+    for (int s = 0; s < kTmaStages; ++s) {
+        mbar_init(&r->full[s], 1);
+        mbar_init(&r->empty[s], kTmaConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// y[s0, s1) = mix(x[s0, s1)) by the whole CTA (kTmaThreads threads). `it`
+// counts the ring's chunks used so far by this CTA (identical in every
+// thread), so a persistent CTA can call this once per work item.
+__device__ __forceinline__ void tma_mix_slice(const uint32_t* x, uint32_t* y, unsigned long long s0,
+                                              unsigned long long s1, unsigned char* sm, TmaRing* ring,
+                                              uint32_t& it) {
+    const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;  // 16-B aligned interior
+    if (v0 >= v1) {
+        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) y[i] = mix32(__ldg(x + i));
+        return;
+    }
+    for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) y[i] = mix32(__ldg(x + i));
+    for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) y[i] = mix32(__ldg(x + i));
+    constexpr unsigned long long kChunkV = kTmaChunk / 16;  // uint4 per stage
+    const unsigned long long nv = v1 - v0;
+    const uint32_t n_chunks = uint32_t((nv + kChunkV - 1) / kChunkV);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint4* x4 = reinterpret_cast<const uint4*>(x) + v0;
+    uint4* y4 = reinterpret_cast<uint4*>(y) + v0;
+    if (warp == kTmaConsumerWarps) {  // producer
+        if (lane == 0) {
+            for (uint32_t c = 0; c < n_chunks; ++c) {
+                const uint32_t idx = it + c, s = idx % kTmaStages, k = idx / kTmaStages;
+                if (k > 0) mbar_wait(&ring->empty[s], (k - 1) & 1);
+                const unsigned long long nc = min(kChunkV, nv - c * kChunkV);
+                mbar_expect_tx(&ring->full[s], uint32_t(nc * 16));
+                bulk_g2s(sm + s * kTmaChunk, x4 + c * kChunkV, uint32_t(nc * 16), &ring->full[s]);
+            }
+        }
+    } else {
+        const int t = threadIdx.x;  // < kTmaConsumerWarps * 32
+        for (uint32_t c = 0; c < n_chunks; ++c) {
+            const uint32_t idx = it + c, s = idx % kTmaStages, k = idx / kTmaStages;
+            const unsigned long long nc = min(kChunkV, nv - c * kChunkV);
+            mbar_wait(&ring->full[s], k & 1);
+            const uint4* buf = reinterpret_cast<const uint4*>(sm + s * kTmaChunk);
+            uint4* dst = y4 + c * kChunkV;
+#pragma unroll 4
+            for (unsigned long long i = t; i < nc; i += kTmaConsumerWarps * 32) {
+                uint4 r = buf[i];
+                r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w);
+                __stcs(dst + i, r);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ring->empty[s]);
+        }
+    }
+    it += n_chunks;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) k2_mix_tma(const NodeArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ TmaRing ring;
+    __shared__ unsigned long long t0s;
+    if (threadIdx.x == 0) {
+        t0s = gtimer();
+        tma_ring_init(&ring);
+    }
+    __syncthreads();
+    unsigned long long s0, s1;
+    cta_slice(a, s0, s1);
+    uint32_t it = 0;
+    tma_mix_slice(a.x, a.y, s0, s1, sm, &ring, it);
+    __syncthreads();
+    stamp_exit(a, t0s);
+}
+
 __global__ void k2_init(uint32_t* x, unsigned long long n, uint32_t seed, int fp, uint32_t* y) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
@@ -340,36 +447,7 @@ __global__ void __launch_bounds__(1024, 1) k3_persistent(const PArgs a) {
         __syncthreads();
         const unsigned long long len = e.hi - e.lo;
         const unsigned long long s0 = e.lo + len * w.rank / e.m, s1 = e.lo + len * (w.rank + 1) / e.m;
-        const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
-        if (v0 >= v1) {
-            for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
-        } else {
-            for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
-            for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) e.y[i] = mix32(__ldg(e.x + i));
-            const uint4* x4 = reinterpret_cast<const uint4*>(e.x);
-            uint4* y4 = reinterpret_cast<uint4*>(e.y);
-            const unsigned long long step = blockDim.x;
-            unsigned long long i = v0 + threadIdx.x;
-            for (; i + 3 * step < v1; i += 4 * step) {
-                uint4 r0 = __ldcs(x4 + i), r1 = __ldcs(x4 + i + step), r2 = __ldcs(x4 + i + 2 * step),
-                      r3 = __ldcs(x4 + i + 3 * step);
-#define DS_MIX4(r) r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w)
-                DS_MIX4(r0);
-                DS_MIX4(r1);
-                DS_MIX4(r2);
-                DS_MIX4(r3);
-                __stcs(y4 + i, r0);
-                __stcs(y4 + i + step, r1);
-                __stcs(y4 + i + 2 * step, r2);
-                __stcs(y4 + i + 3 * step, r3);
-            }
-            for (; i < v1; i += step) {
-                uint4 r = __ldcs(x4 + i);
-                DS_MIX4(r);
-                __stcs(y4 + i, r);
-            }
-#undef DS_MIX4
-        }
+        mix_ldg_slice<4>(e.x, e.y, s0, s1);
         __syncthreads();
         if (threadIdx.x == 0) {
             const unsigned long long t1 = gtimer();
@@ -385,6 +463,361 @@ __global__ void __launch_bounds__(1024, 1) k3_persistent(const PArgs a) {
             }
             __threadfence();
             atomicAdd(a.done + w.ent, 1u);
+        }
+    }
+}
+
+// ------------------------------------------------ dynamic persistent engine
+// One resident CTA per SM for the whole DAG, work-conserving, with look-ahead
+// claiming. Per entity e (quota m_e, augmented-graph predecessors P(e)):
+//   claimed[e]     ranks of e handed out so far (an entity is m_e items, so it
+//                  never holds more than its quota of SMs; a CTA runs one item
+//                  at a time, so concurrent entities sit on disjoint SMs);
+//   pend_claim[e]  sum over P(e) of ranks not yet claimed;
+//   pend_done[e]   sum over P(e) of ranks not yet finished.
+// Warp 0 of an idle CTA scans the entities in plan order (= schedule
+// priority), 32 per coalesced probe, and claims a rank of the first entity
+// that can start (pend_done = 0) or, failing that, of the first whose
+// predecessors are all claimed (pend_claim = 0) — then waits for its
+// pend_done to reach 0. The claim round trip thus overlaps the predecessors'
+// execution, and the dependency hand-off on the critical path is one fence +
+// fire-and-forget reductions (RED) in the finishing CTA and one acquire poll
+// in the waiting one, the same as a static CTA assignment, without its
+// mis-placements. Deadlock-free: the earliest (topological) waiting rank has
+// every predecessor rank claimed, hence running, hence finishing.
+struct DEnt {
+    const uint32_t* x;
+    uint32_t* y;
+    unsigned long long lo, hi;
+    uint32_t m, slot, succ_off, n_succ, pred_ranks;
+};
+struct DArgs {
+    const DEnt* ents;
+    const uint32_t* succs;
+    const uint32_t* quota;      // [n] m_e (read-only copy for the warp probes)
+    uint32_t n, n_init;
+    unsigned int* claimed;      // [n]
+    unsigned int* pend_claim;   // [n]
+    unsigned int* pend_done;    // [n]
+    unsigned int* idle;         // [1] stream engine: CTAs with nothing in flight
+    int rec;                    // recorded replay slot, < 0: not recorded
+    unsigned long long* stamps;
+    uint32_t* smids;
+    unsigned long long* span;
+    uint32_t total;
+};
+
+__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void k3_dyn_reset(const DArgs a) {
+    for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+        a.claimed[i] = 0;
+        a.pend_claim[i] = a.ents[i].pred_ranks;
+        a.pend_done[i] = a.ents[i].pred_ranks;
+    }
+    if (threadIdx.x == 0 && a.idle) *a.idle = 0;
+}
+
+template <bool kTma>
+__global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const DArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ TmaRing ring;
+    __shared__ unsigned long long t0s;
+    __shared__ uint32_t s_ent, s_rank;
+    if (kTma && threadIdx.x == 0) tma_ring_init(&ring);
+    const int lane = threadIdx.x & 31;
+    uint32_t it = 0;   // TMA ring chunks used by this CTA
+    uint32_t cur = 0;  // entities before cur are fully handed out (warp 0)
+#pragma unroll 1
+    while (true) {
+        if (threadIdx.x < 32) {
+            uint32_t ent = ~0u, rank = 0;
+            while (cur < a.n) {
+                bool got = false;
+                for (uint32_t base = cur; base < a.n && !got; base += 32) {
+                    const uint32_t e = base + lane;
+                    const bool valid = e < a.n;
+                    const uint32_t m = valid ? __ldg(a.quota + e) : 0;
+                    const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
+                    const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
+                    const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
+                    const bool open = valid && cl < m;
+                    const unsigned open_mask = __ballot_sync(~0u, open);
+                    if (base == cur) cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
+                    unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
+                    if (!pick) pick = __ballot_sync(~0u, open && pc == 0);
+                    while (pick && !got) {
+                        const int l = __ffs(pick) - 1;
+                        pick &= pick - 1;
+                        uint32_t c = 0;
+                        if (lane == l) c = atomicAdd(a.claimed + e, 1u);
+                        c = __shfl_sync(~0u, c, l);
+                        const uint32_t ml = __shfl_sync(~0u, m, l);
+                        if (c < ml) {
+                            got = true;
+                            ent = base + l;
+                            rank = c;
+                        }
+                    }
+                }
+                if (got) break;
+                __nanosleep(32);
+            }
+            if (lane == 0 && ent != ~0u) {
+                const DEnt& d = a.ents[ent];
+                for (uint32_t k = 0; k < d.n_succ; ++k) atomicSub(a.pend_claim + a.succs[d.succ_off + k], 1u);
+                while (ld_acquire(a.pend_done + ent) != 0) {
+                }  // tight: every reserved rank of ent starts within one L2 round trip
+                t0s = gtimer();
+            }
+            if (lane == 0) {
+                s_ent = ent;
+                s_rank = rank;
+            }
+        }
+        __syncthreads();
+        const uint32_t ent = s_ent, rank = s_rank;
+        const unsigned long long my_t0 = t0s;
+        if (ent == ~0u) break;
+        const DEnt e = a.ents[ent];
+        const unsigned long long len = e.hi - e.lo;
+        const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
+        if constexpr (kTma) tma_mix_slice(e.x, e.y, s0, s1, sm, &ring, it);
+        else mix_ldg_slice<4>(e.x, e.y, s0, s1);
+        __syncthreads();
+        // completion in warp 1 while warp 0 already claims the next item: the
+        // fence (waits for this CTA's stores, observed through the barrier)
+        // overlaps the claim's round trips
+        if (threadIdx.x == 32) {
+            const unsigned long long t0s = my_t0;
+            const unsigned long long t1 = gtimer();
+            __threadfence();  // this item's stores before its completion
+            for (uint32_t k = 0; k < e.n_succ; ++k) atomicSub(a.pend_done + a.succs[e.succ_off + k], 1u);
+            if (a.rec >= 0) {
+                const unsigned long long idx = (unsigned long long)a.rec * a.total + e.slot + rank;
+                if (a.stamps) {
+                    a.stamps[2 * idx] = t0s;
+                    a.stamps[2 * idx + 1] = t1;
+                }
+                if (a.smids) a.smids[idx] = smid();
+                atomicMin(&a.span[2 * a.rec], t0s);
+                atomicMax(&a.span[2 * a.rec + 1], t1);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------ streaming persistent engine
+// The dynamic engine's claiming (look-ahead reservations, pend_claim /
+// pend_done counters) with the TMA ring of k2_mix_tma kept streaming ACROSS
+// items: the producer warp is also the CTA's scheduler. When its ring still
+// holds the tail of the current item and no other CTA is idle (contention),
+// it claims the next startable item and issues that item's bulk loads into
+// the stages the consumers free up, so the SM goes from one entity to the
+// next without a drain/launch bubble; with idle CTAs around it leaves new
+// work to them. Every stage carries (destination, length, item slot,
+// first/last flags) next to its data. Consumers process stages in order; at
+// an item's last stage every consumer warp fences its stores, and the last
+// one to finish releases the successors (RED on pend_done) and stamps the
+// item: start = when the last consumer warp began its first stage, end =
+// when the last one finished its last stage, so the items of one SM never
+// overlap in their stamps (an SM still computes one entity at a time; only
+// the prefetch of the next entity's input overlaps the current one's tail).
+constexpr int kItemSlots = 8;  // > kTmaStages items can be in the ring at once
+constexpr uint32_t kTagFirst = 1u << 8, kTagLast = 1u << 9, kTagExit = 1u << 10;
+struct StreamMeta {
+    uint4* dst;
+    uint32_t nvec;
+    uint32_t tag;  // item slot | flags
+};
+struct ItemRec {
+    unsigned long long t0;
+    uint32_t ent, rank, done_warps, pad;
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// warp-wide probe of the entity table in plan order (see k3_dynamic): claim a
+// rank of the first startable entity, or (reserve) of the first whose
+// predecessors are all claimed; returns ~0u when nothing was claimed
+__device__ __forceinline__ uint32_t claim_rank(const DArgs& a, uint32_t& cur, bool reserve, uint32_t& rank) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t base = cur; base < a.n; base += 32) {
+        const uint32_t e = base + lane;
+        const bool valid = e < a.n;
+        const uint32_t m = valid ? __ldg(a.quota + e) : 0;
+        const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
+        const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
+        const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
+        const bool open = valid && cl < m;
+        const unsigned open_mask = __ballot_sync(~0u, open);
+        if (base == cur) cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
+        unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
+        if (!pick && reserve) pick = __ballot_sync(~0u, open && pc == 0);
+        while (pick) {
+            const int l = __ffs(pick) - 1;
+            pick &= pick - 1;
+            uint32_t c = 0;
+            if (lane == l) c = atomicAdd(a.claimed + e, 1u);
+            c = __shfl_sync(~0u, c, l);
+            if (c < __shfl_sync(~0u, m, l)) {
+                rank = c;
+                return base + l;
+            }
+        }
+    }
+    return ~0u;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) k3_stream(const DArgs a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ TmaRing ring;
+    __shared__ StreamMeta meta[kTmaStages];
+    __shared__ ItemRec items[kItemSlots];
+    if (threadIdx.x == 0) tma_ring_init(&ring);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr unsigned long long kChunkV = kTmaChunk / 16;
+    if (warp == kTmaConsumerWarps) {
+        // ------------------------------------------------ producer / scheduler
+        uint32_t it = 0, cur = 0, n_items = 0;
+        bool counted_idle = false;
+#pragma unroll 1
+        while (true) {
+            bool drained = true;
+            if (it) {
+                const uint32_t last = it - 1;
+                drained = mbar_test(&ring.empty[last % kTmaStages], (last / kTmaStages) & 1);
+            }
+            drained = __shfl_sync(~0u, drained ? 1 : 0, 0) != 0;
+            if (drained && !counted_idle) {
+                if (lane == 0) atomicAdd(a.idle, 1u);
+                counted_idle = true;
+            }
+            uint32_t ent = ~0u, rank = 0;
+            if (cur < a.n) {
+                uint32_t others_idle = lane == 0 ? ld_relaxed(a.idle) : 0;
+                others_idle = __shfl_sync(~0u, others_idle, 0);
+                if (drained || others_idle == 0) ent = claim_rank(a, cur, drained, rank);
+            }
+            if (ent == ~0u) {
+                if (cur >= a.n) {  // everything handed out: close the ring
+                    if (lane == 0) {
+                        const uint32_t idx = it++, st = idx % kTmaStages, k = idx / kTmaStages;
+                        if (k > 0) mbar_wait(&ring.empty[st], (k - 1) & 1);
+                        meta[st].tag = kTagExit;
+                        mbar_arrive(&ring.full[st]);
+                    }
+                    break;
+                }
+                __nanosleep(32);
+                continue;
+            }
+            if (counted_idle) {
+                if (lane == 0) atomicSub(a.idle, 1u);
+                counted_idle = false;
+            }
+            const DEnt e = a.ents[ent];
+            if (lane == 0) {
+                for (uint32_t k = 0; k < e.n_succ; ++k) atomicSub(a.pend_claim + a.succs[e.succ_off + k], 1u);
+                while (ld_acquire(a.pend_done + ent) != 0) {
+                }
+            }
+            __syncwarp();
+            const unsigned long long len = e.hi - e.lo;
+            const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
+            unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
+            if (v0 >= v1) v0 = v1 = s1 >> 2;  // no aligned interior: all scalar
+            // unaligned head/tail elements by the producer lanes, fenced before
+            // the item can complete (its completion follows its last stage)
+            const unsigned long long h1 = v0 < v1 ? (v0 << 2) : s1, t0e = v0 < v1 ? (v1 << 2) : s1;
+            bool scalars = false;
+            for (unsigned long long i = s0 + lane; i < h1; i += 32) e.y[i] = mix32(__ldg(e.x + i)), scalars = true;
+            for (unsigned long long i = t0e + lane; i < s1; i += 32) e.y[i] = mix32(__ldg(e.x + i)), scalars = true;
+            if (__any_sync(~0u, scalars)) __threadfence();
+            if (lane == 0) {
+                const uint32_t slot = n_items++ % kItemSlots;
+                items[slot].t0 = 0;
+                items[slot].ent = ent;
+                items[slot].rank = rank;
+                items[slot].done_warps = 0;
+                const unsigned long long nv = v1 - v0;
+                const uint32_t n_chunks = nv ? uint32_t((nv + kChunkV - 1) / kChunkV) : 1u;
+                const uint4* x4 = reinterpret_cast<const uint4*>(e.x) + v0;
+                uint4* y4 = reinterpret_cast<uint4*>(e.y) + v0;
+                for (uint32_t c = 0; c < n_chunks; ++c) {
+                    const uint32_t idx = it++, st = idx % kTmaStages, k = idx / kTmaStages;
+                    if (k > 0) mbar_wait(&ring.empty[st], (k - 1) & 1);
+                    const unsigned long long nc = nv ? min(kChunkV, nv - c * kChunkV) : 0;
+                    meta[st].dst = y4 + c * kChunkV;
+                    meta[st].nvec = uint32_t(nc);
+                    meta[st].tag = slot | (c == 0 ? kTagFirst : 0u) | (c + 1 == n_chunks ? kTagLast : 0u);
+                    if (nc) {
+                        mbar_expect_tx(&ring.full[st], uint32_t(nc * 16));
+                        bulk_g2s(sm + st * kTmaChunk, x4 + c * kChunkV, uint32_t(nc * 16), &ring.full[st]);
+                    } else {
+                        mbar_arrive(&ring.full[st]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------ consumers
+        const int t = threadIdx.x;
+#pragma unroll 1
+        for (uint32_t it = 0;; ++it) {
+            const uint32_t st = it % kTmaStages, k = it / kTmaStages;
+            mbar_wait(&ring.full[st], k & 1);
+            const StreamMeta m = meta[st];
+            if (m.tag & kTagExit) break;
+            const uint32_t slot = m.tag & 0xffu;
+            if ((m.tag & kTagFirst) && lane == 0) atomicMax(&items[slot].t0, gtimer());
+            const uint4* buf = reinterpret_cast<const uint4*>(sm + st * kTmaChunk);
+#pragma unroll 4
+            for (uint32_t i = t; i < m.nvec; i += kTmaConsumerWarps * 32) {
+                uint4 r = buf[i];
+                r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w);
+                __stcs(m.dst + i, r);
+            }
+            if (m.tag & kTagLast) {
+                __syncwarp();
+                // cta-scope release of this warp's stores; the last warp's
+                // gpu-scope fence below is cumulative over what it observed
+                if (lane == 0) __threadfence_block();
+                if (lane == 0 && atomicAdd(&items[slot].done_warps, 1u) == kTmaConsumerWarps - 1) {
+                    const unsigned long long t1 = gtimer();
+                    __threadfence();
+                    const uint32_t ent = items[slot].ent, rank = items[slot].rank;
+                    const unsigned long long t0 = items[slot].t0;
+                    const DEnt& e = a.ents[ent];
+                    for (uint32_t q = 0; q < e.n_succ; ++q) atomicSub(a.pend_done + a.succs[e.succ_off + q], 1u);
+                    if (a.rec >= 0) {
+                        const unsigned long long idx = (unsigned long long)a.rec * a.total + e.slot + rank;
+                        if (a.stamps) {
+                            a.stamps[2 * idx] = t0;
+                            a.stamps[2 * idx + 1] = t1;
+                        }
+                        if (a.smids) a.smids[idx] = smid();
+                        atomicMin(&a.span[2 * a.rec], t0);
+                        atomicMax(&a.span[2 * a.rec + 1], t1);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ring.empty[st]);
         }
     }
 }

@@ -69,6 +69,9 @@ struct Exec {
     unsigned int* d_done = nullptr;
     unsigned int epoch = 0;
     uint32_t grid = 0;
+    // dynamic engine
+    DArgs dyn{};
+    std::vector<void*> dyn_bufs;
 };
 
 // Persistent engine tables: per group, entities take consecutive CTA slots
@@ -153,18 +156,115 @@ int build_persistent(Exec* E, const ds_exec_plan* plan) {
     return DS_OK;
 }
 
+// Dynamic engine tables: per entity its successors in the augmented graph
+// (plan edges, plus every member of group g-1 -> every member of group g when
+// the plan keeps group barriers), sorted by plan index so entities released
+// together enter the ready queue in schedule order.
+int build_dynamic(Exec* E, const ds_exec_plan* plan) {
+    const int n = plan->n_entities;
+    int max_group = -1;
+    for (int i = 0; i < n; ++i) {
+        if (plan->entities[i].parallelism > E->sm_count) return fail(DS_EINVAL, "entity wider than the device");
+        max_group = std::max(max_group, int(plan->entities[i].group));
+    }
+    std::vector<std::vector<uint32_t>> succ(n);
+    std::vector<uint32_t> npred(n, 0);
+    auto edge = [&](uint32_t p, uint32_t i) {
+        succ[p].push_back(i);
+        npred[i]++;
+    };
+    for (int i = 0; i < n; ++i) {
+        const ds_exec_entity& e = plan->entities[i];
+        for (uint32_t k = 0; k < e.n_preds; ++k) {
+            const uint32_t p = plan->preds[e.pred_off + k];
+            if (p >= uint32_t(i)) return fail(DS_EINVAL, "plan is not topologically ordered");
+            edge(p, uint32_t(i));
+        }
+    }
+    if (plan->barrier_groups && max_group > 0) {
+        std::vector<std::vector<uint32_t>> members(max_group + 1);
+        for (int i = 0; i < n; ++i) {
+            if (plan->entities[i].group < 0) return fail(DS_EINVAL, "group barriers need grouped entities");
+            members[plan->entities[i].group].push_back(uint32_t(i));
+        }
+        for (int g = 1; g <= max_group; ++g)
+            for (uint32_t i : members[g])
+                for (uint32_t p : members[g - 1]) {
+                    if (p >= i) return fail(DS_EINVAL, "plan is not in group order");
+                    edge(p, i);
+                }
+    }
+    std::vector<DEnt> ents(n);
+    std::vector<uint32_t> succs;
+    uint32_t slot = 0;
+    for (int i = 0; i < n; ++i) {
+        const ds_exec_entity& e = plan->entities[i];
+        std::sort(succ[i].begin(), succ[i].end());
+        succ[i].erase(std::unique(succ[i].begin(), succ[i].end()), succ[i].end());
+        DEnt& d = ents[i];
+        d.x = E->x[e.node];
+        d.y = E->y[e.node];
+        d.lo = e.elem_lo;
+        d.hi = e.elem_hi;
+        d.m = uint32_t(e.parallelism);
+        d.slot = slot;
+        slot += d.m;
+        d.succ_off = uint32_t(succs.size());
+        d.n_succ = uint32_t(succ[i].size());
+        succs.insert(succs.end(), succ[i].begin(), succ[i].end());
+    }
+    // duplicate edges were removed from the successor lists: recount, in
+    // predecessor ranks (every rank of a predecessor signals its successors)
+    std::vector<uint32_t> quota(n);
+    for (int i = 0; i < n; ++i) {
+        quota[i] = ents[i].m;
+        ents[i].pred_ranks = 0;
+    }
+    for (int i = 0; i < n; ++i)
+        for (uint32_t k = 0; k < ents[i].n_succ; ++k) ents[succs[ents[i].succ_off + k]].pred_ranks += ents[i].m;
+    auto dev = [&](void** p, size_t bytes, const void* src) -> int {
+        DS_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 4)));
+        E->dyn_bufs.push_back(*p);
+        if (src && bytes) DS_CUDA(cudaMemcpy(*p, src, bytes, cudaMemcpyHostToDevice));
+        return DS_OK;
+    };
+    DArgs& a = E->dyn;
+    a.n = uint32_t(n);
+    int rc = 0;
+    if ((rc = dev((void**)&a.ents, ents.size() * sizeof(DEnt), ents.data())) ||
+        (rc = dev((void**)&a.succs, succs.size() * 4, succs.data())) ||
+        (rc = dev((void**)&a.quota, quota.size() * 4, quota.data())) ||
+        (rc = dev((void**)&a.claimed, size_t(n) * 4, nullptr)) ||
+        (rc = dev((void**)&a.pend_claim, size_t(n) * 4, nullptr)) ||
+        (rc = dev((void**)&a.pend_done, size_t(n) * 4, nullptr)) || (rc = dev((void**)&a.idle, 4, nullptr)))
+        return rc;
+    const bool tma = E->workload == DS_WL_MIX32_TMA || E->engine == DS_ENGINE_STREAM;
+    void* k = E->engine == DS_ENGINE_STREAM ? reinterpret_cast<void*>(k3_stream)
+              : tma                         ? reinterpret_cast<void*>(k3_dynamic<true>)
+                                            : reinterpret_cast<void*>(k3_dynamic<false>);
+    DS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tma ? kTmaSmem : kNodeSmem));
+    E->grid = uint32_t(E->sm_count);
+    return DS_OK;
+}
+
 void* kernel_of(int wl) {
     switch (wl) {
         case DS_WL_AXPY32: return reinterpret_cast<void*>(k2_axpy);
         case DS_WL_MIX32_BULK: return reinterpret_cast<void*>(k2_mix_bulk);
-        default: return reinterpret_cast<void*>(k2_mix);
+        case DS_WL_MIX32_TMA: return reinterpret_cast<void*>(k2_mix_tma);
+        case DS_WL_MIX32_LDG8: return reinterpret_cast<void*>(k2_mix<8>);
+        default: return reinterpret_cast<void*>(k2_mix<4>);
     }
 }
 
-int smem_of(int wl) { return wl == DS_WL_MIX32_BULK ? kBulkStages * kBulkChunk : kNodeSmem; }
+// dynamic shared memory per CTA: every node kernel takes more than half an
+// SM's 228 KB, so an entity launched with grid = m holds exactly m SMs
+int smem_of(int wl) { return wl == DS_WL_MIX32_TMA ? kTmaSmem : kNodeSmem; }
+
+int threads_of(int wl, int requested) { return wl == DS_WL_MIX32_TMA ? kTmaThreads : requested; }
 
 int set_attrs(int wl) {
-    DS_CUDA(cudaFuncSetAttribute(kernel_of(wl), cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem));
+    DS_CUDA(cudaFuncSetAttribute(kernel_of(wl), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(wl)));
     return DS_OK;
 }
 
@@ -257,6 +357,7 @@ void destroy(Exec* E) {
     if (E->d_item_off) cudaFree(E->d_item_off);
     if (E->d_items) cudaFree(E->d_items);
     if (E->d_done) cudaFree(E->d_done);
+    for (void* p : E->dyn_bufs) cudaFree(p);
     if (E->s) cudaStreamDestroy(E->s);
     }
     if (E->gctx) driver().greenDestroy(E->gctx);
@@ -336,8 +437,8 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
             kp.sharedMemBytes = 0;
         } else {
             kp.gridDim = dim3(unsigned(e.parallelism));
-            kp.blockDim = dim3(unsigned(E->threads));
-            kp.sharedMemBytes = unsigned(smem_of(E->workload) > kNodeSmem ? smem_of(E->workload) : kNodeSmem);
+            kp.blockDim = dim3(unsigned(threads_of(E->workload, E->threads)));
+            kp.sharedMemBytes = unsigned(smem_of(E->workload));
         }
         kp.kernelParams = params;
         DS_CUDA(cudaGraphAddKernelNode(&node[i], E->graph, deps.data(), deps.size(), &kp));
@@ -379,11 +480,29 @@ struct ExecHandle {
     PlanCopy P;
 };
 
+// Placement probe: one CTA per SM, only the SMs in `mask` (by %smid) stream
+// `elems` elements each; the span tells whether SMs sharing a TPC/GPC share
+// bandwidth (tools/node_bw_sweep.py --placement).
+__global__ void __launch_bounds__(1024, 1) k2_place(const uint32_t* x, uint32_t* y, const uint32_t* mask,
+                                                    unsigned long long base, unsigned long long elems,
+                                                    unsigned long long* span) {
+    const uint32_t sid = smid();
+    if (!((mask[sid >> 5] >> (sid & 31)) & 1u)) return;
+    __shared__ unsigned long long t0;
+    if (threadIdx.x == 0) t0 = gtimer();
+    mix_ldg_slice<4>(x, y, base + sid * elems, base + (sid + 1) * elems);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMin(span, t0);
+        atomicMax(span + 1, gtimer());
+    }
+}
+
 extern "C" {
 
 int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device, void** exec) {
     if (!plan || !cfg || !exec || plan->n_entities < 1 || plan->n_nodes < 1) return fail(DS_EINVAL, "bad plan");
-    if (cfg->workload < DS_WL_MIX32 || cfg->workload > DS_WL_MIX32_BULK) return fail(DS_EINVAL, "bad workload");
+    if (cfg->workload < DS_WL_MIX32 || cfg->workload > DS_WL_LAST) return fail(DS_EINVAL, "bad workload");
     const int threads = cfg->block_threads > 0 ? cfg->block_threads : 1024;
     if (threads > 1024 || threads % 32) return fail(DS_EINVAL, "block_threads must be a multiple of 32 <= 1024");
     auto* H = new ExecHandle();
@@ -448,6 +567,10 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     if (E->engine == DS_ENGINE_PERSISTENT) {
         if (E->workload != DS_WL_MIX32) return bail(fail(DS_EINVAL, "persistent engine runs the mix32 workload"));
         if (int rc = build_persistent(E, &H->P.plan)) return bail(rc);
+    } else if (E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM) {
+        if (E->workload != DS_WL_MIX32 && E->workload != DS_WL_MIX32_TMA)
+            return bail(fail(DS_EINVAL, "dynamic engines run the mix32 workloads"));
+        if (int rc = build_dynamic(E, &H->P.plan)) return bail(rc);
     } else if (E->engine != DS_ENGINE_GRAPH && E->engine != DS_ENGINE_GRAPH_FREE) {
         return bail(fail(DS_EINVAL, "unknown engine"));
     }
@@ -471,7 +594,8 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     if (replays < 1 || warmup < 0 || !trace || !trace->span) return fail(DS_EINVAL, "bad run arguments");
     CtxGuard guard(E);
     const bool want_stamps = trace->stamps || trace->smids;
-    const bool persistent = E->engine == DS_ENGINE_PERSISTENT;
+    const bool persistent =
+        E->engine == DS_ENGINE_PERSISTENT || E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM;
     if (replays > E->cap || (!persistent && !E->exec) || (want_stamps && !E->stamps)) {
         if (E->span) cudaFree(E->span);
         if (E->stamps) cudaFree(E->stamps);
@@ -503,7 +627,25 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     for (auto& e : ev) DS_CUDA(cudaEventCreate(&e));
     for (int r = -warmup; r < replays; ++r) {
         if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
-        if (persistent) {
+        if (E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM) {
+            DArgs da = E->dyn;
+            da.rec = r;
+            da.stamps = E->stamps;
+            da.smids = E->smids;
+            da.span = E->span;
+            da.total = E->total_ctas;
+            k3_dyn_reset<<<1, 512, 0, E->s>>>(da);
+            if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
+            const bool stream = E->engine == DS_ENGINE_STREAM;
+            const bool tma = E->workload == DS_WL_MIX32_TMA || stream;
+            void* kargs[] = {&da};
+            DS_CUDA(cudaLaunchCooperativeKernel(
+                stream ? reinterpret_cast<void*>(k3_stream)
+                : tma  ? reinterpret_cast<void*>(k3_dynamic<true>)
+                       : reinterpret_cast<void*>(k3_dynamic<false>),
+                dim3(E->grid), dim3(tma ? unsigned(kTmaThreads) : 1024u), kargs, size_t(tma ? kTmaSmem : kNodeSmem),
+                E->s));
+        } else if (persistent) {
             PArgs pa{E->d_ents, E->d_preds, E->d_item_off, E->d_items, E->d_done, E->epoch++, r,
                      E->stamps, E->smids, E->span, E->total_ctas};
             void* kargs[] = {&pa};
@@ -548,38 +690,44 @@ int ds_exec_free(void* exec) {
 int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int block_threads, int reps,
                          float* ms_per_launch, uint64_t* span_ns, int device) {
     if (ctas < 1 || reps < 1 || elems_per_cta < 4) return fail(DS_EINVAL, "bad bench arguments");
-    if (workload < DS_WL_MIX32 || workload > DS_WL_MIX32_BULK) return fail(DS_EINVAL, "bad workload");
-    const int threads = block_threads > 0 ? block_threads : 1024;
+    if (workload < DS_WL_MIX32 || workload > DS_WL_LAST) return fail(DS_EINVAL, "bad workload");
+    const int threads = threads_of(workload, block_threads > 0 ? block_threads : 1024);
     DS_CUDA(cudaSetDevice(device));
     if (int rc = set_attrs(workload)) return rc;
     const uint64_t n = uint64_t(ctas) * elems_per_cta;
+    // consecutive launches walk `regions` disjoint ranges whose total (x and y)
+    // is >= 512 MB, so every launch streams from HBM, not from the 126 MB L2
+    const uint64_t regions = std::max<uint64_t>(1, ((512ull << 20) / 8 + n - 1) / n);
     uint32_t *x = nullptr, *y = nullptr;
     int* replay = nullptr;
     unsigned long long* span = nullptr;
-    DS_CUDA(cudaMalloc(&x, n * 4));
-    DS_CUDA(cudaMalloc(&y, n * 4));
+    DS_CUDA(cudaMalloc(&x, n * regions * 4));
+    DS_CUDA(cudaMalloc(&y, n * regions * 4));
     DS_CUDA(cudaMalloc(&replay, sizeof(int)));
     DS_CUDA(cudaMalloc(&span, 16));
-    k2_init<<<592, 512>>>(x, n, 7u, workload == DS_WL_AXPY32, y);
+    k2_init<<<592, 512>>>(x, n * regions, 7u, workload == DS_WL_AXPY32, y);
     const int zero = 0;
     const unsigned long long sinit[2] = {~0ull, 0};
     DS_CUDA(cudaMemcpy(replay, &zero, sizeof(int), cudaMemcpyHostToDevice));
     NodeArgs a{};
     a.x = x;
     a.y = y;
-    a.lo = 0;
-    a.hi = n;
     a.span = span;
     a.replay = replay;
     a.total = uint32_t(ctas);
     a.a = 0.75f;
     a.cap = 1;
-    const size_t sm = size_t(smem_of(workload) > kNodeSmem ? smem_of(workload) : kNodeSmem);
+    const size_t sm = size_t(smem_of(workload));
+    uint64_t launches = 0;
     auto launch = [&]() {
+        a.lo = (launches++ % regions) * n;
+        a.hi = a.lo + n;
         switch (workload) {
             case DS_WL_AXPY32: k2_axpy<<<ctas, threads, sm>>>(a); break;
             case DS_WL_MIX32_BULK: k2_mix_bulk<<<ctas, threads, sm>>>(a); break;
-            default: k2_mix<<<ctas, threads, sm>>>(a);
+            case DS_WL_MIX32_TMA: k2_mix_tma<<<ctas, threads, sm>>>(a); break;
+            case DS_WL_MIX32_LDG8: k2_mix<8><<<ctas, threads, sm>>>(a); break;
+            default: k2_mix<4><<<ctas, threads, sm>>>(a);
         }
     };
     for (int i = 0; i < 3; ++i) launch();  // warm-up
@@ -606,6 +754,39 @@ int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int blo
     cudaFree(span);
     if (ms_per_launch) *ms_per_launch = ms / reps;
     if (span_ns) *span_ns = s[1] - s[0];
+    return DS_OK;
+}
+
+int ds_node_placement_bench(const uint32_t* mask8, uint64_t elems, int reps, double* avg_span_ns, int device) {
+    if (!mask8 || elems < 4 || reps < 1) return fail(DS_EINVAL, "bad placement arguments");
+    DS_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    DS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const uint64_t per = 256 * elems;  // indexed by smid < 256
+    const uint64_t regions = std::max<uint64_t>(1, ((1024ull << 20) / 8 + per - 1) / per);
+    uint32_t *x = nullptr, *y = nullptr, *m = nullptr;
+    unsigned long long* span = nullptr;
+    DS_CUDA(cudaMalloc(&x, per * regions * 4));
+    DS_CUDA(cudaMalloc(&y, per * regions * 4));
+    DS_CUDA(cudaMalloc(&m, 32));
+    DS_CUDA(cudaMalloc(&span, 16 * (reps + 2)));
+    DS_CUDA(cudaMemcpy(m, mask8, 32, cudaMemcpyHostToDevice));
+    DS_CUDA(cudaFuncSetAttribute(k2_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem));
+    k2_init<<<592, 512>>>(x, per * regions, 3u, 0, y);
+    std::vector<unsigned long long> init(2 * (reps + 2));
+    for (size_t i = 0; i < init.size(); i += 2) init[i] = ~0ull, init[i + 1] = 0;
+    DS_CUDA(cudaMemcpy(span, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+    for (int r = 0; r < reps + 2; ++r)
+        k2_place<<<sms, 1024, kNodeSmem>>>(x, y, m, (r % regions) * per, elems, span + 2 * r);
+    DS_CUDA(cudaDeviceSynchronize());
+    DS_CUDA(cudaMemcpy(init.data(), span, init.size() * 8, cudaMemcpyDeviceToHost));
+    double tot = 0;
+    for (int r = 2; r < reps + 2; ++r) tot += double(init[2 * r + 1] - init[2 * r]);
+    *avg_span_ns = tot / reps;
+    cudaFree(x);
+    cudaFree(y);
+    cudaFree(m);
+    cudaFree(span);
     return DS_OK;
 }
 

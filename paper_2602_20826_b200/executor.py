@@ -26,8 +26,8 @@ import numpy as np
 from . import _abi
 from ._lib import check, lib
 
-WL_MIX32, WL_AXPY32, WL_MIX32_BULK = 0, 1, 2
-BYTES_PER_ELEM = {WL_MIX32: 8, WL_AXPY32: 12, WL_MIX32_BULK: 8}
+WL_MIX32, WL_AXPY32, WL_MIX32_BULK, WL_MIX32_TMA, WL_MIX32_LDG8 = 0, 1, 2, 3, 4
+BYTES_PER_ELEM = {WL_MIX32: 8, WL_AXPY32: 12, WL_MIX32_BULK: 8, WL_MIX32_TMA: 8, WL_MIX32_LDG8: 8}
 
 
 class ds_exec_entity(C.Structure):
@@ -47,7 +47,7 @@ class ds_exec_cfg(C.Structure):
                 ("sm_limit", C.c_int32), ("engine", C.c_int32), ("reserved", C.c_int32)]
 
 
-ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE = 0, 1, 2
+ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAM = 0, 1, 2, 3, 4
 FREE_CTA_FACTOR = 4  # DS_FREE_CTA_FACTOR
 
 

@@ -30,7 +30,7 @@ def _scheme_and_loads(dag, M):
     return schemes[0], loads, edges
 
 
-@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_BULK])
+@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_BULK, X.WL_MIX32_TMA, X.WL_MIX32_LDG8])
 @pytest.mark.parametrize("name,dag,M", [("fig2_M8_split", workloads.make_example_task(), 8),
                                         ("c1_fan", workloads.c1_fork_join(), 148),
                                         ("c4", workloads.oversized_dag(1, 148), 148)])
@@ -104,7 +104,7 @@ def test_baselines_run_and_respect_edges(kind):
 
 
 def test_node_kernel_bench_sane():
-    for wl in (X.WL_MIX32, X.WL_MIX32_BULK, X.WL_AXPY32):
+    for wl in (X.WL_MIX32, X.WL_MIX32_BULK, X.WL_MIX32_TMA, X.WL_MIX32_LDG8, X.WL_AXPY32):
         ms, span = X.node_kernel_bench(wl, 148, 1 << 20, reps=5)
         gbs = 148 * (1 << 20) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
         assert 500 < gbs < 9000, (wl, gbs)
@@ -147,4 +147,44 @@ def test_persistent_engine(barrier):
                 assert X.group_overlap_violations(plan, res, r) == 0
         for v in range(len(loads)):
             assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+        ex.close()
+
+
+@pytest.mark.parametrize("engine,workload", [(X.ENGINE_DYNAMIC, X.WL_MIX32), (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA),
+                                             (X.ENGINE_STREAM, X.WL_MIX32_TMA)])
+@pytest.mark.parametrize("barrier", [True, False])
+def test_dynamic_engine(barrier, engine, workload):
+    """DS_ENGINE_DYNAMIC: resident CTAs claim (entity, rank) items from a
+    device-side ready queue — every item runs exactly once per replay, outputs
+    bit-exact, precedence / SM-exclusivity / group-order contracts hold."""
+    cases = [(workloads.make_example_task(), 8), (workloads.oversized_dag(2, 148), 148),
+             (workloads.inception_dag(), 148), (workloads.c1_fork_join(), 148)]
+    for dag, M in cases:
+        s, loads, edges = _scheme_and_loads(dag, M)
+        plan = X.plan_from_scheme(s, loads, UNIT + 5, barrier_groups=barrier)
+        ex = X.Executor(plan, workload=workload, engine=engine, sm_limit=0 if M == 148 else 8)
+        res = ex.run(8, warmup=2)
+        for r in range(8):
+            st = res.stamps[r]
+            assert (st[:, 0] > 0).all() and (st[:, 1] >= st[:, 0]).all()
+            assert X.check_precedence(plan, res, r) == []
+            assert X.check_sm_exclusive(plan, res, r) == 0
+            if barrier:
+                assert X.group_overlap_violations(plan, res, r) == 0
+        for v in range(len(loads)):
+            assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+        ex.close()
+
+
+def test_dynamic_engine_runs_baseline_plans():
+    dag = workloads.inception_dag()
+    loads = [l for _, l in dag[0]]
+    for kind, engine in (("serial", X.ENGINE_DYNAMIC), ("multistream", X.ENGINE_DYNAMIC),
+                         ("multistream", X.ENGINE_STREAM)):
+        plan = X.plan_baseline(kind, loads, dag[1], 148, 4096 + 7)
+        ex = X.Executor(plan, engine=engine, workload=X.WL_MIX32_TMA)
+        res = ex.run(5, warmup=1)
+        for r in range(5):
+            assert X.check_precedence(plan, res, r) == []
+            assert X.check_sm_exclusive(plan, res, r) == 0
         ex.close()

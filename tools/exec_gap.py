@@ -75,30 +75,37 @@ def main():
     ap.add_argument("--replays", type=int, default=30)
     ap.add_argument("--unit", type=int, default=1 << 17)
     ap.add_argument("--workload", type=int, default=X.WL_MIX32)
-    ap.add_argument("--variants", default="proposed_deps,persistent_deps,multistream,multistream_free")
+    ap.add_argument("--variants", default="proposed,proposed_deps,persistent_deps,dynamic,dynamic_deps,dynamic_deps_tma,multistream,multistream_tma,dyn_multistream,multistream_free")
+    ap.add_argument("--sm-limit", type=int, default=0)
+    ap.add_argument("--avg-load", type=int, default=20)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "exec_gap.json"))
     args = ap.parse_args()
+    M = args.sm_limit or 148
     peak = 6539.2
-    corpus = _lib.Corpus(600, seed=1)
+    corpus = _lib.Corpus(600, seed=1, avg_load=args.avg_load)
     b = corpus.batch()
     sizes = np.diff(b.node_off.astype(np.int64))
     picked = [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:args.dags]
     dags = [dag_from_batch(b, d) for d in picked]
-    schemes, st = scheme.schedule_batch(pack(dags), 148)
+    schemes, st = scheme.schedule_batch(pack(dags), M)
     bpe = X.BYTES_PER_ELEM[args.workload]
     out = []
     for (loads, edges), sch in zip(dags, schemes):
         row = {"n": len(loads), "groups": len(sch.groups)}
         tot = sum(X.node_elements(loads, args.unit)) * bpe
-        row["work_us"] = tot / (peak * 1e3)
+        row["work_us"] = tot / (peak * 1e3) * 148 / M
         for kind in args.variants.split(","):
             engine = (X.ENGINE_PERSISTENT if kind.startswith("persistent") else
+                      X.ENGINE_STREAM if kind.startswith("str") else
+                      X.ENGINE_DYNAMIC if kind.startswith("dyn") else
                       X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
-            if kind.startswith(("proposed", "persistent")):
-                plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=not kind.endswith("_deps"))
+            wl = X.WL_MIX32_TMA if kind.endswith("_tma") or kind.startswith("str") else args.workload
+            kind_ = kind.replace("_tma", "")
+            if kind_.startswith(("proposed", "persistent", "dynamic", "stream")):
+                plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=not kind_.endswith("_deps"))
             else:
-                plan = X.plan_baseline(kind.replace("_free", ""), loads, edges, 148, args.unit)
-            ex = X.Executor(plan, workload=args.workload, engine=engine)
+                plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("str_", ""), loads, edges, M, args.unit)
+            ex = X.Executor(plan, workload=wl, engine=engine, sm_limit=args.sm_limit)
             res = ex.run(args.replays, warmup=3, stamps=True)
             if engine == X.ENGINE_GRAPH_FREE:
                 plan._slots = ex.slots
