@@ -1381,6 +1381,241 @@ __global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
     }
 }
 
+// k1_back_lane: p_schedule with ONE LANE per DAG. The schedule is a
+// sequential greedy over the executed groups (scheduler.cpp:214-359): in
+// k1_back a warp walks it warp-uniformly, so 31 of 32 lanes replicate the
+// scalar control flow (11 groups per C5 DAG, 70% singletons). Here every lane
+// runs its own DAG's walk over the same k1_front/k1_mid state (read through
+// L1 straight from the hand-off: the 32 DAGs of a warp are adjacent in it),
+// so a warp instruction advances 32 DAGs. Same u32 words and the same
+// helpers (exact rationals, overflow in-band as den 0); a DAG that overflows
+// u32, or has more than kLaneMembers pending members in one group or more
+// than kLaneSplits segmented nodes, goes to the retry tiers, which recompute
+// it from scratch.
+constexpr int kLaneMembers = 16;
+constexpr int kLaneSplits = 8;
+constexpr int kLaneRetry = -2;
+constexpr int kLaneWarps = 4;
+// Measured alternatives (ms, 1M C5 DAGs): this form 3.2-3.4; walking the groups
+// in warp lock-step (__syncwarp per group) 3.64; the same walk as a state
+// struct 3.66; staging the warp's 32 DAGs in shared memory 7.3 (residency
+// fell to 12 warps/SM and the walk is latency bound). k1_back (warp per DAG)
+// 4.40.
+
+__device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
+                                             const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
+    const u64* __restrict__ pred = a.h.pred + n0;
+    const u64* __restrict__ anc = a.h.anc + n0;
+    const u64* __restrict__ desc = a.h.desc + n0;
+    const u64* __restrict__ divg = a.h.divg + n0;
+    const u32* __restrict__ ln = a.h.ln + n0;
+    const u32* __restrict__ ldn = a.h.ld + n0;
+    const uint16_t* __restrict__ ro = a.h.ro + n0;
+    // residual loads of segmented nodes (scheduler.cpp:318-328), newest last
+    int n_over = 0;
+    int over_v[kLaneSplits];
+    u32 over_n[kLaneSplits], over_d[kLaneSplits];
+    auto load = [&](int v) -> RatT<u32> {
+        for (int k = n_over - 1; k >= 0; --k) {
+            if (over_v[k] == v) return RatT<u32>{over_n[k], over_d[k]};
+        }
+        return RatT<u32>{__ldg(ln + v), __ldg(ldn + v)};
+    };
+    bool ovf = false;
+    const u64 V = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    RatT<u32> proposed{0, 1};
+    u64 done = 0;
+    int gidx = 0;
+#pragma unroll 1
+    for (int g = 0; g < ndiv; ++g) {
+        const u64 G = __ldg(divg + g);
+        const u64 org = G & ~done;
+        if (!org) continue;  // fully absorbed by earlier launches
+        RatT<u32> R{0, 1};
+        int used = 0;
+        u64 conc = 0;  // union of the members' concurrent sets (+ themselves)
+        if (!(org & (org - 1))) {
+            // one pending member: m = min(m^max, M), no shed/fill
+            const int v = __ffsll(org) - 1;
+            const RatT<u32> l = load(v);
+            int cp = q_max_par(l, P);
+            if (cp < 0) {
+                ovf = true;
+                cp = 1;
+            }
+            cp = min(cp, P.M);
+            R = q_exec(l, cp, P);
+            ovf |= R.d == 0;
+            used = cp;
+            conc = ~(__ldg(anc + v) | __ldg(desc + v));
+        } else {
+            // apportion (scheduler.cpp:35-95) over the pending loads
+            int nm = 0;
+            int mv[kLaneMembers], mq[kLaneMembers], cap[kLaneMembers];
+            u32 rn[kLaneMembers], rd[kLaneMembers];
+            RatT<u32> Wt{0, 1};
+#pragma unroll 1
+            for (u64 b = org; b; b &= b - 1) {
+                if (nm == kLaneMembers) return kLaneRetry;
+                const int v = __ffsll(b) - 1;
+                mv[nm++] = v;
+                Wt = q_add(Wt, load(v));
+            }
+            if (Wt.d == 0 || Wt.n == 0) return DS_EOVERFLOW;
+            int tot = 0, capsum = 0;
+#pragma unroll 1
+            for (int k = 0; k < nm; ++k) {
+                const RatT<u32> l = load(mv[k]);
+                int cp = q_max_par(l, P);
+                if (cp < 0) {
+                    ovf = true;
+                    cp = 1;
+                }
+                cp = min(cp, P.M);
+                // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n); floor and remainder
+                const u32 qn = mulc(mulc(l.n, u32(P.M), ovf), Wt.d, ovf);
+                const u32 qd = mulc(l.d, Wt.n, ovf);
+                if (qd == 0) return DS_EOVERFLOW;
+                const u32 fl = qn / qd;
+                const long long flc = fl > 0x7fffffffu ? 0x7fffffffll : (long long)fl;
+                const int base = int(max(1ll, min(flc, (long long)cp)));
+                mq[k] = base;
+                cap[k] = cp;
+                rn[k] = qn - fl * qd;
+                rd[k] = qd;
+                tot += base;
+                capsum += cp;
+            }
+            const int target = min(P.M, capsum);
+#pragma unroll 1
+            while (tot > P.M || tot < target) {
+                const bool shed = tot > P.M;
+                Pick<u32> c{{0, 1}, {0, 1}, -1};
+                int ck = -1;
+#pragma unroll 1
+                for (int k = 0; k < nm; ++k) {
+                    const int m = mq[k];
+                    if (shed ? m <= 1 : m >= cap[k]) continue;
+                    const Pick<u32> x{q_exec_raw(load(mv[k]), shed ? m - 1 : m, P),
+                                      shed ? RatT<u32>{0, 1} : RatT<u32>{rn[k], rd[k]}, mv[k]};
+                    ovf |= x.k1.d == 0;
+                    if (pick_better<u32>(x, c, shed)) {
+                        c = x;
+                        ck = k;
+                    }
+                }
+                if (ck < 0) return DS_EINVARIANT;
+                const int step = shed ? -1 : 1;
+                mq[ck] += step;
+                tot += step;
+            }
+            // members: exec, response = first strict max
+            int bott = -1;
+#pragma unroll 1
+            for (int k = 0; k < nm; ++k) {
+                const RatT<u32> e = q_exec(load(mv[k]), mq[k], P);
+                ovf |= e.d == 0;
+                if (bott < 0 || q_cmp(e, R) > 0) {
+                    R = e;
+                    bott = k;
+                }
+                used += mq[k];
+                conc |= ~(__ldg(anc + mv[k]) | __ldg(desc + mv[k]));
+            }
+        }
+        const int spare0 = P.M - used;
+        // candidates (scheduler.cpp:253-280): sources of the pool that are
+        // released, launched in rank order (:286-330)
+        const u64 pool = V & conc & ~G;
+        const u64 avail = pool & ~done;
+        u64 whole = 0;
+        if (avail && spare0 >= 1) {
+            u64 rm = 0;
+#pragma unroll 1
+            for (u64 b = avail; b; b &= b - 1) {
+                const int c = __ffsll(b) - 1;
+                const u64 p = __ldg(pred + c);
+                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(ro + c) & 0xff);
+            }
+            int spare = spare0;
+#pragma unroll 1
+            for (; rm && spare >= 1; rm &= rm - 1) {
+                const int c = __ldg(ro + (__ffsll(rm) - 1)) >> 8;
+                const RatT<u32> l = load(c);
+                int mp = q_max_par(l, P);
+                if (mp < 0) {
+                    ovf = true;
+                    mp = 1;
+                }
+                const int mc = min(mp, spare);
+                const RatT<u32> dur = q_exec(l, mc, P);
+                ovf |= dur.d == 0;
+                spare -= mc;
+                if (q_cmp(dur, R) <= 0) {
+                    whole |= 1ull << c;
+                } else {  // split: the residual replaces the origin
+                    const RatT<u32> pl = n_mul_int(R, u32(mc));
+                    const RatT<u32> rl = n_sub(l, pl);
+                    ovf |= pl.d == 0 || rl.d == 0;
+                    if (n_over == kLaneSplits) return kLaneRetry;
+                    over_v[n_over] = c;
+                    over_n[n_over] = rl.n;
+                    over_d[n_over] = rl.d;
+                    ++n_over;
+                    break;
+                }
+            }
+        }
+        done |= org | whole;
+        proposed = q_add(proposed, R);
+        ovf |= proposed.d == 0;
+        ++gidx;
+    }
+    if (ovf) return DS_EOVERFLOW;
+    if (done != V) return DS_EINVARIANT;  // "scheduling finished with unplaced kernels"
+    bound = proposed;
+    n_groups = gidx;
+    return DS_OK;
+}
+
+#ifndef DS_LANE_MIN_BLOCKS
+#define DS_LANE_MIN_BLOCKS 12  // 40 registers: 3.23 ms vs 3.44 at 70 (1M C5 DAGs)
+#endif
+template <bool UNUSED = false>
+__global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_lane(const K1Args a) {
+    const int lane = threadIdx.x & 31;
+    const u32 nbase = a.node_off[0];
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+#pragma unroll 1
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(a.retry_count + 5, 32u);
+        t = __shfl_sync(FULL, t, 0);
+        if (t >= a.n_dags) break;
+        const u64 d = u64(t) + lane;
+        if (d >= a.n_dags || a.status[d] != kStPending) continue;
+        const u32 n0 = a.node_off[d] - nbase;
+        const int n = int(a.node_off[d + 1] - nbase - n0);
+        RatT<u32> bound{0, 0};
+        int ng = 0;
+        const int st = schedule_lane(a, n0, n, a.h.ndiv[d], P, bound, ng);
+        if (st == DS_EOVERFLOW || st == kLaneRetry) {  // recomputed from scratch in wider words
+            a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
+            a.status[d] = kStRetried;
+            continue;
+        }
+        int64_t* b = a.bounds + 10 * d;
+        if (st == DS_OK) {
+            b[0] = (long long)bound.n;
+            b[1] = (long long)bound.d;
+        } else {
+            for (int k = 0; k < 10; ++k) b[k] = 0;
+        }
+        a.status[d] = st;
+        if (a.n_groups) a.n_groups[d] = (unsigned short)(st == DS_OK ? ng : 0);
+    }
+}
+
 // Retry passes over the DAGs queued by the narrower tier: T = u64 reads
 // retry/retry_count and queues its own overflows in retry2; T = u128 is final.
 template <bool DETAIL, class T>

@@ -15,6 +15,7 @@ struct K1Occupancy {
     int grid_front = 0;  // split bounds pass (k1_front / k1_mid / k1_back)
     int grid_mid = 0;
     int grid_back = 0;
+    int grid_back_lane = 0;  // k1_back_lane (one lane per DAG)
 };
 
 constexpr int kWarpsSmall = 4;  // WarpState<1,u64> per warp, 4 warps per CTA

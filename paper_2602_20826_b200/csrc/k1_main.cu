@@ -43,7 +43,10 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
             return e;
         if ((e = cudaFuncSetAttribute(k1_back<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
             return e;
-        int of = 0, om = 0, ob = 0;
+        int of = 0, om = 0, ob = 0, obl = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obl, k1_back_lane<>, 32 * kLaneWarps, 0))) return e;
+        if (obl < 1) return cudaErrorInvalidConfiguration;
+        occ.grid_back_lane = sms * obl;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k1_front<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k1_mid<>, 32 * kWarpsSmall, kSmemSmall)))
@@ -101,7 +104,18 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
     if (split && (a.mask & DS_M_PROPOSED)) {
         k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = mark("k1_mid")) != cudaSuccess) return e;
-        k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        // one lane per DAG (default) or one warp per DAG (DS_K1_BACK=warp)
+        static const bool warp_back = [] {
+            const char* env = getenv("DS_K1_BACK");
+            return env && env[0] == 'w';
+        }();
+        if (warp_back) {
+            k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        } else {
+            const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
+            k1_back_lane<><<<int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane)), 32 * kLaneWarps, 0,
+                             s>>>(a);
+        }
         if ((e = mark("k1_back")) != cudaSuccess) return e;
     }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with

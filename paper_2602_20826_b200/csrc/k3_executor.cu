@@ -432,6 +432,9 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
         cudaKernelNodeParams kp{};
         kp.func = kernel_of(E->workload);
         if (E->engine == DS_ENGINE_GRAPH_FREE) {  // unconstrained launch shape: CTAs share SMs
+            // the shared-memory-staged kernels need their ring (and the TMA
+            // one its producer warp): the free launch runs the plain LDG body
+            if (E->workload == DS_WL_MIX32_TMA || E->workload == DS_WL_MIX32_BULK) kp.func = kernel_of(DS_WL_MIX32);
             kp.gridDim = dim3(unsigned(e.parallelism) * DS_FREE_CTA_FACTOR);
             kp.blockDim = dim3(256u);
             kp.sharedMemBytes = 0;

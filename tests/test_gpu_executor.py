@@ -188,3 +188,18 @@ def test_dynamic_engine_runs_baseline_plans():
             assert X.check_precedence(plan, res, r) == []
             assert X.check_sm_exclusive(plan, res, r) == 0
         ex.close()
+
+
+@pytest.mark.parametrize("workload", [X.WL_MIX32_TMA, X.WL_MIX32_BULK, X.WL_MIX32])
+def test_free_launch_runs_every_workload(workload):
+    """GRAPH_FREE launches 4m 256-thread CTAs without the shared-memory ring:
+    the staged workloads run their plain LDG body there (same outputs)."""
+    dag = workloads.make_fan(4, 6, 2)
+    loads = [l for _, l in dag[0]]
+    plan = X.plan_baseline("multistream", loads, dag[1], 148, UNIT + 3)
+    ex = X.Executor(plan, workload=workload, engine=X.ENGINE_GRAPH_FREE)
+    res = ex.run(3, warmup=1, stamps=False)
+    assert (res.makespan_us > 0).all()
+    for v in range(len(loads)):
+        assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+    ex.close()
