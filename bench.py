@@ -8,9 +8,11 @@ inputs resident in HBM. Ranks are independent shards (no collective on the
 data path: DAGs are independent), so scaling is weak: N GPUs analyse N x 1M
 DAGs. ``value`` = all ranks' DAGs / max-over-ranks device time.
 
-e2e: the same metric through the public C-ABI (ds_analyze_batch) with pinned
-HOST buffers; H2D of the packed DAGs and D2H of statuses/bounds are inside
-the timed region every step.
+e2e: the same metric through the public C-ABI with pinned HOST buffers —
+ds_analyze_batch16 (the compact wire form: 16-bit loads and edges, 2.4x fewer
+PCIe bytes) when the corpus fits it, else ds_analyze_batch (--wide forces
+it); H2D of the packed DAGs and D2H of statuses/bounds are inside the timed
+region every step.
 
 --impl reference: the reference's own CPU implementation of the path —
 evaluate_corpus (experiment.cpp:52-79) + lower_bound from the reference
@@ -136,7 +138,7 @@ def kernel_alg_bytes(name, n, N, E, integer, n_div):
         return offs + loads + 4 * E + 68 * n + handoff_masks + handoff_loads
     if name == "k1_mid":     # status + pred/anc + loads in; ranks, division groups, status out
         return 4 * n + 4 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 2 * n + 4 * n
-    if name == "k1_back":    # status + hand-off in; proposed bound, status, groups out
+    if name in ("k1_back", "k1_back_lane"):  # status + hand-off in; proposed bound, status, groups out
         return 4 * n + 4 * n + 2 * n + handoff_masks + handoff_loads + 2 * N + 8 * n_div + 16 * n + 4 * n + 2 * n
     return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
 
@@ -266,6 +268,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-makespan", action="store_true")
+    ap.add_argument("--wide", action="store_true", help="e2e through ds_analyze_batch (64-bit loads, 32-bit edges)")
     ap.add_argument("--makespan-replays", type=int, default=200)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -334,21 +337,34 @@ def main():
     res_groups = torch.zeros(n, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)
     import ctypes as C
     r = _abi.ds_results(res_status.ctypes.data, res_bounds.ctypes.data, res_groups.ctypes.data)
-    cb = batch.as_c()
     pl = _lib.platform(SM_COUNT)
     L = _lib.lib()
-    _lib.check(L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank, None, 0))
+    # the caller's host arrays in the compact wire form when the batch fits it
+    # (integer loads < 2^16, <= 256 nodes: every C5 corpus), pinned; the
+    # conversion is the caller's packing, outside the timed region
+    compact = batch.compact16_ok() and not args.wide
+    if compact:
+        pin16 = (torch.empty(batch.load_num.shape[0], dtype=torch.int16, pin_memory=True).numpy().view(np.uint16),
+                 torch.empty(batch.edges.shape[0], dtype=torch.int16, pin_memory=True).numpy().view(np.uint16))
+        load16, edges16 = batch.compact16(out=pin16)
+        cb = batch.as_c16(load16, edges16)
+        call = lambda: L.ds_analyze_batch16(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank)  # noqa: E731
+    else:
+        cb = batch.as_c()
+        call = lambda: L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank, None, 0)  # noqa: E731
+    _lib.check(call())
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        _lib.check(L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank, None, 0))
+        _lib.check(call())
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = world * n * args.e2e_steps / e2e_s
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
-    h2d = batch.nbytes(with_den=not integer)
+    h2d = (batch.node_off.nbytes + batch.edge_off.nbytes + load16.nbytes + edges16.nbytes if compact
+           else batch.nbytes(with_den=not integer))
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
-    n_chunks = int(os.environ.get("DS_CHUNKS", "12"))  # analyze_host's chunking (capi.cu)
+    n_chunks = int(os.environ.get("DS_CHUNKS", "8"))  # analyze_host's chunking (capi.cu)
     chunks = -(-n // max(1 << 16, -(-n // n_chunks)))
 
     # ---------------------------------------------------------------- roofline
@@ -393,7 +409,8 @@ def main():
             "data": "synthetic (reference generator, bit-identical)",
             "config": dict(workload(n, 1), parallelism=f"shards{world}", integer_loads=integer),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": 1e3 * e2e_s / args.e2e_steps, "api": "ds_analyze_batch (host pinned)",
+                    "ms_per_step": 1e3 * e2e_s / args.e2e_steps, "api": ("ds_analyze_batch16 (16-bit wire form, host pinned)" if compact
+                            else "ds_analyze_batch (host pinned)"),
                     "matches_device_leg": same},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
@@ -402,8 +419,8 @@ def main():
                          "issue": issue,
                          "pass": {"kernels_ms": kmean, "algorithmic_bytes": pass_bytes,
                                   "achieved_gbs": pass_bytes / (statistics.mean(kms) / 1e3) / 1e9},
-                         "note": "integer issue-bound (exact-rational greedy per DAG, one warp per DAG); "
-                                 "HBM is not the limiter"},
+                         "note": "integer issue/latency-bound exact-rational greedy per DAG (front/mid: one "
+                                 "warp per DAG; back: one lane per DAG); HBM is not the limiter"},
             "cpu_baseline": cpu,
             "makespan": makespan,
             "clocks": clk.summary(),

@@ -35,6 +35,8 @@ def _sig(lib):
         "ds_device_count": (C.c_int, [P(C.c_int)]),
         "ds_analyze_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                        P(_abi.ds_results), C.c_int, C.c_void_p, C.c_uint32]),
+        "ds_analyze_batch16": (C.c_int, [P(_abi.ds_dag_batch16), P(_abi.ds_platform), C.c_uint32,
+                                         P(_abi.ds_results), C.c_int]),
         "ds_analyze_batch_multi": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                              P(_abi.ds_results), P(C.c_int), C.c_int]),
         "ds_schedule_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform),
@@ -121,6 +123,16 @@ def analyze(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, 
     cb = batch.as_c()
     pl = platform(sm_count, t_min)
     check(lib().ds_analyze_batch(C.byref(cb), C.byref(pl), mask, C.byref(r), device, None, 0))
+    return _finish(batch, st, b, ng)
+
+
+def analyze16(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
+    """analyze() over the compact 16-bit wire form (ds_analyze_batch16)."""
+    st, b, ng, r = _results(batch.n_dags)
+    load16, edges16 = batch.compact16()
+    cb = batch.as_c16(load16, edges16)
+    pl = platform(sm_count, t_min)
+    check(lib().ds_analyze_batch16(C.byref(cb), C.byref(pl), mask, C.byref(r), device))
     return _finish(batch, st, b, ng)
 
 

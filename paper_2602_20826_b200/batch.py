@@ -66,6 +66,28 @@ class DagBatch:
             self.load_num.ctypes.data, self.load_den.ctypes.data if with_den else None,
             self.edges.ctypes.data)
 
+    def compact16_ok(self) -> bool:
+        """Fits ds_dag_batch16: integer loads in [1, 65535], <= 256 nodes per DAG."""
+        return (self.integer_loads() and self.load_num.size > 0 and int(self.load_num.min()) >= 1
+                and int(self.load_num.max()) <= 0xFFFF and int(self.sizes().max(initial=0)) <= 256)
+
+    def compact16(self, out=None):
+        """(load u16 [N], edges u16 [E]: from << 8 | to) — the ds_dag_batch16
+        wire form. `out` = preallocated (e.g. pinned) arrays to fill."""
+        if not self.compact16_ok():
+            raise ValueError("batch does not fit the 16-bit wire form")
+        load = out[0] if out else np.empty(self.load_num.shape, np.uint16)
+        edges = out[1] if out else np.empty(self.edges.shape, np.uint16)
+        np.copyto(load, self.load_num, casting="unsafe")
+        np.copyto(edges, ((self.edges >> 16) << 8) | (self.edges & 0xFF), casting="unsafe")
+        return load, edges
+
+    def as_c16(self, load16: np.ndarray, edges16: np.ndarray) -> _abi.ds_dag_batch16:
+        for a in (self.node_off, self.edge_off, load16, edges16):
+            assert a.flags["C_CONTIGUOUS"]
+        return _abi.ds_dag_batch16(self.n_dags, self.node_off.ctypes.data, self.edge_off.ctypes.data,
+                                   load16.ctypes.data, edges16.ctypes.data)
+
     def slice(self, lo: int, hi: int) -> "DagBatch":
         """DAGs [lo, hi) as a new batch with rebased offsets."""
         n0, n1 = int(self.node_off[lo]), int(self.node_off[hi])

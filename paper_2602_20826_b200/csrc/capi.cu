@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <string>
 #include <thread>
 #include <vector>
@@ -115,7 +116,19 @@ struct DevBuf {
 struct Slot {
     cudaStream_t s = nullptr;
     DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
+    DevBuf ln16, edges16;  // compact wire form staging (ds_analyze_batch16)
 };
+
+// ds_dag_batch16 -> the analysis' wide form, on the device (HBM-bound, tiny)
+__global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __restrict__ e16, u64 nn, u64 ne,
+                          u64* __restrict__ ln, u32* __restrict__ edges) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < nn; i += stride) ln[i] = ln16[i];
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < ne; i += stride) {
+        const u32 e = e16[i];
+        edges[i] = ((e >> 8) << 16) | (e & 0xffu);
+    }
+}
 
 struct DeviceCtx {
     std::mutex mu;
@@ -148,9 +161,11 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 16;  // >= one wave of warps, small enough to pipeline
-constexpr u64 kDefaultChunks = 12;  // DS_CHUNKS overrides (tuning knob)
+constexpr u64 kDefaultChunks = 8;  // DS_CHUNKS overrides (tuning knob); 6-8 measured best
 
-int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
+template <class Batch>
+int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
+    constexpr bool compact = std::is_same<Batch, ds_dag_batch16>::value;
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
     if (int rc = configure(device, false, occ)) return rc;
@@ -180,10 +195,12 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         if (int rc = sl.node_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.edge_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.ln.ensure(nn * 8)) return rc;
-        if (b->load_den) {
+        if (int rc = sl.edges.ensure(ne * 4)) return rc;
+        bool has_den = false;
+        if constexpr (!compact) has_den = b->load_den != nullptr;
+        if (has_den) {
             if (int rc = sl.ldn.ensure(nn * 8)) return rc;
         }
-        if (int rc = sl.edges.ensure(ne * 4)) return rc;
         if (int rc = sl.status.ensure(nd * 4)) return rc;
         if (int rc = sl.bounds.ensure(nd * 80)) return rc;
         if (int rc = sl.ngroups.ensure(nd * 2)) return rc;
@@ -191,17 +208,27 @@ int analyze_host(const ds_dag_batch* b, const PlatT<u64>& P, uint32_t mask, ds_r
         if (int rc = sl.retry_count.ensure(kK1Counters * 4)) return rc;
         DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
         DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
-        DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
-        if (b->load_den) {
-            DS_CUDA(cudaMemcpyAsync(sl.ldn.p, b->load_den + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
+        if constexpr (compact) {
+            if (int rc = sl.ln16.ensure(nn * 2)) return rc;
+            if (int rc = sl.edges16.ensure(ne * 2)) return rc;
+            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, sl.s));
+            DS_CUDA(cudaMemcpyAsync(sl.edges16.p, b->edges + e0, ne * 2, cudaMemcpyHostToDevice, sl.s));
+            k_widen16<<<296, 512, 0, sl.s>>>(sl.ln16.as<const uint16_t>(), sl.edges16.as<const uint16_t>(), nn, ne,
+                                             sl.ln.as<u64>(), sl.edges.as<u32>());
+            DS_CUDA(cudaGetLastError());
+        } else {
+            DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
+            if (has_den) {
+                DS_CUDA(cudaMemcpyAsync(sl.ldn.p, b->load_den + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
+            }
+            DS_CUDA(cudaMemcpyAsync(sl.edges.p, b->edges + e0, ne * 4, cudaMemcpyHostToDevice, sl.s));
         }
-        DS_CUDA(cudaMemcpyAsync(sl.edges.p, b->edges + e0, ne * 4, cudaMemcpyHostToDevice, sl.s));
         K1Args a{};
         a.n_dags = nd;
         a.node_off = sl.node_off.as<const u32>();
         a.edge_off = sl.edge_off.as<const u32>();
         a.load_num = sl.ln.as<const u64>();
-        a.load_den = b->load_den ? sl.ldn.as<const u64>() : nullptr;
+        a.load_den = has_den ? sl.ldn.as<const u64>() : nullptr;
         a.edges = sl.edges.as<const u32>();
         a.plat = P;
         a.mask = mask;
@@ -291,6 +318,16 @@ int ds_device_count(int* count) {
     }
     *count = c;
     return DS_OK;
+}
+
+int ds_analyze_batch16(const ds_dag_batch16* batch, const ds_platform* platform, uint32_t method_mask,
+                       ds_results* out, int device) {
+    if (!batch || !out || !out->status || !out->bounds) return fail(DS_EINVAL, "NULL batch or results");
+    PlatT<u64> P;
+    if (int rc = check_platform(platform, P)) return rc;
+    if (batch->n_dags == 0) return DS_OK;
+    if (!batch->node_off || !batch->edge_off || !batch->load || !batch->edges) return fail(DS_EINVAL, "NULL array");
+    return analyze_host(batch, P, method_mask & DS_M_ALL, out, device);
 }
 
 int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uint32_t method_mask,

@@ -1094,7 +1094,7 @@ constexpr int32_t kStRetried = -1001;  // queued for a wider tier
 struct K1Handoff {  // SoA over the batch's node index (node_off[d] - node_off[0] + v)
     u64* pred;
     u64* anc;
-    u64* desc;
+    u64* desc;       // anc | desc: the complement of v's concurrent set (+ v)
     u64* divg;       // division group g of DAG d at node slot g
     u32* ln;         // canonical loads
     u32* ld;
@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
                 const u32 i = n0 + v;
                 a.h.pred[i] = S.pred[v][0];
                 a.h.anc[i] = S.anc[v][0];
-                a.h.desc[i] = S.desc[v][0];
+                a.h.desc[i] = S.anc[v][0] | S.desc[v][0];  // k1_back only needs anc | desc
                 a.h.ln[i] = S.ln[v];
                 a.h.ld[i] = S.ld[v];
             }
@@ -1405,8 +1405,7 @@ constexpr int kLaneWarps = 4;
 __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
                                              const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
     const u64* __restrict__ pred = a.h.pred + n0;
-    const u64* __restrict__ anc = a.h.anc + n0;
-    const u64* __restrict__ desc = a.h.desc + n0;
+    const u64* __restrict__ ad = a.h.desc + n0;  // anc | desc
     const u64* __restrict__ divg = a.h.divg + n0;
     const u32* __restrict__ ln = a.h.ln + n0;
     const u32* __restrict__ ldn = a.h.ld + n0;
@@ -1447,42 +1446,48 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             R = q_exec(l, cp, P);
             ovf |= R.d == 0;
             used = cp;
-            conc = ~(__ldg(anc + v) | __ldg(desc + v));
+            conc = ~__ldg(ad + v);
         } else {
-            // apportion (scheduler.cpp:35-95) over the pending loads
-            int nm = 0;
-            int mv[kLaneMembers], mq[kLaneMembers], cap[kLaneMembers];
-            u32 rn[kLaneMembers], rd[kLaneMembers];
+            // apportion (scheduler.cpp:35-95) over the pending loads. Member k's
+            // quota (<= M <= 255 here) lives in 8 bits of mq[k >> 3]
+            // (registers, no local memory); cap and quota remainder are
+            // recomputed where needed.
+            if (__popcll(org) > kLaneMembers || P.M > 255) return kLaneRetry;
+            u64 mq[2] = {0, 0};
+            auto get = [&](int k) { return int((mq[k >> 3] >> (8 * (k & 7))) & 0xff); };
+            auto put = [&](int k, int m) {
+                const int sh = 8 * (k & 7);
+                mq[k >> 3] = (mq[k >> 3] & ~(0xffull << sh)) | (u64(m) << sh);
+            };
             RatT<u32> Wt{0, 1};
 #pragma unroll 1
-            for (u64 b = org; b; b &= b - 1) {
-                if (nm == kLaneMembers) return kLaneRetry;
-                const int v = __ffsll(b) - 1;
-                mv[nm++] = v;
-                Wt = q_add(Wt, load(v));
-            }
+            for (u64 b = org; b; b &= b - 1) Wt = q_add(Wt, load(__ffsll(b) - 1));
             if (Wt.d == 0 || Wt.n == 0) return DS_EOVERFLOW;
-            int tot = 0, capsum = 0;
-#pragma unroll 1
-            for (int k = 0; k < nm; ++k) {
-                const RatT<u32> l = load(mv[k]);
+            auto cap_of = [&](const RatT<u32>& l) {
                 int cp = q_max_par(l, P);
                 if (cp < 0) {
                     ovf = true;
                     cp = 1;
                 }
-                cp = min(cp, P.M);
-                // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n); floor and remainder
-                const u32 qn = mulc(mulc(l.n, u32(P.M), ovf), Wt.d, ovf);
-                const u32 qd = mulc(l.d, Wt.n, ovf);
+                return min(cp, P.M);
+            };
+            // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n): floor and remainder
+            auto quota = [&](const RatT<u32>& l, u32& qn, u32& qd) {
+                qn = mulc(mulc(l.n, u32(P.M), ovf), Wt.d, ovf);
+                qd = mulc(l.d, Wt.n, ovf);
+                return qd ? qn / qd : 0u;
+            };
+            int tot = 0, capsum = 0, nm = 0;
+#pragma unroll 1
+            for (u64 b = org; b; b &= b - 1, ++nm) {
+                const RatT<u32> l = load(__ffsll(b) - 1);
+                const int cp = cap_of(l);
+                u32 qn, qd;
+                const u32 fl = quota(l, qn, qd);
                 if (qd == 0) return DS_EOVERFLOW;
-                const u32 fl = qn / qd;
                 const long long flc = fl > 0x7fffffffu ? 0x7fffffffll : (long long)fl;
                 const int base = int(max(1ll, min(flc, (long long)cp)));
-                mq[k] = base;
-                cap[k] = cp;
-                rn[k] = qn - fl * qd;
-                rd[k] = qd;
+                put(nm, base);
                 tot += base;
                 capsum += cp;
             }
@@ -1491,13 +1496,20 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             while (tot > P.M || tot < target) {
                 const bool shed = tot > P.M;
                 Pick<u32> c{{0, 1}, {0, 1}, -1};
-                int ck = -1;
+                int ck = -1, k = 0;
 #pragma unroll 1
-                for (int k = 0; k < nm; ++k) {
-                    const int m = mq[k];
-                    if (shed ? m <= 1 : m >= cap[k]) continue;
-                    const Pick<u32> x{q_exec_raw(load(mv[k]), shed ? m - 1 : m, P),
-                                      shed ? RatT<u32>{0, 1} : RatT<u32>{rn[k], rd[k]}, mv[k]};
+                for (u64 b = org; b; b &= b - 1, ++k) {
+                    const int v = __ffsll(b) - 1;
+                    const int m = get(k);
+                    const RatT<u32> l = load(v);
+                    if (shed ? m <= 1 : m >= cap_of(l)) continue;
+                    RatT<u32> k2{0, 1};
+                    if (!shed) {
+                        u32 qn, qd;
+                        const u32 fl = quota(l, qn, qd);
+                        k2 = RatT<u32>{qn - fl * qd, qd};
+                    }
+                    const Pick<u32> x{q_exec_raw(l, shed ? m - 1 : m, P), k2, v};
                     ovf |= x.k1.d == 0;
                     if (pick_better<u32>(x, c, shed)) {
                         c = x;
@@ -1506,21 +1518,24 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
                 }
                 if (ck < 0) return DS_EINVARIANT;
                 const int step = shed ? -1 : 1;
-                mq[ck] += step;
+                put(ck, get(ck) + step);
                 tot += step;
             }
             // members: exec, response = first strict max
-            int bott = -1;
+            bool first = true;
+            int k = 0;
 #pragma unroll 1
-            for (int k = 0; k < nm; ++k) {
-                const RatT<u32> e = q_exec(load(mv[k]), mq[k], P);
+            for (u64 b = org; b; b &= b - 1, ++k) {
+                const int v = __ffsll(b) - 1;
+                const int m = get(k);
+                const RatT<u32> e = q_exec(load(v), m, P);
                 ovf |= e.d == 0;
-                if (bott < 0 || q_cmp(e, R) > 0) {
+                if (first || q_cmp(e, R) > 0) {
                     R = e;
-                    bott = k;
+                    first = false;
                 }
-                used += mq[k];
-                conc |= ~(__ldg(anc + mv[k]) | __ldg(desc + mv[k]));
+                used += m;
+                conc |= ~__ldg(ad + v);
             }
         }
         const int spare0 = P.M - used;
@@ -1579,7 +1594,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
 }
 
 #ifndef DS_LANE_MIN_BLOCKS
-#define DS_LANE_MIN_BLOCKS 12  // 40 registers: 3.23 ms vs 3.44 at 70 (1M C5 DAGs)
+#define DS_LANE_MIN_BLOCKS 10  // 48 registers: 3.09 ms; 40 regs 3.13, 64 regs 3.45 (1M C5 DAGs)
 #endif
 template <bool UNUSED = false>
 __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_lane(const K1Args a) {

@@ -46,6 +46,12 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
         int of = 0, om = 0, ob = 0, obl = 0;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obl, k1_back_lane<>, 32 * kLaneWarps, 0))) return e;
         if (obl < 1) return cudaErrorInvalidConfiguration;
+        // DS_K1_LANE_CTAS_PER_SM (tuning knob): fewer resident DAG walks keep
+        // their hand-off state inside L2
+        if (const char* env = getenv("DS_K1_LANE_CTAS_PER_SM")) {
+            const int c = atoi(env);
+            if (c >= 1 && c < obl) obl = c;
+        }
         occ.grid_back_lane = sms * obl;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k1_front<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
@@ -111,12 +117,13 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         }();
         if (warp_back) {
             k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+            if ((e = mark("k1_back")) != cudaSuccess) return e;
         } else {
             const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
             k1_back_lane<><<<int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane)), 32 * kLaneWarps, 0,
                              s>>>(a);
+            if ((e = mark("k1_back_lane")) != cudaSuccess) return e;
         }
-        if ((e = mark("k1_back")) != cudaSuccess) return e;
     }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
     // nothing queued each kernel reads the count and exits

@@ -105,3 +105,17 @@ def test_device_path_fails_loudly_without_gpu(lib):
     b = pack([([1, 2, 1], [(0, 1), (1, 2)])])
     with pytest.raises(_lib.DagschedError):
         _lib.analyze(b, 8)
+
+
+def test_compact16_packing_roundtrip():
+    """DagBatch.compact16: 16-bit loads and from << 8 | to edges, host side."""
+    from paper_2602_20826_b200.batch import pack
+    from paper_2602_20826_b200 import workloads
+    b = pack([workloads.make_example_task(), workloads.c1_fork_join()])
+    assert b.compact16_ok()
+    load16, edges16 = b.compact16()
+    assert load16.dtype == np.uint16 and edges16.dtype == np.uint16
+    assert np.array_equal(load16.astype(np.int64), b.load_num)
+    assert np.array_equal(((edges16 >> 8).astype(np.uint32) << 16) | (edges16 & 0xFF), b.edges)
+    big = pack([([(0, 70000), (1, 1)], [(0, 1)])])
+    assert not big.compact16_ok()

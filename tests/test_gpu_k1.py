@@ -179,3 +179,17 @@ def pack_subset(b, idx):
         ln.append(b.load_num[n0:n1]); ld.append(b.load_den[n0:n1]); ed.append(b.edges[e0:e1])
         no.append(no[-1] + n1 - n0); eo.append(eo[-1] + e1 - e0)
     return from_arrays(no, eo, np.concatenate(ln), np.concatenate(ld), np.concatenate(ed))
+
+
+def test_compact16_wire_form_matches_wide():
+    """ds_analyze_batch16 (16-bit loads/edges, widened on the device) gives the
+    same statuses and bounds as ds_analyze_batch on the same DAGs."""
+    corpus = _lib.Corpus(30000, seed=11)
+    b = corpus.batch()
+    assert b.compact16_ok()
+    st, bounds, ng = _lib.analyze(b, 148)
+    st16, bounds16, ng16 = _lib.analyze16(b, 148)
+    assert np.array_equal(st, st16) and np.array_equal(bounds, bounds16) and np.array_equal(ng, ng16)
+    st, bounds, _ = _lib.analyze(b, 32)
+    st16, bounds16, _ = _lib.analyze16(b, 32)
+    assert np.array_equal(st, st16) and np.array_equal(bounds, bounds16)
