@@ -139,7 +139,8 @@ def kernel_alg_bytes(name, n, N, E, integer, n_div):
     if name == "k1_mid":     # status + pred/anc + loads in; ranks, division groups, status out
         return 4 * n + 4 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 2 * n + 4 * n
     if name in ("k1_back", "k1_back_lane"):  # status + hand-off in; proposed bound, status, groups out
-        return 4 * n + 4 * n + 2 * n + handoff_masks + handoff_loads + 2 * N + 8 * n_div + 16 * n + 4 * n + 2 * n
+        # (per node: pred, anc|desc, load, rank/order of its K1Node record)
+        return 4 * n + 4 * n + 2 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 16 * n + 4 * n + 2 * n
     return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
 
 

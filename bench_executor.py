@@ -20,8 +20,9 @@ SMs:
 M = 148 runs on the whole GPU; M < 148 runs inside a green context of M SMs
 (the paper's contended regime: Jetson M=8, RTX 3060 M=30).
 
-Time unit (per partition, executor.calibrate): tau = p99 time of one unit of
-work on every SM at once; delta = latency per group boundary. The bound in
+Time unit (per partition, executor.calibrate): tau = worst time of one unit
+of work on every SM at once; delta = worst latency per group boundary (both
+over the calibration samples without a platform stall). The bound in
 microseconds is bound_units * tau + (|groups| - 1) * delta.
 
 Writes one JSON document (default profiles/r01_executor.json).
@@ -43,6 +44,7 @@ from paper_2602_20826_b200 import _lib, scheme, workloads  # noqa: E402
 from paper_2602_20826_b200 import executor as X  # noqa: E402
 from paper_2602_20826_b200.batch import pack  # noqa: E402
 
+STALL_US = X.STALL_US
 VARIANTS = ("proposed", "proposed_deps", "dynamic", "dynamic_deps", "serial", "multistream", "multistream_free")
 
 
@@ -94,10 +96,18 @@ def run_dag(loads, edges, sch, M, sm_limit, cal, args):
                 vs += X.check_sm_exclusive(plan, r, k)
             vg += X.group_overlap_violations(plan, r, k)
         ex.close()
+        # platform stalls: a replay >= 1 ms above the median (the CUDA-event
+        # launch time shows the same excess). tools/stall_probe.py measures them
+        # in every engine and workload, with and without green contexts
+        # (~1.7-2.9 ms, every ~0.3-3 s), i.e. outside the executor
+        stalled = r.makespan_us > np.median(r.makespan_us) + STALL_US
+        over = r.makespan_us > bound_us
         out[kind] = {"makespan_us": stats(r.makespan_us), "graph_launch_us": stats(r.launch_ms * 1e3),
                      "precedence_violations": vp, "sm_overlap_violations": vs, "group_order_violations": vg,
                      "checked_replays": len(checked),
-                     "over_bound_replays": int((r.makespan_us > bound_us).sum()),
+                     "stalled_replays": int(stalled.sum()),
+                     "over_bound_unstalled": int((over & ~stalled).sum()),
+                     "over_bound_replays": int(over.sum()),
                      "ratio_to_bound": stats(r.makespan_us / bound_us)}
     return out
 
@@ -114,6 +124,8 @@ def summarise(results, prefix):
             "mean_max_us": float(np.mean([r[kind]["makespan_us"]["max"] for r in sel])),
             "mean_std_us": float(np.mean([r[kind]["makespan_us"]["std"] for r in sel])),
             "replays_over_bound": int(sum(r[kind]["over_bound_replays"] for r in sel)),
+            "stalled_replays": int(sum(r[kind]["stalled_replays"] for r in sel)),
+            "over_bound_unstalled": int(sum(r[kind]["over_bound_unstalled"] for r in sel)),
             "max_ratio_to_bound": float(max(r[kind]["ratio_to_bound"]["max"] for r in sel)),
             "trace_violations": int(sum(r[kind]["precedence_violations"] + r[kind]["sm_overlap_violations"]
                                         for r in sel)),
@@ -202,6 +214,7 @@ def main():
         for k, v in p["summary"].items():
             if v:
                 row[k] = {"over": v["proposed"]["replays_over_bound"],
+                          "over_unstalled": v["proposed"]["over_bound_unstalled"],
                           "maxratio": round(v["proposed"]["max_ratio_to_bound"], 3),
                           "p50": [round(v[x]["mean_p50_us"], 1) for x in VARIANTS],
                           "deps_over": v["proposed_deps"]["replays_over_bound"]}

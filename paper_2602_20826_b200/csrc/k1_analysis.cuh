@@ -1091,14 +1091,23 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
 constexpr int32_t kStMid = -999;       // k1_front done, k1_mid pending
 constexpr int32_t kStPending = -1000;  // k1_mid done, k1_back pending
 constexpr int32_t kStRetried = -1001;  // queued for a wider tier
-struct K1Handoff {  // SoA over the batch's node index (node_off[d] - node_off[0] + v)
-    u64* pred;
-    u64* anc;
-    u64* desc;       // anc | desc: the complement of v's concurrent set (+ v)
+// Per node, what k1_back reads, in one 32-byte record (one sector): the
+// one-lane-per-DAG walk touches a node's pred, anc|desc, load and rank/order
+// together, so an array of records costs it one L1/L2 line where four
+// separate arrays cost four.
+struct K1Node {
+    u64 pred;
+    u64 ad;          // anc | desc: the complement of v's concurrent set (+ v)
+    u32 ln, ld;      // canonical load
+    uint16_t ro;     // rank[v] | order[v] << 8 (k1_mid)
+    uint16_t pad0;
+    u32 pad1;
+};
+static_assert(sizeof(K1Node) == 32, "K1Node is one sector");
+struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] + v)
+    K1Node* node;
+    u64* anc;        // k1_mid's block construction
     u64* divg;       // division group g of DAG d at node slot g
-    u32* ln;         // canonical loads
-    u32* ld;
-    uint16_t* ro;    // rank[v] | order[v] << 8
     uint16_t* ndiv;  // per DAG
 };
 
@@ -1119,7 +1128,7 @@ struct K1Args {
     u32* retry_count;
     u32* retry2;           // ... and whose 64-bit pass overflowed
     u32* retry2_count;
-    K1Handoff h;           // split mode when h.pred != nullptr (bounds mode only)
+    K1Handoff h;           // split mode when h.node != nullptr (bounds mode only)
 };
 
 template <int W, class T, bool DETAIL>
@@ -1253,11 +1262,12 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
 #pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 const u32 i = n0 + v;
-                a.h.pred[i] = S.pred[v][0];
+                K1Node& nd = a.h.node[i];
+                nd.pred = S.pred[v][0];
+                nd.ad = S.anc[v][0] | S.desc[v][0];  // k1_back only needs anc | desc
+                nd.ln = S.ln[v];
+                nd.ld = S.ld[v];
                 a.h.anc[i] = S.anc[v][0];
-                a.h.desc[i] = S.anc[v][0] | S.desc[v][0];  // k1_back only needs anc | desc
-                a.h.ln[i] = S.ln[v];
-                a.h.ld[i] = S.ld[v];
             }
         }
         if (lane == 0) {
@@ -1289,9 +1299,10 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
 #pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             const u32 i = n0 + v;
-            S.pred[v][0] = a.h.pred[i];
+            const K1Node& nd = a.h.node[i];
+            S.pred[v][0] = nd.pred;
             S.anc[v][0] = a.h.anc[i];
-            const RatT<u32> l{a.h.ln[i], a.h.ld[i]};
+            const RatT<u32> l{nd.ln, nd.ld};
             S.ln[v] = l.n;
             S.ld[v] = l.d;
             integer &= l.d == 1;
@@ -1312,7 +1323,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
 #pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             const u32 i = n0 + v;
-            a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
+            a.h.node[i].ro = uint16_t(S.rank[v] | (S.order[v] << 8));
             if (v < ndiv) a.h.divg[i] = S.divg[v][0];
         }
         if (lane == 0) {
@@ -1344,12 +1355,13 @@ __global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
 #pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             const u32 i = n0 + v;
-            S.pred[v][0] = a.h.pred[i];
-            S.anc[v][0] = a.h.anc[i];
-            S.desc[v][0] = a.h.desc[i];
-            S.pn[v] = a.h.ln[i];
-            S.pd[v] = a.h.ld[i];
-            const uint16_t ro = a.h.ro[i];
+            const K1Node& nd = a.h.node[i];
+            S.pred[v][0] = nd.pred;
+            S.anc[v][0] = nd.ad;  // p_schedule only uses anc | desc
+            S.desc[v][0] = 0;
+            S.pn[v] = nd.ln;
+            S.pd[v] = nd.ld;
+            const uint16_t ro = nd.ro;
             S.rank[v] = short(ro & 0xff);
             S.order[v] = short(ro >> 8);
             S.gen[v] = 0;
@@ -1404,12 +1416,8 @@ constexpr int kLaneWarps = 4;
 
 __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
                                              const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
-    const u64* __restrict__ pred = a.h.pred + n0;
-    const u64* __restrict__ ad = a.h.desc + n0;  // anc | desc
+    const K1Node* __restrict__ nodes = a.h.node + n0;
     const u64* __restrict__ divg = a.h.divg + n0;
-    const u32* __restrict__ ln = a.h.ln + n0;
-    const u32* __restrict__ ldn = a.h.ld + n0;
-    const uint16_t* __restrict__ ro = a.h.ro + n0;
     // residual loads of segmented nodes (scheduler.cpp:318-328), newest last
     int n_over = 0;
     int over_v[kLaneSplits];
@@ -1418,7 +1426,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
         for (int k = n_over - 1; k >= 0; --k) {
             if (over_v[k] == v) return RatT<u32>{over_n[k], over_d[k]};
         }
-        return RatT<u32>{__ldg(ln + v), __ldg(ldn + v)};
+        return RatT<u32>{__ldg(&nodes[v].ln), __ldg(&nodes[v].ld)};
     };
     bool ovf = false;
     const u64 V = n >= 64 ? ~0ull : ((1ull << n) - 1);
@@ -1446,7 +1454,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             R = q_exec(l, cp, P);
             ovf |= R.d == 0;
             used = cp;
-            conc = ~__ldg(ad + v);
+            conc = ~__ldg(&nodes[v].ad);
         } else {
             // apportion (scheduler.cpp:35-95) over the pending loads. Member k's
             // quota (<= M <= 255 here) lives in 8 bits of mq[k >> 3]
@@ -1535,7 +1543,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
                     first = false;
                 }
                 used += m;
-                conc |= ~__ldg(ad + v);
+                conc |= ~__ldg(&nodes[v].ad);
             }
         }
         const int spare0 = P.M - used;
@@ -1549,13 +1557,13 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
 #pragma unroll 1
             for (u64 b = avail; b; b &= b - 1) {
                 const int c = __ffsll(b) - 1;
-                const u64 p = __ldg(pred + c);
-                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(ro + c) & 0xff);
+                const u64 p = __ldg(&nodes[c].pred);
+                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(&nodes[c].ro) & 0xff);
             }
             int spare = spare0;
 #pragma unroll 1
             for (; rm && spare >= 1; rm &= rm - 1) {
-                const int c = __ldg(ro + (__ffsll(rm) - 1)) >> 8;
+                const int c = __ldg(&nodes[__ffsll(rm) - 1].ro) >> 8;
                 const RatT<u32> l = load(c);
                 int mp = q_max_par(l, P);
                 if (mp < 0) {

@@ -24,19 +24,15 @@ constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
-    return size_t(n_nodes) * (4 * 8 + 2 * 4 + 2) + size_t(n_dags) * 2 + 64;
+    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8) + size_t(n_dags) * 2 + 64;
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;
-    u64* m = static_cast<u64*>(base);
-    h.pred = m;
-    h.anc = m + n_nodes;
-    h.desc = m + 2 * n_nodes;
-    h.divg = m + 3 * n_nodes;
-    h.ln = reinterpret_cast<u32*>(m + 4 * n_nodes);
-    h.ld = h.ln + n_nodes;
-    h.ro = reinterpret_cast<uint16_t*>(h.ld + n_nodes);
-    h.ndiv = h.ro + n_nodes;
+    h.node = static_cast<K1Node*>(base);
+    u64* m = reinterpret_cast<u64*>(h.node + n_nodes);
+    h.anc = m;
+    h.divg = m + n_nodes;
+    h.ndiv = reinterpret_cast<uint16_t*>(m + 2 * n_nodes);
     (void)n_dags;
     return h;
 }

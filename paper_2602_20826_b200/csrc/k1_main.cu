@@ -94,7 +94,7 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
     if (e != cudaSuccess) return e;
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     auto cap = [&](int g) { return int(need_small < u64(g) ? need_small : u64(g)); };
-    const bool split = !DETAIL && a.h.pred != nullptr;
+    const bool split = !DETAIL && a.h.node != nullptr;
     if (split) {
         k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = mark("k1_front")) != cudaSuccess) return e;

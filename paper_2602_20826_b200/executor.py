@@ -334,14 +334,18 @@ def group_overlap_violations(plan: Plan, res: RunResult, r: int):
     return bad
 
 
+STALL_US = 1000.0  # a replay / sample this far above the median is a platform stall
+
+
 def calibrate(unit_elems: int, sm_limit: int = 0, workload: int = WL_MIX32, replays: int = 200, groups: int = 16,
               device: int = 0):
     """Time unit and per-group latency, measured through the executor itself.
 
-    tau: p99 makespan of one entity holding every SM of the partition, each CTA
-    processing one unit (full HBM contention — the most any group member can
-    see). delta: extra latency per group boundary, from a chain of `groups`
-    such groups joined by barriers. A schedule's bound in microseconds is then
+    tau: worst makespan of one entity holding every SM of the partition, each
+    CTA processing one unit (full HBM contention — the most any group member
+    can see). delta: worst extra latency per group boundary, from a chain of
+    `groups` such groups joined by barriers. Worst = max over the samples
+    without a platform stall. A schedule's bound in microseconds is then
     bound * tau + (|groups| - 1) * delta <= bound * (tau + delta), since every
     group's response is at least t_min = 1 unit.
     """
@@ -363,7 +367,14 @@ def calibrate(unit_elems: int, sm_limit: int = 0, workload: int = WL_MIX32, repl
         w = entity_windows(chain, rc, r)
         dur += [(b - a) / 1e3 for a, b in w]
         gap += [(w[g + 1][0] - w[g][1]) / 1e3 for g in range(groups - 1)]
-    tau, delta = float(np.percentile(dur, 99)), float(np.percentile(gap, 99))
+    # worst case over the calibration samples (a real-time bound wants the
+    # WCET, not a percentile), leaving out platform stalls: samples >= 1 ms
+    # above the median, which hit every engine alike (tools/stall_probe.py)
+    def wc(xs):
+        xs = np.asarray(xs, np.float64)
+        return float(xs[xs <= np.median(xs) + STALL_US].max())
+
+    tau, delta = wc(dur), wc(gap)
     # launch stagger: the same chain with k = 8 entities of sms/8 SMs per group
     k = min(8, sms)
     eps = 0.0
@@ -383,8 +394,8 @@ def calibrate(unit_elems: int, sm_limit: int = 0, workload: int = WL_MIX32, repl
                 if g + 1 < groups:  # barrier latency after a k-wide group
                     end = max(w[g * k + j][1] for j in range(k))
                     gap.append((min(w[(g + 1) * k + j][0] for j in range(k)) - end) / 1e3)
-        eps = float(np.percentile(stag, 99))
-        delta = float(np.percentile(gap, 99))
+        eps = wc(stag)
+        delta = wc(gap)
     return {"sm_count": sms, "tau_us": tau, "tau_p50_us": float(np.median(dur)), "delta_us": delta,
             "delta_p50_us": float(np.median(gap)), "eps_us": eps, "groups": groups,
             "working_set_mb": groups * n * BYTES_PER_ELEM[workload] / 2 ** 20}
