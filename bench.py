@@ -144,6 +144,19 @@ def kernel_alg_bytes(name, n, N, E, integer, n_div):
     return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
 
 
+def host_chunks(n: int) -> int:
+    """How many chunks analyze_host (capi.cu) streams an n-DAG host batch in."""
+    k = int(os.environ.get("DS_CHUNKS", "0") or 0)
+    weights = [1] * (k if 1 <= k <= 64 else 8)
+    wsum, bounds, acc = sum(weights), [0], 0
+    for w in weights:
+        acc += w
+        hi = min(n, -(-n * acc // wsum))
+        if hi - bounds[-1] >= 1 << 14 or (hi == n and hi > bounds[-1]):
+            bounds.append(hi)
+    return max(1, len(bounds) - 1)
+
+
 def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_dags=1_000_000):
     """Time the reference CPU path on a bounded sample of the same workload."""
     from oracle import bindings
@@ -365,8 +378,7 @@ def main():
     h2d = (batch.node_off.nbytes + batch.edge_off.nbytes + load16.nbytes + edges16.nbytes if compact
            else batch.nbytes(with_den=not integer))
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
-    n_chunks = int(os.environ.get("DS_CHUNKS", "8"))  # analyze_host's chunking (capi.cu)
-    chunks = -(-n // max(1 << 16, -(-n // n_chunks)))
+    chunks = host_chunks(n)
 
     # ---------------------------------------------------------------- roofline
     # dominant kernel of the step, timed live with CUDA events on its stream

@@ -1091,23 +1091,24 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
 constexpr int32_t kStMid = -999;       // k1_front done, k1_mid pending
 constexpr int32_t kStPending = -1000;  // k1_mid done, k1_back pending
 constexpr int32_t kStRetried = -1001;  // queued for a wider tier
-// Per node, what k1_back reads, in one 32-byte record (one sector): the
-// one-lane-per-DAG walk touches a node's pred, anc|desc, load and rank/order
-// together, so an array of records costs it one L1/L2 line where four
-// separate arrays cost four.
+// Per node, what k1_back reads from k1_front, in one 32-byte record (one
+// sector, written whole so L2 never has to fill it from DRAM): the
+// one-lane-per-DAG walk touches a node's pred, anc|desc and load together, so
+// a record costs it one line where three arrays cost three. k1_mid's
+// rank/order goes to its own array (a 2-byte update of the record would make
+// every sector dirty again).
 struct K1Node {
     u64 pred;
     u64 ad;          // anc | desc: the complement of v's concurrent set (+ v)
     u32 ln, ld;      // canonical load
-    uint16_t ro;     // rank[v] | order[v] << 8 (k1_mid)
-    uint16_t pad0;
-    u32 pad1;
+    u64 pad;
 };
 static_assert(sizeof(K1Node) == 32, "K1Node is one sector");
 struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] + v)
     K1Node* node;
     u64* anc;        // k1_mid's block construction
     u64* divg;       // division group g of DAG d at node slot g
+    uint16_t* ro;    // rank[v] | order[v] << 8 (k1_mid)
     uint16_t* ndiv;  // per DAG
 };
 
@@ -1262,11 +1263,13 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
 #pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 const u32 i = n0 + v;
-                K1Node& nd = a.h.node[i];
+                K1Node nd;
                 nd.pred = S.pred[v][0];
                 nd.ad = S.anc[v][0] | S.desc[v][0];  // k1_back only needs anc | desc
                 nd.ln = S.ln[v];
                 nd.ld = S.ld[v];
+                nd.pad = 0;
+                a.h.node[i] = nd;
                 a.h.anc[i] = S.anc[v][0];
             }
         }
@@ -1323,7 +1326,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
 #pragma unroll 1
         for (int v = lane; v < n; v += 32) {
             const u32 i = n0 + v;
-            a.h.node[i].ro = uint16_t(S.rank[v] | (S.order[v] << 8));
+            a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
             if (v < ndiv) a.h.divg[i] = S.divg[v][0];
         }
         if (lane == 0) {
@@ -1361,7 +1364,7 @@ __global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
             S.desc[v][0] = 0;
             S.pn[v] = nd.ln;
             S.pd[v] = nd.ld;
-            const uint16_t ro = nd.ro;
+            const uint16_t ro = a.h.ro[i];
             S.rank[v] = short(ro & 0xff);
             S.order[v] = short(ro >> 8);
             S.gen[v] = 0;
@@ -1417,6 +1420,7 @@ constexpr int kLaneWarps = 4;
 __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
                                              const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
     const K1Node* __restrict__ nodes = a.h.node + n0;
+    const uint16_t* __restrict__ ro = a.h.ro + n0;
     const u64* __restrict__ divg = a.h.divg + n0;
     // residual loads of segmented nodes (scheduler.cpp:318-328), newest last
     int n_over = 0;
@@ -1558,12 +1562,12 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             for (u64 b = avail; b; b &= b - 1) {
                 const int c = __ffsll(b) - 1;
                 const u64 p = __ldg(&nodes[c].pred);
-                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(&nodes[c].ro) & 0xff);
+                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(ro + c) & 0xff);
             }
             int spare = spare0;
 #pragma unroll 1
             for (; rm && spare >= 1; rm &= rm - 1) {
-                const int c = __ldg(&nodes[__ffsll(rm) - 1].ro) >> 8;
+                const int c = __ldg(ro + (__ffsll(rm) - 1)) >> 8;
                 const RatT<u32> l = load(c);
                 int mp = q_max_par(l, P);
                 if (mp < 0) {

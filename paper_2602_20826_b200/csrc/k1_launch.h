@@ -24,7 +24,7 @@ constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
-    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8) + size_t(n_dags) * 2 + 64;
+    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64;
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;
@@ -32,7 +32,8 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     u64* m = reinterpret_cast<u64*>(h.node + n_nodes);
     h.anc = m;
     h.divg = m + n_nodes;
-    h.ndiv = reinterpret_cast<uint16_t*>(m + 2 * n_nodes);
+    h.ro = reinterpret_cast<uint16_t*>(m + 2 * n_nodes);
+    h.ndiv = h.ro + n_nodes;
     (void)n_dags;
     return h;
 }
