@@ -399,7 +399,7 @@ def main():
         ips = kn["warp_instructions_per_dag"] * n / (kmean[dom] / 1e3)
         issue = {"achieved": ips, "peak": peak_ips, "unit": "warp-instr/s", "frac": ips / peak_ips,
                  "source": "instruction count per DAG from the ncu capture in profiles/, time live"}
-    pass_bytes = h2d + d2h
+    pass_bytes = batch.nbytes(with_den=not integer) + d2h  # the device pass: packed DAGs in, results out
     makespan = None
     if rank == 0 and not args.no_makespan:
         try:
