@@ -140,7 +140,7 @@ def summarise(results, prefix):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--configs", default="c1,c2,c3,c4,paper")
     ap.add_argument("--sm-limits", default="0,32,8", help="0 = whole GPU (148 SMs); else green-context size")
     ap.add_argument("--replays", type=int, default=1000)
     ap.add_argument("--c2-dags", type=int, default=100)
@@ -175,6 +175,10 @@ def main():
         if "c4" in cfgs:
             for s in range(3):
                 cases.append((f"c4_oversized_{s}", workloads.oversized_dag(s, M)))
+        if "paper" in cfgs:  # Tables 1-2 families at C_avg = 4 and 20
+            for avg in (4, 20):
+                for fam, dag in workloads.paper_benchmarks(avg).items():
+                    cases.append((f"paper_{fam}_avg{avg}", dag))
         if "c2" in cfgs:
             corpus = _lib.Corpus(600, seed=1)
             b = corpus.batch()
@@ -201,7 +205,8 @@ def main():
                   + " ".join(f"{k}={r[k]['makespan_us']['p50']:.0f}" for k in VARIANTS)
                   + f" | over={r['proposed']['over_bound_replays']}", flush=True)
         part = {"sm_limit": sm_limit, "M": M, "calibration": cal, "dags": results,
-                "summary": {k: summarise(results, k) for k in ("c1", "c2_", "c2avg4", "c3", "c4")}}
+                "summary": {k: summarise(results, k) for k in ("c1", "c2_", "c2avg4", "c3", "c4", "paper_",
+                                                               "paper_gaussian", "paper_laplace", "paper_stencil")}}
         doc["partitions"].append(part)
     doc["wall_s"] = time.time() - t_start
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

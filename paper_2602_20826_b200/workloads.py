@@ -121,3 +121,74 @@ def oversized_dag(seed: int = 0, sm_count: int = 148):
     nodes.append((sink, 2))
     edges += [(v, sink) for v in second]
     return nodes, edges
+
+
+# ---------------------------------------------------------------------------
+# The paper's Tables 1-2 benchmark DAG families (Gaussian
+# elimination, Laplace, Stencil). The reference does not ship them
+# (data/fixtures is absent, proj/tests/CMakeLists.txt:25), so they are authored
+# here in their textbook shapes, each with one source and one sink
+# (dag.cpp:97-108). Loads: uniform integers in avg * [1 - jitter, 1 + jitter]
+# (the paper's C_avg = 4 for Table 1, 20 for Table 2), at least 1.
+
+def _loads(count: int, avg: float, jitter: float, seed: int):
+    rnd = random.Random(seed)
+    lo, hi = max(1, round(avg * (1 - jitter))), max(1, round(avg * (1 + jitter)))
+    return [rnd.randint(lo, hi) for _ in range(count)]
+
+
+def gaussian_elimination_dag(m: int = 8, avg: float = 4, jitter: float = 0.5, seed: int = 0):
+    """Gaussian elimination on an m x m matrix: step k has a pivot task T(k,k)
+    and updates T(k,j), j > k; T(k,k) -> T(k,j), T(k,j) -> T(k+1,j). Source
+    T(1,1), sink T(m-1,m); (m^2 + m - 2) / 2 tasks (35 at m = 8)."""
+    ids = {}
+    for k in range(1, m):
+        ids[(k, k)] = len(ids)
+        for j in range(k + 1, m + 1):
+            ids[(k, j)] = len(ids)
+    edges = []
+    for k in range(1, m):
+        for j in range(k + 1, m + 1):
+            edges.append((ids[(k, k)], ids[(k, j)]))
+            if k + 1 < m:
+                edges.append((ids[(k, j)], ids[(k + 1, j)]))
+    loads = _loads(len(ids), avg, jitter, seed)
+    return [(i, loads[i]) for i in range(len(ids))], edges
+
+
+def laplace_dag(n: int = 6, avg: float = 4, jitter: float = 0.5, seed: int = 0):
+    """Laplace-equation wavefront on an n x n grid: (i,j) -> (i+1,j), (i,j+1).
+    Source (0,0), sink (n-1,n-1); n^2 tasks (36 at n = 6)."""
+    idx = lambda i, j: i * n + j  # noqa: E731
+    edges = []
+    for i in range(n):
+        for j in range(n):
+            if i + 1 < n:
+                edges.append((idx(i, j), idx(i + 1, j)))
+            if j + 1 < n:
+                edges.append((idx(i, j), idx(i, j + 1)))
+    loads = _loads(n * n, avg, jitter, seed)
+    return [(i, loads[i]) for i in range(n * n)], edges
+
+
+def stencil_dag(width: int = 6, depth: int = 5, avg: float = 4, jitter: float = 0.5, seed: int = 0):
+    """1-D three-point stencil over `depth` time steps: (t,i) -> (t+1,i-1),
+    (t+1,i), (t+1,i+1); plus a source feeding step 0 and a sink after the last
+    step; width * depth + 2 tasks (32 at 6 x 5)."""
+    src, sink = 0, width * depth + 1
+    idx = lambda t, i: 1 + t * width + i  # noqa: E731
+    edges = [(src, idx(0, i)) for i in range(width)]
+    for t in range(depth - 1):
+        for i in range(width):
+            for d in (-1, 0, 1):
+                if 0 <= i + d < width:
+                    edges.append((idx(t, i), idx(t + 1, i + d)))
+    edges += [(idx(depth - 1, i), sink) for i in range(width)]
+    loads = _loads(width * depth + 2, avg, jitter, seed)
+    return [(i, loads[i]) for i in range(width * depth + 2)], edges
+
+
+def paper_benchmarks(avg: float):
+    """The three Tables 1-2 families at C_avg = avg (4: Table 1, 20: Table 2)."""
+    return {"gaussian": gaussian_elimination_dag(8, avg), "laplace": laplace_dag(6, avg),
+            "stencil": stencil_dag(6, 5, avg)}

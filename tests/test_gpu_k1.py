@@ -193,3 +193,19 @@ def test_compact16_wire_form_matches_wide():
     st, bounds, _ = _lib.analyze(b, 32)
     st16, bounds16, _ = _lib.analyze16(b, 32)
     assert np.array_equal(st, st16) and np.array_equal(bounds, bounds16)
+
+
+def test_paper_benchmark_families_vs_oracle(orc):
+    """Tables 1-2 DAG families on the GPU: bounds and group structure bit-exact."""
+    from paper_2602_20826_b200 import scheme, workloads
+    dags = [d for avg in (4, 20) for d in workloads.paper_benchmarks(avg).values()]
+    b = pack(dags)
+    for M in (8, 30, 32, 148):
+        st, bounds, _ = _lib.analyze(b, M)
+        st_o, b_o, _ = orc.corpus(b).evaluate(M)
+        assert (st == 0).all() and np.array_equal(st, st_o) and np.array_equal(bounds, b_o), M
+        schemes, st2 = scheme.schedule_batch(b, M)
+        c = orc.corpus(b)
+        for d, s in enumerate(schemes):
+            got = helpers.normalise_scheme(scheme.to_reference_json(s))
+            assert got == helpers.normalise_scheme(c.scheme(d, M)), (M, d)

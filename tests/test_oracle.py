@@ -122,3 +122,22 @@ def test_restatement_vs_reference_on_random_general_dags(orc, seed, tmin):
         for d in range(0, 300, 15):
             if sa[d] == 0:
                 assert a.scheme(d, M, tmin) == o.scheme(d, M, tmin), (M, d)
+
+
+@pytest.mark.skipif(not bindings.available("ref"), reason="oracle/_ref not built (needs /root/reference)")
+def test_paper_benchmark_families_vs_reference(orc):
+    """Tables 1-2 DAG families (Gaussian elimination, Laplace, Stencil): the
+    restatement's bounds and schemes equal the reference library's."""
+    from paper_2602_20826_b200 import workloads
+    from paper_2602_20826_b200.batch import from_arrays, pack
+    dags = [d for avg in (4, 20) for d in workloads.paper_benchmarks(avg).values()]
+    b = pack(dags)
+    assert (b.pack_status == 0).all()
+    raw = from_arrays(b.node_off, b.edge_off, b.load_num, b.load_den, b.edges)
+    a, o = bindings.Checker("ref").corpus(raw), orc.corpus(raw)
+    for M in (8, 30, 32, 148):
+        sa, ba, _ = a.evaluate(M)
+        so, bo, _ = o.evaluate(M)
+        assert (sa == 0).all() and np.array_equal(sa, so) and np.array_equal(ba, bo), M
+        for d in range(len(dags)):
+            assert a.scheme(d, M) == o.scheme(d, M), (M, d)
