@@ -43,7 +43,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_struct_layouts_match_c():
-    structs = ["ds_platform", "ds_dag_batch", "ds_results", "ds_gen_config", "ds_entity_rec",
+    structs = ["ds_platform", "ds_dag_batch", "ds_dag_batch16", "ds_results", "ds_gen_config", "ds_entity_rec",
                "ds_group_rec", "ds_scheme_out"]
     src = '#include <stdio.h>\n#include "dagsched_b200.h"\nint main(){\n' + "".join(
         f'printf("{s} %zu\\n", sizeof({s}));\n' for s in structs) + "return 0;}\n"
@@ -119,3 +119,19 @@ def test_compact16_packing_roundtrip():
     assert np.array_equal(((edges16 >> 8).astype(np.uint32) << 16) | (edges16 & 0xFF), b.edges)
     big = pack([([(0, 70000), (1, 1)], [(0, 1)])])
     assert not big.compact16_ok()
+
+
+def test_compact16_entry_validates_arguments(lib):
+    """ds_analyze_batch16 rejects NULL arrays with DS_EINVAL before touching a
+    device, and without a GPU the compute call fails loudly (no CPU path)."""
+    L = _lib.lib()
+    b = pack([([1, 2, 1], [(0, 1), (1, 2)])])
+    st = np.zeros(1, np.int32)
+    bo = np.zeros((1, 10), np.int64)
+    r = _abi.ds_results(st.ctypes.data, bo.ctypes.data, None)
+    pl = _lib.platform(8)
+    bad = _abi.ds_dag_batch16(1, b.node_off.ctypes.data, b.edge_off.ctypes.data, None, None)
+    assert L.ds_analyze_batch16(C.byref(bad), C.byref(pl), _abi.DS_M_ALL, C.byref(r), 0) == _abi.DS_EINVAL
+    if _lib.device_count() == 0:
+        with pytest.raises(_lib.DagschedError):
+            _lib.analyze16(b, 8)
