@@ -16,6 +16,7 @@ struct K1Occupancy {
     int grid_mid = 0;
     int grid_back = 0;
     int grid_back_lane = 0;  // k1_back_lane (one lane per DAG)
+    int grid_back_coop = 0;  // k1_back_coop (lanes + warp-cooperative apportion)
 };
 
 constexpr int kWarpsSmall = 4;  // WarpState<1,u64> per warp, 4 warps per CTA

@@ -45,6 +45,10 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
             return e;
         int of = 0, om = 0, ob = 0, obl = 0;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obl, k1_back_lane<>, 32 * kLaneWarps, 0))) return e;
+        int obc = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obc, k1_back_coop<>, 32 * kCoopWarps, 0))) return e;
+        if (obc < 1) return cudaErrorInvalidConfiguration;
+        occ.grid_back_coop = sms * obc;
         if (obl < 1) return cudaErrorInvalidConfiguration;
         // DS_K1_LANE_CTAS_PER_SM (tuning knob): fewer resident DAG walks keep
         // their hand-off state inside L2
@@ -110,12 +114,20 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
     if (split && (a.mask & DS_M_PROPOSED)) {
         k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = mark("k1_mid")) != cudaSuccess) return e;
-        // one lane per DAG (default) or one warp per DAG (DS_K1_BACK=warp)
-        static const bool warp_back = [] {
+        // one lane per DAG (default, 3.06 ms per 1M C5 DAGs); DS_K1_BACK=coop
+        // adds warp-cooperative apportion at rendezvous points (4.25 ms: the
+        // lanes wait for each other), DS_K1_BACK=warp one warp per DAG (4.40)
+        static const int back_kind = [] {
             const char* env = getenv("DS_K1_BACK");
-            return env && env[0] == 'w';
+            return env && env[0] == 'w' ? 2 : (env && env[0] == 'c' ? 0 : 1);
         }();
-        if (warp_back) {
+        const bool warp_back = back_kind == 2;
+        if (back_kind == 0) {
+            const u64 need = (a.n_dags + 32 * kCoopWarps - 1) / (32 * kCoopWarps);
+            k1_back_coop<><<<int(need < u64(occ.grid_back_coop) ? need : u64(occ.grid_back_coop)), 32 * kCoopWarps, 0,
+                             s>>>(a);
+            if ((e = mark("k1_back_coop")) != cudaSuccess) return e;
+        } else if (warp_back) {
             k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
             if ((e = mark("k1_back")) != cudaSuccess) return e;
         } else {

@@ -209,3 +209,24 @@ def test_paper_benchmark_families_vs_oracle(orc):
         for d, s in enumerate(schemes):
             got = helpers.normalise_scheme(scheme.to_reference_json(s))
             assert got == helpers.normalise_scheme(c.scheme(d, M)), (M, d)
+
+
+@pytest.mark.parametrize("kind", ["warp", "coop"])
+def test_back_kernel_variants_agree(kind):
+    """DS_K1_BACK=warp / coop (the alternative k1_back kernels) give the same
+    results as the default one-lane-per-DAG walk (run in a subprocess: the
+    selection is read once per process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = ("import json,sys; sys.path.insert(0,'.'); from paper_2602_20826_b200 import _lib; "
+            "b=_lib.Corpus(20000, seed=5).batch(); st,bo,ng=_lib.analyze(b,148); st2,bo2,_=_lib.analyze(b,16); "
+            "print(json.dumps([int(st.sum()), int(bo.sum() % 1000000007), int(ng.sum()), int(bo2.sum() % 1000000007)]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k in ("lane", kind):
+        env = dict(os.environ, DS_K1_BACK=k)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
