@@ -438,7 +438,8 @@ def main():
             "makespan": makespan,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
-            "e2e_gpu_launches": chunks * launches_per_step * args.e2e_steps,
+            # per chunk: the K1 sequence, plus the 16-bit form's widening kernel
+            "e2e_gpu_launches": chunks * (launches_per_step + int(compact)) * args.e2e_steps,
             "dags_ok": ok, "generation_s": gen_s,
             "kernel_ms": {"mean": statistics.mean(kms), "min": min(kms), "max": max(kms)},
         }

@@ -130,10 +130,11 @@ __global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __r
     }
 }
 
+constexpr int kMaxSlots = 8;
 struct DeviceCtx {
     std::mutex mu;
     bool init = false;
-    Slot slot[3];
+    Slot slot[kMaxSlots];
     DevBuf retry, retry_count, handoff;  // scratch for the device-pointer entry point
 };
 
@@ -195,9 +196,15 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     }
     if (bounds.back() != n) bounds.back() = n;  // small batches: one (or few) chunks
     if (bounds.size() == 1) bounds.push_back(n);
+    // streams (and buffer sets) the chunks rotate over; DS_STREAMS overrides
+    static const int n_slots = [] {
+        const char* e = getenv("DS_STREAMS");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1 && v <= kMaxSlots ? v : 3;
+    }();
     for (size_t c = 0; c + 1 < bounds.size(); ++c) {
         const u64 lo = bounds[c], hi = bounds[c + 1], nd = hi - lo;
-        Slot& sl = ctx.slot[c % 3];
+        Slot& sl = ctx.slot[c % n_slots];
         // indices are relative to node_off[0] / edge_off[0] (header contract)
         const u64 n0 = b->node_off[lo] - b->node_off[0], n1 = b->node_off[hi] - b->node_off[0];
         const u64 e0 = b->edge_off[lo] - b->edge_off[0], e1 = b->edge_off[hi] - b->edge_off[0];
