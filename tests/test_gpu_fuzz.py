@@ -68,3 +68,20 @@ def helpers_raw(b):
     """The packed batch as the checkers take it (same arrays, id-free)."""
     from paper_2602_20826_b200.batch import from_arrays
     return from_arrays(b.node_off, b.edge_off, b.load_num, b.load_den, b.edges)
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_fuzz_compact16_matches_wide(seed):
+    """Integer-load fuzz DAGs (shuffled ids, n up to 200, oversized loads)
+    through the 16-bit wire form: same statuses and bounds as the wide form,
+    which the oracle pins above."""
+    dags = fuzz_dags.corpus(seed, 600, max_n=200)
+    dags = [(nodes, edges) for nodes, edges in dags
+            if all(Fraction(l).denominator == 1 and 1 <= Fraction(l) <= 0xFFFF for _, l in nodes)]
+    assert len(dags) > 100
+    b = pack(dags)
+    assert b.compact16_ok()
+    for M in (3, 8, 148):
+        st, bounds, ng = _lib.analyze(b, M)
+        st16, bounds16, ng16 = _lib.analyze16(b, M)
+        assert np.array_equal(st, st16) and np.array_equal(bounds, bounds16) and np.array_equal(ng, ng16), M
