@@ -216,7 +216,11 @@ typedef struct ds_exec_cfg {
                                this many SMs (multiple of 8 on sm_90+) — an
                                M-SM device for the paper's contended regime   */
     int32_t engine;         /* DS_ENGINE_*                                       */
-    int32_t reserved;
+    int32_t chunk_elems;    /* DS_ENGINE_DYNAMIC: 0 = rank r of an m-rank entity
+                               processes the fixed slice r/m; > 0 = its ranks
+                               claim chunks of this many elements from the
+                               entity's range until it is done (still at most
+                               m SMs at a time; late ranks take less)         */
 } ds_exec_cfg;
 
 /* Executor engines. GRAPH: one CUDA Graph kernel node per entity (any plan).

@@ -500,6 +500,8 @@ struct DArgs {
     unsigned int* pend_claim;   // [n]
     unsigned int* pend_done;    // [n]
     unsigned int* idle;         // [1] stream engine: CTAs with nothing in flight
+    unsigned int* next_chunk;   // [n] chunked ranks: next chunk of the entity
+    unsigned long long chunk;   // elements per chunk, 0 = fixed slices
     int rec;                    // recorded replay slot, < 0: not recorded
     unsigned long long* stamps;
     uint32_t* smids;
@@ -518,6 +520,7 @@ __global__ void k3_dyn_reset(const DArgs a) {
         a.claimed[i] = 0;
         a.pend_claim[i] = a.ents[i].pred_ranks;
         a.pend_done[i] = a.ents[i].pred_ranks;
+        if (a.next_chunk) a.next_chunk[i] = 0;
     }
     if (threadIdx.x == 0 && a.idle) *a.idle = 0;
 }
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ TmaRing ring;
     __shared__ unsigned long long t0s;
-    __shared__ uint32_t s_ent, s_rank;
+    __shared__ uint32_t s_ent, s_rank, s_chunk;
     if (kTma && threadIdx.x == 0) tma_ring_init(&ring);
     const int lane = threadIdx.x & 31;
     uint32_t it = 0;   // TMA ring chunks used by this CTA
@@ -585,9 +588,28 @@ __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const
         if (ent == ~0u) break;
         const DEnt e = a.ents[ent];
         const unsigned long long len = e.hi - e.lo;
-        const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
-        if constexpr (kTma) tma_mix_slice(e.x, e.y, s0, s1, sm, &ring, it);
-        else mix_ldg_slice<4>(e.x, e.y, s0, s1);
+        if (a.chunk == 0) {
+            const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
+            if constexpr (kTma) tma_mix_slice(e.x, e.y, s0, s1, sm, &ring, it);
+            else mix_ldg_slice<4>(e.x, e.y, s0, s1);
+        } else {
+            // chunked ranks: claim chunk after chunk of the entity's range; the
+            // next claim is issued before the current chunk is processed
+            const unsigned long long nch = (len + a.chunk - 1) / a.chunk;
+            if (threadIdx.x == 0) s_chunk = atomicAdd(a.next_chunk + ent, 1u);
+            __syncthreads();
+            unsigned long long c = s_chunk;
+#pragma unroll 1
+            while (c < nch) {
+                __syncthreads();  // every thread has read s_chunk
+                if (threadIdx.x == 0) s_chunk = atomicAdd(a.next_chunk + ent, 1u);
+                const unsigned long long s0 = e.lo + c * a.chunk, s1 = min(e.hi, s0 + a.chunk);
+                if constexpr (kTma) tma_mix_slice(e.x, e.y, s0, s1, sm, &ring, it);
+                else mix_ldg_slice<4>(e.x, e.y, s0, s1);
+                __syncthreads();
+                c = s_chunk;
+            }
+        }
         __syncthreads();
         // completion in warp 1 while warp 0 already claims the next item: the
         // fence (waits for this CTA's stores, observed through the barrier)

@@ -71,6 +71,7 @@ struct Exec {
     uint32_t grid = 0;
     // dynamic engine
     DArgs dyn{};
+    unsigned long long chunk_elems = 0;
     std::vector<void*> dyn_bufs;
 };
 
@@ -236,8 +237,10 @@ int build_dynamic(Exec* E, const ds_exec_plan* plan) {
         (rc = dev((void**)&a.quota, quota.size() * 4, quota.data())) ||
         (rc = dev((void**)&a.claimed, size_t(n) * 4, nullptr)) ||
         (rc = dev((void**)&a.pend_claim, size_t(n) * 4, nullptr)) ||
-        (rc = dev((void**)&a.pend_done, size_t(n) * 4, nullptr)) || (rc = dev((void**)&a.idle, 4, nullptr)))
+        (rc = dev((void**)&a.pend_done, size_t(n) * 4, nullptr)) || (rc = dev((void**)&a.idle, 4, nullptr)) ||
+        (rc = dev((void**)&a.next_chunk, size_t(n) * 4, nullptr)))
         return rc;
+    a.chunk = E->chunk_elems;
     const bool tma = E->workload == DS_WL_MIX32_TMA || E->engine == DS_ENGINE_STREAM;
     void* k = E->engine == DS_ENGINE_STREAM ? reinterpret_cast<void*>(k3_stream)
               : tma                         ? reinterpret_cast<void*>(k3_dynamic<true>)
@@ -514,6 +517,12 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     E->workload = cfg->workload;
     E->engine = cfg->engine;
     E->threads = threads;
+    if (cfg->chunk_elems < 0) {
+        destroy(E);
+        delete H;
+        return fail(DS_EINVAL, "chunk_elems must be >= 0");
+    }
+    E->chunk_elems = (unsigned long long)cfg->chunk_elems;
     auto bail = [&](int rc) {
         destroy(E);
         delete H;

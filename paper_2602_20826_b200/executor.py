@@ -44,7 +44,7 @@ class ds_exec_plan(C.Structure):
 
 class ds_exec_cfg(C.Structure):
     _fields_ = [("workload", C.c_int32), ("block_threads", C.c_int32), ("seed", C.c_uint32),
-                ("sm_limit", C.c_int32), ("engine", C.c_int32), ("reserved", C.c_int32)]
+                ("sm_limit", C.c_int32), ("engine", C.c_int32), ("chunk_elems", C.c_int32)]
 
 
 ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAM = 0, 1, 2, 3, 4
@@ -198,7 +198,7 @@ class RunResult:
 
 class Executor:
     def __init__(self, plan: Plan, workload: int = WL_MIX32, threads: int = 1024, seed: int = 1, device: int = 0,
-                 sm_limit: int = 0, engine: int = ENGINE_GRAPH):
+                 sm_limit: int = 0, engine: int = ENGINE_GRAPH, chunk_elems: int = 0):
         """sm_limit > 0 runs inside a green context of that many SMs; engine
         ENGINE_PERSISTENT runs a group-structured plan as one resident CTA per
         SM with completion counters instead of one kernel per entity."""
@@ -208,7 +208,7 @@ class Executor:
         self.seed = seed
         self.h = C.c_void_p()
         self._cplan = plan.to_c()
-        cfg = ds_exec_cfg(workload, threads, seed, int(sm_limit), int(engine), 0)
+        cfg = ds_exec_cfg(workload, threads, seed, int(sm_limit), int(engine), int(chunk_elems))
         check(L.ds_exec_create(C.byref(self._cplan), C.byref(cfg), device, C.byref(self.h)))
         t = C.c_uint64()
         check(L.ds_exec_total_ctas(self.h, C.byref(t)))

@@ -150,10 +150,13 @@ def test_persistent_engine(barrier):
         ex.close()
 
 
-@pytest.mark.parametrize("engine,workload", [(X.ENGINE_DYNAMIC, X.WL_MIX32), (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA),
-                                             (X.ENGINE_STREAM, X.WL_MIX32_TMA)])
+@pytest.mark.parametrize("engine,workload,chunk", [(X.ENGINE_DYNAMIC, X.WL_MIX32, 0),
+                                                   (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA, 0),
+                                                   (X.ENGINE_DYNAMIC, X.WL_MIX32, 1000),
+                                                   (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA, 4099),
+                                                   (X.ENGINE_STREAM, X.WL_MIX32_TMA, 0)])
 @pytest.mark.parametrize("barrier", [True, False])
-def test_dynamic_engine(barrier, engine, workload):
+def test_dynamic_engine(barrier, engine, workload, chunk):
     """DS_ENGINE_DYNAMIC: resident CTAs claim (entity, rank) items from a
     device-side ready queue — every item runs exactly once per replay, outputs
     bit-exact, precedence / SM-exclusivity / group-order contracts hold."""
@@ -162,7 +165,7 @@ def test_dynamic_engine(barrier, engine, workload):
     for dag, M in cases:
         s, loads, edges = _scheme_and_loads(dag, M)
         plan = X.plan_from_scheme(s, loads, UNIT + 5, barrier_groups=barrier)
-        ex = X.Executor(plan, workload=workload, engine=engine, sm_limit=0 if M == 148 else 8)
+        ex = X.Executor(plan, workload=workload, engine=engine, sm_limit=0 if M == 148 else 8, chunk_elems=chunk)
         res = ex.run(8, warmup=2)
         for r in range(8):
             st = res.stamps[r]

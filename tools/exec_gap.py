@@ -99,13 +99,16 @@ def main():
                       X.ENGINE_STREAM if kind.startswith("str") else
                       X.ENGINE_DYNAMIC if kind.startswith("dyn") else
                       X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
+            chunk = 0
+            if "_c" in kind and kind.startswith("dyn"):  # e.g. dynamic_deps_c32768: chunked ranks
+                kind, chunk = kind.split("_c")[0], int(kind.split("_c")[1])
             wl = X.WL_MIX32_TMA if kind.endswith("_tma") or kind.startswith("str") else args.workload
             kind_ = kind.replace("_tma", "")
             if kind_.startswith(("proposed", "persistent", "dynamic", "stream")):
                 plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=not kind_.endswith("_deps"))
             else:
                 plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("str_", ""), loads, edges, M, args.unit)
-            ex = X.Executor(plan, workload=wl, engine=engine, sm_limit=args.sm_limit)
+            ex = X.Executor(plan, workload=wl, engine=engine, sm_limit=args.sm_limit, chunk_elems=chunk)
             res = ex.run(args.replays, warmup=3, stamps=True)
             if engine == X.ENGINE_GRAPH_FREE:
                 plan._slots = ex.slots
@@ -113,7 +116,7 @@ def main():
                     e.parallelism *= X.FREE_CTA_FACTOR
             a = [analyse(plan, res, r, bpe) for r in range(args.replays)]
             med = int(np.argsort([x["makespan_us"] for x in a])[len(a) // 2])
-            row[kind] = a[med]
+            row[kind + (f"_c{chunk}" if chunk else "")] = a[med]
             ex.close()
         out.append(row)
         print(json.dumps({k: (v if not isinstance(v, dict) else {kk: vv for kk, vv in v.items()
