@@ -157,8 +157,10 @@ def host_chunks(n: int) -> int:
     return max(1, len(bounds) - 1)
 
 
-def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_dags=1_000_000):
-    """Time the reference CPU path on a bounded sample of the same workload."""
+def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_dags=1_000_000, gpu=None):
+    """Time the reference CPU path on a bounded sample of the same workload;
+    with gpu = (status, bounds) of the device pass, also count how many of
+    the sampled DAGs the device got bit-exact (status and all ten num/den)."""
     from oracle import bindings
     from paper_2602_20826_b200 import _abi
 
@@ -167,11 +169,16 @@ def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_d
     n = min(min_dags, batch.n_dags)
     while True:
         c = chk.corpus(batch.slice(0, n))
-        _, _, secs = c.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=True)
+        st_c, b_c, secs = c.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=True)
         if secs >= target_s / 4 or n >= min(max_dags, batch.n_dags):
             break
         n = min(max_dags, batch.n_dags, int(n * max(2.0, target_s / max(secs, 1e-3))))
-    return {"value": n / secs, "unit": UNIT, "cores": cpu_cores(),
+    parity = None
+    if gpu is not None:
+        st_g, b_g = gpu[0][:n], gpu[1][:n]
+        same = (st_g == st_c) & (b_g == b_c).all(1)
+        parity = {"dags": int(n), "bit_exact": int(same.sum()), "checker": "oracle/_ref" if kind == "ref" else "oracle"}
+    return {"value": n / secs, "unit": UNIT, "cores": cpu_cores(), "parity_vs_gpu": parity,
             "kind": "reference" if kind == "ref" else "port",
             "sample": f"first {n} DAGs of the rank-0 shard, evaluate_corpus(parallel=true, OpenMP "
                       f"{cpu_cores()} threads) + lower_bound, {secs:.2f} s",
@@ -410,7 +417,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_run(batch)
+            cpu = cpu_baseline_run(batch, gpu=(st, bounds))
         except Exception as e:  # the baseline is reported, never required
             cpu = {"error": str(e)}
 
