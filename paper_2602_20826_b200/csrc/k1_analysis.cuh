@@ -1606,7 +1606,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
 }
 
 #ifndef DS_LANE_MIN_BLOCKS
-#define DS_LANE_MIN_BLOCKS 10  // 48 registers: 3.09 ms; 40 regs 3.13, 64 regs 3.45 (1M C5 DAGs)
+#define DS_LANE_MIN_BLOCKS 9  // 56 registers: 3.02 ms; 64 regs 3.09, 48 regs 3.07, 40 regs 3.09 (1M C5 DAGs)
 #endif
 template <bool UNUSED = false>
 __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_lane(const K1Args a) {
