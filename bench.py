@@ -61,17 +61,48 @@ def cpu_cores():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle-reason sampling during the timed region
+    (B200_PROFILING.md): NVML every 5 ms from a thread (the timed region is
+    ~0.2 s), else `nvidia-smi -lms 200`."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits (nvml.h: nvmlClocksEventReason*)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.nvml = None
+        self.samples = []
+        self.mx = None
+
+    def _poll(self):
+        import pynvml as N
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((float(sm), int(rs)))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        try:
+            import threading
+
+            import pynvml as N
+            N.nvmlInit()
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.stop = threading.Event()
+            self.nvml = threading.Thread(target=self._poll, daemon=True)
+            self.nvml.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -82,6 +113,9 @@ class Clocks:
 
     def __exit__(self, *a):
         self.lines = []
+        if self.nvml is not None:
+            self.stop.set()
+            self.nvml.join(timeout=2)
         if self.p:
             self.p.terminate()
             try:
@@ -91,7 +125,12 @@ class Clocks:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons = [], self.mx, set()
+        for clk, bits in self.samples:
+            sm.append(clk)
+            for name, b in self.BITS.items():
+                if bits & b:
+                    reasons.add(name)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
@@ -106,7 +145,8 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml 5 ms" if self.samples else "nvidia-smi 200 ms"}
 
 
 def measured_peak():
