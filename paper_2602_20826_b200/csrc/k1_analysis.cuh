@@ -1417,6 +1417,7 @@ constexpr int kLaneWarps = 4;
 // fell to 12 warps/SM and the walk is latency bound). k1_back (warp per DAG)
 // 4.40.
 
+template <int QB>  // bits per packed quota field: 8 (M <= 255) or 16 (M <= 65535)
 __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
                                              const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
     const K1Node* __restrict__ nodes = a.h.node + n0;
@@ -1461,15 +1462,20 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             conc = ~__ldg(&nodes[v].ad);
         } else {
             // apportion (scheduler.cpp:35-95) over the pending loads. Member k's
-            // quota (<= M <= 255 here) lives in 8 bits of mq[k >> 3]
-            // (registers, no local memory); cap and quota remainder are
-            // recomputed where needed.
-            if (__popcll(org) > kLaneMembers || P.M > 255) return kLaneRetry;
-            u64 mq[2] = {0, 0};
-            auto get = [&](int k) { return int((mq[k >> 3] >> (8 * (k & 7))) & 0xff); };
+            // quota (<= M) lives in an 8-bit field (M <= 255) or a 16-bit
+            // field (M <= 65535) of the packed words mq (registers, no local
+            // memory); cap and quota remainder are recomputed where needed.
+            if (__popcll(org) > kLaneMembers || P.M >= (1 << QB)) return kLaneRetry;
+            u64 mq[QB == 8 ? 2 : 4] = {};
+            constexpr int lw = QB == 8 ? 3 : 4;  // log2 bits per field
+            constexpr int lper = 6 - lw;         // log2 fields per word
+            constexpr u64 fmask = (1ull << QB) - 1;
+            auto get = [&](int k) {
+                return int((mq[k >> lper] >> ((k & ((1 << lper) - 1)) << lw)) & fmask);
+            };
             auto put = [&](int k, int m) {
-                const int sh = 8 * (k & 7);
-                mq[k >> 3] = (mq[k >> 3] & ~(0xffull << sh)) | (u64(m) << sh);
+                const int sh = (k & ((1 << lper) - 1)) << lw;
+                mq[k >> lper] = (mq[k >> lper] & ~(fmask << sh)) | (u64(m) << sh);
             };
             RatT<u32> Wt{0, 1};
 #pragma unroll 1
@@ -1608,7 +1614,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
 #ifndef DS_LANE_MIN_BLOCKS
 #define DS_LANE_MIN_BLOCKS 9  // 56 registers: 3.02 ms; 64 regs 3.09, 48 regs 3.07, 40 regs 3.09 (1M C5 DAGs)
 #endif
-template <bool UNUSED = false>
+template <bool UNUSED = false, int QB = 8>
 __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_lane(const K1Args a) {
     const int lane = threadIdx.x & 31;
     const u32 nbase = a.node_off[0];
@@ -1625,7 +1631,7 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
         const int n = int(a.node_off[d + 1] - nbase - n0);
         RatT<u32> bound{0, 0};
         int ng = 0;
-        const int st = schedule_lane(a, n0, n, a.h.ndiv[d], P, bound, ng);
+        const int st = schedule_lane<QB>(a, n0, n, a.h.ndiv[d], P, bound, ng);
         if (st == DS_EOVERFLOW || st == kLaneRetry) {  // recomputed from scratch in wider words
             a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
             a.status[d] = kStRetried;

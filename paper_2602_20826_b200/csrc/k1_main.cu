@@ -132,8 +132,9 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
             if ((e = mark("k1_back")) != cudaSuccess) return e;
         } else {
             const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
-            k1_back_lane<><<<int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane)), 32 * kLaneWarps, 0,
-                             s>>>(a);
+            const int g = int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane));
+            if (a.plat.M <= 255) k1_back_lane<false, 8><<<g, 32 * kLaneWarps, 0, s>>>(a);
+            else k1_back_lane<false, 16><<<g, 32 * kLaneWarps, 0, s>>>(a);
             if ((e = mark("k1_back_lane")) != cudaSuccess) return e;
         }
     }

@@ -230,3 +230,14 @@ def test_back_kernel_variants_agree(kind):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
+
+
+def test_lane_walk_wide_platform_matches_oracle(orc):
+    """M > 255 (the paper's Fig. 4 sweep reaches M = 256): 16-bit quota
+    fields in the one-lane-per-DAG walk; bit-exact vs the oracle."""
+    corpus = _lib.Corpus(20000, seed=9, avg_load=200, max_width=16)
+    b = corpus.batch()
+    for M in (256, 300, 1000):
+        st, bounds, _ = _lib.analyze(b, M)
+        st_o, b_o, _ = orc.corpus(b).evaluate(M)
+        assert np.array_equal(st, st_o) and np.array_equal(bounds, b_o), M

@@ -21,7 +21,8 @@ for i, row in enumerate(r):
         h, rows = row, r[i + 1:]
         break
 mangled = {"k1_front": "_ZN2ds8k1_frontILb0EEEvNS_6K1ArgsE", "k1_mid": "_ZN2ds6k1_midILb0EEEvNS_6K1ArgsE",
-           "k1_back": "_ZN2ds7k1_backILb0EEEvNS_6K1ArgsE"}.get(kname, kname)
+           "k1_back": "_ZN2ds7k1_backILb0EEEvNS_6K1ArgsE",
+           "k1_back_lane": "_ZN2ds12k1_back_laneILb0ELi8EEEvNS_6K1ArgsE"}.get(kname, kname)
 ins = sh.load_sass(sass, mangled)
 print("rows", len(rows), "sass", len(ins))
 ie, tt = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
