@@ -260,13 +260,17 @@ def makespan_summary(device, replays, n_c2=8, unit=1 << 17):
     # proposed: CUDA graph, group barriers (simulate_scheme semantics, the
     # Theorem-1 setting); proposed_dynamic: the same schedule's augmented graph
     # on the dynamic persistent engine (device ready queue, quota-capped)
-    p50 = {"proposed": [], "proposed_dynamic": [], "serial": [], "multistream": []}
+    # multistream: the Greedy baseline captured as a CUDA graph; multistream_host:
+    # naive multi-stream launch (host launches per node on its own stream, events)
+    p50 = {"proposed": [], "proposed_dynamic": [], "serial": [], "multistream": [], "multistream_host": []}
     for (loads, edges), sch in zip(norm, schemes):
         bus = X.bound_us(sch, cal)
         for kind in p50:
-            engine = X.ENGINE_DYNAMIC if kind == "proposed_dynamic" else X.ENGINE_GRAPH
+            engine = (X.ENGINE_DYNAMIC if kind == "proposed_dynamic" else
+                      X.ENGINE_STREAMS if kind == "multistream_host" else X.ENGINE_GRAPH)
             plan = (X.plan_from_scheme(sch, loads, unit, barrier_groups=kind == "proposed")
-                    if kind.startswith("proposed") else X.plan_baseline(kind, loads, edges, M, unit))
+                    if kind.startswith("proposed") else
+                    X.plan_baseline(kind.replace("_host", ""), loads, edges, M, unit))
             ex = X.Executor(plan, device=device, workload=wl, engine=engine)
             r = ex.run(replays, warmup=3, stamps=False)
             ex.close()
@@ -274,12 +278,14 @@ def makespan_summary(device, replays, n_c2=8, unit=1 << 17):
             if kind in ratio:
                 ratio[kind].extend((r.makespan_us / bus).tolist())
                 over[kind] += int((r.makespan_us > bus).sum())
-            launches += (1 if engine == X.ENGINE_DYNAMIC else len(plan.entities)) * replays
+            launches += (1 if engine == X.ENGINE_DYNAMIC else len(plan.entities) + 1) * replays
     out = {"dags": names, "replays_per_dag": replays, "sm_count": M, "node_kernel": "k2_mix_tma (all variants)",
            "tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
            "measured_over_bound": {}, "replays_over_bound": over,
            "mean_p50_us": {k: float(np.mean(v)) for k, v in p50.items()},
            "dynamic_beats_multistream_p50": int(sum(a < b for a, b in zip(p50["proposed_dynamic"], p50["multistream"]))),
+           "dynamic_beats_multistream_host_p50": int(sum(a < b for a, b in zip(p50["proposed_dynamic"],
+                                                                               p50["multistream_host"]))),
            "executor_kernel_launches": launches}
     for k, v in ratio.items():
         v = np.asarray(v)

@@ -13,8 +13,11 @@ SMs:
                  per SM, device-side claiming of quota-capped entity ranks)
   dynamic_deps   = proposed_deps on the dynamic engine
   serial         one chain in topological order, m = min(m^max, M)
-  multistream    original DAG edges only, m = min(m^max, M) — naive
-                 multi-stream launch / Greedy
+  multistream    original DAG edges only, m = min(m^max, M) — the Greedy of
+                 PAPER.md:533 captured as a CUDA graph (a strong baseline)
+  multistream_host  the same launched by the host every iteration, one stream
+                 per node, cudaStreamWaitEvent on the predecessors: naive
+                 multi-stream launch as an application writes it
   multistream_free  the same with 4 m unconstrained 256-thread CTAs
 
 M = 148 runs on the whole GPU; M < 148 runs inside a green context of M SMs
@@ -45,7 +48,8 @@ from paper_2602_20826_b200 import executor as X  # noqa: E402
 from paper_2602_20826_b200.batch import pack  # noqa: E402
 
 STALL_US = X.STALL_US
-VARIANTS = ("proposed", "proposed_deps", "dynamic", "dynamic_deps", "serial", "multistream", "multistream_free")
+VARIANTS = ("proposed", "proposed_deps", "dynamic", "dynamic_deps", "serial", "multistream", "multistream_host",
+            "multistream_free")
 
 
 def stats(a):
@@ -79,13 +83,14 @@ def run_dag(loads, edges, sch, M, sm_limit, cal, args):
            "greedy_units": str(sch.bounds["greedy"]), "bound_us": bound_us}
     for kind in VARIANTS:
         engine = (X.ENGINE_DYNAMIC if kind.startswith("dynamic") else
+                  X.ENGINE_STREAMS if kind.endswith("_host") else
                   X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
         if kind in ("proposed", "dynamic"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=True)
         elif kind in ("proposed_deps", "dynamic_deps"):
             plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=False)
         else:
-            plan = X.plan_baseline(kind.replace("_free", ""), loads, edges, M, args.unit)
+            plan = X.plan_baseline(kind.replace("_free", "").replace("_host", ""), loads, edges, M, args.unit)
         ex = X.Executor(plan, workload=args.workload, sm_limit=sm_limit, engine=engine)
         r = ex.run(args.replays, warmup=3, stamps=True)
         vp = vs = vg = 0
@@ -132,8 +137,9 @@ def summarise(results, prefix):
         }
     for kind in ("proposed", "proposed_deps", "dynamic", "dynamic_deps"):
         for q in ("p50", "p99", "max"):
-            s[f"{kind}_beats_multistream_{q}"] = int(sum(r[kind]["makespan_us"][q] < r["multistream"]["makespan_us"][q]
-                                                         for r in sel))
+            for base in ("multistream", "multistream_host"):
+                s[f"{kind}_beats_{base}_{q}"] = int(sum(r[kind]["makespan_us"][q] < r[base]["makespan_us"][q]
+                                                        for r in sel))
     s["group_order_violations"] = int(sum(r["proposed"]["group_order_violations"] for r in sel))
     return s
 

@@ -250,6 +250,11 @@ typedef struct ds_exec_cfg {
  * without a launch/drain bubble. Runs the DS_WL_MIX32 computation through
  * DS_WL_MIX32_TMA's ring (544 threads per CTA). */
 #define DS_ENGINE_STREAM 4
+/* STREAMS: no graph — every replay the host launches each entity's kernel on
+ * its own stream after cudaStreamWaitEvent on its predecessors' events (and,
+ * with group barriers, on the previous group's): naive multi-stream launch as
+ * an application writes it. */
+#define DS_ENGINE_STREAMS 5
 
 /* Per-replay device-timed spans and, for every replay, per-CTA stamps. */
 typedef struct ds_exec_trace {

@@ -60,6 +60,10 @@ struct Exec {
     uint32_t* smids = nullptr;
     int cap = 0;
     std::vector<NodeArgs> args;  // kernel-node parameters (stable storage)
+    // host-launched streams engine (naive multi-stream launch)
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> ent_ev;
+    cudaEvent_t start_ev = nullptr;
     // persistent engine
     int engine = DS_ENGINE_GRAPH;
     PEnt* d_ents = nullptr;
@@ -347,6 +351,12 @@ void destroy(Exec* E) {
     {
     CtxGuard g(E);
     if (E->s) cudaStreamSynchronize(E->s);
+    for (auto st : E->streams) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    for (auto ev : E->ent_ev) cudaEventDestroy(ev);
+    if (E->start_ev) cudaEventDestroy(E->start_ev);
     if (E->exec) cudaGraphExecDestroy(E->exec);
     if (E->graph) cudaGraphDestroy(E->graph);
     for (auto* p : E->x) cudaFree(p);
@@ -583,6 +593,30 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
         if (E->workload != DS_WL_MIX32 && E->workload != DS_WL_MIX32_TMA)
             return bail(fail(DS_EINVAL, "dynamic engines run the mix32 workloads"));
         if (int rc = build_dynamic(E, &H->P.plan)) return bail(rc);
+    } else if (E->engine == DS_ENGINE_STREAMS) {
+        // one stream per entity (up to 64, reused round-robin), one event each
+        const int n = plan->n_entities;
+        const int k = std::min(n, 64);
+        for (int i = 0; i < k; ++i) {
+            cudaStream_t st = nullptr;
+            if (E->gctx) {
+                CUstream cs;
+                if (driver().greenStream(&cs, E->gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+                    return bail(fail(DS_ECUDA, "green-context stream"));
+                st = reinterpret_cast<cudaStream_t>(cs);
+            } else if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+                return bail(fail(DS_ECUDA, "stream"));
+            }
+            E->streams.push_back(st);
+        }
+        for (int i = 0; i < n; ++i) {
+            cudaEvent_t ev;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(DS_ECUDA, "event"));
+            E->ent_ev.push_back(ev);
+        }
+        if (cudaEventCreateWithFlags(&E->start_ev, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(DS_ECUDA, "event"));
     } else if (E->engine != DS_ENGINE_GRAPH && E->engine != DS_ENGINE_GRAPH_FREE) {
         return bail(fail(DS_EINVAL, "unknown engine"));
     }
@@ -665,6 +699,40 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
             // they wait on each other's completion counters
             DS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k3_persistent), dim3(E->grid),
                                                 dim3(unsigned(E->threads)), kargs, size_t(kNodeSmem), E->s));
+        } else if (E->engine == DS_ENGINE_STREAMS) {
+            // naive multi-stream launch: the host walks the plan in order and
+            // launches every entity on its stream after cudaStreamWaitEvent on
+            // its predecessors' events (and, with group barriers, on every
+            // member of the previous group) — what an application without a
+            // graph does each iteration
+            const ds_exec_plan& P = H->P.plan;
+            DS_CUDA(cudaEventRecord(E->start_ev, E->s));
+            const size_t ns = E->streams.size();
+            for (size_t j = 0; j < ns; ++j) DS_CUDA(cudaStreamWaitEvent(E->streams[j], E->start_ev, 0));
+            int prev_group = -1;
+            std::vector<int> prev_members, cur_members;
+            for (int i = 0; i < P.n_entities; ++i) {
+                const ds_exec_entity& e = P.entities[i];
+                cudaStream_t st = E->streams[size_t(i) % ns];
+                if (P.barrier_groups && e.group != prev_group) {
+                    prev_members.swap(cur_members);
+                    cur_members.clear();
+                    prev_group = e.group;
+                }
+                for (uint32_t q = 0; q < e.n_preds; ++q)
+                    DS_CUDA(cudaStreamWaitEvent(st, E->ent_ev[P.preds[e.pred_off + q]], 0));
+                if (P.barrier_groups)
+                    for (int j : prev_members) DS_CUDA(cudaStreamWaitEvent(st, E->ent_ev[j], 0));
+                void* kargs[] = {&E->args[i]};
+                DS_CUDA(cudaLaunchKernel(kernel_of(E->workload), dim3(unsigned(e.parallelism)),
+                                         dim3(unsigned(threads_of(E->workload, E->threads))), kargs,
+                                         size_t(smem_of(E->workload)), st));
+                DS_CUDA(cudaEventRecord(E->ent_ev[i], st));
+                if (P.barrier_groups) cur_members.push_back(i);
+            }
+            for (int i = 0; i < P.n_entities; ++i) DS_CUDA(cudaStreamWaitEvent(E->s, E->ent_ev[i], 0));
+            k2_tick<<<1, 1, 0, E->s>>>(E->replay);
+            DS_CUDA(cudaGetLastError());
         } else {
             DS_CUDA(cudaGraphLaunch(E->exec, E->s));
         }

@@ -47,7 +47,7 @@ class ds_exec_cfg(C.Structure):
                 ("sm_limit", C.c_int32), ("engine", C.c_int32), ("chunk_elems", C.c_int32)]
 
 
-ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAM = 0, 1, 2, 3, 4
+ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAM, ENGINE_STREAMS = 0, 1, 2, 3, 4, 5
 FREE_CTA_FACTOR = 4  # DS_FREE_CTA_FACTOR
 
 

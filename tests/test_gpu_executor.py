@@ -206,3 +206,25 @@ def test_free_launch_runs_every_workload(workload):
     for v in range(len(loads)):
         assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
     ex.close()
+
+
+
+@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_TMA])
+def test_host_streams_engine(workload):
+    """DS_ENGINE_STREAMS (host-launched kernels on per-entity streams with
+    events): outputs bit-exact and the trace contracts hold, for a baseline
+    plan and for the schedule with group barriers."""
+    dag = workloads.inception_dag()
+    loads = [l for _, l in dag[0]]
+    plan = X.plan_baseline("multistream", loads, dag[1], 148, 4096 + 3)
+    s, loads2, edges2 = _scheme_and_loads(workloads.oversized_dag(1, 148), 148)
+    for pl, lds in ((plan, loads), (X.plan_from_scheme(s, loads2, 4096 + 3, barrier_groups=True), loads2)):
+        ex = X.Executor(pl, workload=workload, engine=X.ENGINE_STREAMS)
+        res = ex.run(4, warmup=1)
+        for r in range(4):
+            assert X.check_precedence(pl, res, r) == []
+            assert X.check_sm_exclusive(pl, res, r) == 0
+            assert X.group_overlap_violations(pl, res, r) == 0
+        for v in range(len(lds)):
+            assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, pl.node_elems[v])))
+        ex.close()

@@ -96,6 +96,7 @@ def main():
         row["work_us"] = tot / (peak * 1e3) * 148 / M
         for kind in args.variants.split(","):
             engine = (X.ENGINE_PERSISTENT if kind.startswith("persistent") else
+                      X.ENGINE_STREAMS if kind.endswith("_host") else
                       X.ENGINE_STREAM if kind.startswith("str") else
                       X.ENGINE_DYNAMIC if kind.startswith("dyn") else
                       X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
@@ -107,7 +108,7 @@ def main():
             if kind_.startswith(("proposed", "persistent", "dynamic", "stream")):
                 plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=not kind_.endswith("_deps"))
             else:
-                plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("str_", ""), loads, edges, M, args.unit)
+                plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("str_", "").replace("_host", ""), loads, edges, M, args.unit)
             ex = X.Executor(plan, workload=wl, engine=engine, sm_limit=args.sm_limit, chunk_elems=chunk)
             res = ex.run(args.replays, warmup=3, stamps=True)
             if engine == X.ENGINE_GRAPH_FREE:
