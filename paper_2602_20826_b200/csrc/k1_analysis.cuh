@@ -1110,6 +1110,13 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     u64* divg;       // division group g of DAG d at node slot g
     uint16_t* ro;    // rank[v] | order[v] << 8 (k1_mid)
     uint16_t* ndiv;  // per DAG
+    // walk order for k1_back_lane: k1_mid keys every DAG by its shape (group
+    // count, which division groups have several members), a radix sort
+    // orders the DAG indices, and the lanes of a warp then walk DAGs that take
+    // the same branches (skey/sperm in, skey2/sperm2 out)
+    u32 *skey, *sperm, *skey2, *sperm2;
+    void* sort_tmp;
+    size_t sort_tmp_bytes;
 };
 
 struct K1Args {
@@ -1130,6 +1137,7 @@ struct K1Args {
     u32* retry2;           // ... and whose 64-bit pass overflowed
     u32* retry2_count;
     K1Handoff h;           // split mode when h.node != nullptr (bounds mode only)
+    const u32* perm;       // k1_back_lane's DAG order (nullptr: index order)
 };
 
 template <int W, class T, bool DETAIL>
@@ -1295,6 +1303,10 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
         if (lane == 0) t = atomicAdd(a.retry_count + 3, 1u);
         const u64 d = __shfl_sync(FULL, t, 0);
         if (d >= a.n_dags) break;
+        if (a.h.skey && lane == 0) {
+            a.h.skey[d] = 0xffffffffu;  // not walked by k1_back_lane: sorts last
+            a.h.sperm[d] = u32(d);
+        }
         if (a.status[d] != kStMid) continue;
         const u32 n0 = a.node_off[d] - nbase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
@@ -1329,9 +1341,13 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
             a.h.ro[i] = uint16_t(S.rank[v] | (S.order[v] << 8));
             if (v < ndiv) a.h.divg[i] = S.divg[v][0];
         }
+        // shape key: group count, then which of the first 20 division groups
+        // have several members (group g -> bit 19 - g, lexicographic order)
+        const unsigned multi = __ballot_sync(FULL, lane < ndiv && __popcll(S.divg[lane][0]) > 1);
         if (lane == 0) {
             a.h.ndiv[d] = uint16_t(ndiv);
             a.status[d] = kStPending;
+            if (a.h.skey) a.h.skey[d] = (u32(min(ndiv, 63)) << 20) | (__brev(multi) >> 12);
         }
         __syncwarp();
     }
@@ -1625,8 +1641,10 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
         if (lane == 0) t = atomicAdd(a.retry_count + 5, 32u);
         t = __shfl_sync(FULL, t, 0);
         if (t >= a.n_dags) break;
-        const u64 d = u64(t) + lane;
-        if (d >= a.n_dags || a.status[d] != kStPending) continue;
+        const u64 q = u64(t) + lane;
+        if (q >= a.n_dags) continue;
+        const u64 d = a.perm ? u64(a.perm[q]) : q;
+        if (a.status[d] != kStPending) continue;
         const u32 n0 = a.node_off[d] - nbase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
         RatT<u32> bound{0, 0};

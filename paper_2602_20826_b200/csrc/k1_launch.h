@@ -6,6 +6,8 @@
 
 #include "k1_analysis.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace ds {
 
 struct K1Occupancy {
@@ -24,8 +26,15 @@ constexpr int kWarpsBig = 1;    // WarpState<4,u64> (~50 KB) per CTA
 constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 bytes)
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
+inline size_t k1_sort_tmp_bytes(u64 n_dags) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr),
+                                    static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr), int(n_dags), 0, 26);
+    return (b + 255) & ~size_t(255);
+}
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
-    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64;
+    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 16 +
+           k1_sort_tmp_bytes(n_dags);
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;
@@ -35,7 +44,13 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     h.divg = m + n_nodes;
     h.ro = reinterpret_cast<uint16_t*>(m + 2 * n_nodes);
     h.ndiv = h.ro + n_nodes;
-    (void)n_dags;
+    uintptr_t p = (reinterpret_cast<uintptr_t>(h.ndiv + n_dags) + 255) & ~uintptr_t(255);
+    h.skey = reinterpret_cast<u32*>(p);
+    h.sperm = h.skey + n_dags;
+    h.skey2 = h.sperm + n_dags;
+    h.sperm2 = h.skey2 + n_dags;
+    h.sort_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(h.sperm2 + n_dags) + 255) & ~uintptr_t(255));
+    h.sort_tmp_bytes = k1_sort_tmp_bytes(n_dags);
     return h;
 }
 

@@ -122,6 +122,21 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
             return env && env[0] == 'w' ? 2 : (env && env[0] == 'c' ? 0 : 1);
         }();
         const bool warp_back = back_kind == 2;
+        // shape-sorted walk order for the lane kernel (DS_K1_SORT=0: index order)
+        static const bool sort_walks = [] {
+            const char* env = getenv("DS_K1_SORT");
+            return !(env && env[0] == '0');
+        }();
+        K1Args b = a;
+        b.perm = nullptr;
+        if (back_kind == 1 && sort_walks && a.h.skey) {
+            size_t tb = a.h.sort_tmp_bytes;
+            if ((e = cub::DeviceRadixSort::SortPairs(a.h.sort_tmp, tb, a.h.skey, a.h.skey2, a.h.sperm, a.h.sperm2,
+                                                     int(a.n_dags), 0, 26, s)) != cudaSuccess)
+                return e;
+            if ((e = mark("k1_sort")) != cudaSuccess) return e;
+            b.perm = a.h.sperm2;
+        }
         if (back_kind == 0) {
             const u64 need = (a.n_dags + 32 * kCoopWarps - 1) / (32 * kCoopWarps);
             k1_back_coop<><<<int(need < u64(occ.grid_back_coop) ? need : u64(occ.grid_back_coop)), 32 * kCoopWarps, 0,
@@ -133,8 +148,8 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         } else {
             const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
             const int g = int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane));
-            if (a.plat.M <= 255) k1_back_lane<false, 8><<<g, 32 * kLaneWarps, 0, s>>>(a);
-            else k1_back_lane<false, 16><<<g, 32 * kLaneWarps, 0, s>>>(a);
+            if (a.plat.M <= 255) k1_back_lane<false, 8><<<g, 32 * kLaneWarps, 0, s>>>(b);
+            else k1_back_lane<false, 16><<<g, 32 * kLaneWarps, 0, s>>>(b);
             if ((e = mark("k1_back_lane")) != cudaSuccess) return e;
         }
     }
