@@ -1081,6 +1081,11 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     return int(r & 0xff);
 }
 
+#ifndef DS_SORT_WINDOW
+#define DS_SORT_WINDOW 4096
+#endif
+constexpr u64 kSortWindow = DS_SORT_WINDOW;  // DAGs per walk-order sort window (0: global)
+
 // Three-kernel split of the 32-bit W=1 bounds pass. As one kernel it is
 // instruction-fetch bound (its hot code exceeds the SM's 32 KB L1.5
 // instruction cache; ncu: ~60% of stall samples "no_instructions"), so it runs
@@ -1351,7 +1356,10 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
         if (lane == 0) {
             a.h.ndiv[d] = uint16_t(ndiv);
             a.status[d] = kStPending;
-            if (a.h.skey) a.h.skey[d] = shape;
+            // within windows of kSortWindow consecutive DAGs (the window
+            // index in the high bits), so a warp's walks stay near each other
+            // in the hand-off and share L2 lines
+            if (a.h.skey) a.h.skey[d] = kSortWindow ? (u32(d / kSortWindow) << 20) | (shape >> 6) : shape;
         }
         __syncwarp();
     }

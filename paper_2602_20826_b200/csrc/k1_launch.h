@@ -29,7 +29,7 @@ constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 
 inline size_t k1_sort_tmp_bytes(u64 n_dags) {
     size_t b = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr),
-                                    static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr), int(n_dags), 0, 26);
+                                    static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr), int(n_dags), 0, 32);
     return (b + 255) & ~size_t(255);
 }
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {

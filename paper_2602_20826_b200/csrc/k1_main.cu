@@ -132,7 +132,7 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         if (back_kind == 1 && sort_walks && a.h.skey) {
             size_t tb = a.h.sort_tmp_bytes;
             if ((e = cub::DeviceRadixSort::SortPairs(a.h.sort_tmp, tb, a.h.skey, a.h.skey2, a.h.sperm, a.h.sperm2,
-                                                     int(a.n_dags), 0, 26, s)) != cudaSuccess)
+                                                     int(a.n_dags), 0, 32, s)) != cudaSuccess)
                 return e;
             if ((e = mark("k1_sort")) != cudaSuccess) return e;
             b.perm = a.h.sperm2;
