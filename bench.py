@@ -187,7 +187,7 @@ def kernel_alg_bytes(name, n, N, E, integer, n_div):
 def host_chunks(n: int) -> int:
     """How many chunks analyze_host (capi.cu) streams an n-DAG host batch in."""
     k = int(os.environ.get("DS_CHUNKS", "0") or 0)
-    weights = [1] * (k if 1 <= k <= 64 else 8)
+    weights = [1] * (k if 1 <= k <= 64 else 3)
     wsum, bounds, acc = sum(weights), [0], 0
     for w in weights:
         acc += w

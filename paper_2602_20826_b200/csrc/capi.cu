@@ -162,7 +162,7 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 14;  // smallest chunk worth a launch sequence
-constexpr u64 kDefaultChunks = 8;
+constexpr u64 kDefaultChunks = 3;  // one per stream slot (1M C5 DAGs e2e: 3 chunks 101 M/s, 6: 99, 8: 95, 4: 93)
 
 template <class Batch>
 int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
@@ -178,9 +178,8 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     }
     const u64 n = b->n_dags;
     // a few equal chunks: enough to hide the copies behind the analysis, few
-    // enough that the per-launch tail (uneven per-DAG cost) is paid rarely
-    // (1M C5 DAGs: 8 chunks 10.65 ms end to end; 12 chunks 11.06; smaller
-    // first/last chunks 11.0). DS_CHUNKS=k overrides (tuning knob).
+    // enough that every launch sequence fills the GPU (smaller first/last
+    // chunks measured slower too). DS_CHUNKS=k overrides (tuning knob).
     static const std::vector<u64> weights = [] {
         const char* e = getenv("DS_CHUNKS");
         const long v = e ? atol(e) : 0;
