@@ -1466,9 +1466,11 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
     RatT<u32> proposed{0, 1};
     u64 done = 0;
     int gidx = 0;
+    u64 G_next = ndiv > 0 ? __ldg(divg) : 0;  // one group ahead: off the dependent-load chain
 #pragma unroll 1
     for (int g = 0; g < ndiv; ++g) {
-        const u64 G = __ldg(divg + g);
+        const u64 G = G_next;
+        if (g + 1 < ndiv) G_next = __ldg(divg + g + 1);
         const u64 org = G & ~done;
         if (!org) continue;  // fully absorbed by earlier launches
         RatT<u32> R{0, 1};
