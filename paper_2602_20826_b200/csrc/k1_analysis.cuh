@@ -1594,11 +1594,19 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
         u64 whole = 0;
         if (avail && spare0 >= 1) {
             u64 rm = 0;
+            // two candidates per step: their loads are independent
 #pragma unroll 1
-            for (u64 b = avail; b; b &= b - 1) {
-                const int c = __ffsll(b) - 1;
-                const u64 p = __ldg(&nodes[c].pred);
-                if (!(p & pool) && !(p & ~done)) rm |= 1ull << (__ldg(ro + c) & 0xff);
+            for (u64 b = avail; b;) {
+                const int c0 = __ffsll(b) - 1;
+                b &= b - 1;
+                const int c1 = b ? __ffsll(b) - 1 : -1;
+                b &= b - 1;
+                const u64 p0 = __ldg(&nodes[c0].pred);
+                const u64 p1 = c1 >= 0 ? __ldg(&nodes[c1].pred) : ~0ull;
+                const uint16_t r0 = __ldg(ro + c0);
+                const uint16_t r1 = c1 >= 0 ? __ldg(ro + c1) : 0;
+                if (!(p0 & pool) && !(p0 & ~done)) rm |= 1ull << (r0 & 0xff);
+                if (c1 >= 0 && !(p1 & pool) && !(p1 & ~done)) rm |= 1ull << (r1 & 0xff);
             }
             int spare = spare0;
 #pragma unroll 1
