@@ -15,9 +15,9 @@ it); H2D of the packed DAGs and D2H of statuses/bounds are inside the timed
 region every step.
 
 --impl reference: the reference's own CPU implementation of the path —
-evaluate_corpus (experiment.cpp:52-79) + lower_bound from the reference
-sources compiled in oracle/_ref (or the restated oracle when that library is
-absent) — on all host cores, on a bounded sample of the same workload.
+generate_corpus + evaluate_corpus (experiment.cpp:52-79) + lower_bound from
+the reference sources compiled in oracle/_ref — on all host cores, on a
+bounded sample of the same workload; the product library is never loaded.
 """
 from __future__ import annotations
 
@@ -167,21 +167,12 @@ def ncu_summary():
     return {}
 
 
-def kernel_alg_bytes(name, n, N, E, integer, n_div):
-    """Algorithmic bytes one launch of K1 kernel `name` must move: its inputs
-    read once and its outputs written once. N nodes, E edges,
-    n DAGs, n_div division groups in the batch."""
-    loads = N * (8 if integer else 16)
-    offs = 8 * (n + 1)
-    handoff_masks, handoff_loads = 24 * N, 8 * N
-    if name == "k1_front":   # packed DAGs in; bounds 2..9 + status + the hand-off out
-        return offs + loads + 4 * E + 68 * n + handoff_masks + handoff_loads
-    if name == "k1_mid":     # status + pred/anc + loads in; ranks, division groups, status out
-        return 4 * n + 4 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 2 * n + 4 * n
-    if name in ("k1_back", "k1_back_lane"):  # status + hand-off in; proposed bound, status, groups out
-        # (per node: pred, anc|desc, load, rank/order of its K1Node record)
-        return 4 * n + 4 * n + 2 * n + 16 * N + handoff_loads + 2 * N + 8 * n_div + 16 * n + 4 * n + 2 * n
-    return offs + loads + 4 * E + 86 * n  # single-kernel pass: DAGs in, results out
+def pass_alg_bytes(n, N):
+    """SURVEY.md §8(d) algorithmic bytes of one analysis pass: per DAG a 16 B
+    header + per node (8 B int64 load numerator + 8 B u64 predecessor mask)
+    in, 5 bounds x 16 B + per node 2 B (group index, quota) + 4 B status out
+    = 100 + 18 n bytes. n DAGs, N nodes in the batch."""
+    return 100 * n + 18 * N
 
 
 def host_chunks(n: int) -> int:
@@ -198,9 +189,12 @@ def host_chunks(n: int) -> int:
 
 
 def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_dags=1_000_000, gpu=None):
-    """Time the reference CPU path on a bounded sample of the same workload;
-    with gpu = (status, bounds) of the device pass, also count how many of
-    the sampled DAGs the device got bit-exact (status and all ten num/den)."""
+    """Time the reference CPU path on a bounded sample of the same workload
+    (the corpus_bench protocol, corpus_bench.cpp:31-59: warm-up, then a
+    1-core serial pass and an OpenMP pass on every host core), at M=148 (the
+    headline config) and M=32 (corpus_bench's own platform). With gpu =
+    (status, bounds) of the device pass, also count how many of the sampled
+    DAGs the device got bit-exact (status and all ten num/den)."""
     from oracle import bindings
     from paper_2602_20826_b200 import _abi
 
@@ -218,10 +212,24 @@ def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_d
         st_g, b_g = gpu[0][:n], gpu[1][:n]
         same = (st_g == st_c) & (b_g == b_c).all(1)
         parity = {"dags": int(n), "bit_exact": int(same.sum()), "checker": "oracle/_ref" if kind == "ref" else "oracle"}
+    # corpus_bench protocol points on smaller samples (same corpus prefix)
+    ns = min(20000, batch.n_dags)
+    cs = chk.corpus(batch.slice(0, ns))
+    cs.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=False)  # warm-up (corpus_bench.cpp:43)
+    ser = cs.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=False)[2]
+    n32 = min(200000, batch.n_dags)
+    c32 = chk.corpus(batch.slice(0, n32))
+    par32 = c32.evaluate(32, 1, _abi.DS_M_ALL, parallel=True)[2]
+    ser32 = cs.evaluate(32, 1, _abi.DS_M_ALL, parallel=False)[2]
     return {"value": n / secs, "unit": UNIT, "cores": cpu_cores(), "parity_vs_gpu": parity,
             "kind": "reference" if kind == "ref" else "port",
             "sample": f"first {n} DAGs of the rank-0 shard, evaluate_corpus(parallel=true, OpenMP "
                       f"{cpu_cores()} threads) + lower_bound, {secs:.2f} s",
+            "protocol": {"M148": {"serial_1core": ns / ser, "parallel": n / secs, "speedup": (n / secs) / (ns / ser)},
+                         "M32": {"serial_1core": ns / ser32, "parallel": n32 / par32,
+                                 "speedup": (n32 / par32) / (ns / ser32)},
+                         "samples": {"serial": ns, "parallel_M148": n, "parallel_M32": n32},
+                         "unit": UNIT, "ref": "corpus_bench.cpp:31-59 (serial and OpenMP evaluate_corpus)"},
             "source": "oracle/_ref (reference sources compiled against oracle/shim)" if kind == "ref"
                       else "oracle/src restatement"}
 
@@ -295,30 +303,50 @@ def makespan_summary(device, replays, n_c2=8, unit=1 << 17):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path.
+
+    Runs ONLY oracle/_ref (the reference's proj/src/*.cpp compiled against
+    oracle/shim; oracle/Makefile): the corpus comes from the reference's own
+    generate_corpus (generator.cpp:98-108, GenConfig{} defaults, seed 1 — the
+    first DAGs of this arm's rank-0 shard, bit-identical), and every step
+    times evaluate_corpus(parallel=true) (experiment.cpp:52-79, OpenMP on all
+    host cores) + lower_bound over it. The product library is never loaded
+    on this arm. `config` equals the device arm's; each step is a bounded
+    sample of that workload (the first --ref-sample DAGs), declared in
+    cpu_baseline.sample."""
     rank, _, world = env_rank()
     if rank != 0:
         return 0
     from oracle import bindings
-    from paper_2602_20826_b200 import _abi, _lib
 
-    kind = "ref" if bindings.available("ref") else "oracle"
-    chk = bindings.Checker(kind)
-    corpus = _lib.Corpus(args.ref_sample, seed=1)
-    c = chk.corpus(corpus.batch())
+    if not bindings.available("ref"):
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "oracle/_ref/libdagsched_ref.so not built (make -C oracle ref)"}), flush=True)
+        return 0
+    M_ALL = 0x1F  # proposed, greedy, greedy_unaware, graham_para + lower (include/dagsched_b200.h)
+    chk = bindings.Checker("ref")
+    n = args.ref_sample
+    t0 = time.perf_counter()
+    c = chk.generate(n, seed=1)  # the reference's generate_corpus(GenConfig{}, 1, n)
+    gen_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        c.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=True)
-    secs = [c.evaluate(SM_COUNT, 1, _abi.DS_M_ALL, parallel=True)[2] for _ in range(args.steps)]
+        c.evaluate(SM_COUNT, 1, M_ALL, parallel=True)
+    secs = [c.evaluate(SM_COUNT, 1, M_ALL, parallel=True)[2] for _ in range(args.steps)]
     tot = sum(secs)
-    value = args.ref_sample * args.steps / tot
+    value = n * args.steps / tot
+    maps = open("/proc/self/maps").read()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64 (exact rationals)", "data": "synthetic",
-            "impl": "reference", "config": dict(workload(N_PER_GPU, 1), sample=args.ref_sample),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(),
-                             "kind": "reference" if kind == "ref" else "port",
-                             "sample": f"{args.ref_sample} DAGs of the C5 corpus per step (seed 1), "
-                                       f"evaluate_corpus(parallel) + lower_bound on {cpu_cores()} threads"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64 (exact rationals)",
+            "data": "synthetic (reference generator)", "impl": "reference",
+            "config": dict(workload(N_PER_GPU, 1), parallelism=f"shards{world}", integer_loads=True),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "reference",
+                             "sample": f"first {n} DAGs of the C5 corpus (reference generate_corpus, seed 1) per "
+                                       f"step: evaluate_corpus(parallel=true, OpenMP {cpu_cores()} threads) + "
+                                       f"lower_bound, M=148, t_min=1; generation {gen_s:.1f} s excluded",
+                             "source": "oracle/_ref (reference proj/src compiled against oracle/shim)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "product_library_mapped": "libdagsched_b200" in maps,
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
     return 0
@@ -332,7 +360,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-dags", type=int, default=N_PER_GPU)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--ref-sample", type=int, default=100000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-makespan", action="store_true")
     ap.add_argument("--wide", action="store_true", help="e2e through ds_analyze_batch (64-bit loads, 32-bit edges)")
@@ -434,25 +462,27 @@ def main():
     chunks = host_chunks(n)
 
     # ---------------------------------------------------------------- roofline
-    # dominant kernel of the step, timed live with CUDA events on its stream
+    # algorithmic bytes of the pass = 100 + 18 n per DAG; the
+    # dominant kernel of the step is timed live with CUDA events on its stream
     peak, peak_kind = measured_peak()
     kmean = {k: statistics.mean(v) for k, v in per_kernel.items()}
     dom = max(kmean, key=kmean.get)
     N = int(batch.node_off[-1] - batch.node_off[0])
-    E = int(batch.edge_off[-1] - batch.edge_off[0])
-    ncu = ncu_summary()
-    n_div = int(round(ncu.get("division_groups_per_dag", 0) * n))
-    alg_bytes = kernel_alg_bytes(dom, n, N, E, integer, n_div)
+    alg_bytes = pass_alg_bytes(n, N)
     achieved = alg_bytes / (kmean[dom] / 1e3) / 1e9
-    kn = ncu.get("kernels", {}).get(dom, {})
-    traffic = kn["dram_bytes_per_dag"] * n if kn.get("dram_bytes_per_dag") else None
+    step_ms = statistics.mean(kms)
+    ncu = ncu_summary()
+    kn = ncu.get("kernels", {})
+    traffic_step = (sum(k["dram_bytes_per_dag"] for k in kn.values() if k.get("dram_bytes_per_dag")) * n
+                    if kn else None)
+    traffic_dom = kn.get(dom, {}).get("dram_bytes_per_dag")
     issue = None
-    if kn.get("warp_instructions_per_dag") and ncu.get("sm_clock_mhz"):
+    if kn.get(dom, {}).get("warp_instructions_per_dag") and ncu.get("sm_clock_mhz"):
         peak_ips = 4 * ncu["sm_count"] * ncu["sm_clock_mhz"] * 1e6  # 4 schedulers x 1 warp-instr / clk
-        ips = kn["warp_instructions_per_dag"] * n / (kmean[dom] / 1e3)
+        ips = kn[dom]["warp_instructions_per_dag"] * n / (kmean[dom] / 1e3)
         issue = {"achieved": ips, "peak": peak_ips, "unit": "warp-instr/s", "frac": ips / peak_ips,
-                 "source": "instruction count per DAG from the ncu capture in profiles/, time live"}
-    pass_bytes = batch.nbytes(with_den=not integer) + d2h  # the device pass: packed DAGs in, results out
+                 "threads_per_warp_instr": {k: v.get("threads_per_warp_instr") for k, v in kn.items()},
+                 "source": "instruction counts per DAG from the ncu capture in profiles/, time live"}
     makespan = None
     if rank == 0 and not args.no_makespan:
         try:
@@ -479,14 +509,19 @@ def main():
                             else "ds_analyze_batch (host pinned)"),
                     "matches_device_leg": same},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic_step, "peak_source": peak_kind,
                          "kernel": dom, "kernel_ms": kmean[dom],
                          "algorithmic_bytes_per_launch": alg_bytes,
+                         "algorithmic_bytes_rule": "SURVEY 8(d): 100 + 18 n B per DAG (n nodes) for the pass, "
+                                                   "over the dominant kernel's time",
+                         "traffic_scope": "whole step (ncu dram read+write, all K1 kernels, profiles/k1_ncu_summary.json)",
+                         "traffic_dominant_kernel": traffic_dom * n if traffic_dom else None,
+                         "traffic_over_algorithmic": traffic_step / alg_bytes if traffic_step else None,
                          "issue": issue,
-                         "pass": {"kernels_ms": kmean, "algorithmic_bytes": pass_bytes,
-                                  "achieved_gbs": pass_bytes / (statistics.mean(kms) / 1e3) / 1e9},
-                         "note": "integer issue/latency-bound exact-rational greedy per DAG (front/mid: one "
-                                 "warp per DAG; back: one lane per DAG); HBM is not the limiter"},
+                         "pass": {"kernels_ms": kmean, "step_ms": step_ms, "algorithmic_bytes": alg_bytes,
+                                  "achieved_gbs": alg_bytes / (step_ms / 1e3) / 1e9,
+                                  "frac": alg_bytes / (step_ms / 1e3) / 1e9 / peak},
+                         "note": "integer issue/latency-bound exact-rational greedy per DAG; HBM is not the limiter"},
             "cpu_baseline": cpu,
             "makespan": makespan,
             "clocks": clk.summary(),

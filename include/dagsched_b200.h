@@ -68,10 +68,20 @@ extern "C" {
                               * current CUDA device (K5), copy into the host arrays  */
 
 /* --------------------------------------------------------------- inputs */
-/* Platform (exec_model.hpp:11-19): M identical SMs and the time floor t_min. */
+/* Platform (exec_model.hpp:11-19): M identical SMs and the time floor t_min,
+ * plus how the device applies DagTask::make's load floor (dag.cpp:35-41) to a
+ * packed batch. `flags` = 0: min_load = t_min (generate() makes its tasks
+ * that way, generator.cpp:94-95); DS_PF_MIN_LOAD_ONE: min_load = 1 (the
+ * default argument of DagTask::make, dag.hpp:38-41); DS_PF_PREMADE: the tasks
+ * were already made on the host (the kept C++ API), only load > 0 is checked.
+ * Independently of the floor, a load below t_min fails only the proposed
+ * method, with DS_E_LOAD_TMIN (schedule()'s own check, scheduler.cpp:177-182);
+ * the other bounds are computed as the reference computes them. */
+#define DS_PF_MIN_LOAD_ONE 1
+#define DS_PF_PREMADE 2
 typedef struct ds_platform {
     int32_t sm_count;
-    int32_t reserved;
+    int32_t flags;
     int64_t tmin_num;
     int64_t tmin_den;
 } ds_platform;

@@ -84,6 +84,19 @@ class Checker:
         h = self._f["corpus_from_packed"](C.byref(cb), m.numerator, m.denominator, st.ctypes.data)
         return Corpus(self, h, batch.n_dags, st)
 
+    def corpus_with_ids(self, batch: DagBatch, node_ids, min_load=1) -> "Corpus":
+        """corpus() with the tasks' real node ids (flat, ascending per DAG):
+        the reference's write_scheme then names entities by id (ref only)."""
+        m = Fraction(min_load)
+        st = np.zeros(batch.n_dags, np.int32)
+        ids = np.ascontiguousarray(node_ids, np.int64)
+        cb = batch.as_c(with_den=True)
+        f = self.lib.ref_corpus_from_packed_ids
+        f.restype = C.c_void_p
+        f.argtypes = [C.POINTER(_abi.ds_dag_batch), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        h = f(C.byref(cb), m.numerator, m.denominator, ids.ctypes.data, st.ctypes.data)
+        return Corpus(self, h, batch.n_dags, st)
+
     def generate(self, count: int, **cfg) -> "Corpus":
         g = gen_config(**cfg)
         h = self._f["corpus_generate"](C.byref(g), int(count))

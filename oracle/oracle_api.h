@@ -48,6 +48,11 @@ extern "C" {
 ORACLE_DECLARE(ref_)
 ORACLE_DECLARE(orc_)
 
+/* corpus_from_packed with the tasks' real node ids ([N], ascending per DAG);
+ * write_scheme then prints ids instead of ranks. ref_ only. */
+void* ref_corpus_from_packed_ids(const ds_dag_batch* batch, int64_t min_load_num, int64_t min_load_den,
+                                 const int64_t* node_ids, int32_t* status);
+
 /* The reference's run_validation (experiment.cpp:163-240) on
  * generate_corpus(cfg, corpus_size); ref_ only. out = {tasks, runs,
  * violations} and dbl = {mean_tightness_worst, mean_tightness_scaled}. */

@@ -14,6 +14,7 @@
 
 #include "oracle_api.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -118,6 +119,40 @@ void* ref_corpus_from_packed(const ds_dag_batch* b, int64_t min_num, int64_t min
         }
         for (uint32_t e = b->edge_off[d]; e < b->edge_off[d + 1]; ++e) {
             edges.emplace_back(b->edges[e - b->edge_off[0]] >> 16, b->edges[e - b->edge_off[0]] & 0xffffu);
+        }
+        int st = guarded([&] {
+            c->tasks.push_back(DagTask::make(std::move(nodes), std::move(edges),
+                                             std::nullopt, rat(min_num, min_den)));
+            c->index.push_back(d);
+        });
+        if (status) status[d] = st;
+    }
+    return c.release();
+}
+
+// The same with the tasks' real node ids (node_ids[i - node_off[0]] for node
+// i of the batch, ascending within a DAG; a local index >= n, the packer's
+// "unknown endpoint", maps to an id above every node's) so write_scheme
+// prints ids, as the reference does for a task read from JSON.
+void* ref_corpus_from_packed_ids(const ds_dag_batch* b, int64_t min_num, int64_t min_den,
+                                 const int64_t* node_ids, int32_t* status) {
+    auto c = std::make_unique<Corpus>();
+    c->n_dags = b->n_dags;
+    c->tasks.reserve(b->n_dags);
+    for (std::uint64_t d = 0; d < b->n_dags; ++d) {
+        std::vector<DagNode> nodes;
+        std::vector<std::pair<NodeId, NodeId>> edges;
+        const uint32_t n0 = b->node_off[d] - b->node_off[0], n = b->node_off[d + 1] - b->node_off[d];
+        NodeId top = 0;
+        for (uint32_t k = 0; k < n; ++k) top = std::max<NodeId>(top, NodeId(node_ids[n0 + k]));
+        auto id_of = [&](uint32_t k) { return k < n ? NodeId(node_ids[n0 + k]) : NodeId(top + 1 + (k - n)); };
+        for (uint32_t k = 0; k < n; ++k) {
+            int64_t den = b->load_den ? b->load_den[n0 + k] : 1;
+            nodes.push_back(DagNode{id_of(k), rat(b->load_num[n0 + k], den)});
+        }
+        for (uint32_t e = b->edge_off[d]; e < b->edge_off[d + 1]; ++e) {
+            const uint32_t w = b->edges[e - b->edge_off[0]];
+            edges.emplace_back(id_of(w >> 16), id_of(w & 0xffffu));
         }
         int st = guarded([&] {
             c->tasks.push_back(DagTask::make(std::move(nodes), std::move(edges),

@@ -24,6 +24,8 @@ DS_E_CYCLE = 16
 DS_E_SOURCES = 17
 DS_E_SINKS = 18
 DS_E_LOAD_TMIN = 19
+DS_PF_MIN_LOAD_ONE = 1  # ds_platform.flags: DagTask::make floor = 1 (else t_min)
+DS_PF_PREMADE = 2       # tasks made on the host: only load > 0 is checked
 
 DS_MAX_NODES = 256
 
@@ -46,7 +48,7 @@ STATUS_NAMES = {
 
 
 class ds_platform(C.Structure):
-    _fields_ = [("sm_count", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("sm_count", C.c_int32), ("flags", C.c_int32),
                 ("tmin_num", C.c_int64), ("tmin_den", C.c_int64)]
 
 

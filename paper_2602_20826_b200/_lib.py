@@ -83,10 +83,14 @@ def device_count() -> int:
     return n.value if rc == _abi.DS_OK else 0
 
 
-def platform(sm_count: int, t_min=1) -> _abi.ds_platform:
+def platform(sm_count: int, t_min=1, min_load=None) -> _abi.ds_platform:
+    """ds_platform for M = sm_count SMs and t_min. min_load is DagTask::make's
+    load floor on the device: None -> t_min (generate()'s tasks), 1 -> 1
+    (make's default argument), "premade" -> tasks already validated."""
     from fractions import Fraction
     t = Fraction(t_min)
-    return _abi.ds_platform(int(sm_count), 0, t.numerator, t.denominator)
+    flags = {None: 0, 1: _abi.DS_PF_MIN_LOAD_ONE, "premade": _abi.DS_PF_PREMADE}[min_load]
+    return _abi.ds_platform(int(sm_count), flags, t.numerator, t.denominator)
 
 
 def gen_config(depth_min=5, depth_max=8, max_width=8, avg_load=20, load_jitter=0.5,
@@ -117,29 +121,31 @@ def _finish(batch: DagBatch, st, b, ng):
     return status, b, ng
 
 
-def analyze(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
-    """Batched bound analysis on one GPU -> (status[n], bounds[n, 10], n_groups[n])."""
+def analyze(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0, min_load=None):
+    """Batched bound analysis on one GPU -> (status[n], bounds[n, 10], n_groups[n]).
+    min_load: DagTask::make's load floor on the device (see platform())."""
     st, b, ng, r = _results(batch.n_dags)
     cb = batch.as_c()
-    pl = platform(sm_count, t_min)
+    pl = platform(sm_count, t_min, min_load)
     check(lib().ds_analyze_batch(C.byref(cb), C.byref(pl), mask, C.byref(r), device, None, 0))
     return _finish(batch, st, b, ng)
 
 
-def analyze16(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0):
+def analyze16(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0,
+              min_load=None):
     """analyze() over the compact 16-bit wire form (ds_analyze_batch16)."""
     st, b, ng, r = _results(batch.n_dags)
     load16, edges16 = batch.compact16()
     cb = batch.as_c16(load16, edges16)
-    pl = platform(sm_count, t_min)
+    pl = platform(sm_count, t_min, min_load)
     check(lib().ds_analyze_batch16(C.byref(cb), C.byref(pl), mask, C.byref(r), device))
     return _finish(batch, st, b, ng)
 
 
-def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = _abi.DS_M_ALL):
+def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = _abi.DS_M_ALL, min_load=None):
     st, b, ng, r = _results(batch.n_dags)
     cb = batch.as_c()
-    pl = platform(sm_count, t_min)
+    pl = platform(sm_count, t_min, min_load)
     devs = (C.c_int * len(devices))(*devices)
     check(lib().ds_analyze_batch_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
     return _finish(batch, st, b, ng)

@@ -40,11 +40,11 @@ class DagBatch:
 
     @property
     def n_nodes(self) -> int:
-        return int(self.node_off[-1])
+        return int(self.node_off[-1]) - int(self.node_off[0])  # indices are relative to node_off[0]
 
     @property
     def n_edges(self) -> int:
-        return int(self.edge_off[-1])
+        return int(self.edge_off[-1]) - int(self.edge_off[0])
 
     def sizes(self) -> np.ndarray:
         return np.diff(self.node_off.astype(np.int64))

@@ -27,7 +27,7 @@ Packed pack(const std::vector<const DagTask*>& tasks) {
 
 ds_platform platform_of(const Platform& p) {
     p.check();
-    return ds_platform{p.sm_count, 0, to_int64(numerator(p.t_min)), to_int64(denominator(p.t_min))};
+    return ds_platform{p.sm_count, DS_PF_PREMADE, to_int64(numerator(p.t_min)), to_int64(denominator(p.t_min))};
 }
 
 void raise(int st, const std::string& what) {
@@ -36,7 +36,7 @@ void raise(int st, const std::string& what) {
         case DS_EINVAL: throw std::invalid_argument(what);
         case DS_EOVERFLOW: throw std::overflow_error(what);
         case DS_EINVARIANT: throw std::logic_error(what);
-        case DS_E_LOAD:
+        case DS_E_LOAD: throw ValidationError(what + ": load below minimum");
         case DS_E_LOAD_TMIN: throw ValidationError(what + ": load below the platform time unit");
         default:
             if (st >= DS_E_EMPTY && st <= DS_E_LOAD_TMIN) throw ValidationError(what);

@@ -56,7 +56,9 @@ BalancedGroupList build_groups(const DagTask& task, const Platform& platform) {
     std::vector<int16_t> blk(n), div(n);
     ds_scheme_out out{&st, &ne, &ng, &nd, blk.data(), div.data(), nullptr, nullptr, nullptr};
     detail::check(ds_schedule_batch(&b, &pl, &out, 0));
-    detail::raise(st, "build_groups");
+    // build_groups has no t_min check of its own (division.cpp:67-126): the
+    // device still fills the division when only schedule() would refuse
+    if (st != DS_E_LOAD_TMIN) detail::raise(st, "build_groups");
     BalancedGroupList g;
     g.groups.assign(nd, {});
     for (std::size_t i = 0; i < n; ++i) g.groups[div[i]].push_back(task.nodes()[i].id);

@@ -10,6 +10,8 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <map>
+#include <stdexcept>
 
 namespace dagsched {
 
@@ -79,6 +81,36 @@ Rational rat(int64_t n, int64_t d) { return Rational(BigInt(n), BigInt(d)); }
 
 EntityId eid(const DagTask& t, const ds_entity_rec& r) {
     return EntityId{t.nodes()[r.origin].id, r.generation, EntityId::Part(r.part)};
+}
+
+// The reference's closing self-checks (scheduler.cpp:389-424): the augmented
+// graph is acyclic (Kahn over the entity preds) and no group holds more than
+// M SMs; either failure is a scheduler bug -> std::logic_error, as there.
+void verify(const ScheduleScheme& s, int M) {
+    std::map<EntityId, std::size_t> idx;
+    for (std::size_t i = 0; i < s.entities.size(); ++i) idx[s.entities[i].id] = i;
+    std::vector<std::size_t> indeg(s.entities.size(), 0), queue;
+    std::vector<std::vector<std::size_t>> succ(s.entities.size());
+    for (std::size_t i = 0; i < s.entities.size(); ++i) {
+        for (const EntityId& p : s.entities[i].preds) {
+            auto it = idx.find(p);
+            if (it == idx.end()) throw std::logic_error("entity predecessor is not an entity");
+            succ[it->second].push_back(i);
+            ++indeg[i];
+        }
+    }
+    for (std::size_t i = 0; i < indeg.size(); ++i)
+        if (indeg[i] == 0) queue.push_back(i);
+    for (std::size_t h = 0; h < queue.size(); ++h)
+        for (std::size_t v : succ[queue[h]])
+            if (--indeg[v] == 0) queue.push_back(v);
+    if (queue.size() != s.entities.size()) throw std::logic_error("augmented dependency graph has a cycle");
+    for (const GroupPlan& g : s.groups) {
+        long long total = 0;
+        for (const MemberPlan& mp : g.members) total += mp.parallelism;
+        for (const LaunchRecord& l : g.launches) total += l.parallelism;
+        if (total > M) throw std::logic_error("group allocation exceeds the device");
+    }
 }
 
 ScheduleScheme materialise(const DagTask& t, const Platform& plat, const ds_entity_rec* er, int ne,
@@ -153,6 +185,7 @@ ScheduleScheme materialise(const DagTask& t, const Platform& plat, const ds_enti
         return a.id < b.id;
     });
     s.extra_deps.assign(extra.begin(), extra.end());
+    verify(s, plat.sm_count);
     return s;
 }
 

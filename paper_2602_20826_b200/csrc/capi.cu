@@ -59,8 +59,10 @@ int check_platform(const ds_platform* p, PlatT<u64>& out) {
         a = b;
         b = t;
     }
+    if (p->flags & ~(DS_PF_MIN_LOAD_ONE | DS_PF_PREMADE)) return fail(DS_EINVAL, "unknown platform flags");
     out.M = p->sm_count;
     out.tmin = RatT<u64>{u64(n) / a, u64(d) / a};
+    out.minl = (p->flags & DS_PF_PREMADE) ? 2 : ((p->flags & DS_PF_MIN_LOAD_ONE) ? 1 : 0);
     return DS_OK;
 }
 

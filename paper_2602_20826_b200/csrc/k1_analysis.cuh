@@ -222,12 +222,13 @@ struct DetailOut {
 };
 
 // --------------------------------------------------------------- phase: loads
-// dag.cpp:35-41 (load >= min_load; min_load = t_min on this path).
-// Returns status | (integer_loads << 8).
+// dag.cpp:35-41: load >= min_load (P.minl: t_min, 1, or only > 0). A load
+// below t_min is also flagged: it fails schedule() (scheduler.cpp:177-182),
+// not the other bounds. Returns status | (integer_loads << 8) | (low_t << 9).
 template <int W, class T>
 K1_PHASE int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* __restrict__ lnum,
                                    const u64* __restrict__ lden, const PlatT<T> P) {
-    bool bad_load = false, bad_arg = false, frac = false, ovf = false;
+    bool bad_load = false, bad_arg = false, frac = false, ovf = false, low_t = false;
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         long long a = (long long)lnum[v];
@@ -245,7 +246,13 @@ K1_PHASE int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* 
         } else if (a > 0 && b > 0) {
             l = n_reduce<T>(T(u64(a)), T(u64(b)));
         }
-        if (a <= 0 || (!too_wide && n_cmp(l, P.tmin) < 0)) bad_load = true;
+        if (a <= 0) {
+            bad_load = true;
+        } else if (!too_wide) {
+            const bool lt = n_cmp(l, P.tmin) < 0;
+            low_t |= lt;
+            bad_load |= P.minl == 0 ? lt : (P.minl == 1 && l.n < l.d);  // canonical: l < 1 iff n < d
+        }
         frac |= l.d != 1;
         S.ln[v] = l.n;
         S.ld[v] = l.d;
@@ -268,7 +275,7 @@ K1_PHASE int p_load(WarpState<W, T>& S, const int lane, const int n, const u64* 
     if (__any_sync(FULL, bad_arg)) return DS_EINVAL;
     if (__any_sync(FULL, bad_load)) return DS_E_LOAD;
     if (__any_sync(FULL, ovf)) return DS_EOVERFLOW;
-    return DS_OK | ((!__any_sync(FULL, frac)) << 8);
+    return DS_OK | ((!__any_sync(FULL, frac)) << 8) | (__any_sync(FULL, low_t) << 9);
 }
 
 // --------------------------------------------------------------- phase: edges
@@ -1058,6 +1065,7 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     int st = p_load<W, T>(S, lane, n, lnum, lden, P);
     if ((st & 0xff) != DS_OK) return st & 0xff;
     const bool integer = (st >> 8) & 1;
+    const bool low_t = (st >> 9) & 1;
     __syncwarp();
     if ((st = p_edges<W, T>(S, lane, n, edges, n_edges)) != DS_OK) return st;
     const bool lower = mask & DS_M_LOWER;
@@ -1066,6 +1074,11 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     if (closure == -2) return DS_EOVERFLOW;
     const int rounds = closure;  // hop count | kFlatPath, decoded by p_bounds
     if ((st = p_ends<W, T>(S, lane, n)) != DS_OK) return st;
+    // DagTask::make succeeded; method_bound(proposed) comes first in
+    // evaluate_corpus's order and schedule() throws on a load below t_min
+    // (detail mode still forms the division first: build_groups has no such
+    // check, division.cpp:67-126)
+    if (low_t && (mask & DS_M_PROPOSED) && !DETAIL) return DS_E_LOAD_TMIN;
     if constexpr (W == 1) p_desc_transpose<T>(S, lane, n);
     else p_closure<W, T, false>(S, lane, n, false, P);
     if (mask & (DS_M_GREEDY | DS_M_GREEDY_UNAWARE | DS_M_GRAHAM_PARA | DS_M_LOWER)) {
@@ -1075,6 +1088,7 @@ __device__ __forceinline__ int analyse_dag(WarpState<W, T>& S, const int lane, c
     const int n_joins = p_rank<W, T>(S, lane, n, integer);
     if (n_joins < 0) return DS_EOVERFLOW;
     n_div = p_division<W, T, DETAIL>(S, lane, n, n_joins, P.M, det);
+    if (DETAIL && low_t) return DS_E_LOAD_TMIN;
     const long long r = p_schedule<W, T, DETAIL>(S, lane, n, n_div, P, det);
     n_groups = int((r >> 8) & 0xfff);
     n_ent = int(r >> 20);
@@ -1207,7 +1221,7 @@ __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];  // offsets are relative to element 0
     // a t_min that needs more than 32 bits sends every DAG to the wider tiers
     const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
     // W=1 takes DAGs dynamically (one atomic per DAG) so the per-DAG cost
     // spread does not leave a tail of idle SMs; W=4 only picks out the rare
     // big DAGs, statically.
@@ -1241,7 +1255,7 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
     const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
     const bool proposed = a.mask & DS_M_PROPOSED;
 #pragma unroll 1
     for (;;) {
@@ -1301,7 +1315,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
     const int lane = threadIdx.x & 31;
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
     const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
@@ -1372,7 +1386,7 @@ __global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
     const int lane = threadIdx.x & 31;
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
     const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
@@ -1656,7 +1670,7 @@ template <bool UNUSED = false, int QB = 8>
 __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_lane(const K1Args a) {
     const int lane = threadIdx.x & 31;
     const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
@@ -1961,7 +1975,7 @@ __global__ void __launch_bounds__(32 * kCoopWarps) k1_back_coop(const K1Args a) 
     u32* on = s_on[threadIdx.x];
     u32* od = s_od[threadIdx.x];
     const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}};
+    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
     const unsigned lt = (1u << lane) - 1;
     CoopLane c;
     c.st = DS_OK;
@@ -2057,7 +2071,7 @@ __global__ void __launch_bounds__(32) k1_analyse_retry(const K1Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     WarpState<4, T>& S = *reinterpret_cast<WarpState<4, T>*>(smem_raw);
-    const PlatT<T> P{a.plat.M, RatT<T>{T(a.plat.tmin.n), T(a.plat.tmin.d)}};
+    const PlatT<T> P{a.plat.M, RatT<T>{T(a.plat.tmin.n), T(a.plat.tmin.d)}, a.plat.minl};
     const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
     constexpr bool wide = sizeof(T) == 16;
     const u32* list = wide ? a.retry2 : a.retry;

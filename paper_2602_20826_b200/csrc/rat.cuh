@@ -262,6 +262,7 @@ template <class T>
 struct PlatT {
     int M;
     RatT<T> tmin;
+    int minl;  // DagTask::make's load floor: 0 t_min, 1 one, 2 positive only (ds_platform.flags)
 };
 
 // exec_model.cpp:16-23: max(1, floor(load / t_min)), saturating at INT_MAX.

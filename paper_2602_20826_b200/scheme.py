@@ -73,6 +73,7 @@ class Scheme:
     node_div_group: list
     n_div_groups: int
     bounds: dict
+    node_ids: list | None = None  # original node id of each local index (None: ids = indices)
 
     def entity(self, eid: EntityId) -> Entity:
         for e in self.entities:
@@ -89,8 +90,12 @@ def _fs(q: Fraction) -> str:  # format_exact (rational.cpp:87-91)
     return str(q.numerator) if q.denominator == 1 else f"{q.numerator}/{q.denominator}"
 
 
-def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0):
-    """Run ds_schedule_batch -> list of Scheme (None where status != OK), status."""
+def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0, min_load=None):
+    """Run ds_schedule_batch -> list of Scheme (None where status != OK), status.
+
+    Entities are kept in local-index space (origin = rank of the node id, what
+    the executor indexes by); ``Scheme.node_ids`` maps them back to the task's
+    ids for ``to_reference_json``. min_load: see ``_lib.platform``."""
     n, N = batch.n_dags, batch.n_nodes
     st = np.zeros(n, np.int32)
     ne = np.zeros(n, np.uint16)
@@ -105,7 +110,7 @@ def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0):
                              nb.ctypes.data, ndg.ctypes.data, C.addressof(ents), C.addressof(grps),
                              bnd.ctypes.data)
     cb = batch.as_c()
-    pl = platform(sm_count, t_min)
+    pl = platform(sm_count, t_min, min_load)
     check(lib().ds_schedule_batch(C.byref(cb), C.byref(pl), C.byref(out), device))
     status = combine_status(batch.pack_status, st)
     tmin = Fraction(t_min)
@@ -114,8 +119,9 @@ def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0):
         if status[d] != _abi.DS_OK:
             schemes.append(None)
             continue
-        n0, n1 = int(batch.node_off[d]), int(batch.node_off[d + 1])
-        e0, e1 = int(batch.edge_off[d]), int(batch.edge_off[d + 1])
+        # device outputs are indexed relative to node_off[0] (header contract)
+        n0, n1 = int(batch.node_off[d] - batch.node_off[0]), int(batch.node_off[d + 1] - batch.node_off[0])
+        e0, e1 = int(batch.edge_off[d] - batch.edge_off[0]), int(batch.edge_off[d + 1] - batch.edge_off[0])
         succ = [[] for _ in range(n1 - n0)]
         pred = [[] for _ in range(n1 - n0)]
         for w in batch.edges[e0:e1]:
@@ -126,6 +132,8 @@ def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0):
             sm_count, tmin, [ents[2 * n0 + i] for i in range(int(ne[d]))],
             [grps[n0 + i] for i in range(int(ng[d]))], pred, succ,
             [int(x) for x in nb[n0:n1]], [int(x) for x in ndg[n0:n1]], int(nd[d]), bnd[d]))
+        if batch.node_ids is not None:
+            schemes[-1].node_ids = list(batch.node_ids[d])
     return schemes, status
 
 
@@ -180,14 +188,45 @@ def _materialise(M, tmin, erecs, grecs, pred, succ, node_block, node_div, n_div,
         e.preds = sorted(ps)
     bounds = {name: (None if int(brow[2 * k + 1]) == 0 else _q(brow[2 * k], brow[2 * k + 1]))
               for k, name in enumerate(_abi.BOUND_NAMES)}
-    return Scheme(M, tmin, groups, segs, sorted(extra), sorted(ents, key=lambda e: e.id), node_block,
-                  node_div, n_div, bounds)
+    s = Scheme(M, tmin, groups, segs, sorted(extra), sorted(ents, key=lambda e: e.id), node_block,
+               node_div, n_div, bounds)
+    verify(s)
+    return s
+
+
+def verify(s: Scheme) -> None:
+    """The reference's closing self-checks (scheduler.cpp:389-424): the
+    augmented graph is acyclic and no group holds more than M SMs; a failure
+    is a scheduler bug (logic_error there, DS_EINVARIANT here)."""
+    from ._lib import DagschedError
+    idx = {e.id: i for i, e in enumerate(s.entities)}
+    indeg = [0] * len(s.entities)
+    succ = [[] for _ in s.entities]
+    for i, e in enumerate(s.entities):
+        for p in e.preds:
+            if p not in idx:
+                raise DagschedError(_abi.DS_EINVARIANT, f"entity predecessor {p} is not an entity")
+            succ[idx[p]].append(i)
+            indeg[i] += 1
+    queue = [i for i, d in enumerate(indeg) if d == 0]
+    for u in queue:
+        for v in succ[u]:
+            indeg[v] -= 1
+            if indeg[v] == 0:
+                queue.append(v)
+    if len(queue) != len(s.entities):
+        raise DagschedError(_abi.DS_EINVARIANT, "augmented dependency graph has a cycle")
+    for g in s.groups:
+        if sum(m.parallelism for m in g.members) + sum(l.parallelism for l in g.launches) > s.sm_count:
+            raise DagschedError(_abi.DS_EINVARIANT, "group allocation exceeds the device")
 
 
 def to_reference_json(s: Scheme) -> dict:
-    """The reference's write_scheme() structure (task_io.cpp:94-148)."""
+    """The reference's write_scheme() structure (task_io.cpp:94-148), entities
+    named by node id (to_string, scheduler.cpp:9-17)."""
     def ent(e):
-        return str(e)
+        o = s.node_ids[e.origin] if s.node_ids is not None else e.origin
+        return str(EntityId(o, e.generation, e.part))
     return {
         "platform": {"sm_count": s.sm_count, "t_min": _fs(s.t_min)},
         "groups": [{

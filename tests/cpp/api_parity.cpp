@@ -57,9 +57,9 @@ std::string scheme_json(const ScheduleScheme& s) {
     return o.str();
 }
 
-DagTask fig2() {  // paper Fig. 2 with ids 0..6 (the golden fixtures' local ids)
-    return DagTask::make({{0, 1}, {1, 4}, {2, 3}, {3, 3}, {4, 2}, {5, 2}, {6, 1}},
-                         {{0, 1}, {0, 2}, {0, 3}, {2, 4}, {3, 4}, {3, 5}, {1, 6}, {4, 6}, {5, 6}});
+DagTask fig2() {  // paper Fig. 2, make_example_task (test_fixtures.hpp:12-21): ids 1..7
+    return DagTask::make({{1, 1}, {2, 4}, {3, 3}, {4, 3}, {5, 2}, {6, 2}, {7, 1}},
+                         {{1, 2}, {1, 3}, {1, 4}, {3, 5}, {4, 5}, {4, 6}, {2, 7}, {5, 7}, {6, 7}});
 }
 DagTask fan() {
     std::vector<DagNode> nodes{{0, 1}};

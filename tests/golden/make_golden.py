@@ -91,20 +91,35 @@ def fixtures():
     F.append(("load_below_min", ([(3, "1/2")], []), 4, 1))
     F.append(("unknown_endpoint", ([(0, 1)], [(0, 9)]), 4, 1))
     F.append(("duplicate_edges", ([(0, 1), (1, 2), (2, 1)], [(0, 1), (0, 1), (1, 2), (0, 2)]), 4, 1))
+    # tasks made with DagTask::make's default floor (min_load = 1) on a
+    # platform whose t_min is above some load: only schedule() refuses them
+    # (scheduler.cpp:177-182); the other bounds exist (analysis.cpp:40-81)
+    F.append(("load_below_tmin", ([(10, 1), (11, 5), (12, 2), (13, 3)], [(10, 11), (10, 12), (11, 13), (12, 13)]),
+              8, 2, 1))
+    F.append(("load_below_tmin_frac", ([(0, "3/2"), (1, 7), (2, 1)], [(0, 1), (1, 2)]), 4, "5/2", 1))
     return F
 
 
 def main():
     ref = Checker("ref")
     cases = []
-    for name, (nodes, edges), M, tmin in fixtures():
+    for name, (nodes, edges), M, tmin, *minl in fixtures():
         b = raw_pack([(nodes, edges)])
-        c = ref.corpus(b, min_load=Fraction(tmin))
-        st, bounds, _ = c.evaluate(M, Fraction(tmin))
+        ids = sorted(int(i) for i, _ in nodes)
+        min_load = Fraction(minl[0]) if minl else Fraction(tmin)
+        # the tasks carry their real node ids, so write_scheme names entities by id
+        c = ref.corpus_with_ids(b, ids, min_load=min_load)
+        # serial: an exception inside the reference's OpenMP loop would terminate
+        st, bounds, _ = c.evaluate(M, Fraction(tmin), parallel=False)
         case = {"name": name, "nodes": [[int(i), str(Fraction(l))] for i, l in nodes],
                 "edges": [[int(u), int(v)] for u, v in edges], "sm_count": M,
                 "t_min": str(Fraction(tmin)), "status": int(st[0]),
                 "bounds": [int(x) for x in bounds[0]]}
+        if minl:
+            case["min_load"] = str(min_load)
+            st2, b2, _ = c.evaluate(M, Fraction(tmin), mask=0x1E, parallel=False)  # every method but proposed
+            case["status_no_proposed"] = int(st2[0])
+            case["bounds_no_proposed"] = [int(x) for x in b2[0]]
         if st[0] == 0:
             case["analyze"] = c.analyze(0, M, Fraction(tmin))
             case["scheme"] = c.scheme(0, M, Fraction(tmin))
@@ -166,6 +181,13 @@ def main():
                      "csv": ref_run_experiment(sweep, values, M, n, **cfg)})
     with open(os.path.join(OUT, "experiments.json"), "w") as f:
         json.dump(exps, f, indent=1)
+    # build_blocks / local_paths / build_groups / scale_parallelism /
+    # parallel_candidates: tests/cpp/division_dump.cpp against the reference
+    import subprocess
+    dump = os.path.join(os.path.dirname(OUT), "..", "oracle", "_ref", "ref_division_dump")
+    text = subprocess.run([dump], capture_output=True, text=True, check=True).stdout
+    with gzip.open(os.path.join(OUT, "division.json.gz"), "wt", compresslevel=9) as f:
+        f.write(text)
     print("golden fixtures written to", OUT)
 
 

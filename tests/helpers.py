@@ -28,6 +28,39 @@ def fixture_raw_batch(case):
                        [l.denominator for _, l in nodes], words)
 
 
+def rename_scheme(j, mapping):
+    """write_scheme JSON with every entity's origin mapped through `mapping`
+    (e.g. node id -> local index, to compare with a checker that names
+    entities by index)."""
+    def name(s):
+        o, sep, rest = s.partition(":")
+        return str(mapping[int(o)]) + sep + rest
+    j = json.loads(json.dumps(j))
+    for g in j["groups"]:
+        g["bottleneck"] = name(g["bottleneck"])
+        for m in g["members"] + g["launches"]:
+            m["entity"] = name(m["entity"])
+    for s in j["segmentations"]:
+        for k in ("source", "parallel", "residual"):
+            s[k] = name(s[k])
+    j["extra_deps"] = [[name(a), name(b)] for a, b in j["extra_deps"]]
+    for e in j["entities"]:
+        e["id"] = name(e["id"])
+        e["preds"] = [name(p) for p in e["preds"]]
+    return j
+
+
+def id_to_rank(case):
+    ids = sorted(int(i) for i, _ in case["nodes"])
+    return {i: k for k, i in enumerate(ids)}
+
+
+def min_load_arg(case):
+    """The device's DagTask::make floor for a fixture: its min_load when the
+    golden was made with one other than t_min (None = t_min)."""
+    return 1 if case.get("min_load") == "1" else None
+
+
 def fixture_batch(case):
     """Pack a fixture through the product packer (id-level validation included)."""
     return pack([([(int(i), Fraction(l)) for i, l in case["nodes"]], [tuple(e) for e in case["edges"]])])

@@ -135,3 +135,29 @@ def test_compact16_entry_validates_arguments(lib):
     if _lib.device_count() == 0:
         with pytest.raises(_lib.DagschedError):
             _lib.analyze16(b, 8)
+
+
+def test_scheme_self_checks_reject_cycles_and_oversubscription():
+    """scheduler.cpp:389-424: an augmented-graph cycle or a group holding more
+    than M SMs is a scheduler bug -> DS_EINVARIANT (logic_error there)."""
+    from fractions import Fraction as F
+
+    from paper_2602_20826_b200 import scheme as S
+
+    def ent(o, m=1):
+        return S.Entity(S.EntityId(o), F(1), m, F(1), 0, False)
+
+    a, b = ent(0), ent(1)
+    g = S.Group(0, [a, b], [], 0, F(1), a.id, 0)
+    ok = S.Scheme(2, F(1), [g], [], [], [a, b], [0, 0], [0, 0], 1, {})
+    b.preds = [a.id]
+    S.verify(ok)  # a -> b, 2 SMs on M = 2
+    a.preds = [b.id]
+    with pytest.raises(_lib.DagschedError) as e:
+        S.verify(ok)
+    assert e.value.code == _abi.DS_EINVARIANT and "cycle" in str(e.value)
+    a.preds = []
+    over = S.Scheme(1, F(1), [g], [], [], [a, b], [0, 0], [0, 0], 1, {})
+    with pytest.raises(_lib.DagschedError) as e:
+        S.verify(over)
+    assert "exceeds the device" in str(e.value)

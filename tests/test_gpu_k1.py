@@ -25,9 +25,14 @@ def orc():
 def test_fixtures_bounds_and_status():
     for case in helpers.fixtures():
         b = helpers.fixture_batch(case)
-        st, bounds, _ = _lib.analyze(b, case["sm_count"], case["t_min"])
+        ml = helpers.min_load_arg(case)
+        st, bounds, _ = _lib.analyze(b, case["sm_count"], case["t_min"], min_load=ml)
         assert int(st[0]) == case["status"], case["name"]
         assert [int(x) for x in bounds[0]] == case["bounds"], case["name"]
+        if "status_no_proposed" in case:  # load < t_min fails only schedule() (scheduler.cpp:177-182)
+            st, bounds, _ = _lib.analyze(b, case["sm_count"], case["t_min"], mask=0x1E, min_load=ml)
+            assert int(st[0]) == case["status_no_proposed"], case["name"]
+            assert [int(x) for x in bounds[0]] == case["bounds_no_proposed"], case["name"]
 
 
 def test_fixture_schemes_match_reference_write_scheme():

@@ -22,14 +22,19 @@ def orc():
 def test_fixture_bounds_status_schemes(orc):
     for case in helpers.fixtures():
         b = helpers.fixture_raw_batch(case)
-        c = orc.corpus(b, min_load=case["t_min"])
-        st, bounds, _ = c.evaluate(case["sm_count"], case["t_min"])
+        c = orc.corpus(b, min_load=case.get("min_load", case["t_min"]))
+        st, bounds, _ = c.evaluate(case["sm_count"], case["t_min"], parallel=False)
         assert int(st[0]) == case["status"], case["name"]
         assert [int(x) for x in bounds[0]] == case["bounds"], case["name"]
+        if "status_no_proposed" in case:
+            st, bounds, _ = c.evaluate(case["sm_count"], case["t_min"], mask=0x1E, parallel=False)
+            assert int(st[0]) == case["status_no_proposed"], case["name"]
+            assert [int(x) for x in bounds[0]] == case["bounds_no_proposed"], case["name"]
         if case["status"] == 0:
             assert c.analyze(0, case["sm_count"], case["t_min"]) == case["analyze"], case["name"]
+            # the restatement names entities by local index; the golden by node id
             assert helpers.normalise_scheme(c.scheme(0, case["sm_count"], case["t_min"])) == \
-                helpers.normalise_scheme(case["scheme"]), case["name"]
+                helpers.normalise_scheme(helpers.rename_scheme(case["scheme"], helpers.id_to_rank(case))), case["name"]
 
 
 def test_appendix_a_goldens(orc):
@@ -38,8 +43,8 @@ def test_appendix_a_goldens(orc):
     a1 = by[("fig2", 6)]["analyze"]
     assert (a1["proposed"], a1["greedy"], a1["graham_para"], a1["lower"]) == ("5", "7", "6", "4")
     a2 = by[("fig2", 8)]["scheme"]
-    # entity names use local indices: node id 2 of Fig. 2 is index 1
-    assert [s["parallel"] for s in a2["segmentations"]] == ["1:p1"]
+    # entities are named by node id (Fig. 2's ids are 1..7): node 2 is split
+    assert [s["parallel"] for s in a2["segmentations"]] == ["2:p1"]
     assert by[("fig2", 148)]["analyze"]["proposed"] == "4"
     a4 = by[("c1_fan_8_20_1", 148)]["analyze"]
     assert (a4["proposed"], a4["graham_para"], a4["lower"]) == ("28/9", "603/148", "3")

@@ -32,7 +32,7 @@ def main():
                  "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9, "MHz": 1e6, "GHz": 1e9, "Mhz": 1e6, "Ghz": 1e9}.get(u, 1)
         return x * scale
 
-    out = {"round": 1, "version": a.version, "command": a.command, "dags": a.dags,
+    out = {"round": 2, "version": a.version, "command": a.command, "dags": a.dags,
            "division_groups_per_dag": a.div_groups_per_dag, "kernels": {}}
     for r in rows[2:]:
         name = re.sub(r"^void ", "", r[col["Kernel Name"]])
@@ -49,6 +49,10 @@ def main():
              "warps_active_per_sm": val(r, "sm__warps_active.avg.per_cycle_active"),
              "registers_per_thread": val(r, "launch__registers_per_thread"),
              "top_stalls_pct": top}
+        for k in ("smsp__thread_inst_executed.sum", "smsp__thread_inst_executed_pred_on.sum"):
+            if k in col and d["warp_instructions"]:
+                d["threads_per_warp_instr" if k.endswith("executed.sum") else "pred_on_threads_per_warp_instr"] = \
+                    val(r, k) / d["warp_instructions"]
         d["dram_bytes_per_dag"] = (d["dram_bytes_read"] + d["dram_bytes_write"]) / a.dags
         d["warp_instructions_per_dag"] = d["warp_instructions"] / a.dags
         out["kernels"][name] = d
