@@ -56,7 +56,8 @@ def test_fuzz_schemes_vs_reference(M):
     dags = fuzz_dags.corpus(11, 150, max_n=80)
     b = pack(dags)
     schemes, st = scheme.schedule_batch(b, M)
-    ref = bindings.Checker("ref").corpus(helpers_raw(b))
+    # the tasks keep their (sparse, shuffled) node ids on both sides
+    ref = bindings.Checker("ref").corpus_with_ids(helpers_raw(b), np.concatenate([np.asarray(i) for i in b.node_ids]))
     for d in range(len(dags)):
         if st[d] != 0:
             continue
