@@ -234,72 +234,128 @@ def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_d
                       else "oracle/src restatement"}
 
 
-def makespan_summary(device, replays, n_c2=8, unit=1 << 17):
-    """First half of the BASELINE metric, small: measured DAG makespan vs the
-    analysed bound on this B200 (C1 fork-join + the first n_c2 C2 DAGs, M=148),
-    next to serial-stream and naive multi-stream launch. The full C1-C4 study
-    (1000 replays, 100 C2 DAGs, green-context partitions) is bench_executor.py
-    -> profiles/r01_executor.json."""
+MAKESPAN_MAIN = ("dynamic_prio", "multistream_host", "multistream")
+MAKESPAN_OTHER = ("proposed", "proposed_deps", "dynamic_deps", "serial")
+
+
+def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_other=20, unit=1 << 17):
+    """First half of the BASELINE metric: measured DAG makespan vs the analysed
+    bound on this B200 (M = 148), configs C1 (fork-join), C2 (the first n_c2
+    generated DAGs with 20-50 nodes), C3 (Inception-style) and C4 (three
+    oversized-kernel DAGs), next to serial-stream and naive multi-stream launch.
+
+    Variants (all on the same K2 TMA node kernel, same SMs):
+      dynamic_prio     the schedule on the dynamic engine, precedence edges +
+                       group-priority claiming (DS_PLAN_PRIORITY) — the product
+      proposed         the schedule as a CUDA graph with group barriers
+                       (simulate_scheme semantics, the Theorem-1 setting)
+      proposed_deps    the schedule's augmented graph (Ē) as a CUDA graph
+      dynamic_deps     the augmented graph on the dynamic engine
+      serial           one stream, topological order, m = min(m^max, M)
+      multistream      original edges, m = min(m^max, M), captured as a graph
+      multistream_host the same launched by the host per node on its own
+                       stream with events: naive multi-stream launch
+    Every replay of a proposed variant is compared with its bound in µs
+    (bound units x tau + group latencies, executor.bound_us) — raw counts,
+    nothing excluded. Replays >= 1 ms above their DAG's median are also
+    counted (`stall_like`) but stay in every statistic."""
     from paper_2602_20826_b200 import _lib, executor as X, scheme, workloads
     from paper_2602_20826_b200.batch import pack
 
-    wl = X.WL_MIX32_TMA  # every variant runs the same node kernel
+    wl = X.WL_MIX32_TMA
+    t_start = time.perf_counter()
     cal = X.calibrate(unit, device=device, workload=wl)
+    wall = {"calibrate": time.perf_counter() - t_start, "setup": 0.0, "replays": 0.0}
     M = cal["sm_count"]
-    corpus = _lib.Corpus(200, seed=1)
-    b = corpus.batch()
-    sizes = np.diff(b.node_off.astype(np.int64))
-    dags = [workloads.c1_fork_join()]
-    names = ["c1"]
-    for d in [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:n_c2]:
-        n0, n1, e0, e1 = (int(b.node_off[d]), int(b.node_off[d + 1]), int(b.edge_off[d]), int(b.edge_off[d + 1]))
-        dags.append(([int(x) for x in b.load_num[n0:n1]],
-                     [(int(w) >> 16, int(w) & 0xFFFF) for w in b.edges[e0:e1]]))
-        names.append(f"c2_seed{1 + d}")
-    norm = []
-    for nodes, edges in dags:
+
+    def norm(nodes, edges):
         if isinstance(nodes[0], tuple):
             idx = {i: k for k, (i, _) in enumerate(sorted(nodes))}
-            norm.append(([l for _, l in sorted(nodes)], [(idx[u], idx[v]) for u, v in edges]))
-        else:
-            norm.append((nodes, edges))
-    schemes, st = scheme.schedule_batch(pack(norm), M, device=device)
-    ratio, over, launches = {"proposed": [], "proposed_dynamic": []}, {"proposed": 0, "proposed_dynamic": 0}, 0
-    # proposed: CUDA graph, group barriers (simulate_scheme semantics, the
-    # Theorem-1 setting); proposed_dynamic: the same schedule's augmented graph
-    # on the dynamic persistent engine (device ready queue, quota-capped)
-    # multistream: the Greedy baseline captured as a CUDA graph; multistream_host:
-    # naive multi-stream launch (host launches per node on its own stream, events)
-    p50 = {"proposed": [], "proposed_dynamic": [], "serial": [], "multistream": [], "multistream_host": []}
-    for (loads, edges), sch in zip(norm, schemes):
+            return [l for _, l in sorted(nodes)], [(idx[u], idx[v]) for u, v in edges]
+        return list(nodes), list(edges)
+
+    dags = [("C1", "c1", norm(*workloads.c1_fork_join())), ("C3", "c3", norm(*workloads.inception_dag()))]
+    dags += [("C4", f"c4_{s}", norm(*workloads.oversized_dag(s, M))) for s in range(3)]
+    b = _lib.Corpus(400, seed=1).batch()
+    sizes = np.diff(b.node_off.astype(np.int64))
+    for d in [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:n_c2]:
+        n0, n1, e0, e1 = (int(b.node_off[d]), int(b.node_off[d + 1]), int(b.edge_off[d]), int(b.edge_off[d + 1]))
+        dags.append(("C2", f"c2_seed{1 + d}", ([int(x) for x in b.load_num[n0:n1]],
+                                                [(int(w) >> 16, int(w) & 0xFFFF) for w in b.edges[e0:e1]])))
+    schemes, st = scheme.schedule_batch(pack([d for _, _, d in dags]), M, device=device)
+
+    def plan_of(kind, sch, loads, edges):
+        if kind == "dynamic_prio":
+            return X.plan_from_scheme(sch, loads, unit, mode=X.PLAN_PRIORITY), X.ENGINE_DYNAMIC
+        if kind in ("proposed", "proposed_deps", "dynamic_deps"):
+            mode = X.PLAN_BARRIERS if kind == "proposed" else X.PLAN_DEPS
+            return (X.plan_from_scheme(sch, loads, unit, mode=mode),
+                    X.ENGINE_DYNAMIC if kind.startswith("dynamic") else X.ENGINE_GRAPH)
+        engine = X.ENGINE_STREAMS if kind == "multistream_host" else X.ENGINE_GRAPH
+        return X.plan_baseline(kind.replace("_host", ""), loads, edges, M, unit), engine
+
+    proposed_kinds = ("dynamic_prio", "proposed", "proposed_deps", "dynamic_deps")
+    per = {}  # (config, kind) -> list of per-DAG arrays
+    ratios, over, stall_like, launches = {}, {}, {}, 0
+    p50 = {}
+    contracts = {"checked_replays": 0, "precedence_violations": 0, "sm_overlap_violations": 0}
+    c2_seen = 0
+    for (cfg, name, (loads, edges)), sch in zip(dags, schemes):
         bus = X.bound_us(sch, cal)
-        for kind in p50:
-            engine = (X.ENGINE_DYNAMIC if kind == "proposed_dynamic" else
-                      X.ENGINE_STREAMS if kind == "multistream_host" else X.ENGINE_GRAPH)
-            plan = (X.plan_from_scheme(sch, loads, unit, barrier_groups=kind == "proposed")
-                    if kind.startswith("proposed") else
-                    X.plan_baseline(kind.replace("_host", ""), loads, edges, M, unit))
+        c2_seen += cfg == "C2"
+        for kind in MAKESPAN_MAIN + MAKESPAN_OTHER:
+            if kind not in MAKESPAN_MAIN and cfg == "C2" and c2_seen > n_c2_other:
+                continue  # the secondary variants run on the first n_c2_other C2 DAGs
+            plan, engine = plan_of(kind, sch, loads, edges)
+            reps = replays if kind in MAKESPAN_MAIN else replays_other
+            t0 = time.perf_counter()
             ex = X.Executor(plan, device=device, workload=wl, engine=engine)
-            r = ex.run(replays, warmup=3, stamps=False)
+            t1 = time.perf_counter()
+            r = ex.run(reps, warmup=3, stamps=False)
+            wall["setup"] += t1 - t0
+            wall["replays"] += time.perf_counter() - t1
+            if kind == "dynamic_prio" and (cfg != "C2" or name in ("c2_seed2", "c2_seed3")):
+                rs = ex.run(10, warmup=1, stamps=True)  # trace contracts on stamped replays
+                for k in range(10):
+                    contracts["precedence_violations"] += len(X.check_precedence(plan, rs, k))
+                    contracts["sm_overlap_violations"] += X.check_sm_exclusive(plan, rs, k)
+                    contracts["checked_replays"] += 1
             ex.close()
-            p50[kind].append(float(np.median(r.makespan_us)))
-            if kind in ratio:
-                ratio[kind].extend((r.makespan_us / bus).tolist())
-                over[kind] += int((r.makespan_us > bus).sum())
-            launches += (1 if engine == X.ENGINE_DYNAMIC else len(plan.entities) + 1) * replays
-    out = {"dags": names, "replays_per_dag": replays, "sm_count": M, "node_kernel": "k2_mix_tma (all variants)",
-           "tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
-           "measured_over_bound": {}, "replays_over_bound": over,
-           "mean_p50_us": {k: float(np.mean(v)) for k, v in p50.items()},
-           "dynamic_beats_multistream_p50": int(sum(a < b for a, b in zip(p50["proposed_dynamic"], p50["multistream"]))),
-           "dynamic_beats_multistream_host_p50": int(sum(a < b for a, b in zip(p50["proposed_dynamic"],
-                                                                               p50["multistream_host"]))),
-           "executor_kernel_launches": launches}
-    for k, v in ratio.items():
-        v = np.asarray(v)
-        out["measured_over_bound"][k] = {"p50": float(np.percentile(v, 50)), "p99": float(np.percentile(v, 99)),
-                                         "max": float(v.max())}
-    return out
+            mk = r.makespan_us
+            per.setdefault((cfg, kind), []).append(mk)
+            p50.setdefault(kind, {})[name] = float(np.median(mk))
+            stall_like[kind] = stall_like.get(kind, 0) + int((mk > np.median(mk) + 1000.0).sum())
+            if kind in proposed_kinds:
+                ratios.setdefault(kind, []).append(mk / bus)
+                over[kind] = over.get(kind, 0) + int((mk > bus).sum())
+            launches += (2 if engine == X.ENGINE_DYNAMIC else len(plan.entities) + 1) * (reps + 3)
+    configs = {}
+    for (cfg, kind), arrs in per.items():
+        allr = np.concatenate(arrs)
+        c = configs.setdefault(cfg, {})
+        c[kind] = {"dags": len(arrs), "p50_us": float(np.mean([np.median(a) for a in arrs])),  # mean of per-DAG p50
+                   "p99_us": float(np.mean([np.percentile(a, 99) for a in arrs])),
+                   "max_us": float(allr.max()), "replays": int(allr.size)}
+    for cfg, c in configs.items():
+        names = [n for g, n, _ in dags if g == cfg]
+        c["dynamic_prio_beats_multistream_host_p50"] = int(sum(p50["dynamic_prio"][n] < p50["multistream_host"][n]
+                                                               for n in names))
+        c["dynamic_prio_beats_multistream_p50"] = int(sum(p50["dynamic_prio"][n] < p50["multistream"][n]
+                                                          for n in names))
+    mob = {}
+    for k, v in ratios.items():
+        v = np.concatenate(v)
+        mob[k] = {"p50": float(np.percentile(v, 50)), "p99": float(np.percentile(v, 99)), "max": float(v.max()),
+                  "replays": int(v.size)}
+    wall["total"] = time.perf_counter() - t_start
+    return {"sm_count": M, "node_kernel": "k2_mix_tma (all variants)", "unit_elems": unit,
+            "replays": {"main": replays, "other": replays_other, "main_variants": list(MAKESPAN_MAIN),
+                        "other_variants_c2_dags": n_c2_other},
+            "wall_s": wall,
+            "tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
+            "configs": configs, "measured_over_bound": mob,
+            "replays_over_bound_raw": over, "stall_like_replays": stall_like,
+            "trace_contracts_dynamic_prio": contracts, "executor_kernel_launches": launches}
 
 
 def run_reference(args):
@@ -364,7 +420,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-makespan", action="store_true")
     ap.add_argument("--wide", action="store_true", help="e2e through ds_analyze_batch (64-bit loads, 32-bit edges)")
-    ap.add_argument("--makespan-replays", type=int, default=200)
+    ap.add_argument("--makespan-replays", type=int, default=1000)
+    ap.add_argument("--makespan-c2", type=int, default=100)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -486,7 +543,7 @@ def main():
     makespan = None
     if rank == 0 and not args.no_makespan:
         try:
-            makespan = makespan_summary(local_rank, args.makespan_replays)
+            makespan = makespan_summary(local_rank, args.makespan_replays, n_c2=args.makespan_c2)
         except Exception as e:  # reported, never required for the headline line
             makespan = {"error": str(e)}
 

@@ -162,7 +162,7 @@ def main():
     peaks_p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak = json.load(open(peaks_p))["hbm_gbs"] if os.path.exists(peaks_p) else 6650.0
     roof = {}
-    for wl, name in ((X.WL_MIX32, "mix32_ldg128"), (X.WL_MIX32_BULK, "mix32_bulk_tma"), (X.WL_AXPY32, "axpy_fp32")):
+    for wl, name in ((X.WL_MIX32, "mix32_ldg128"), (X.WL_MIX32_TMA, "mix32_tma_ring"), (X.WL_AXPY32, "axpy_fp32")):
         ms, _ = X.node_kernel_bench(wl, 148, 1 << 22, reps=20)
         gbs = 148 * (1 << 22) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
         roof[name] = {"ms": ms, "GB/s": gbs, "frac_of_measured_peak": gbs / peak}

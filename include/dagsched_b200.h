@@ -186,8 +186,7 @@ typedef struct ds_scheme_out {
  * per-CTA start/end are stamped with %globaltimer and %smid. */
 #define DS_WL_MIX32 0   /* y[i] = mix(x[i]), uint32, LDG.128/STG.128: 8 B/elem   */
 #define DS_WL_AXPY32 1  /* y[i] = a*x[i] + y[i], fp32 (no FMA contraction): 12 B  */
-#define DS_WL_MIX32_BULK 2 /* DS_WL_MIX32 staged through shared memory with
-                              cp.async.bulk (TMA engine) + mbarrier: 8 B/elem   */
+/* (2: retired — an older 4 x 24 KB bulk-copy ring, superseded by 3)       */
 #define DS_WL_MIX32_TMA 3  /* DS_WL_MIX32 through a warp-specialised 6 x 32 KB
                               cp.async.bulk ring (1 producer + 16 consumer
                               warps, 544 threads per CTA): 8 B/elem            */
@@ -213,10 +212,24 @@ typedef struct ds_exec_plan {
     const ds_exec_entity* entities;
     const uint32_t* preds;       /* entity indices (graph edges pred -> entity)  */
     const uint64_t* node_elems;  /* [n_nodes] buffer length per node             */
-    int32_t barrier_groups;      /* 1: group g+1 starts after all of group g
-                                    (simulate_scheme semantics, simulator.cpp:44-94) */
+    int32_t barrier_groups;      /* DS_PLAN_*: how groups are ordered             */
     int32_t reserved;
 } ds_exec_plan;
+
+/* ds_exec_plan.barrier_groups. DEPS: only the plan's edges order entities
+ * (the augmented graph: original edges + extra dependencies Ē). BARRIERS:
+ * group g+1 starts after all of group g (simulate_scheme semantics,
+ * simulator.cpp:44-94). PRIORITY (DS_ENGINE_DYNAMIC only): the plan's edges
+ * are the precedence edges alone (original edges resolved to segment chains,
+ * no Ē) and the engine enforces the group order itself — no rank of a
+ * group-(g+1) entity is claimed while a group-g entity still has unclaimed
+ * ranks — so a group's entities always find their quota of SMs free, every
+ * group ends within its response after the previous group's last rank (the
+ * Theorem-1 induction), and SMs that finish early take the next group's
+ * ranks instead of idling behind Ē. */
+#define DS_PLAN_DEPS 0
+#define DS_PLAN_BARRIERS 1
+#define DS_PLAN_PRIORITY 2
 
 typedef struct ds_exec_cfg {
     int32_t workload;       /* DS_WL_*                                           */
@@ -233,14 +246,11 @@ typedef struct ds_exec_cfg {
                                m SMs at a time; late ranks take less)         */
 } ds_exec_cfg;
 
-/* Executor engines. GRAPH: one CUDA Graph kernel node per entity (any plan).
- * PERSISTENT: one resident CTA per SM for the whole DAG; each CTA walks its
- * list of (entity, slice) items in group order and waits on per-entity
- * completion counters instead of kernel boundaries (no launch latency).
- * Needs a group-structured plan (every entity's group >= 0, sum of
- * parallelism per group <= SMs): the proposed schedule. */
+/* Executor engines. GRAPH: one CUDA Graph kernel node per entity (plans
+ * DS_PLAN_DEPS / DS_PLAN_BARRIERS). (1 and 4 are retired engines: a static
+ * list-scheduled persistent kernel and a ring-streaming variant of DYNAMIC,
+ * both measured slower than DYNAMIC.) */
 #define DS_ENGINE_GRAPH 0
-#define DS_ENGINE_PERSISTENT 1
 /* GRAPH_FREE: the graph engine with the launch shape a developer would use
  * without quota control — 4 x parallelism CTAs of 256 threads, no shared
  * memory — so concurrent kernels share SMs and interfere (the naive
@@ -250,16 +260,10 @@ typedef struct ds_exec_cfg {
 #define DS_FREE_CTA_FACTOR 4
 /* DYNAMIC: one resident CTA per SM, work-conserving: an entity enters a
  * device-side ready queue (plan order = schedule priority) when its last
- * augmented-graph predecessor completes, and idle CTAs claim its m ranks, so
- * it never holds more than its quota of SMs. Any topologically ordered plan;
- * workloads DS_WL_MIX32 and DS_WL_MIX32_TMA. */
+ * predecessor completes, and idle CTAs claim its m ranks, so it never holds
+ * more than its quota of SMs. Any topologically ordered plan, and the only
+ * engine for DS_PLAN_PRIORITY; workloads DS_WL_MIX32 and DS_WL_MIX32_TMA. */
 #define DS_ENGINE_DYNAMIC 3
-/* STREAM: DYNAMIC's claiming with one TMA ring per SM kept streaming across
- * items — under contention the producer warp claims the next startable item
- * while the ring drains the current one, so an SM moves between entities
- * without a launch/drain bubble. Runs the DS_WL_MIX32 computation through
- * DS_WL_MIX32_TMA's ring (544 threads per CTA). */
-#define DS_ENGINE_STREAM 4
 /* STREAMS: no graph — every replay the host launches each entity's kernel on
  * its own stream after cudaStreamWaitEvent on its predecessors' events (and,
  * with group barriers, on the previous group's): naive multi-stream launch as

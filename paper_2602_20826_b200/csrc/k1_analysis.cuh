@@ -1130,12 +1130,13 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     uint16_t* ro;    // rank[v] | order[v] << 8 (k1_mid)
     uint16_t* ndiv;  // per DAG
     // walk order for k1_back_lane: k1_mid keys every DAG by its shape (group
-    // count, which division groups have several members), a radix sort
-    // orders the DAG indices, and the lanes of a warp then walk DAGs that take
-    // the same branches (skey/sperm in, skey2/sperm2 out)
-    u32 *skey, *sperm, *skey2, *sperm2;
-    void* sort_tmp;
-    size_t sort_tmp_bytes;
+    // count, which division groups have several members), k1_wsort orders
+    // the DAG indices by it within windows of kSortWindow DAGs, and the lanes
+    // of a warp then walk DAGs that take the same branches
+    u32* skey;       // per DAG: walk-order key (k1_fast / k1_mid)
+    u32* perm;       // walk order out of k1_wsort
+    u32* fb;         // DAGs k1_fast left to the general kernels (count: retry_count[7])
+    u32* l64;        // DAGs with 32 < n <= 64 for k1_fast<64> (count: retry_count[8])
 };
 
 struct K1Args {
@@ -1157,6 +1158,7 @@ struct K1Args {
     u32* retry2_count;
     K1Handoff h;           // split mode when h.node != nullptr (bounds mode only)
     const u32* perm;       // k1_back_lane's DAG order (nullptr: index order)
+    int fb_only;           // k1_front / k1_mid take only the DAGs k1_fast queued (h.fb)
 };
 
 template <int W, class T, bool DETAIL>
@@ -1257,12 +1259,18 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
     const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;
     const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
     const bool proposed = a.mask & DS_M_PROPOSED;
+    const u32 n_fb = a.fb_only ? a.retry_count[7] : 0u;  // written by k1_fast
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
         if (lane == 0) t = atomicAdd(a.retry_count + 2, 1u);
-        const u64 d = __shfl_sync(FULL, t, 0);
+        t = __shfl_sync(FULL, t, 0);
+        if (a.fb_only && t >= n_fb) break;
+        const u64 d = a.fb_only ? a.h.fb[t] : t;
         if (d >= a.n_dags) break;
+        if (!a.fb_only && a.h.skey && lane == 0) {
+            a.h.skey[d] = 0xffffffffu;  // not walked by k1_back_lane unless k1_mid keys it
+        }
         const u32 n0 = a.node_off[d] - nbase, e0 = a.edge_off[d] - ebase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
         if (n > 64 && n <= DS_MAX_NODES) continue;  // k1_analyse<4>
@@ -1316,16 +1324,15 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
     WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
     const u32 nbase = a.node_off[0];
     const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
+    const u32 n_fb = a.fb_only ? a.retry_count[7] : 0u;
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
         if (lane == 0) t = atomicAdd(a.retry_count + 3, 1u);
-        const u64 d = __shfl_sync(FULL, t, 0);
+        t = __shfl_sync(FULL, t, 0);
+        if (a.fb_only && t >= n_fb) break;
+        const u64 d = a.fb_only ? a.h.fb[t] : t;
         if (d >= a.n_dags) break;
-        if (a.h.skey && lane == 0) {
-            a.h.skey[d] = 0xffffffffu;  // not walked by k1_back_lane: sorts last
-            a.h.sperm[d] = u32(d);
-        }
         if (a.status[d] != kStMid) continue;
         const u32 n0 = a.node_off[d] - nbase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
@@ -1374,65 +1381,6 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
             // index in the high bits), so a warp's walks stay near each other
             // in the hand-off and share L2 lines
             if (a.h.skey) a.h.skey[d] = kSortWindow ? (u32(d / kSortWindow) << 20) | (shape >> 6) : shape;
-        }
-        __syncwarp();
-    }
-}
-
-// k1_back: p_schedule over the state k1_front left behind.
-template <bool UNUSED = false>
-__global__ void __launch_bounds__(128, 9) k1_back(const K1Args a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    WarpState<1, u32>& S = reinterpret_cast<WarpState<1, u32>*>(smem_raw)[threadIdx.x >> 5];
-    const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
-#pragma unroll 1
-    for (;;) {
-        u32 t = 0;
-        if (lane == 0) t = atomicAdd(a.retry_count + 4, 1u);
-        const u64 d = __shfl_sync(FULL, t, 0);
-        if (d >= a.n_dags) break;
-        if (a.status[d] != kStPending) continue;
-        const u32 n0 = a.node_off[d] - nbase;
-        const int n = int(a.node_off[d + 1] - nbase - n0);
-        const int ndiv = a.h.ndiv[d];
-#pragma unroll 1
-        for (int v = lane; v < n; v += 32) {
-            const u32 i = n0 + v;
-            const K1Node& nd = a.h.node[i];
-            S.pred[v][0] = nd.pred;
-            S.anc[v][0] = nd.ad;  // p_schedule only uses anc | desc
-            S.desc[v][0] = 0;
-            S.pn[v] = nd.ln;
-            S.pd[v] = nd.ld;
-            const uint16_t ro = a.h.ro[i];
-            S.rank[v] = short(ro & 0xff);
-            S.order[v] = short(ro >> 8);
-            S.gen[v] = 0;
-            S.ppart[v] = 0;
-            if (v < ndiv) S.divg[v][0] = a.h.divg[i];
-        }
-        __syncwarp();
-        const long long r = p_schedule<1, u32, false>(S, lane, n, ndiv, P, DetailOut{});
-        const int st = int(r & 0xff);
-        if (st == DS_EOVERFLOW) {
-            if (lane == 0) {
-                a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
-                a.status[d] = kStRetried;
-            }
-            __syncwarp();
-            continue;
-        }
-        int64_t* b = a.bounds + 10 * d;
-        if (st == DS_OK) {
-            if (lane < 2) b[lane] = (long long)(lane ? S.bd[DS_BOUND_PROPOSED] : S.bn[DS_BOUND_PROPOSED]);
-        } else if (lane < 10) {
-            b[lane] = 0;
-        }
-        if (lane == 0) {
-            a.status[d] = st;
-            if (a.n_groups) a.n_groups[d] = (unsigned short)((r >> 8) & 0xfff);
         }
         __syncwarp();
     }
@@ -1700,367 +1648,6 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
         }
         a.status[d] = st;
         if (a.n_groups) a.n_groups[d] = (unsigned short)(st == DS_OK ? ng : 0);
-    }
-}
-
-// k1_back_coop (DS_K1_BACK=coop; measured slower, 4.25 vs 3.06 ms per 1M C5
-// DAGs — the rendezvous makes lanes wait for each other's singleton stretches
-// and 80 registers halve residency): the one-lane-per-DAG walk with the
-// warp's help where the walk is rare and heavy. ncu on k1_back_lane: 44% of its warp instructions ran
-// with < 2 active threads — the apportion of multi-member groups (30% of the
-// groups, quota divisions and the shed/fill loop) executed by one lane while
-// the other 31 wait. Here a lane walks its DAG's singleton groups alone and
-// stops at a multi-member group; at that rendezvous the warp apportions every
-// pending group one after the other with one member per lane (warp sums,
-// butterfly arg-best under pick_better's order, first-strict-max response)
-// and hands (response, SMs used, concurrent set) back to its lane, which
-// finishes the group's candidates and launches alone. Lanes whose DAG is done
-// take the next DAG of the warp's batch at the same rendezvous (a batch of 32
-// is claimed with one atomic), so no lane idles until the batch's slowest
-// DAG ends. Residual-load overrides live in shared memory so any lane can
-// read the requester's. Same rationals and tie rules as p_schedule
-// (scheduler.cpp:35-95, 214-359); overflow and > 32 pending members send the
-// DAG to the retry tiers.
-constexpr int kCoopWarps = 4;
-
-struct CoopLane {
-    const K1Node* nodes;
-    const uint16_t* ro;
-    const u64* divg;
-    u64 d;           // DAG index
-    u64 V, done;
-    u64 G, org;      // group waiting for the warp's apportion
-    u64 conc;        // its result: union of the members' concurrent sets
-    RatT<u32> proposed, R;
-    int g, nd, gidx, n_over, st, used;
-    bool ovf;
-};
-
-__device__ __forceinline__ RatT<u32> coop_load(const CoopLane& c, const int* ov, const u32* on, const u32* od,
-                                               int v) {
-    for (int k = c.n_over - 1; k >= 0; --k) {
-        if (ov[k] == v) return RatT<u32>{on[k], od[k]};
-    }
-    return RatT<u32>{__ldg(&c.nodes[v].ln), __ldg(&c.nodes[v].ld)};
-}
-
-// candidates and launches of the group (scheduler.cpp:253-346), then commit
-__device__ __forceinline__ void coop_finish_group(CoopLane& c, int* ov, u32* on, u32* od, const u64 G, const u64 org,
-                                                  const RatT<u32> R, const int used, const u64 conc,
-                                                  const PlatT<u32>& P) {
-    const int spare0 = P.M - used;
-    const u64 pool = c.V & conc & ~G;
-    const u64 avail = pool & ~c.done;
-    u64 whole = 0;
-    if (avail && spare0 >= 1) {
-        u64 rm = 0;
-#pragma unroll 1
-        for (u64 b = avail; b; b &= b - 1) {
-            const int v = __ffsll(b) - 1;
-            const u64 p = __ldg(&c.nodes[v].pred);
-            if (!(p & pool) && !(p & ~c.done)) rm |= 1ull << (__ldg(c.ro + v) & 0xff);
-        }
-        int spare = spare0;
-#pragma unroll 1
-        for (; rm && spare >= 1; rm &= rm - 1) {
-            const int v = __ldg(c.ro + (__ffsll(rm) - 1)) >> 8;
-            const RatT<u32> l = coop_load(c, ov, on, od, v);
-            int mp = q_max_par(l, P);
-            if (mp < 0) {
-                c.ovf = true;
-                mp = 1;
-            }
-            const int mc = min(mp, spare);
-            const RatT<u32> dur = q_exec(l, mc, P);
-            c.ovf |= dur.d == 0;
-            spare -= mc;
-            if (q_cmp(dur, R) <= 0) {
-                whole |= 1ull << v;
-            } else {  // split: the residual replaces the origin
-                const RatT<u32> pl = n_mul_int(R, u32(mc));
-                const RatT<u32> rl = n_sub(l, pl);
-                c.ovf |= pl.d == 0 || rl.d == 0;
-                if (c.n_over == kLaneSplits) {
-                    c.st = kLaneRetry;
-                    return;
-                }
-                ov[c.n_over] = v;
-                on[c.n_over] = rl.n;
-                od[c.n_over] = rl.d;
-                ++c.n_over;
-                break;
-            }
-        }
-    }
-    c.done |= org | whole;
-    c.proposed = q_add(c.proposed, R);
-    c.ovf |= c.proposed.d == 0;
-    ++c.gidx;
-}
-
-// walk singleton groups alone; true = stopped at a multi-member group
-__device__ __forceinline__ bool coop_advance(CoopLane& c, int* ov, u32* on, u32* od, const PlatT<u32>& P) {
-#pragma unroll 1
-    while (c.g < c.nd && c.st == DS_OK) {
-        const u64 G = __ldg(c.divg + c.g);
-        const u64 org = G & ~c.done;
-        if (!org) {  // fully absorbed by earlier launches
-            ++c.g;
-            continue;
-        }
-        if (org & (org - 1)) {
-            c.G = G;
-            c.org = org;
-            return true;
-        }
-        const int v = __ffsll(org) - 1;  // one pending member: m = min(m^max, M)
-        const RatT<u32> l = coop_load(c, ov, on, od, v);
-        int cp = q_max_par(l, P);
-        if (cp < 0) {
-            c.ovf = true;
-            cp = 1;
-        }
-        cp = min(cp, P.M);
-        const RatT<u32> R = q_exec(l, cp, P);
-        c.ovf |= R.d == 0;
-        coop_finish_group(c, ov, on, od, G, org, R, cp, ~__ldg(&c.nodes[v].ad), P);
-        ++c.g;
-    }
-    return false;
-}
-
-__device__ __forceinline__ u64 shfl64(u64 x, int src) {
-    return (u64(__shfl_sync(FULL, u32(x >> 32), src)) << 32) | __shfl_sync(FULL, u32(x), src);
-}
-__device__ __forceinline__ u64 shfl_xor64(u64 x, int o) {
-    return (u64(__shfl_xor_sync(FULL, u32(x >> 32), o)) << 32) | __shfl_xor_sync(FULL, u32(x), o);
-}
-
-// The whole (converged) warp apportions lane r's pending group; lane r
-// receives R / used / conc (or an error status).
-__device__ __forceinline__ void coop_apportion(CoopLane& c, const int r, const int lane, const int* ov_r,
-                                               const u32* on_r, const u32* od_r, const PlatT<u32>& P) {
-    const u64 org = shfl64(c.org, r);
-    const K1Node* nodes = reinterpret_cast<const K1Node*>(shfl64(reinterpret_cast<u64>(c.nodes), r));
-    const int n_over = __shfl_sync(FULL, c.n_over, r);
-    const int nm = __popcll(org);
-    int err = DS_OK;
-    bool ovf = false;
-    if (nm > 32) err = kLaneRetry;
-    // member j = the j-th set bit of org, on lane j
-    const bool mem = lane < nm;
-    int v = 0;
-    if (mem) {
-        const u32 lo = u32(org), hi = u32(org >> 32);
-        const int clo = __popc(lo);
-        v = lane < clo ? int(__fns(lo, 0, lane + 1)) : 32 + int(__fns(hi, 0, lane - clo + 1));
-    }
-    RatT<u32> l{0, 1};
-    if (mem) {
-        bool hit = false;
-        for (int k = n_over - 1; k >= 0 && !hit; --k) {
-            if (ov_r[k] == v) {
-                l = RatT<u32>{on_r[k], od_r[k]};
-                hit = true;
-            }
-        }
-        if (!hit) l = RatT<u32>{__ldg(&nodes[v].ln), __ldg(&nodes[v].ld)};
-    }
-    // W = sum of the pending loads: integer loads by a 64-bit warp sum, else
-    // the members' ordered rational sum (rare: fractional loads, residuals)
-    RatT<u32> Wt{0, 1};
-    if (__all_sync(FULL, !mem || l.d == 1)) {
-        u64 s = mem ? l.n : 0;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) s += shfl_xor64(s, o);
-        if (s >> 32) err = DS_EOVERFLOW;
-        Wt = RatT<u32>{u32(s), 1};
-    } else {
-#pragma unroll 1
-        for (int j = 0; j < nm; ++j) {
-            const RatT<u32> x{__shfl_sync(FULL, l.n, j), __shfl_sync(FULL, l.d, j)};
-            Wt = q_add(Wt, x);
-        }
-        if (Wt.d == 0) err = DS_EOVERFLOW;
-    }
-    if (Wt.n == 0) err = DS_EOVERFLOW;
-    int m = 0, cp = 0;
-    u32 rn = 0, rd = 1;
-    if (err == DS_OK && mem) {
-        cp = q_max_par(l, P);
-        if (cp < 0) {
-            ovf = true;
-            cp = 1;
-        }
-        cp = min(cp, P.M);
-        // quota = l*M/W = (l.n*M*W.d) / (l.d*W.n): floor and remainder
-        const u32 qn = mulc(mulc(l.n, u32(P.M), ovf), Wt.d, ovf);
-        const u32 qd = mulc(l.d, Wt.n, ovf);
-        const u32 fl = qd ? qn / qd : 0u;
-        if (!qd) ovf = true;
-        const long long flc = fl > 0x7fffffffu ? 0x7fffffffll : (long long)fl;
-        m = int(max(1ll, min(flc, (long long)cp)));
-        rn = qn - fl * qd;
-        rd = qd;
-    }
-    int tot = __reduce_add_sync(FULL, unsigned(m));
-    const int capsum = __reduce_add_sync(FULL, unsigned(cp));
-    if (__any_sync(FULL, ovf)) err = DS_EOVERFLOW;
-    const int target = min(P.M, capsum);
-#pragma unroll 1
-    while (err == DS_OK && (tot > P.M || tot < target)) {
-        const bool shed = tot > P.M;
-        Pick<u32> x{{0, 1}, {0, 1}, -1};
-        if (mem && (shed ? m > 1 : m < cp)) {
-            bool o = false;
-            x.k1 = exec_raw(l, shed ? m - 1 : m, P, o);
-            ovf |= o;
-            x.k2 = shed ? RatT<u32>{0, 1} : RatT<u32>{rn, rd};
-            x.idx = v;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const Pick<u32> y{{__shfl_xor_sync(FULL, x.k1.n, o), __shfl_xor_sync(FULL, x.k1.d, o)},
-                              {__shfl_xor_sync(FULL, x.k2.n, o), __shfl_xor_sync(FULL, x.k2.d, o)},
-                              __shfl_xor_sync(FULL, x.idx, o)};
-            if (pick_better<u32>(y, x, shed)) x = y;
-        }
-        if (x.idx < 0) {
-            err = DS_EINVARIANT;
-            break;
-        }
-        const int step = shed ? -1 : 1;
-        if (mem && v == x.idx) m += step;
-        tot += step;
-    }
-    if (__any_sync(FULL, ovf) && err == DS_OK) err = DS_EOVERFLOW;
-    // members: exec; response = the first (smallest id) member attaining the max
-    RatT<u32> e{0, 1};
-    int ev = mem ? v : 0x7fffffff;
-    if (err == DS_OK && mem) {
-        e = q_exec(l, m, P);
-        if (e.d == 0) ovf = true;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const RatT<u32> y{__shfl_xor_sync(FULL, e.n, o), __shfl_xor_sync(FULL, e.d, o)};
-        const int yv = __shfl_xor_sync(FULL, ev, o);
-        const int cmp = yv == 0x7fffffff ? -1 : (ev == 0x7fffffff ? 1 : rat_cmp(y, e));
-        if (cmp > 0 || (cmp == 0 && yv < ev)) {
-            e = y;
-            ev = yv;
-        }
-    }
-    if (__any_sync(FULL, ovf) && err == DS_OK) err = DS_EOVERFLOW;
-    const int used = __reduce_add_sync(FULL, unsigned(m));
-    const u64 cm = mem ? ~__ldg(&nodes[v].ad) : 0ull;
-    const u64 conc = (u64(__reduce_or_sync(FULL, u32(cm >> 32))) << 32) | __reduce_or_sync(FULL, u32(cm));
-    if (lane == r) {
-        if (err != DS_OK) {
-            c.st = err;
-        } else {
-            c.R = e;
-            c.used = used;
-            c.conc = conc;
-        }
-    }
-}
-
-template <bool UNUSED = false>
-__global__ void __launch_bounds__(32 * kCoopWarps) k1_back_coop(const K1Args a) {
-    __shared__ int s_ov[kCoopWarps * 32][kLaneSplits];
-    __shared__ u32 s_on[kCoopWarps * 32][kLaneSplits], s_od[kCoopWarps * 32][kLaneSplits];
-    const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
-    int* ov = s_ov[threadIdx.x];
-    u32* on = s_on[threadIdx.x];
-    u32* od = s_od[threadIdx.x];
-    const u32 nbase = a.node_off[0];
-    const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
-    const unsigned lt = (1u << lane) - 1;
-    CoopLane c;
-    c.st = DS_OK;
-    bool active = false;
-    u64 bnext = 0, bend = 0;
-    bool exhausted = false;
-#pragma unroll 1
-    while (true) {
-        // refill idle lanes from the warp's batch (one atomic per 32 DAGs)
-        unsigned idle = __ballot_sync(FULL, !active);
-#pragma unroll 1
-        while (idle && !exhausted) {
-            if (bnext == bend) {
-                u32 t = 0;
-                if (lane == 0) t = atomicAdd(a.retry_count + 5, 32u);
-                t = __shfl_sync(FULL, t, 0);
-                if (t >= a.n_dags) {
-                    exhausted = true;
-                    break;
-                }
-                bnext = t;
-                bend = min(u64(t) + 32, a.n_dags);
-            }
-            const unsigned take = min(unsigned(__popc(idle)), unsigned(bend - bnext));
-            const unsigned rank = __popc(idle & lt);
-            if (!active && rank < take) {
-                const u64 d = bnext + rank;
-                if (a.status[d] == kStPending) {
-                    const u32 n0 = a.node_off[d] - nbase;
-                    const int n = int(a.node_off[d + 1] - nbase - n0);
-                    c.nodes = a.h.node + n0;
-                    c.ro = a.h.ro + n0;
-                    c.divg = a.h.divg + n0;
-                    c.d = d;
-                    c.V = n >= 64 ? ~0ull : ((1ull << n) - 1);
-                    c.done = 0;
-                    c.proposed = RatT<u32>{0, 1};
-                    c.g = 0;
-                    c.nd = a.h.ndiv[d];
-                    c.gidx = 0;
-                    c.n_over = 0;
-                    c.st = DS_OK;
-                    c.ovf = false;
-                    active = true;
-                }
-            }
-            bnext += take;
-            idle = __ballot_sync(FULL, !active);
-        }
-        if (!__any_sync(FULL, active)) break;
-        bool need = false;
-        if (active) {
-            need = coop_advance(c, ov, on, od, P);
-            if (!need) {  // the DAG is done: results
-                int st = c.st;
-                if (st == DS_OK && c.ovf) st = DS_EOVERFLOW;
-                if (st == DS_OK && c.done != c.V) st = DS_EINVARIANT;  // "scheduling finished with unplaced kernels"
-                if (st == DS_EOVERFLOW || st == kLaneRetry) {  // recomputed from scratch in wider words
-                    a.retry[atomicAdd(a.retry_count, 1u)] = u32(c.d);
-                    a.status[c.d] = kStRetried;
-                } else {
-                    int64_t* b = a.bounds + 10 * c.d;
-                    if (st == DS_OK) {
-                        b[0] = (long long)c.proposed.n;
-                        b[1] = (long long)c.proposed.d;
-                    } else {
-                        for (int k = 0; k < 10; ++k) b[k] = 0;
-                    }
-                    a.status[c.d] = st;
-                    if (a.n_groups) a.n_groups[c.d] = (unsigned short)(st == DS_OK ? c.gidx : 0);
-                }
-                active = false;
-            }
-        }
-        unsigned req = __ballot_sync(FULL, need);
-#pragma unroll 1
-        while (req) {
-            const int r = __ffs(req) - 1;
-            req &= req - 1;
-            coop_apportion(c, r, lane, s_ov[wbase + r], s_on[wbase + r], s_od[wbase + r], P);
-        }
-        if (need) {
-            if (c.st == DS_OK) coop_finish_group(c, ov, on, od, c.G, c.org, c.R, c.used, c.conc, P);
-            ++c.g;
-        }
     }
 }
 

@@ -6,7 +6,7 @@
 
 #include "k1_analysis.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
+#include "k1_fast.cuh"
 
 namespace ds {
 
@@ -14,27 +14,19 @@ struct K1Occupancy {
     int grid_small = 0;  // persistent grid of the n <= 64 kernel (CTAs)
     int grid_big = 0;    // n <= 256 kernel
     int grid_retry = 0;  // 128-bit retry kernel
-    int grid_front = 0;  // split bounds pass (k1_front / k1_mid / k1_back)
+    int grid_front = 0;  // split bounds pass (k1_front / k1_mid / k1_back_lane)
     int grid_mid = 0;
-    int grid_back = 0;
     int grid_back_lane = 0;  // k1_back_lane (one lane per DAG)
-    int grid_back_coop = 0;  // k1_back_coop (lanes + warp-cooperative apportion)
+    int grid_fast = 0;       // k1_fast
 };
 
 constexpr int kWarpsSmall = 4;  // WarpState<1,u64> per warp, 4 warps per CTA
 constexpr int kWarpsBig = 1;    // WarpState<4,u64> (~50 KB) per CTA
-constexpr int kK1Counters = 8;  // u32 work counters at K1Args::retry_count (32 bytes)
+constexpr int kK1Counters = 12;  // u32 work counters at K1Args::retry_count (48 bytes)
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
-inline size_t k1_sort_tmp_bytes(u64 n_dags) {
-    size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr),
-                                    static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr), int(n_dags), 0, 32);
-    return (b + 255) & ~size_t(255);
-}
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
-    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 16 +
-           k1_sort_tmp_bytes(n_dags);
+    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 16;
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;
@@ -46,11 +38,9 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     h.ndiv = h.ro + n_nodes;
     uintptr_t p = (reinterpret_cast<uintptr_t>(h.ndiv + n_dags) + 255) & ~uintptr_t(255);
     h.skey = reinterpret_cast<u32*>(p);
-    h.sperm = h.skey + n_dags;
-    h.skey2 = h.sperm + n_dags;
-    h.sperm2 = h.skey2 + n_dags;
-    h.sort_tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(h.sperm2 + n_dags) + 255) & ~uintptr_t(255));
-    h.sort_tmp_bytes = k1_sort_tmp_bytes(n_dags);
+    h.perm = h.skey + n_dags;
+    h.fb = h.perm + n_dags;
+    h.l64 = h.fb + n_dags;
     return h;
 }
 
@@ -60,7 +50,7 @@ cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ);
 // Optional per-launch markers: an event recorded after each kernel launch
 // (bench.py times the kernels one by one inside the timed region).
 struct K1Marks {
-    static constexpr int kMax = 8;
+    static constexpr int kMax = 10;
     cudaEvent_t ev[kMax];
     const char* name[kMax];
     int n = 0;

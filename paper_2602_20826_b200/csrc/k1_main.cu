@@ -41,14 +41,8 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
             return e;
         if ((e = cudaFuncSetAttribute(k1_mid<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
             return e;
-        if ((e = cudaFuncSetAttribute(k1_back<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
-            return e;
-        int of = 0, om = 0, ob = 0, obl = 0;
+        int of = 0, om = 0, obl = 0;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obl, k1_back_lane<>, 32 * kLaneWarps, 0))) return e;
-        int obc = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&obc, k1_back_coop<>, 32 * kCoopWarps, 0))) return e;
-        if (obc < 1) return cudaErrorInvalidConfiguration;
-        occ.grid_back_coop = sms * obc;
         if (obl < 1) return cudaErrorInvalidConfiguration;
         // DS_K1_LANE_CTAS_PER_SM (tuning knob): fewer resident DAG walks keep
         // their hand-off state inside L2
@@ -57,16 +51,17 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
             if (c >= 1 && c < obl) obl = c;
         }
         occ.grid_back_lane = sms * obl;
+        int ofa = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ofa, k1_fast<32>, 32 * kFastWarps, 0))) return e;
+        if (ofa < 1) return cudaErrorInvalidConfiguration;
+        occ.grid_fast = sms * ofa;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k1_front<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k1_mid<>, 32 * kWarpsSmall, kSmemSmall)))
             return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k1_back<>, 32 * kWarpsSmall, kSmemSmall)))
-            return e;
-        if (of < 1 || om < 1 || ob < 1) return cudaErrorInvalidConfiguration;
+        if (of < 1 || om < 1) return cudaErrorInvalidConfiguration;
         occ.grid_front = sms * of;
         occ.grid_mid = sms * om;
-        occ.grid_back = sms * ob;
     }
     // one full wave; warps stride over the DAGs. DS_K1_CTAS_PER_SM (tuning
     // knob) caps the resident CTAs per SM below the occupancy limit.
@@ -99,8 +94,27 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
     const u64 need_small = (a.n_dags + kWarpsSmall - 1) / kWarpsSmall;
     auto cap = [&](int g) { return int(need_small < u64(g) ? need_small : u64(g)); };
     const bool split = !DETAIL && a.h.node != nullptr;
+    // the fused integer fast path (k1_fast.cuh) when the batch can use it:
+    // t_min = 1, integer loads, M <= 1023 (DS_K1_FAST=0 disables it)
+    static const bool fast_on = [] {
+        const char* env = getenv("DS_K1_FAST");
+        return !(env && env[0] == '0');
+    }();
+    const bool fast = split && fast_on && a.load_den == nullptr && a.plat.tmin.n == 1 && a.plat.tmin.d == 1 &&
+                      a.plat.M <= 1023;
+    K1Args af = a;
+    af.fb_only = fast ? 1 : 0;
+    if (fast) {
+        const u64 need = (a.n_dags + kFastWarps - 1) / kFastWarps;
+        const int gf = int(need < u64(occ.grid_fast) ? need : u64(occ.grid_fast));
+        k1_fast<32><<<gf, 32 * kFastWarps, 0, s>>>(af);
+        if ((e = mark("k1_fast<32>")) != cudaSuccess) return e;
+        k1_fast<64><<<gf, 32 * kFastWarps, 0, s>>>(af);
+        if ((e = mark("k1_fast<64>")) != cudaSuccess) return e;
+    }
     if (split) {
-        k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        // every DAG, or (fast path) only those k1_fast queued
+        k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(af);
         if ((e = mark("k1_front")) != cudaSuccess) return e;
     } else {
         k1_analyse<1, DETAIL><<<cap(occ.grid_small), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
@@ -112,16 +126,8 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         if ((e = mark("k1_analyse<4>")) != cudaSuccess) return e;
     }
     if (split && (a.mask & DS_M_PROPOSED)) {
-        k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
+        k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(af);
         if ((e = mark("k1_mid")) != cudaSuccess) return e;
-        // one lane per DAG (default, 3.06 ms per 1M C5 DAGs); DS_K1_BACK=coop
-        // adds warp-cooperative apportion at rendezvous points (4.25 ms: the
-        // lanes wait for each other), DS_K1_BACK=warp one warp per DAG (4.40)
-        static const int back_kind = [] {
-            const char* env = getenv("DS_K1_BACK");
-            return env && env[0] == 'w' ? 2 : (env && env[0] == 'c' ? 0 : 1);
-        }();
-        const bool warp_back = back_kind == 2;
         // shape-sorted walk order for the lane kernel (DS_K1_SORT=0: index order)
         static const bool sort_walks = [] {
             const char* env = getenv("DS_K1_SORT");
@@ -129,23 +135,13 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         }();
         K1Args b = a;
         b.perm = nullptr;
-        if (back_kind == 1 && sort_walks && a.h.skey) {
-            size_t tb = a.h.sort_tmp_bytes;
-            if ((e = cub::DeviceRadixSort::SortPairs(a.h.sort_tmp, tb, a.h.skey, a.h.skey2, a.h.sperm, a.h.sperm2,
-                                                     int(a.n_dags), 0, 32, s)) != cudaSuccess)
-                return e;
-            if ((e = mark("k1_sort")) != cudaSuccess) return e;
-            b.perm = a.h.sperm2;
+        if (sort_walks && a.h.skey) {
+            k1_wsort<><<<int((a.n_dags + kSortWindow - 1) / kSortWindow), kWsortThreads, 0, s>>>(a.h.skey, a.h.perm,
+                                                                                                a.n_dags);
+            if ((e = mark("k1_wsort")) != cudaSuccess) return e;
+            b.perm = a.h.perm;
         }
-        if (back_kind == 0) {
-            const u64 need = (a.n_dags + 32 * kCoopWarps - 1) / (32 * kCoopWarps);
-            k1_back_coop<><<<int(need < u64(occ.grid_back_coop) ? need : u64(occ.grid_back_coop)), 32 * kCoopWarps, 0,
-                             s>>>(a);
-            if ((e = mark("k1_back_coop")) != cudaSuccess) return e;
-        } else if (warp_back) {
-            k1_back<><<<cap(occ.grid_back), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
-            if ((e = mark("k1_back")) != cudaSuccess) return e;
-        } else {
+        {
             const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
             const int g = int(need < u64(occ.grid_back_lane) ? need : u64(occ.grid_back_lane));
             if (a.plat.M <= 255) k1_back_lane<false, 8><<<g, 32 * kLaneWarps, 0, s>>>(b);

@@ -15,8 +15,7 @@
 //   k2_mix        LDG.128/STG.128, 4 independent 16-B loads in flight per
 //                 thread per iteration (8 B/elem algorithmic traffic)
 //   k2_axpy       fp32 y = a*x + y, no FMA contraction (12 B/elem)
-//   k2_mix_bulk   cp.async.bulk global->shared (TMA engine, mbarrier
-//                 complete_tx) and shared->global bulk stores, 4-stage ring
+//   k2_mix_tma    warp-specialised cp.async.bulk (TMA engine) ring, below
 #pragma once
 
 #include <cstdint>
@@ -38,8 +37,6 @@ struct NodeArgs {
 };
 
 constexpr int kNodeSmem = 120 * 1024;  // > 114 KB: at most one node CTA per SM
-constexpr int kBulkStages = 4;
-constexpr int kBulkChunk = 24 * 1024;  // bytes per stage (4 x 24 KB ring)
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -216,66 +213,6 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__global__ void __launch_bounds__(1024, 1) k2_mix_bulk(const NodeArgs a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ unsigned long long t0s;
-    __shared__ __align__(8) uint64_t bars[kBulkStages];
-    if (threadIdx.x == 0) {
-        t0s = gtimer();
-        for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    unsigned long long s0, s1;
-    cta_slice(a, s0, s1);
-    const unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;  // 16-B aligned interior
-    if (v0 >= v1) {
-        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-    } else {
-        for (unsigned long long i = s0 + threadIdx.x; i < (v0 << 2); i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-        for (unsigned long long i = (v1 << 2) + threadIdx.x; i < s1; i += blockDim.x) a.y[i] = mix32(__ldg(a.x + i));
-        const unsigned long long base = v0 << 2, n_el = (v1 - v0) << 2;  // elements in the interior
-        constexpr unsigned long long kChunkEl = kBulkChunk / 4;
-        const unsigned long long n_chunks = (n_el + kChunkEl - 1) / kChunkEl;
-        auto issue = [&](unsigned long long c) {  // thread 0: load chunk c into stage c % S
-            const int s = int(c % kBulkStages);
-            const unsigned long long e0 = base + c * kChunkEl;
-            const unsigned long long ne = min(kChunkEl, base + n_el - e0);
-            mbar_expect_tx(&bars[s], uint32_t(ne * 4));
-            bulk_g2s(sm + s * kBulkChunk, a.x + e0, uint32_t(ne * 4), &bars[s]);
-        };
-        if (threadIdx.x == 0) {
-            for (unsigned long long c = 0; c < n_chunks && c < kBulkStages; ++c) issue(c);
-        }
-        for (unsigned long long c = 0; c < n_chunks; ++c) {
-            const int s = int(c % kBulkStages);
-            const unsigned long long e0 = base + c * kChunkEl;
-            const unsigned long long ne = min(kChunkEl, base + n_el - e0);
-            mbar_wait(&bars[s], uint32_t((c / kBulkStages) & 1));
-            uint4* buf = reinterpret_cast<uint4*>(sm + s * kBulkChunk);
-            for (unsigned long long i = threadIdx.x; i < ne / 4; i += blockDim.x) {
-                uint4 r = buf[i];
-                r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w);
-                buf[i] = r;
-            }
-            fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk copy
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                bulk_s2g(a.y + e0, buf, uint32_t(ne * 4));
-                bulk_commit();
-                if (c + kBulkStages < n_chunks) {
-                    // stage s is reloaded: its store must have finished reading smem
-                    bulk_wait_read<0>();
-                    issue(c + kBulkStages);
-                }
-            }
-        }
-        if (threadIdx.x == 0) bulk_wait_all();
-    }
-    __syncthreads();
-    stamp_exit(a, t0s);
-}
-
 // ------------------------------------ warp-specialised TMA streaming variant
 // One producer warp (one elected lane) streams the CTA's slice through a
 // ring of kTmaStages x kTmaChunk shared-memory stages with cp.async.bulk
@@ -392,79 +329,11 @@ __global__ void k2_init(uint32_t* x, unsigned long long n, uint32_t seed, int fp
 
 __global__ void k2_tick(int* replay) { *replay += 1; }
 
-// ------------------------------------------------ persistent engine (K3)
-// One CTA per SM for the whole DAG. CTA b walks items[item_off[b] ..
-// item_off[b+1]) — (entity, rank) pairs in group order — waits until every
-// predecessor entity has all of its CTAs done for this epoch (counters only
-// grow: entity p is complete in epoch k when done[p] >= m_p * (k+1)), runs its
-// slice of the entity's element range with the k2_mix body, then publishes
-// completion (fence + atomicAdd). Deadlock-free: predecessors always sit in
-// strictly earlier groups, and every CTA walks its items in group order.
-struct PEnt {
-    const uint32_t* x;
-    uint32_t* y;
-    unsigned long long lo, hi;
-    uint32_t m, slot, pred_off, n_preds;
-};
-struct PItem {
-    uint32_t ent, rank;
-};
-struct PArgs {
-    const PEnt* ents;
-    const uint32_t* preds;
-    const uint32_t* item_off;
-    const PItem* items;
-    unsigned int* done;
-    unsigned int epoch;
-    int rec;  // recorded replay slot, < 0: not recorded
-    unsigned long long* stamps;
-    uint32_t* smids;
-    unsigned long long* span;
-    uint32_t total;
-};
-
+// acquire load of a completion counter (dependency hand-off)
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-
-__global__ void __launch_bounds__(1024, 1) k3_persistent(const PArgs a) {
-    __shared__ unsigned long long t0s;
-    const uint32_t b = blockIdx.x;
-#pragma unroll 1
-    for (uint32_t it = a.item_off[b]; it < a.item_off[b + 1]; ++it) {
-        const PItem w = a.items[it];
-        const PEnt e = a.ents[w.ent];
-        if (threadIdx.x == 0) {
-            for (uint32_t k = 0; k < e.n_preds; ++k) {
-                const uint32_t p = a.preds[e.pred_off + k];
-                const unsigned int need = a.ents[p].m * (a.epoch + 1);
-                while (ld_acquire(a.done + p) < need) __nanosleep(32);
-            }
-            t0s = gtimer();
-        }
-        __syncthreads();
-        const unsigned long long len = e.hi - e.lo;
-        const unsigned long long s0 = e.lo + len * w.rank / e.m, s1 = e.lo + len * (w.rank + 1) / e.m;
-        mix_ldg_slice<4>(e.x, e.y, s0, s1);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned long long t1 = gtimer();
-            if (a.rec >= 0) {
-                const unsigned long long idx = (unsigned long long)a.rec * a.total + e.slot + w.rank;
-                if (a.stamps) {
-                    a.stamps[2 * idx] = t0s;
-                    a.stamps[2 * idx + 1] = t1;
-                }
-                if (a.smids) a.smids[idx] = smid();
-                atomicMin(&a.span[2 * a.rec], t0s);
-                atomicMax(&a.span[2 * a.rec + 1], t1);
-            }
-            __threadfence();
-            atomicAdd(a.done + w.ent, 1u);
-        }
-    }
 }
 
 // ------------------------------------------------ dynamic persistent engine
@@ -485,6 +354,11 @@ __global__ void __launch_bounds__(1024, 1) k3_persistent(const PArgs a) {
 // in the waiting one, the same as a static CTA assignment, without its
 // mis-placements. Deadlock-free: the earliest (topological) waiting rank has
 // every predecessor rank claimed, hence running, hence finishing.
+// With egroup (DS_PLAN_PRIORITY) the probe only considers entities of the
+// group of the first entity that still has unclaimed ranks (`cur`; plans are
+// in group order): group g+1 is not touched while a group-g rank is
+// unclaimed, so every group-g entity finds its quota of CTAs, and CTAs that
+// finish their group-g rank early move on to group g+1 instead of idling.
 struct DEnt {
     const uint32_t* x;
     uint32_t* y;
@@ -495,6 +369,7 @@ struct DArgs {
     const DEnt* ents;
     const uint32_t* succs;
     const uint32_t* quota;      // [n] m_e (read-only copy for the warp probes)
+    const uint32_t* egroup;     // [n] group of e (DS_PLAN_PRIORITY), else nullptr
     uint32_t n, n_init;
     unsigned int* claimed;      // [n]
     unsigned int* pend_claim;   // [n]
@@ -541,16 +416,26 @@ __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const
             uint32_t ent = ~0u, rank = 0;
             while (cur < a.n) {
                 bool got = false;
-                for (uint32_t base = cur; base < a.n && !got; base += 32) {
+                uint32_t gcur = ~0u;  // group of `cur` (priority plans)
+                bool stop = false;
+                for (uint32_t base = cur; base < a.n && !got && !stop; base += 32) {
                     const uint32_t e = base + lane;
                     const bool valid = e < a.n;
                     const uint32_t m = valid ? __ldg(a.quota + e) : 0;
                     const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
                     const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
                     const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
-                    const bool open = valid && cl < m;
+                    bool open = valid && cl < m;
                     const unsigned open_mask = __ballot_sync(~0u, open);
-                    if (base == cur) cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
+                    if (base == cur) {
+                        cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
+                        if (a.egroup && cur < a.n) gcur = __ldg(a.egroup + cur);
+                    }
+                    if (a.egroup) {  // later groups wait until this one is fully claimed
+                        const bool later = valid && __ldg(a.egroup + e) > gcur;
+                        open = open && !later;
+                        stop = __any_sync(~0u, later);  // plan order = group order: nothing after
+                    }
                     unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
                     if (!pick) pick = __ballot_sync(~0u, open && pc == 0);
                     while (pick && !got) {
@@ -629,217 +514,6 @@ __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const
                 atomicMin(&a.span[2 * a.rec], t0s);
                 atomicMax(&a.span[2 * a.rec + 1], t1);
             }
-        }
-    }
-}
-
-// ------------------------------------------------ streaming persistent engine
-// The dynamic engine's claiming (look-ahead reservations, pend_claim /
-// pend_done counters) with the TMA ring of k2_mix_tma kept streaming ACROSS
-// items: the producer warp is also the CTA's scheduler. When its ring still
-// holds the tail of the current item and no other CTA is idle (contention),
-// it claims the next startable item and issues that item's bulk loads into
-// the stages the consumers free up, so the SM goes from one entity to the
-// next without a drain/launch bubble; with idle CTAs around it leaves new
-// work to them. Every stage carries (destination, length, item slot,
-// first/last flags) next to its data. Consumers process stages in order; at
-// an item's last stage every consumer warp fences its stores, and the last
-// one to finish releases the successors (RED on pend_done) and stamps the
-// item: start = when the last consumer warp began its first stage, end =
-// when the last one finished its last stage, so the items of one SM never
-// overlap in their stamps (an SM still computes one entity at a time; only
-// the prefetch of the next entity's input overlaps the current one's tail).
-constexpr int kItemSlots = 8;  // > kTmaStages items can be in the ring at once
-constexpr uint32_t kTagFirst = 1u << 8, kTagLast = 1u << 9, kTagExit = 1u << 10;
-struct StreamMeta {
-    uint4* dst;
-    uint32_t nvec;
-    uint32_t tag;  // item slot | flags
-};
-struct ItemRec {
-    unsigned long long t0;
-    uint32_t ent, rank, done_warps, pad;
-};
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-
-// warp-wide probe of the entity table in plan order (see k3_dynamic): claim a
-// rank of the first startable entity, or (reserve) of the first whose
-// predecessors are all claimed; returns ~0u when nothing was claimed
-__device__ __forceinline__ uint32_t claim_rank(const DArgs& a, uint32_t& cur, bool reserve, uint32_t& rank) {
-    const int lane = threadIdx.x & 31;
-    for (uint32_t base = cur; base < a.n; base += 32) {
-        const uint32_t e = base + lane;
-        const bool valid = e < a.n;
-        const uint32_t m = valid ? __ldg(a.quota + e) : 0;
-        const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
-        const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
-        const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
-        const bool open = valid && cl < m;
-        const unsigned open_mask = __ballot_sync(~0u, open);
-        if (base == cur) cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
-        unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
-        if (!pick && reserve) pick = __ballot_sync(~0u, open && pc == 0);
-        while (pick) {
-            const int l = __ffs(pick) - 1;
-            pick &= pick - 1;
-            uint32_t c = 0;
-            if (lane == l) c = atomicAdd(a.claimed + e, 1u);
-            c = __shfl_sync(~0u, c, l);
-            if (c < __shfl_sync(~0u, m, l)) {
-                rank = c;
-                return base + l;
-            }
-        }
-    }
-    return ~0u;
-}
-
-__global__ void __launch_bounds__(kTmaThreads, 1) k3_stream(const DArgs a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ TmaRing ring;
-    __shared__ StreamMeta meta[kTmaStages];
-    __shared__ ItemRec items[kItemSlots];
-    if (threadIdx.x == 0) tma_ring_init(&ring);
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr unsigned long long kChunkV = kTmaChunk / 16;
-    if (warp == kTmaConsumerWarps) {
-        // ------------------------------------------------ producer / scheduler
-        uint32_t it = 0, cur = 0, n_items = 0;
-        bool counted_idle = false;
-#pragma unroll 1
-        while (true) {
-            bool drained = true;
-            if (it) {
-                const uint32_t last = it - 1;
-                drained = mbar_test(&ring.empty[last % kTmaStages], (last / kTmaStages) & 1);
-            }
-            drained = __shfl_sync(~0u, drained ? 1 : 0, 0) != 0;
-            if (drained && !counted_idle) {
-                if (lane == 0) atomicAdd(a.idle, 1u);
-                counted_idle = true;
-            }
-            uint32_t ent = ~0u, rank = 0;
-            if (cur < a.n) {
-                uint32_t others_idle = lane == 0 ? ld_relaxed(a.idle) : 0;
-                others_idle = __shfl_sync(~0u, others_idle, 0);
-                if (drained || others_idle == 0) ent = claim_rank(a, cur, drained, rank);
-            }
-            if (ent == ~0u) {
-                if (cur >= a.n) {  // everything handed out: close the ring
-                    if (lane == 0) {
-                        const uint32_t idx = it++, st = idx % kTmaStages, k = idx / kTmaStages;
-                        if (k > 0) mbar_wait(&ring.empty[st], (k - 1) & 1);
-                        meta[st].tag = kTagExit;
-                        mbar_arrive(&ring.full[st]);
-                    }
-                    break;
-                }
-                __nanosleep(32);
-                continue;
-            }
-            if (counted_idle) {
-                if (lane == 0) atomicSub(a.idle, 1u);
-                counted_idle = false;
-            }
-            const DEnt e = a.ents[ent];
-            if (lane == 0) {
-                for (uint32_t k = 0; k < e.n_succ; ++k) atomicSub(a.pend_claim + a.succs[e.succ_off + k], 1u);
-                while (ld_acquire(a.pend_done + ent) != 0) {
-                }
-            }
-            __syncwarp();
-            const unsigned long long len = e.hi - e.lo;
-            const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
-            unsigned long long v0 = (s0 + 3) >> 2, v1 = s1 >> 2;
-            if (v0 >= v1) v0 = v1 = s1 >> 2;  // no aligned interior: all scalar
-            // unaligned head/tail elements by the producer lanes, fenced before
-            // the item can complete (its completion follows its last stage)
-            const unsigned long long h1 = v0 < v1 ? (v0 << 2) : s1, t0e = v0 < v1 ? (v1 << 2) : s1;
-            bool scalars = false;
-            for (unsigned long long i = s0 + lane; i < h1; i += 32) e.y[i] = mix32(__ldg(e.x + i)), scalars = true;
-            for (unsigned long long i = t0e + lane; i < s1; i += 32) e.y[i] = mix32(__ldg(e.x + i)), scalars = true;
-            if (__any_sync(~0u, scalars)) __threadfence();
-            if (lane == 0) {
-                const uint32_t slot = n_items++ % kItemSlots;
-                items[slot].t0 = 0;
-                items[slot].ent = ent;
-                items[slot].rank = rank;
-                items[slot].done_warps = 0;
-                const unsigned long long nv = v1 - v0;
-                const uint32_t n_chunks = nv ? uint32_t((nv + kChunkV - 1) / kChunkV) : 1u;
-                const uint4* x4 = reinterpret_cast<const uint4*>(e.x) + v0;
-                uint4* y4 = reinterpret_cast<uint4*>(e.y) + v0;
-                for (uint32_t c = 0; c < n_chunks; ++c) {
-                    const uint32_t idx = it++, st = idx % kTmaStages, k = idx / kTmaStages;
-                    if (k > 0) mbar_wait(&ring.empty[st], (k - 1) & 1);
-                    const unsigned long long nc = nv ? min(kChunkV, nv - c * kChunkV) : 0;
-                    meta[st].dst = y4 + c * kChunkV;
-                    meta[st].nvec = uint32_t(nc);
-                    meta[st].tag = slot | (c == 0 ? kTagFirst : 0u) | (c + 1 == n_chunks ? kTagLast : 0u);
-                    if (nc) {
-                        mbar_expect_tx(&ring.full[st], uint32_t(nc * 16));
-                        bulk_g2s(sm + st * kTmaChunk, x4 + c * kChunkV, uint32_t(nc * 16), &ring.full[st]);
-                    } else {
-                        mbar_arrive(&ring.full[st]);
-                    }
-                }
-            }
-            __syncwarp();
-        }
-    } else {
-        // ------------------------------------------------ consumers
-        const int t = threadIdx.x;
-#pragma unroll 1
-        for (uint32_t it = 0;; ++it) {
-            const uint32_t st = it % kTmaStages, k = it / kTmaStages;
-            mbar_wait(&ring.full[st], k & 1);
-            const StreamMeta m = meta[st];
-            if (m.tag & kTagExit) break;
-            const uint32_t slot = m.tag & 0xffu;
-            if ((m.tag & kTagFirst) && lane == 0) atomicMax(&items[slot].t0, gtimer());
-            const uint4* buf = reinterpret_cast<const uint4*>(sm + st * kTmaChunk);
-#pragma unroll 4
-            for (uint32_t i = t; i < m.nvec; i += kTmaConsumerWarps * 32) {
-                uint4 r = buf[i];
-                r.x = mix32(r.x), r.y = mix32(r.y), r.z = mix32(r.z), r.w = mix32(r.w);
-                __stcs(m.dst + i, r);
-            }
-            if (m.tag & kTagLast) {
-                __syncwarp();
-                // cta-scope release of this warp's stores; the last warp's
-                // gpu-scope fence below is cumulative over what it observed
-                if (lane == 0) __threadfence_block();
-                if (lane == 0 && atomicAdd(&items[slot].done_warps, 1u) == kTmaConsumerWarps - 1) {
-                    const unsigned long long t1 = gtimer();
-                    __threadfence();
-                    const uint32_t ent = items[slot].ent, rank = items[slot].rank;
-                    const unsigned long long t0 = items[slot].t0;
-                    const DEnt& e = a.ents[ent];
-                    for (uint32_t q = 0; q < e.n_succ; ++q) atomicSub(a.pend_done + a.succs[e.succ_off + q], 1u);
-                    if (a.rec >= 0) {
-                        const unsigned long long idx = (unsigned long long)a.rec * a.total + e.slot + rank;
-                        if (a.stamps) {
-                            a.stamps[2 * idx] = t0;
-                            a.stamps[2 * idx + 1] = t1;
-                        }
-                        if (a.smids) a.smids[idx] = smid();
-                        atomicMin(&a.span[2 * a.rec], t0);
-                        atomicMax(&a.span[2 * a.rec + 1], t1);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ring.empty[st]);
         }
     }
 }

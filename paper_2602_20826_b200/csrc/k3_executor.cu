@@ -64,14 +64,7 @@ struct Exec {
     std::vector<cudaStream_t> streams;
     std::vector<cudaEvent_t> ent_ev;
     cudaEvent_t start_ev = nullptr;
-    // persistent engine
     int engine = DS_ENGINE_GRAPH;
-    PEnt* d_ents = nullptr;
-    uint32_t* d_preds = nullptr;
-    uint32_t* d_item_off = nullptr;
-    PItem* d_items = nullptr;
-    unsigned int* d_done = nullptr;
-    unsigned int epoch = 0;
     uint32_t grid = 0;
     // dynamic engine
     DArgs dyn{};
@@ -79,92 +72,11 @@ struct Exec {
     std::vector<void*> dyn_bufs;
 };
 
-// Persistent engine tables: per group, entities take consecutive CTA slots
-// (the scheduler guarantees sum of parallelism <= M per group); each CTA's
-// work list is its slots' (entity, rank) items in group order.
-int build_persistent(Exec* E, const ds_exec_plan* plan) {
-    const int n = plan->n_entities;
-    int max_group = -1;
-    for (int i = 0; i < n; ++i) {
-        if (plan->entities[i].group < 0) return fail(DS_EINVAL, "persistent engine needs a group-structured plan");
-        if (i && plan->entities[i].group < plan->entities[i - 1].group)
-            return fail(DS_EINVAL, "persistent engine needs entities in group order");
-        if (plan->entities[i].parallelism > E->sm_count) return fail(DS_EINVAL, "entity wider than the device");
-        max_group = std::max(max_group, int(plan->entities[i].group));
-    }
-    std::vector<std::vector<int>> members(max_group + 1);
-    for (int i = 0; i < n; ++i) members[plan->entities[i].group].push_back(i);
-    // Place every entity's CTAs on the SM slots that free up first (list
-    // scheduling over the model durations, entities in group order = a
-    // topological order of the augmented graph), so that without barriers a
-    // later group's entity is not queued behind an unrelated earlier item.
-    // Each slot's items stay in that topological order: deadlock-free.
-    const uint32_t grid = uint32_t(E->sm_count);
-    std::vector<double> slot_free(grid, 0.0), finish(n, 0.0);
-    std::vector<std::vector<PItem>> per(grid);
-    std::vector<uint32_t> order(grid);
-    for (int i = 0; i < n; ++i) {
-        const ds_exec_entity& e = plan->entities[i];
-        double ready = 0.0;
-        for (uint32_t k = 0; k < e.n_preds; ++k) ready = std::max(ready, finish[plan->preds[e.pred_off + k]]);
-        if (plan->barrier_groups && e.group > 0)
-            for (int j : members[e.group - 1]) ready = std::max(ready, finish[j]);
-        for (uint32_t c = 0; c < grid; ++c) order[c] = c;
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return slot_free[a] < slot_free[b]; });
-        const double dur = double(e.elem_hi - e.elem_lo) / double(e.parallelism);
-        for (int r = 0; r < e.parallelism; ++r) {
-            const uint32_t c = order[r];
-            const double end = std::max(ready, slot_free[c]) + dur;
-            slot_free[c] = end;
-            finish[i] = std::max(finish[i], end);
-            per[c].push_back(PItem{uint32_t(i), uint32_t(r)});
-        }
-    }
-    std::vector<uint32_t> item_off{0};
-    std::vector<PItem> items;
-    for (auto& v : per) {
-        items.insert(items.end(), v.begin(), v.end());
-        item_off.push_back(uint32_t(items.size()));
-    }
-    std::vector<PEnt> ents(n);
-    std::vector<uint32_t> preds;
-    uint32_t slot = 0;
-    for (int i = 0; i < n; ++i) {
-        const ds_exec_entity& e = plan->entities[i];
-        PEnt& p = ents[i];
-        p.x = E->x[e.node];
-        p.y = E->y[e.node];
-        p.lo = e.elem_lo;
-        p.hi = e.elem_hi;
-        p.m = uint32_t(e.parallelism);
-        p.slot = slot;
-        slot += p.m;
-        p.pred_off = uint32_t(preds.size());
-        for (uint32_t k = 0; k < e.n_preds; ++k) preds.push_back(plan->preds[e.pred_off + k]);
-        if (plan->barrier_groups && e.group > 0)  // simulate_scheme's group windows
-            for (int j : members[e.group - 1]) preds.push_back(uint32_t(j));
-        p.n_preds = uint32_t(preds.size()) - p.pred_off;
-    }
-    DS_CUDA(cudaMalloc(&E->d_ents, ents.size() * sizeof(PEnt)));
-    DS_CUDA(cudaMalloc(&E->d_preds, std::max<size_t>(preds.size(), 1) * 4));
-    DS_CUDA(cudaMalloc(&E->d_item_off, item_off.size() * 4));
-    DS_CUDA(cudaMalloc(&E->d_items, std::max<size_t>(items.size(), 1) * sizeof(PItem)));
-    DS_CUDA(cudaMalloc(&E->d_done, size_t(n) * 4));
-    DS_CUDA(cudaMemcpy(E->d_ents, ents.data(), ents.size() * sizeof(PEnt), cudaMemcpyHostToDevice));
-    if (!preds.empty()) DS_CUDA(cudaMemcpy(E->d_preds, preds.data(), preds.size() * 4, cudaMemcpyHostToDevice));
-    DS_CUDA(cudaMemcpy(E->d_item_off, item_off.data(), item_off.size() * 4, cudaMemcpyHostToDevice));
-    DS_CUDA(cudaMemcpy(E->d_items, items.data(), items.size() * sizeof(PItem), cudaMemcpyHostToDevice));
-    DS_CUDA(cudaMemset(E->d_done, 0, size_t(n) * 4));
-    DS_CUDA(cudaFuncSetAttribute(k3_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, kNodeSmem));
-    E->grid = grid;
-    E->epoch = 0;
-    return DS_OK;
-}
-
-// Dynamic engine tables: per entity its successors in the augmented graph
-// (plan edges, plus every member of group g-1 -> every member of group g when
-// the plan keeps group barriers), sorted by plan index so entities released
-// together enter the ready queue in schedule order.
+// Dynamic engine tables: per entity its successors (plan edges, plus every
+// member of group g-1 -> every member of group g when the plan keeps group
+// barriers), sorted by plan index so entities released together enter the
+// ready queue in schedule order; with DS_PLAN_PRIORITY also each entity's
+// group, which the kernel's claim rule reads.
 int build_dynamic(Exec* E, const ds_exec_plan* plan) {
     const int n = plan->n_entities;
     int max_group = -1;
@@ -186,7 +98,7 @@ int build_dynamic(Exec* E, const ds_exec_plan* plan) {
             edge(p, uint32_t(i));
         }
     }
-    if (plan->barrier_groups && max_group > 0) {
+    if (plan->barrier_groups == DS_PLAN_BARRIERS && max_group > 0) {
         std::vector<std::vector<uint32_t>> members(max_group + 1);
         for (int i = 0; i < n; ++i) {
             if (plan->entities[i].group < 0) return fail(DS_EINVAL, "group barriers need grouped entities");
@@ -244,11 +156,19 @@ int build_dynamic(Exec* E, const ds_exec_plan* plan) {
         (rc = dev((void**)&a.pend_done, size_t(n) * 4, nullptr)) || (rc = dev((void**)&a.idle, 4, nullptr)) ||
         (rc = dev((void**)&a.next_chunk, size_t(n) * 4, nullptr)))
         return rc;
+    a.egroup = nullptr;
+    if (plan->barrier_groups == DS_PLAN_PRIORITY) {
+        std::vector<uint32_t> grp(n);
+        for (int i = 0; i < n; ++i) {
+            if (plan->entities[i].group < 0 || (i && plan->entities[i].group < plan->entities[i - 1].group))
+                return fail(DS_EINVAL, "DS_PLAN_PRIORITY needs grouped entities in group order");
+            grp[i] = uint32_t(plan->entities[i].group);
+        }
+        if ((rc = dev((void**)&a.egroup, grp.size() * 4, grp.data()))) return rc;
+    }
     a.chunk = E->chunk_elems;
-    const bool tma = E->workload == DS_WL_MIX32_TMA || E->engine == DS_ENGINE_STREAM;
-    void* k = E->engine == DS_ENGINE_STREAM ? reinterpret_cast<void*>(k3_stream)
-              : tma                         ? reinterpret_cast<void*>(k3_dynamic<true>)
-                                            : reinterpret_cast<void*>(k3_dynamic<false>);
+    const bool tma = E->workload == DS_WL_MIX32_TMA;
+    void* k = tma ? reinterpret_cast<void*>(k3_dynamic<true>) : reinterpret_cast<void*>(k3_dynamic<false>);
     DS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tma ? kTmaSmem : kNodeSmem));
     E->grid = uint32_t(E->sm_count);
     return DS_OK;
@@ -257,7 +177,6 @@ int build_dynamic(Exec* E, const ds_exec_plan* plan) {
 void* kernel_of(int wl) {
     switch (wl) {
         case DS_WL_AXPY32: return reinterpret_cast<void*>(k2_axpy);
-        case DS_WL_MIX32_BULK: return reinterpret_cast<void*>(k2_mix_bulk);
         case DS_WL_MIX32_TMA: return reinterpret_cast<void*>(k2_mix_tma);
         case DS_WL_MIX32_LDG8: return reinterpret_cast<void*>(k2_mix<8>);
         default: return reinterpret_cast<void*>(k2_mix<4>);
@@ -365,11 +284,6 @@ void destroy(Exec* E) {
     if (E->span) cudaFree(E->span);
     if (E->stamps) cudaFree(E->stamps);
     if (E->smids) cudaFree(E->smids);
-    if (E->d_ents) cudaFree(E->d_ents);
-    if (E->d_preds) cudaFree(E->d_preds);
-    if (E->d_item_off) cudaFree(E->d_item_off);
-    if (E->d_items) cudaFree(E->d_items);
-    if (E->d_done) cudaFree(E->d_done);
     for (void* p : E->dyn_bufs) cudaFree(p);
     if (E->s) cudaStreamDestroy(E->s);
     }
@@ -390,7 +304,7 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
     // group barriers (simulate_scheme: group g+1 starts after all of group g)
     int max_group = -1;
     for (int i = 0; i < n; ++i) max_group = std::max(max_group, int(plan->entities[i].group));
-    const bool barriers = plan->barrier_groups && max_group > 0;
+    const bool barriers = plan->barrier_groups == DS_PLAN_BARRIERS && max_group > 0;
     std::vector<std::vector<int>> members(max_group + 1);
     for (int i = 0; i < n; ++i) {
         if (plan->entities[i].group >= 0) members[plan->entities[i].group].push_back(i);
@@ -447,7 +361,7 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
         if (E->engine == DS_ENGINE_GRAPH_FREE) {  // unconstrained launch shape: CTAs share SMs
             // the shared-memory-staged kernels need their ring (and the TMA
             // one its producer warp): the free launch runs the plain LDG body
-            if (E->workload == DS_WL_MIX32_TMA || E->workload == DS_WL_MIX32_BULK) kp.func = kernel_of(DS_WL_MIX32);
+            if (E->workload == DS_WL_MIX32_TMA) kp.func = kernel_of(DS_WL_MIX32);
             kp.gridDim = dim3(unsigned(e.parallelism) * DS_FREE_CTA_FACTOR);
             kp.blockDim = dim3(256u);
             kp.sharedMemBytes = 0;
@@ -518,7 +432,12 @@ extern "C" {
 
 int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device, void** exec) {
     if (!plan || !cfg || !exec || plan->n_entities < 1 || plan->n_nodes < 1) return fail(DS_EINVAL, "bad plan");
-    if (cfg->workload < DS_WL_MIX32 || cfg->workload > DS_WL_LAST) return fail(DS_EINVAL, "bad workload");
+    if (cfg->workload < DS_WL_MIX32 || cfg->workload > DS_WL_LAST || cfg->workload == 2)
+        return fail(DS_EINVAL, "bad workload");
+    if (plan->barrier_groups < DS_PLAN_DEPS || plan->barrier_groups > DS_PLAN_PRIORITY)
+        return fail(DS_EINVAL, "bad plan ordering mode");
+    if (plan->barrier_groups == DS_PLAN_PRIORITY && cfg->engine != DS_ENGINE_DYNAMIC)
+        return fail(DS_EINVAL, "DS_PLAN_PRIORITY runs on DS_ENGINE_DYNAMIC only (a graph cannot express priorities)");
     const int threads = cfg->block_threads > 0 ? cfg->block_threads : 1024;
     if (threads > 1024 || threads % 32) return fail(DS_EINVAL, "block_threads must be a multiple of 32 <= 1024");
     auto* H = new ExecHandle();
@@ -586,10 +505,7 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
     if (cudaMalloc(&E->replay, sizeof(int)) != cudaSuccess) return bail(fail(DS_ENOMEM, "replay"));
     if (cudaStreamSynchronize(E->s) != cudaSuccess) return bail(fail(DS_ECUDA, "init"));
     E->engine = cfg->engine;
-    if (E->engine == DS_ENGINE_PERSISTENT) {
-        if (E->workload != DS_WL_MIX32) return bail(fail(DS_EINVAL, "persistent engine runs the mix32 workload"));
-        if (int rc = build_persistent(E, &H->P.plan)) return bail(rc);
-    } else if (E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM) {
+    if (E->engine == DS_ENGINE_DYNAMIC) {
         if (E->workload != DS_WL_MIX32 && E->workload != DS_WL_MIX32_TMA)
             return bail(fail(DS_EINVAL, "dynamic engines run the mix32 workloads"));
         if (int rc = build_dynamic(E, &H->P.plan)) return bail(rc);
@@ -640,8 +556,7 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     if (replays < 1 || warmup < 0 || !trace || !trace->span) return fail(DS_EINVAL, "bad run arguments");
     CtxGuard guard(E);
     const bool want_stamps = trace->stamps || trace->smids;
-    const bool persistent =
-        E->engine == DS_ENGINE_PERSISTENT || E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM;
+    const bool persistent = E->engine == DS_ENGINE_DYNAMIC;
     if (replays > E->cap || (!persistent && !E->exec) || (want_stamps && !E->stamps)) {
         if (E->span) cudaFree(E->span);
         if (E->stamps) cudaFree(E->stamps);
@@ -673,7 +588,7 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
     for (auto& e : ev) DS_CUDA(cudaEventCreate(&e));
     for (int r = -warmup; r < replays; ++r) {
         if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
-        if (E->engine == DS_ENGINE_DYNAMIC || E->engine == DS_ENGINE_STREAM) {
+        if (E->engine == DS_ENGINE_DYNAMIC) {
             DArgs da = E->dyn;
             da.rec = r;
             da.stamps = E->stamps;
@@ -682,23 +597,14 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
             da.total = E->total_ctas;
             k3_dyn_reset<<<1, 512, 0, E->s>>>(da);
             if (r >= 0) DS_CUDA(cudaEventRecord(ev[2 * r], E->s));
-            const bool stream = E->engine == DS_ENGINE_STREAM;
-            const bool tma = E->workload == DS_WL_MIX32_TMA || stream;
+            const bool tma = E->workload == DS_WL_MIX32_TMA;
             void* kargs[] = {&da};
+            // cooperative: every CTA (one per SM) resident at once; they wait
+            // on each other's completion counters
             DS_CUDA(cudaLaunchCooperativeKernel(
-                stream ? reinterpret_cast<void*>(k3_stream)
-                : tma  ? reinterpret_cast<void*>(k3_dynamic<true>)
-                       : reinterpret_cast<void*>(k3_dynamic<false>),
+                tma ? reinterpret_cast<void*>(k3_dynamic<true>) : reinterpret_cast<void*>(k3_dynamic<false>),
                 dim3(E->grid), dim3(tma ? unsigned(kTmaThreads) : 1024u), kargs, size_t(tma ? kTmaSmem : kNodeSmem),
                 E->s));
-        } else if (persistent) {
-            PArgs pa{E->d_ents, E->d_preds, E->d_item_off, E->d_items, E->d_done, E->epoch++, r,
-                     E->stamps, E->smids, E->span, E->total_ctas};
-            void* kargs[] = {&pa};
-            // cooperative: all CTAs (one per SM) must be resident together,
-            // they wait on each other's completion counters
-            DS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k3_persistent), dim3(E->grid),
-                                                dim3(unsigned(E->threads)), kargs, size_t(kNodeSmem), E->s));
         } else if (E->engine == DS_ENGINE_STREAMS) {
             // naive multi-stream launch: the host walks the plan in order and
             // launches every entity on its stream after cudaStreamWaitEvent on
@@ -714,21 +620,21 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
             for (int i = 0; i < P.n_entities; ++i) {
                 const ds_exec_entity& e = P.entities[i];
                 cudaStream_t st = E->streams[size_t(i) % ns];
-                if (P.barrier_groups && e.group != prev_group) {
+                if (P.barrier_groups == DS_PLAN_BARRIERS && e.group != prev_group) {
                     prev_members.swap(cur_members);
                     cur_members.clear();
                     prev_group = e.group;
                 }
                 for (uint32_t q = 0; q < e.n_preds; ++q)
                     DS_CUDA(cudaStreamWaitEvent(st, E->ent_ev[P.preds[e.pred_off + q]], 0));
-                if (P.barrier_groups)
+                if (P.barrier_groups == DS_PLAN_BARRIERS)
                     for (int j : prev_members) DS_CUDA(cudaStreamWaitEvent(st, E->ent_ev[j], 0));
                 void* kargs[] = {&E->args[i]};
                 DS_CUDA(cudaLaunchKernel(kernel_of(E->workload), dim3(unsigned(e.parallelism)),
                                          dim3(unsigned(threads_of(E->workload, E->threads))), kargs,
                                          size_t(smem_of(E->workload)), st));
                 DS_CUDA(cudaEventRecord(E->ent_ev[i], st));
-                if (P.barrier_groups) cur_members.push_back(i);
+                if (P.barrier_groups == DS_PLAN_BARRIERS) cur_members.push_back(i);
             }
             for (int i = 0; i < P.n_entities; ++i) DS_CUDA(cudaStreamWaitEvent(E->s, E->ent_ev[i], 0));
             k2_tick<<<1, 1, 0, E->s>>>(E->replay);
@@ -770,7 +676,7 @@ int ds_exec_free(void* exec) {
 int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int block_threads, int reps,
                          float* ms_per_launch, uint64_t* span_ns, int device) {
     if (ctas < 1 || reps < 1 || elems_per_cta < 4) return fail(DS_EINVAL, "bad bench arguments");
-    if (workload < DS_WL_MIX32 || workload > DS_WL_LAST) return fail(DS_EINVAL, "bad workload");
+    if (workload < DS_WL_MIX32 || workload > DS_WL_LAST || workload == 2) return fail(DS_EINVAL, "bad workload");
     const int threads = threads_of(workload, block_threads > 0 ? block_threads : 1024);
     DS_CUDA(cudaSetDevice(device));
     if (int rc = set_attrs(workload)) return rc;
@@ -804,7 +710,6 @@ int ds_node_kernel_bench(int workload, int ctas, uint64_t elems_per_cta, int blo
         a.hi = a.lo + n;
         switch (workload) {
             case DS_WL_AXPY32: k2_axpy<<<ctas, threads, sm>>>(a); break;
-            case DS_WL_MIX32_BULK: k2_mix_bulk<<<ctas, threads, sm>>>(a); break;
             case DS_WL_MIX32_TMA: k2_mix_tma<<<ctas, threads, sm>>>(a); break;
             case DS_WL_MIX32_LDG8: k2_mix<8><<<ctas, threads, sm>>>(a); break;
             default: k2_mix<4><<<ctas, threads, sm>>>(a);

@@ -26,8 +26,10 @@ import numpy as np
 from . import _abi
 from ._lib import check, lib
 
-WL_MIX32, WL_AXPY32, WL_MIX32_BULK, WL_MIX32_TMA, WL_MIX32_LDG8 = 0, 1, 2, 3, 4
-BYTES_PER_ELEM = {WL_MIX32: 8, WL_AXPY32: 12, WL_MIX32_BULK: 8, WL_MIX32_TMA: 8, WL_MIX32_LDG8: 8}
+WL_MIX32, WL_AXPY32, WL_MIX32_TMA, WL_MIX32_LDG8 = 0, 1, 3, 4
+BYTES_PER_ELEM = {WL_MIX32: 8, WL_AXPY32: 12, WL_MIX32_TMA: 8, WL_MIX32_LDG8: 8}
+# ds_exec_plan.barrier_groups (include/dagsched_b200.h DS_PLAN_*)
+PLAN_DEPS, PLAN_BARRIERS, PLAN_PRIORITY = 0, 1, 2
 
 
 class ds_exec_entity(C.Structure):
@@ -47,7 +49,7 @@ class ds_exec_cfg(C.Structure):
                 ("sm_limit", C.c_int32), ("engine", C.c_int32), ("chunk_elems", C.c_int32)]
 
 
-ENGINE_GRAPH, ENGINE_PERSISTENT, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAM, ENGINE_STREAMS = 0, 1, 2, 3, 4, 5
+ENGINE_GRAPH, ENGINE_GRAPH_FREE, ENGINE_DYNAMIC, ENGINE_STREAMS = 0, 2, 3, 5
 FREE_CTA_FACTOR = 4  # DS_FREE_CTA_FACTOR
 
 
@@ -94,7 +96,7 @@ class PlanEntity:
 class Plan:
     entities: list
     node_elems: list
-    barrier_groups: bool
+    barrier_groups: int  # PLAN_DEPS / PLAN_BARRIERS / PLAN_PRIORITY (a bool reads as DEPS / BARRIERS)
     bound_units: Fraction | None = None  # Theorem-1 bound, time units
     n_groups: int = 0
 
@@ -107,7 +109,7 @@ class Plan:
         pa = (C.c_uint32 * max(1, len(preds)))(*preds)
         ne = (C.c_uint64 * len(self.node_elems))(*self.node_elems)
         plan = ds_exec_plan(len(self.entities), len(self.node_elems), C.addressof(ents), C.addressof(pa),
-                            C.addressof(ne), int(self.barrier_groups), 0)
+                            C.addressof(ne), int(self.barrier_groups), 0)  # bool -> DEPS / BARRIERS
         plan._keep = (ents, pa, ne)
         return plan
 
@@ -116,8 +118,18 @@ def node_elements(loads, unit_elems: int):
     return [max(4, int(Fraction(l) * unit_elems)) for l in loads]
 
 
-def plan_from_scheme(scheme, loads, unit_elems: int, barrier_groups: bool = True) -> Plan:
-    """The proposed schedule (scheme.Scheme from ds_schedule_batch)."""
+def plan_from_scheme(scheme, loads, unit_elems: int, barrier_groups: bool = True, mode: int | None = None) -> Plan:
+    """The proposed schedule (scheme.Scheme from ds_schedule_batch).
+
+    mode PLAN_BARRIERS (barrier_groups=True): the augmented graph plus group
+    barriers (simulate_scheme semantics); PLAN_DEPS (barrier_groups=False):
+    the augmented graph alone (original edges + extra dependencies Ē);
+    PLAN_PRIORITY: the precedence edges alone (original edges resolved to
+    segment chains, Ē dropped) — the dynamic engine then enforces the group
+    order by claim priority (include/dagsched_b200.h DS_PLAN_PRIORITY)."""
+    if mode is None:
+        mode = PLAN_BARRIERS if barrier_groups else PLAN_DEPS
+    extra = set(scheme.extra_deps) if mode == PLAN_PRIORITY else set()
     elems = node_elements(loads, unit_elems)
     ordered = []  # group order; launches then members (creation order)
     for g in scheme.groups:
@@ -138,8 +150,9 @@ def plan_from_scheme(scheme, loads, unit_elems: int, barrier_groups: bool = True
             n = int(Fraction(e.load) / Fraction(loads[v]) * elems[v])  # rounded down
             lo, hi = cursor[v], cursor[v] + n
         cursor[v] = hi
-        ents.append(PlanEntity(str(e.id), e.group, e.parallelism, v, [index[p] for p in e.preds], lo, hi, e.exec))
-    return Plan(ents, elems, barrier_groups, scheme.bounds["proposed"], len(scheme.groups))
+        preds = [index[p] for p in e.preds if (p, e.id) not in extra]
+        ents.append(PlanEntity(str(e.id), e.group, e.parallelism, v, preds, lo, hi, e.exec))
+    return Plan(ents, elems, int(mode), scheme.bounds["proposed"], len(scheme.groups))
 
 
 def topo_order(n, edges):
@@ -184,7 +197,7 @@ def plan_baseline(kind: str, loads, edges, sm_count: int, unit_elems: int) -> Pl
             raise ValueError(kind)
         ex = max(Fraction(1), Fraction(loads[v]) * ((m + sm_count - 1) // sm_count) / m)
         ents.append(PlanEntity(str(v), -1, m, v, pr, 0, elems[v], ex))
-    return Plan(ents, elems, False)
+    return Plan(ents, elems, PLAN_DEPS)
 
 
 # ------------------------------------------------------------------ running
@@ -200,8 +213,8 @@ class Executor:
     def __init__(self, plan: Plan, workload: int = WL_MIX32, threads: int = 1024, seed: int = 1, device: int = 0,
                  sm_limit: int = 0, engine: int = ENGINE_GRAPH, chunk_elems: int = 0):
         """sm_limit > 0 runs inside a green context of that many SMs; engine
-        ENGINE_PERSISTENT runs a group-structured plan as one resident CTA per
-        SM with completion counters instead of one kernel per entity."""
+        ENGINE_DYNAMIC runs the plan as one resident CTA per SM claiming
+        entity ranks (the only engine for PLAN_PRIORITY plans)."""
         L = _sig()
         self.plan = plan
         self.workload = workload
@@ -319,8 +332,9 @@ def check_sm_exclusive(plan: Plan, res: RunResult, r: int):
 
 
 def group_overlap_violations(plan: Plan, res: RunResult, r: int):
-    """Entities of group g+1 that started before some entity of group g ended."""
-    if not plan.barrier_groups:
+    """Entities of group g+1 that started before some entity of group g ended
+    (a contract of barrier plans only)."""
+    if int(plan.barrier_groups) != PLAN_BARRIERS:
         return 0
     win = entity_windows(plan, res, r)
     by = {}

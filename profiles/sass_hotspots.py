@@ -16,7 +16,13 @@ def load_ncu(path):
             hdr, rows = row, r[i + 1:]
             break
     iss, iex = hdr.index('Warp Stall Sampling (All Samples)'), hdr.index('Instructions Executed')
-    return [(float(x[iss] or 0), float(x[iex] or 0)) for x in rows if len(x) > iex]
+    out = []
+    for x in rows:
+        try:
+            out.append((float(x[iss] or 0), float(x[iex] or 0)))
+        except (ValueError, IndexError):
+            continue
+    return out
 
 
 def load_sass(path, kernel):

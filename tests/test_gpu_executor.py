@@ -30,7 +30,7 @@ def _scheme_and_loads(dag, M):
     return schemes[0], loads, edges
 
 
-@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_BULK, X.WL_MIX32_TMA, X.WL_MIX32_LDG8])
+@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_TMA, X.WL_MIX32_LDG8])
 @pytest.mark.parametrize("name,dag,M", [("fig2_M8_split", workloads.make_example_task(), 8),
                                         ("c1_fan", workloads.c1_fork_join(), 148),
                                         ("c4", workloads.oversized_dag(1, 148), 148)])
@@ -104,7 +104,7 @@ def test_baselines_run_and_respect_edges(kind):
 
 
 def test_node_kernel_bench_sane():
-    for wl in (X.WL_MIX32, X.WL_MIX32_BULK, X.WL_MIX32_TMA, X.WL_MIX32_LDG8, X.WL_AXPY32):
+    for wl in (X.WL_MIX32, X.WL_MIX32_TMA, X.WL_MIX32_LDG8, X.WL_AXPY32):
         ms, span = X.node_kernel_bench(wl, 148, 1 << 20, reps=5)
         gbs = 148 * (1 << 20) * X.BYTES_PER_ELEM[wl] / (ms * 1e-3) / 1e9
         assert 500 < gbs < 9000, (wl, gbs)
@@ -130,41 +130,26 @@ def test_green_context_partition():
     assert cal["sm_count"] == 16 and cal["tau_us"] > 0
 
 
-@pytest.mark.parametrize("barrier", [True, False])
-def test_persistent_engine(barrier):
-    """DS_ENGINE_PERSISTENT: one resident CTA per SM walking (entity, slice)
-    items with completion counters — outputs bit-exact, contracts hold."""
-    for dag, M in ((workloads.make_example_task(), 8), (workloads.oversized_dag(2, 148), 148),
-                   (workloads.inception_dag(), 148)):
-        s, loads, edges = _scheme_and_loads(dag, M)
-        plan = X.plan_from_scheme(s, loads, UNIT + 5, barrier_groups=barrier)
-        ex = X.Executor(plan, engine=X.ENGINE_PERSISTENT, sm_limit=0 if M == 148 else 8)
-        res = ex.run(8, warmup=2)
-        for r in range(8):
-            assert X.check_precedence(plan, res, r) == []
-            assert X.check_sm_exclusive(plan, res, r) == 0
-            if barrier:
-                assert X.group_overlap_violations(plan, res, r) == 0
-        for v in range(len(loads)):
-            assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
-        ex.close()
-
-
 @pytest.mark.parametrize("engine,workload,chunk", [(X.ENGINE_DYNAMIC, X.WL_MIX32, 0),
                                                    (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA, 0),
                                                    (X.ENGINE_DYNAMIC, X.WL_MIX32, 1000),
-                                                   (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA, 4099),
-                                                   (X.ENGINE_STREAM, X.WL_MIX32_TMA, 0)])
-@pytest.mark.parametrize("barrier", [True, False])
-def test_dynamic_engine(barrier, engine, workload, chunk):
+                                                   (X.ENGINE_DYNAMIC, X.WL_MIX32_TMA, 4099)])
+@pytest.mark.parametrize("mode", [X.PLAN_BARRIERS, X.PLAN_DEPS, X.PLAN_PRIORITY])
+def test_dynamic_engine(mode, engine, workload, chunk):
     """DS_ENGINE_DYNAMIC: resident CTAs claim (entity, rank) items from a
     device-side ready queue — every item runs exactly once per replay, outputs
-    bit-exact, precedence / SM-exclusivity / group-order contracts hold."""
+    bit-exact, precedence / SM-exclusivity / group-order contracts hold; with
+    DS_PLAN_PRIORITY the precedence edges alone order the entities (Ē is
+    replaced by the engine's group-order claiming)."""
+    barrier = mode == X.PLAN_BARRIERS
     cases = [(workloads.make_example_task(), 8), (workloads.oversized_dag(2, 148), 148),
              (workloads.inception_dag(), 148), (workloads.c1_fork_join(), 148)]
     for dag, M in cases:
         s, loads, edges = _scheme_and_loads(dag, M)
-        plan = X.plan_from_scheme(s, loads, UNIT + 5, barrier_groups=barrier)
+        plan = X.plan_from_scheme(s, loads, UNIT + 5, mode=mode)
+        if mode == X.PLAN_PRIORITY:  # no extra dependency edge is left in the plan
+            extra = {(str(a), str(b)) for a, b in s.extra_deps}
+            assert not any((plan.entities[p].name, e.name) in extra for e in plan.entities for p in e.preds)
         ex = X.Executor(plan, workload=workload, engine=engine, sm_limit=0 if M == 148 else 8, chunk_elems=chunk)
         res = ex.run(8, warmup=2)
         for r in range(8):
@@ -182,8 +167,7 @@ def test_dynamic_engine(barrier, engine, workload, chunk):
 def test_dynamic_engine_runs_baseline_plans():
     dag = workloads.inception_dag()
     loads = [l for _, l in dag[0]]
-    for kind, engine in (("serial", X.ENGINE_DYNAMIC), ("multistream", X.ENGINE_DYNAMIC),
-                         ("multistream", X.ENGINE_STREAM)):
+    for kind, engine in (("serial", X.ENGINE_DYNAMIC), ("multistream", X.ENGINE_DYNAMIC)):
         plan = X.plan_baseline(kind, loads, dag[1], 148, 4096 + 7)
         ex = X.Executor(plan, engine=engine, workload=X.WL_MIX32_TMA)
         res = ex.run(5, warmup=1)
@@ -193,7 +177,7 @@ def test_dynamic_engine_runs_baseline_plans():
         ex.close()
 
 
-@pytest.mark.parametrize("workload", [X.WL_MIX32_TMA, X.WL_MIX32_BULK, X.WL_MIX32])
+@pytest.mark.parametrize("workload", [X.WL_MIX32_TMA, X.WL_MIX32])
 def test_free_launch_runs_every_workload(workload):
     """GRAPH_FREE launches 4m 256-thread CTAs without the shared-memory ring:
     the staged workloads run their plain LDG body there (same outputs)."""
@@ -228,3 +212,13 @@ def test_host_streams_engine(workload):
         for v in range(len(lds)):
             assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, pl.node_elems[v])))
         ex.close()
+
+
+def test_priority_plans_need_the_dynamic_engine():
+    """A CUDA graph (or host streams) cannot express claim priorities: a
+    DS_PLAN_PRIORITY plan is refused there instead of running without Ē."""
+    s, loads, edges = _scheme_and_loads(workloads.make_example_task(), 8)
+    plan = X.plan_from_scheme(s, loads, 4096, mode=X.PLAN_PRIORITY)
+    for engine in (X.ENGINE_GRAPH, X.ENGINE_STREAMS):
+        with pytest.raises(_lib.DagschedError):
+            X.Executor(plan, engine=engine)

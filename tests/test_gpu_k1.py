@@ -216,12 +216,11 @@ def test_paper_benchmark_families_vs_oracle(orc):
             assert got == helpers.normalise_scheme(c.scheme(d, M)), (M, d)
 
 
-@pytest.mark.parametrize("kind", ["warp", "coop", "nosort"])
-def test_back_kernel_variants_agree(kind):
-    """DS_K1_BACK=warp / coop (the alternative k1_back kernels) and
-    DS_K1_SORT=0 (walks in index order) give the same results as the default
-    shape-ordered one-lane-per-DAG walk (run in a subprocess: the selection
-    is read once per process)."""
+@pytest.mark.parametrize("kind", ["nosort", "nofast"])
+def test_k1_variants_agree(kind):
+    """DS_K1_SORT=0 (walks in index order) and DS_K1_FAST=0 (no fused fast
+    path: every DAG through k1_front / k1_mid) give the same results as the
+    default (run in a subprocess: the selection is read once per process)."""
     import json
     import os
     import subprocess
@@ -231,8 +230,12 @@ def test_back_kernel_variants_agree(kind):
             "print(json.dumps([int(st.sum()), int(bo.sum() % 1000000007), int(ng.sum()), int(bo2.sum() % 1000000007)]))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for k in ("lane", kind):
-        env = dict(os.environ, DS_K1_BACK=k) if k != "nosort" else dict(os.environ, DS_K1_SORT="0")
+    for k in ("default", kind):
+        env = dict(os.environ)
+        if k == "nosort":
+            env["DS_K1_SORT"] = "0"
+        elif k == "nofast":
+            env["DS_K1_FAST"] = "0"
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]

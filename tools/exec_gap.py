@@ -75,7 +75,7 @@ def main():
     ap.add_argument("--replays", type=int, default=30)
     ap.add_argument("--unit", type=int, default=1 << 17)
     ap.add_argument("--workload", type=int, default=X.WL_MIX32)
-    ap.add_argument("--variants", default="proposed,proposed_deps,persistent_deps,dynamic,dynamic_deps,dynamic_deps_tma,multistream,multistream_tma,dyn_multistream,multistream_free")
+    ap.add_argument("--variants", default="proposed,proposed_deps,dynamic,dynamic_deps,dynamic_deps_tma,multistream,multistream_tma,dyn_multistream,multistream_free")
     ap.add_argument("--sm-limit", type=int, default=0)
     ap.add_argument("--avg-load", type=int, default=20)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "exec_gap.json"))
@@ -95,20 +95,18 @@ def main():
         tot = sum(X.node_elements(loads, args.unit)) * bpe
         row["work_us"] = tot / (peak * 1e3) * 148 / M
         for kind in args.variants.split(","):
-            engine = (X.ENGINE_PERSISTENT if kind.startswith("persistent") else
-                      X.ENGINE_STREAMS if kind.endswith("_host") else
-                      X.ENGINE_STREAM if kind.startswith("str") else
+            engine = (X.ENGINE_STREAMS if kind.endswith("_host") else
                       X.ENGINE_DYNAMIC if kind.startswith("dyn") else
                       X.ENGINE_GRAPH_FREE if kind.endswith("_free") else X.ENGINE_GRAPH)
             chunk = 0
             if "_c" in kind and kind.startswith("dyn"):  # e.g. dynamic_deps_c32768: chunked ranks
                 kind, chunk = kind.split("_c")[0], int(kind.split("_c")[1])
-            wl = X.WL_MIX32_TMA if kind.endswith("_tma") or kind.startswith("str") else args.workload
+            wl = X.WL_MIX32_TMA if kind.endswith("_tma") else args.workload
             kind_ = kind.replace("_tma", "")
-            if kind_.startswith(("proposed", "persistent", "dynamic", "stream")):
+            if kind_.startswith(("proposed", "dynamic")):
                 plan = X.plan_from_scheme(sch, loads, args.unit, barrier_groups=not kind_.endswith("_deps"))
             else:
-                plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("str_", "").replace("_host", ""), loads, edges, M, args.unit)
+                plan = X.plan_baseline(kind_.replace("_free", "").replace("dyn_", "").replace("_host", ""), loads, edges, M, args.unit)
             ex = X.Executor(plan, workload=wl, engine=engine, sm_limit=args.sm_limit, chunk_elems=chunk)
             res = ex.run(args.replays, warmup=3, stamps=True)
             if engine == X.ENGINE_GRAPH_FREE:

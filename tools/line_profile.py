@@ -20,7 +20,7 @@ for i, row in enumerate(r):
     if "Address" in row and "Source" in row:
         h, rows = row, r[i + 1:]
         break
-mangled = {"k1_front": "_ZN2ds8k1_frontILb0EEEvNS_6K1ArgsE", "k1_mid": "_ZN2ds6k1_midILb0EEEvNS_6K1ArgsE",
+mangled = {"k1_fast": "_ZN2ds7k1_fastILb0EEEvNS_6K1ArgsE", "k1_front": "_ZN2ds8k1_frontILb0EEEvNS_6K1ArgsE", "k1_mid": "_ZN2ds6k1_midILb0EEEvNS_6K1ArgsE",
            "k1_back": "_ZN2ds7k1_backILb0EEEvNS_6K1ArgsE",
            "k1_back_lane": "_ZN2ds12k1_back_laneILb0ELi8EEEvNS_6K1ArgsE"}.get(kname, kname)
 ins = sh.load_sass(sass, mangled)

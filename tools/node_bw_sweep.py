@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_20826_b200 import executor as X  # noqa: E402
 
-WLS = {"ldg4": X.WL_MIX32, "ldg8": X.WL_MIX32_LDG8, "bulk4x24k": X.WL_MIX32_BULK, "tma6x32k": X.WL_MIX32_TMA}
+WLS = {"ldg4": X.WL_MIX32, "ldg8": X.WL_MIX32_LDG8, "tma6x32k": X.WL_MIX32_TMA}
 
 
 def placement():
