@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--command", default="")
     ap.add_argument("--version", default="")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--details", default="", help="ncu --page details --csv of the same report (active threads/warp)")
     a = ap.parse_args()
     rows = list(csv.reader(open(a.raw)))
     h, units = rows[0], rows[1]
@@ -36,7 +37,9 @@ def main():
            "division_groups_per_dag": a.div_groups_per_dag, "kernels": {}}
     for r in rows[2:]:
         name = re.sub(r"^void ", "", r[col["Kernel Name"]])
-        name = re.sub(r"<.*", "", name).replace("ds::", "")
+        name = re.sub(r"\(.*", "", name).replace("ds::", "")
+        if not name.startswith("k1_fast"):  # bench.py names k1_fast<32>/<64> by slot count, the rest bare
+            name = re.sub(r"<.*", "", name)
         stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): val(r, k) for k in h
                   if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
         tot = sum(stalls.values()) or 1.0
@@ -59,6 +62,15 @@ def main():
         out["sm_count"] = int(val(r, "device__attribute_multiprocessor_count")) if "device__attribute_multiprocessor_count" in col else 148
         if "sm__cycles_elapsed.avg.per_second" in col and "sm_clock_mhz" not in out:
             out["sm_clock_mhz"] = val(r, "sm__cycles_elapsed.avg.per_second") / 1e6
+    if a.details:
+        for r in csv.reader(open(a.details)):
+            if len(r) > 14 and r[12] in ("Avg. Active Threads Per Warp", "Avg. Not Predicated Off Threads Per Warp"):
+                name = re.sub(r"\(.*", "", re.sub(r"^void ", "", r[4]))
+                if not name.startswith("k1_fast"):
+                    name = re.sub(r"<.*", "", name)
+                key = "threads_per_warp_instr" if "Active" in r[12] else "pred_on_threads_per_warp_instr"
+                if name in out["kernels"]:
+                    out["kernels"][name][key] = float(r[14])
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1)[:3000])
