@@ -428,14 +428,25 @@ def main():
         return run_reference(args)
 
     rank, local_rank, world = env_rank()
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # ranks share the host: cap each rank's OpenMP pool at its share of the cores
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        os.environ["OMP_NUM_THREADS"] = str(max(1, cpu_cores() // local_world))
     import torch
 
-    torch.cuda.set_device(local_rank)
+    # DS_BENCH_SHARE_GPU=1 (test knob): every rank on cuda:0 over gloo, so the
+    # N > 1 code path can be exercised on a one-GPU box
+    share = os.environ.get("DS_BENCH_SHARE_GPU") == "1"
+    dev = 0 if share else local_rank
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
         if dist is not None:
@@ -445,7 +456,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -453,18 +464,20 @@ def main():
 
     n = args.n_dags
     t0 = time.perf_counter()
-    corpus = _lib.Corpus(n, pinned=True, seed=1 + rank * n)
+    # N > 1: each rank generates its shard on its own GPU (K5, bit-identical
+    # to generate_corpus) so N ranks do not contend for the host cores
+    corpus = _lib.Corpus(n, pinned=True, gpu=world > 1, seed=1 + rank * n)
     gen_s = time.perf_counter() - t0
     batch = corpus.batch()
     integer = batch.integer_loads()
 
     # ---------------------------------------------------- device-resident leg
-    sess = _lib.Session(batch, SM_COUNT, 1, _abi.DS_M_ALL, local_rank)
+    sess = _lib.Session(batch, SM_COUNT, 1, _abi.DS_M_ALL, dev)
     for _ in range(args.warmup):
         sess.run()
     barrier()
     per_kernel = {}
-    with Clocks(local_rank) as clk:
+    with Clocks(dev) as clk:
         barrier()
         kms = []
         for _ in range(args.steps):
@@ -500,17 +513,23 @@ def main():
                  torch.empty(batch.edges.shape[0], dtype=torch.int16, pin_memory=True).numpy().view(np.uint16))
         load16, edges16 = batch.compact16(out=pin16)
         cb = batch.as_c16(load16, edges16)
-        call = lambda: L.ds_analyze_batch16(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank)  # noqa: E731
+        call = lambda: L.ds_analyze_batch16(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev)  # noqa: E731
     else:
         cb = batch.as_c()
-        call = lambda: L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), local_rank, None, 0)  # noqa: E731
+        call = lambda: L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev, None, 0)  # noqa: E731
     _lib.check(call())
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         _lib.check(call())
     barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    my_e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(my_e2e_s)
+    per_rank_e2e = [my_e2e_s]
+    if dist is not None:
+        allv = [None] * world
+        dist.all_gather_object(allv, my_e2e_s)
+        per_rank_e2e = allv
     e2e_value = world * n * args.e2e_steps / e2e_s
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
     h2d = (batch.node_off.nbytes + batch.edge_off.nbytes + load16.nbytes + edges16.nbytes if compact
@@ -543,7 +562,7 @@ def main():
     makespan = None
     if rank == 0 and not args.no_makespan:
         try:
-            makespan = makespan_summary(local_rank, args.makespan_replays, n_c2=args.makespan_c2)
+            makespan = makespan_summary(dev, args.makespan_replays, n_c2=args.makespan_c2)
         except Exception as e:  # reported, never required for the headline line
             makespan = {"error": str(e)}
 
@@ -564,7 +583,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": 1e3 * e2e_s / args.e2e_steps, "api": ("ds_analyze_batch16 (16-bit wire form, host pinned)" if compact
                             else "ds_analyze_batch (host pinned)"),
-                    "matches_device_leg": same},
+                    "matches_device_leg": same,
+                    "per_rank_dags_per_s": [n * args.e2e_steps / t for t in per_rank_e2e],
+                    "pcie_bytes_per_rank_per_step": h2d + d2h},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_step, "peak_source": peak_kind,
                          "kernel": dom, "kernel_ms": kmean[dom],

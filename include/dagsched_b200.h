@@ -307,6 +307,18 @@ int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platfor
                            uint32_t method_mask, ds_results* out, const int* devices,
                            int n_devices);
 
+/* ds_analyze_batch16 sharded the same way (the compact wire form: 2.4x fewer
+ * PCIe bytes per device). */
+int ds_analyze_batch16_multi(const ds_dag_batch16* batch, const ds_platform* platform,
+                             uint32_t method_mask, ds_results* out, const int* devices,
+                             int n_devices);
+
+/* The split both multi entry points use: shard i of n_shards owns DAGs
+ * [lo, hi) = [n*i/n_shards, n*(i+1)/n_shards) — the contiguous split of the
+ * reference's OpenMP loop over independent DAGs (experiment.cpp:56-66), and
+ * the per-rank shard of bench.py / shard.py. Host-only, no device needed. */
+int ds_shard_range(uint64_t n_dags, int n_shards, int shard, uint64_t* lo, uint64_t* hi);
+
 /* Full schedule detail — replaces schedule() (scheduler.cpp:175-427) and
  * build_blocks/build_groups (division.cpp:10-126) for a batch; host pointers. */
 int ds_schedule_batch(const ds_dag_batch* batch, const ds_platform* platform,

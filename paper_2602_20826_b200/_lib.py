@@ -39,6 +39,9 @@ def _sig(lib):
                                          P(_abi.ds_results), C.c_int]),
         "ds_analyze_batch_multi": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                              P(_abi.ds_results), P(C.c_int), C.c_int]),
+        "ds_analyze_batch16_multi": (C.c_int, [P(_abi.ds_dag_batch16), P(_abi.ds_platform), C.c_uint32,
+                                               P(_abi.ds_results), P(C.c_int), C.c_int]),
+        "ds_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)]),
         "ds_schedule_batch": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform),
                                         P(_abi.ds_scheme_out), C.c_int]),
         "ds_corpus_generate": (C.c_int, [P(_abi.ds_gen_config), C.c_int64, C.c_uint32, P(C.c_void_p)]),
@@ -149,6 +152,24 @@ def analyze_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = 
     devs = (C.c_int * len(devices))(*devices)
     check(lib().ds_analyze_batch_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
     return _finish(batch, st, b, ng)
+
+
+def analyze16_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int = _abi.DS_M_ALL, min_load=None):
+    """analyze_multi() over the compact 16-bit wire form (ds_analyze_batch16_multi)."""
+    st, b, ng, r = _results(batch.n_dags)
+    load16, edges16 = batch.compact16()
+    cb = batch.as_c16(load16, edges16)
+    pl = platform(sm_count, t_min, min_load)
+    devs = (C.c_int * len(devices))(*devices)
+    check(lib().ds_analyze_batch16_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
+    return _finish(batch, st, b, ng)
+
+
+def shard_range(n_dags: int, n_shards: int, shard: int) -> tuple[int, int]:
+    """The library's contiguous split (ds_shard_range) — host-only."""
+    lo, hi = C.c_uint64(), C.c_uint64()
+    check(lib().ds_shard_range(n_dags, n_shards, shard, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 class Corpus:

@@ -321,6 +321,67 @@ struct DetailBufs {
 
 }  // namespace ds
 
+namespace ds {
+// rank i of N owns DAGs [n*i/N, n*(i+1)/N) (paper_2602_20826_b200/shard.py)
+inline u64 shard_lo(u64 n, int parts, int i) {
+    return u64((unsigned __int128)n * u64(i) / u64(parts));
+}
+
+inline ds_dag_batch sub_batch(const ds_dag_batch* b, u64 lo, u64 hi) {
+    ds_dag_batch sub = *b;
+    const u64 nb = b->node_off[lo] - b->node_off[0], eb = b->edge_off[lo] - b->edge_off[0];
+    sub.n_dags = hi - lo;
+    sub.node_off = b->node_off + lo;
+    sub.edge_off = b->edge_off + lo;
+    sub.load_num = b->load_num + nb;
+    sub.load_den = b->load_den ? b->load_den + nb : nullptr;
+    sub.edges = b->edges + eb;
+    return sub;
+}
+
+inline ds_dag_batch16 sub_batch(const ds_dag_batch16* b, u64 lo, u64 hi) {
+    ds_dag_batch16 sub = *b;
+    sub.n_dags = hi - lo;
+    sub.node_off = b->node_off + lo;
+    sub.edge_off = b->edge_off + lo;
+    sub.load = b->load + (b->node_off[lo] - b->node_off[0]);
+    sub.edges = b->edges + (b->edge_off[lo] - b->edge_off[0]);
+    return sub;
+}
+
+int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev);
+int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev);
+
+// contiguous shards over devices, one host thread per device, no collective
+// (DAGs are independent, experiment.cpp:56-57); results land in DAG order
+template <class Batch>
+int analyze_multi(const Batch* batch, const ds_platform* platform, uint32_t method_mask, ds_results* out,
+                  const int* devices, int n_devices) {
+    if (!batch || !out || !devices || n_devices < 1) return fail(DS_EINVAL, "bad arguments");
+    const u64 n = batch->n_dags;
+    std::vector<int> rcs(n_devices, DS_OK);
+    std::vector<std::string> errs(n_devices);
+    std::vector<std::thread> th;
+    for (int i = 0; i < n_devices; ++i) {
+        const u64 lo = shard_lo(n, n_devices, i), hi = shard_lo(n, n_devices, i + 1);
+        th.emplace_back([&, i, lo, hi] {
+            const Batch sub = sub_batch(batch, lo, hi);  // shifted pointers (relative-index contract)
+            ds_results r = *out;
+            r.status = out->status + lo;
+            r.bounds = out->bounds + 10 * lo;
+            r.n_groups = out->n_groups ? out->n_groups + lo : nullptr;
+            rcs[i] = analyze_one(&sub, platform, method_mask, &r, devices[i]);
+            errs[i] = g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int i = 0; i < n_devices; ++i) {
+        if (rcs[i] != DS_OK) return fail(rcs[i], errs[i]);
+    }
+    return DS_OK;
+}
+}  // namespace ds
+
 using namespace ds;
 
 extern "C" {
@@ -393,42 +454,32 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     return DS_OK;
 }
 
+int ds_shard_range(uint64_t n_dags, int n_shards, int shard, uint64_t* lo, uint64_t* hi) {
+    if (n_shards < 1 || shard < 0 || shard >= n_shards || !lo || !hi) return fail(DS_EINVAL, "bad shard");
+    *lo = shard_lo(n_dags, n_shards, shard);
+    *hi = shard_lo(n_dags, n_shards, shard + 1);
+    return DS_OK;
+}
+
 int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platform, uint32_t method_mask,
                            ds_results* out, const int* devices, int n_devices) {
-    if (!batch || !out || !devices || n_devices < 1) return fail(DS_EINVAL, "bad arguments");
-    const u64 n = batch->n_dags;
-    std::vector<int> rcs(n_devices, DS_OK);
-    std::vector<std::string> errs(n_devices);
-    std::vector<std::thread> th;
-    for (int i = 0; i < n_devices; ++i) {
-        const u64 lo = n * u64(i) / u64(n_devices), hi = n * u64(i + 1) / u64(n_devices);
-        th.emplace_back([&, i, lo, hi] {
-            // contiguous shard = shifted pointers (relative-index contract)
-            ds_dag_batch sub = *batch;
-            sub.n_dags = hi - lo;
-            sub.node_off = batch->node_off + lo;
-            sub.edge_off = batch->edge_off + lo;
-            sub.load_num = batch->load_num + (batch->node_off[lo] - batch->node_off[0]);
-            sub.load_den = batch->load_den ? batch->load_den + (batch->node_off[lo] - batch->node_off[0]) : nullptr;
-            sub.edges = batch->edges + (batch->edge_off[lo] - batch->edge_off[0]);
-            ds_results r = *out;
-            r.status = out->status + lo;
-            r.bounds = out->bounds + 10 * lo;
-            r.n_groups = out->n_groups ? out->n_groups + lo : nullptr;
-            rcs[i] = ds_analyze_batch(&sub, platform, method_mask, &r, devices[i], nullptr, 0);
-            errs[i] = g_err;
-        });
-    }
-    for (auto& t : th) t.join();
-    for (int i = 0; i < n_devices; ++i) {
-        if (rcs[i] != DS_OK) return fail(rcs[i], errs[i]);
-    }
-    return DS_OK;
+    return analyze_multi(batch, platform, method_mask, out, devices, n_devices);
+}
+
+int ds_analyze_batch16_multi(const ds_dag_batch16* batch, const ds_platform* platform, uint32_t method_mask,
+                             ds_results* out, const int* devices, int n_devices) {
+    return analyze_multi(batch, platform, method_mask, out, devices, n_devices);
 }
 
 }  // extern "C"
 
 namespace ds {
+int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
+    return ds_analyze_batch(b, p, mask, r, dev, nullptr, 0);
+}
+int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
+    return ds_analyze_batch16(b, p, mask, r, dev);
+}
 // K1 in detail mode over a host batch; results stay in B (device).
 int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DetailBufs& B) {
     const u64 n = b->n_dags;

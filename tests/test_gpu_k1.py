@@ -138,6 +138,11 @@ def test_session_and_multi_and_device_pointers():
     assert np.array_equal(st, st2) and np.array_equal(bounds, b2) and np.array_equal(ng, ng2)
     st3, b3, _ = _lib.analyze_multi(b, 148, devices=[0, 0, 0])
     assert np.array_equal(st, st3) and np.array_equal(bounds, b3)
+    st4, b4, ng4 = _lib.analyze16_multi(b, 148, devices=[0] * min(4, _lib.device_count() * 4))
+    assert np.array_equal(st, st4) and np.array_equal(bounds, b4) and np.array_equal(ng, ng4)
+    if _lib.device_count() > 1:  # real devices when the box has them
+        st5, b5, _ = _lib.analyze16_multi(b, 148, devices=list(range(_lib.device_count())))
+        assert np.array_equal(st, st5) and np.array_equal(bounds, b5)
     dev = torch.device("cuda:0")
     t = {k: torch.from_numpy(getattr(b, k).view(np.int32) if getattr(b, k).dtype == np.uint32
                              else getattr(b, k)).to(dev) for k in ("node_off", "edge_off", "load_num", "edges")}

@@ -33,7 +33,9 @@ def _worker(rank, world, port, n, out_dir):
     orc = Checker("oracle")
     # (1) shard of a global corpus, as ds_analyze_batch_multi splits it
     full = orc.generate(n, seed=1).pack()
-    lo, hi = shard_bounds(n, world, rank)
+    from paper_2602_20826_b200 import _lib
+    lo, hi = _lib.shard_range(n, world, rank)  # the split capi.cu's multi entry points use
+    assert (lo, hi) == shard_bounds(n, world, rank)
     st, b, _ = orc.corpus(full.slice(lo, hi)).evaluate(148)
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([hi - lo]))
@@ -68,6 +70,19 @@ def test_shard_bounds_partition():
             assert all(a[1] == b[0] for a, b in zip(edges, edges[1:]))
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def test_library_split_equals_shard_py():
+    """ds_shard_range (the split of ds_analyze_batch[16]_multi, capi.cu) is
+    shard.py's split for every rank, including n not divisible by N and
+    n < N, and rejects a bad shard index."""
+    from paper_2602_20826_b200 import _lib
+    for n in (0, 1, 5, 7, 1000, 1_000_003, 2**40 + 17):
+        for world in (1, 2, 3, 7, 8):
+            for r in range(world):
+                assert _lib.shard_range(n, world, r) == shard_bounds(n, world, r)
+    with pytest.raises(_lib.DagschedError):
+        _lib.shard_range(10, 2, 2)
 
 
 def test_world2_gloo_shards_reproduce_single_process(tmp_path):
