@@ -5,10 +5,13 @@
 // written against the reference compiles unchanged: BigInt, Rational,
 // make_rational, parse_rational, floor_to_int, ceil_to_int, to_int64,
 // to_double, format_exact, format_fixed, numerator(), denominator(),
-// .convert_to<T>(), .str(). Implementation is Boost-free: a checked signed
-// __int128 (range +-(2^127 - 1), one bit short of Boost's signed-magnitude
-// 2^128 - 1; out of range -> std::overflow_error) and an always-reduced
-// rational over it. The device twin is csrc/rat.cuh.
+// .convert_to<T>(), .str(). Implementation is Boost-free: a checked
+// signed-magnitude integer over an unsigned __int128 magnitude — Boost's
+// cpp_int_backend<128, 128, signed_magnitude, checked> range +-(2^128 - 1);
+// a result outside it throws std::overflow_error — and an always-reduced
+// rational over it whose + - * / follow Boost.Rational's gcd-first
+// algorithms, so intermediates (and overflow points) match the reference's.
+// The device twin is csrc/rat.cuh.
 #pragma once
 
 #include <cstdint>
@@ -23,46 +26,74 @@ namespace dagsched {
 
 class BigInt {
   public:
+    using u128 = unsigned __int128;
     BigInt() = default;
     template <class T, std::enable_if_t<std::is_integral_v<T>, int> = 0>
-    BigInt(T v) : v_(static_cast<__int128>(v)) {}  // NOLINT (implicit, like Boost)
-
-    static BigInt raw(__int128 v) {
+    BigInt(T v) {  // NOLINT (implicit, like Boost)
+        if constexpr (std::is_signed_v<T>) {
+            if (v < 0) {
+                neg_ = true;
+                mag_ = u128(-(static_cast<long long>(v) + 1)) + 1;
+                return;
+            }
+        }
+        mag_ = static_cast<u128>(v);
+    }
+    static BigInt from_parts(u128 mag, bool neg) {
         BigInt b;
-        b.v_ = v;
+        b.mag_ = mag;
+        b.neg_ = neg && mag != 0;
         return b;
     }
-    __int128 value() const { return v_; }
+    u128 magnitude() const { return mag_; }
+    bool negative() const { return neg_; }
     std::string str() const;
     template <class T>
     T convert_to() const {
-        if constexpr (std::is_floating_point_v<T>) return static_cast<T>(v_);
-        else return v_ > static_cast<__int128>(std::numeric_limits<T>::max())   ? std::numeric_limits<T>::max()
-                    : v_ < static_cast<__int128>(std::numeric_limits<T>::min()) ? std::numeric_limits<T>::min()
-                                                                                : static_cast<T>(v_);
+        if constexpr (std::is_floating_point_v<T>) {
+            const T v = static_cast<T>(mag_);
+            return neg_ ? -v : v;
+        } else {  // saturating, like Boost's conversion of an out-of-range value
+            using L = std::numeric_limits<T>;
+            if (neg_) {
+                if constexpr (std::is_signed_v<T>) {
+                    const u128 lim = u128(-(static_cast<long long>(L::min()) + 1)) + 1;
+                    return mag_ >= lim ? L::min() : static_cast<T>(-static_cast<long long>(mag_));
+                } else {
+                    return 0;
+                }
+            }
+            return mag_ > static_cast<u128>(L::max()) ? L::max() : static_cast<T>(mag_);
+        }
     }
 
     friend BigInt operator+(const BigInt& a, const BigInt& b);
-    friend BigInt operator-(const BigInt& a, const BigInt& b);
+    friend BigInt operator-(const BigInt& a, const BigInt& b) { return a + (-b); }
     friend BigInt operator*(const BigInt& a, const BigInt& b);
     friend BigInt operator/(const BigInt& a, const BigInt& b);
     friend BigInt operator%(const BigInt& a, const BigInt& b);
-    friend BigInt operator-(const BigInt& a) { return BigInt(0) - a; }
+    friend BigInt operator-(const BigInt& a) { return from_parts(a.mag_, !a.neg_); }
     BigInt& operator+=(const BigInt& b) { return *this = *this + b; }
     BigInt& operator-=(const BigInt& b) { return *this = *this - b; }
     BigInt& operator*=(const BigInt& b) { return *this = *this * b; }
     BigInt& operator/=(const BigInt& b) { return *this = *this / b; }
     BigInt& operator++() { return *this += 1; }
     BigInt& operator--() { return *this -= 1; }
-    friend bool operator==(const BigInt& a, const BigInt& b) { return a.v_ == b.v_; }
-    friend bool operator!=(const BigInt& a, const BigInt& b) { return a.v_ != b.v_; }
-    friend bool operator<(const BigInt& a, const BigInt& b) { return a.v_ < b.v_; }
-    friend bool operator>(const BigInt& a, const BigInt& b) { return a.v_ > b.v_; }
-    friend bool operator<=(const BigInt& a, const BigInt& b) { return a.v_ <= b.v_; }
-    friend bool operator>=(const BigInt& a, const BigInt& b) { return a.v_ >= b.v_; }
+    friend int compare(const BigInt& a, const BigInt& b) {
+        if (a.neg_ != b.neg_) return a.neg_ ? -1 : 1;
+        const int c = a.mag_ < b.mag_ ? -1 : (a.mag_ > b.mag_ ? 1 : 0);
+        return a.neg_ ? -c : c;
+    }
+    friend bool operator==(const BigInt& a, const BigInt& b) { return a.neg_ == b.neg_ && a.mag_ == b.mag_; }
+    friend bool operator!=(const BigInt& a, const BigInt& b) { return !(a == b); }
+    friend bool operator<(const BigInt& a, const BigInt& b) { return compare(a, b) < 0; }
+    friend bool operator>(const BigInt& a, const BigInt& b) { return compare(a, b) > 0; }
+    friend bool operator<=(const BigInt& a, const BigInt& b) { return compare(a, b) <= 0; }
+    friend bool operator>=(const BigInt& a, const BigInt& b) { return compare(a, b) >= 0; }
 
   private:
-    __int128 v_ = 0;
+    u128 mag_ = 0;
+    bool neg_ = false;
 };
 
 class Rational {
@@ -77,6 +108,15 @@ class Rational {
                                int> = 0>
     Rational(const A& num, const B& den) {
         set(BigInt(num), BigInt(den));
+    }
+
+    // B200 addition: n/d already in lowest terms with d > 0 (the device's
+    // results are reduced), so no gcd is taken
+    static Rational reduced(const BigInt& n, const BigInt& d) {
+        Rational r;
+        r.n_ = n;
+        r.d_ = d;
+        return r;
     }
 
     const BigInt& num() const { return n_; }

@@ -16,7 +16,7 @@ Rational bound_of(const DagTask& task, const Platform& platform, int slot) {
     ds_results r{&st, bounds, nullptr};
     detail::check(ds_analyze_batch(&b, &pl, 1u << slot, &r, detail::devices().front(), nullptr, 0));
     detail::raise(st, "bound");
-    return Rational(BigInt(bounds[2 * slot]), BigInt(bounds[2 * slot + 1]));
+    return Rational::reduced(BigInt(bounds[2 * slot]), BigInt(bounds[2 * slot + 1]));
 }
 }  // namespace
 
@@ -38,20 +38,17 @@ Rational greedy_unaware_bound(const DagTask& t, const Platform& p) { return boun
 Rational graham_para_bound(const DagTask& t, const Platform& p) { return bound_of(t, p, DS_BOUND_GRAHAM_PARA); }
 Rational lower_bound(const DagTask& t, const Platform& p) { return bound_of(t, p, DS_BOUND_LOWER); }
 
+// One device pass (ds_schedule_batch: K1 in detail mode) yields the schedule
+// and all five bounds; the reference's analyze() runs schedule() and then the
+// four baseline bounds (analysis.cpp:83-99).
 MakespanReport analyze(const DagTask& task, const Platform& platform) {
-    const detail::Packed p = detail::pack({&task});
-    const ds_dag_batch b = p.view();
-    const ds_platform pl = detail::platform_of(platform);
-    int32_t st = 0;
-    int64_t bounds[10] = {};
-    ds_results r{&st, bounds, nullptr};
-    detail::check(ds_analyze_batch(&b, &pl, DS_M_ALL, &r, detail::devices().front(), nullptr, 0));
-    detail::raise(st, "analyze");
-    auto q = [&](int k) { return Rational(BigInt(bounds[2 * k]), BigInt(bounds[2 * k + 1])); };
+    std::vector<int64_t> bounds;
+    const ScheduleScheme s =
+        std::move(detail::schedule_ptrs({&task}, platform, detail::devices().front(), &bounds).front());
+    auto q = [&](int k) { return Rational::reduced(BigInt(bounds[2 * k]), BigInt(bounds[2 * k + 1])); };
     MakespanReport rep;
-    const ScheduleScheme s = schedule(task, platform);
     for (const GroupPlan& g : s.groups) rep.per_group_response.push_back(g.response);
-    rep.proposed = q(DS_BOUND_PROPOSED);
+    rep.proposed = dag_makespan_bound(s);
     rep.greedy = q(DS_BOUND_GREEDY);
     rep.greedy_unaware = q(DS_BOUND_GREEDY_UNAWARE);
     rep.graham_para = q(DS_BOUND_GRAHAM_PARA);

@@ -29,14 +29,19 @@ std::vector<std::vector<Rational>> evaluate_corpus(const std::vector<DagTask>& c
     ds_results r{st.data(), bounds.data(), nullptr};
     const std::vector<int> devs = detail::devices();
     detail::check(ds_analyze_batch_multi(&b, &pl, mask, &r, devs.data(), int(devs.size())));
+    for (std::size_t i = 0; i < corpus.size(); ++i)  // the first failing task, in order
+        if (st[i] != DS_OK) detail::raise(st[i], "evaluate_corpus: task " + std::to_string(i));
     std::vector<std::vector<Rational>> out(corpus.size());
-    for (std::size_t i = 0; i < corpus.size(); ++i) {
-        detail::raise(st[i], "evaluate_corpus: task " + std::to_string(i));
-        for (Method m : methods) {
-            const int k = int(m);
-            out[i].push_back(Rational(BigInt(bounds[10 * i + 2 * k]), BigInt(bounds[10 * i + 2 * k + 1])));
+    detail::parallel_for(corpus.size(), [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            out[i].reserve(methods.size());
+            for (Method m : methods) {
+                const int k = int(m);
+                out[i].push_back(
+                    Rational::reduced(BigInt(bounds[10 * i + 2 * k]), BigInt(bounds[10 * i + 2 * k + 1])));
+            }
         }
-    }
+    });
     return out;
 }
 

@@ -4,6 +4,9 @@
 
 #include "device.hpp"
 
+#include <algorithm>
+#include <mutex>
+
 namespace dagsched {
 
 void GenConfig::check() const {
@@ -26,22 +29,37 @@ std::vector<DagTask> generate_corpus(const GenConfig& c, int count) {
     detail::check(ds_corpus_generate(&g, count, 0, &h));
     ds_dag_batch v;
     ds_corpus_view(h, &v);
-    std::vector<DagTask> out;
-    out.reserve(count);
+    // DagTask::make per DAG on the host's cores (chunks kept in DAG order)
+    std::mutex mu;
+    std::vector<std::pair<std::size_t, std::vector<DagTask>>> done;
     try {
-        for (uint64_t d = 0; d < v.n_dags; ++d) {
-            std::vector<DagNode> nodes;
-            std::vector<std::pair<NodeId, NodeId>> edges;
-            for (uint32_t i = v.node_off[d]; i < v.node_off[d + 1]; ++i)
-                nodes.push_back(DagNode{i - v.node_off[d], Rational(BigInt(v.load_num[i]), BigInt(v.load_den[i]))});
-            for (uint32_t e = v.edge_off[d]; e < v.edge_off[d + 1]; ++e)
-                edges.emplace_back(v.edges[e] >> 16, v.edges[e] & 0xffffu);
-            out.push_back(DagTask::make(std::move(nodes), std::move(edges), std::nullopt, c.t_min));
-        }
+        detail::parallel_for(v.n_dags, [&](std::size_t lo, std::size_t hi) {
+            std::vector<DagTask> mine;
+            mine.reserve(hi - lo);
+            for (std::size_t d = lo; d < hi; ++d) {
+                std::vector<DagNode> nodes;
+                std::vector<std::pair<NodeId, NodeId>> edges;
+                nodes.reserve(v.node_off[d + 1] - v.node_off[d]);
+                edges.reserve(v.edge_off[d + 1] - v.edge_off[d]);
+                for (uint32_t i = v.node_off[d]; i < v.node_off[d + 1]; ++i)
+                    nodes.push_back(
+                        DagNode{i - v.node_off[d], Rational(BigInt(v.load_num[i]), BigInt(v.load_den[i]))});
+                for (uint32_t e = v.edge_off[d]; e < v.edge_off[d + 1]; ++e)
+                    edges.emplace_back(v.edges[e] >> 16, v.edges[e] & 0xffffu);
+                mine.push_back(DagTask::make(std::move(nodes), std::move(edges), std::nullopt, c.t_min));
+            }
+            std::lock_guard<std::mutex> lock(mu);
+            done.emplace_back(lo, std::move(mine));
+        }, 1024);
     } catch (...) {
         ds_corpus_free(h);
         throw;
     }
+    std::sort(done.begin(), done.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<DagTask> out;
+    out.reserve(count);
+    for (auto& [lo, part] : done)
+        for (DagTask& t : part) out.push_back(std::move(t));
     ds_corpus_free(h);
     return out;
 }

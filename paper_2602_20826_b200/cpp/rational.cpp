@@ -6,102 +6,134 @@
 namespace dagsched {
 
 namespace {
-[[noreturn]] void overflow() { throw std::overflow_error("dagsched rational: 128-bit overflow"); }
-__int128 gcd(__int128 a, __int128 b) {
-    if (a < 0) a = -a;
-    if (b < 0) b = -b;
-    while (b) {
-        const __int128 t = a % b;
+using u128 = unsigned __int128;
+[[noreturn]] void overflow(const char* what) { throw std::overflow_error(what); }
+u128 gcd_u(u128 a, u128 b) {
+    // Euclid in 128 bits (software division) only until both fit 64 bits,
+    // then binary gcd on u64 — the common case for every load and bound
+    while (b && ((a >> 64) || (b >> 64))) {
+        const u128 t = a % b;
         a = b;
         b = t;
     }
-    return a;
+    if (b == 0) return a;  // (a may still be wide)
+    std::uint64_t x = std::uint64_t(a), y = std::uint64_t(b);
+    if (x == 0) return y;
+    if (y == 0) return x;
+    const int sh = __builtin_ctzll(x | y);
+    x >>= __builtin_ctzll(x);
+    do {
+        y >>= __builtin_ctzll(y);
+        if (x > y) {
+            const std::uint64_t t = x;
+            x = y;
+            y = t;
+        }
+        y -= x;
+    } while (y);
+    return u128(x) << sh;
 }
+BigInt gcd(const BigInt& a, const BigInt& b) { return BigInt::from_parts(gcd_u(a.magnitude(), b.magnitude()), false); }
+Rational make_raw(const BigInt& n, const BigInt& d);
 }  // namespace
 
 BigInt operator+(const BigInt& a, const BigInt& b) {
-    __int128 r;
-    if (__builtin_add_overflow(a.value(), b.value(), &r)) overflow();
-    return BigInt::raw(r);
-}
-BigInt operator-(const BigInt& a, const BigInt& b) {
-    __int128 r;
-    if (__builtin_sub_overflow(a.value(), b.value(), &r)) overflow();
-    return BigInt::raw(r);
+    if (a.negative() == b.negative()) {
+        const u128 m = a.magnitude() + b.magnitude();
+        if (m < a.magnitude()) overflow("dagsched BigInt: 128-bit addition overflow");
+        return BigInt::from_parts(m, a.negative());
+    }
+    if (a.magnitude() >= b.magnitude()) return BigInt::from_parts(a.magnitude() - b.magnitude(), a.negative());
+    return BigInt::from_parts(b.magnitude() - a.magnitude(), b.negative());
 }
 BigInt operator*(const BigInt& a, const BigInt& b) {
-    __int128 r;
-    if (__builtin_mul_overflow(a.value(), b.value(), &r)) overflow();
-    return BigInt::raw(r);
+    u128 m;
+    if (__builtin_mul_overflow(a.magnitude(), b.magnitude(), &m))
+        overflow("dagsched BigInt: 128-bit multiplication overflow");
+    return BigInt::from_parts(m, a.negative() != b.negative());
 }
-BigInt operator/(const BigInt& a, const BigInt& b) {
-    if (b.value() == 0) throw std::overflow_error("division by zero");
-    return BigInt::raw(a.value() / b.value());
+BigInt operator/(const BigInt& a, const BigInt& b) {  // truncates toward zero
+    if (b.magnitude() == 0) overflow("division by zero");
+    return BigInt::from_parts(a.magnitude() / b.magnitude(), a.negative() != b.negative());
 }
-BigInt operator%(const BigInt& a, const BigInt& b) {
-    if (b.value() == 0) throw std::overflow_error("division by zero");
-    return BigInt::raw(a.value() % b.value());
+BigInt operator%(const BigInt& a, const BigInt& b) {  // sign of the dividend
+    if (b.magnitude() == 0) overflow("division by zero");
+    return BigInt::from_parts(a.magnitude() % b.magnitude(), a.negative());
 }
 
 std::string BigInt::str() const {
-    if (v_ == 0) return "0";
-    unsigned __int128 m = v_ < 0 ? (unsigned __int128)(-(v_ + 1)) + 1 : (unsigned __int128)v_;
+    if (mag_ == 0) return "0";
+    u128 m = mag_;
     std::string s;
     while (m) {
         s.insert(s.begin(), char('0' + int(m % 10)));
         m /= 10;
     }
-    return v_ < 0 ? "-" + s : s;
+    return neg_ ? "-" + s : s;
 }
 
 void Rational::set(BigInt n, BigInt d) {
-    if (d == 0) throw std::overflow_error("division by zero");
+    if (d == 0) overflow("division by zero");
     if (d < 0) {
         n = -n;
         d = -d;
     }
-    const __int128 g = gcd(n.value(), d.value());
     if (n == 0) {
         n_ = 0;
         d_ = 1;
         return;
     }
-    n_ = BigInt::raw(n.value() / g);
-    d_ = BigInt::raw(d.value() / g);
+    const BigInt g = gcd(n, d);
+    n_ = n / g;
+    d_ = d / g;
 }
 
 std::string Rational::str() const { return format_exact(*this); }
 
-// same gcd-first algorithms as Boost.Rational, so intermediates stay small
+namespace {
+Rational make_raw(const BigInt& n, const BigInt& d) { return Rational(n, d); }
+}  // namespace
+
+// Boost.Rational's algorithms: g = gcd(d1, d2); n = n1*(d2/g) + n2*(d1/g);
+// g2 = gcd(n, g); (n/g2) / ((d1/g) * (d2/g2)) — the same intermediates, so a
+// 128-bit overflow happens where the reference's checked backend throws
 Rational operator+(const Rational& a, const Rational& b) {
-    const BigInt g = BigInt::raw(gcd(a.den().value(), b.den().value()));
+    const BigInt g = gcd(a.den(), b.den());
     const BigInt ad = a.den() / g, bd = b.den() / g;
-    return Rational(a.num() * bd + b.num() * ad, a.den() * bd);
+    const BigInt n = a.num() * bd + b.num() * ad;
+    if (n == 0) return Rational();
+    const BigInt g2 = gcd(n, g);
+    return make_raw(n / g2, ad * (b.den() / g2));
 }
 Rational operator-(const Rational& a, const Rational& b) { return a + (-b); }
 Rational operator*(const Rational& a, const Rational& b) {
     if (a.num() == 0 || b.num() == 0) return Rational();
-    const BigInt g1 = BigInt::raw(gcd(a.num().value(), b.den().value()));
-    const BigInt g2 = BigInt::raw(gcd(b.num().value(), a.den().value()));
-    return Rational((a.num() / g1) * (b.num() / g2), (a.den() / g2) * (b.den() / g1));
+    const BigInt g1 = gcd(a.num(), b.den());
+    const BigInt g2 = gcd(b.num(), a.den());
+    return make_raw((a.num() / g1) * (b.num() / g2), (a.den() / g2) * (b.den() / g1));
 }
 Rational operator/(const Rational& a, const Rational& b) {
-    if (b.num() == 0) throw std::overflow_error("division by zero");
-    return a * Rational(b.den(), b.num());
+    if (b.num() == 0) overflow("division by zero");
+    if (a.num() == 0) return Rational();
+    const BigInt g1 = gcd(a.num(), b.num());
+    const BigInt g2 = gcd(b.den(), a.den());
+    return make_raw((a.num() / g1) * (b.den() / g2), (a.den() / g2) * (b.num() / g1));
 }
 
 int compare(const Rational& a, const Rational& b) {
-    // exact without wide products: integer parts first, then the reciprocals
-    // of the fractional parts (ra/ad < rb/bd  <=>  bd/rb < ad/ra)
-    __int128 an = a.num().value(), ad = a.den().value(), bn = b.num().value(), bd = b.den().value();
+    const bool an = a.num().negative(), bn = b.num().negative();
+    if (an != bn) return an ? -1 : 1;
+    // exact on magnitudes without wide products: integer parts first, then
+    // the reciprocals of the fractional parts (ra/ad < rb/bd <=> bd/rb < ad/ra)
+    u128 xn = a.num().magnitude(), xd = a.den().magnitude(), yn = b.num().magnitude(), yd = b.den().magnitude();
+    int sign = an ? -1 : 1;
     for (;;) {
-        __int128 qa = an / ad, ra = an % ad, qb = bn / bd, rb = bn % bd;
-        if (ra < 0) --qa, ra += ad;
-        if (rb < 0) --qb, rb += bd;
-        if (qa != qb) return qa < qb ? -1 : 1;
-        if (ra == 0 || rb == 0) return (ra == 0 && rb == 0) ? 0 : (ra == 0 ? -1 : 1);
-        const __int128 n1 = bd, d1 = rb, n2 = ad, d2 = ra;
-        an = n1, ad = d1, bn = n2, bd = d2;
+        const u128 qx = xn / xd, rx = xn % xd, qy = yn / yd, ry = yn % yd;
+        if (qx != qy) return qx < qy ? -sign : sign;
+        if (rx == 0 || ry == 0) return (rx == 0 && ry == 0) ? 0 : (rx == 0 ? -sign : sign);
+        // rx/xd < ry/yd  <=>  xd/rx > yd/ry: recurse on the reciprocals, order flipped
+        xn = xd, xd = rx, yn = yd, yd = ry;
+        sign = -sign;
     }
 }
 

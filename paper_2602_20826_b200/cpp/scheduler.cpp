@@ -228,10 +228,10 @@ std::vector<NodeId> parallel_candidates(const std::vector<NodeId>& group, const 
     return out;
 }
 
-std::vector<ScheduleScheme> schedule_batch(const std::vector<DagTask>& tasks, const Platform& platform, int device) {
-    std::vector<const DagTask*> ptrs;
-    for (const DagTask& t : tasks) ptrs.push_back(&t);
-    const detail::Packed p = detail::pack(ptrs);
+namespace detail {
+std::vector<ScheduleScheme> schedule_ptrs(const std::vector<const DagTask*>& tasks, const Platform& platform,
+                                          int device, std::vector<int64_t>* bounds) {
+    const detail::Packed p = detail::pack(tasks);
     const ds_dag_batch b = p.view();
     const ds_platform pl = detail::platform_of(platform);
     const std::size_t nd = tasks.size(), N = p.num.size();
@@ -239,20 +239,29 @@ std::vector<ScheduleScheme> schedule_batch(const std::vector<DagTask>& tasks, co
     std::vector<uint16_t> ne(nd), ng(nd), ndv(nd);
     std::vector<ds_entity_rec> ents(std::max<std::size_t>(2 * N, 1));
     std::vector<ds_group_rec> grps(std::max<std::size_t>(N, 1));
+    if (bounds) bounds->assign(nd * 10, 0);
     ds_scheme_out out{st.data(), ne.data(), ng.data(), ndv.data(), nullptr, nullptr, ents.data(), grps.data(),
-                      nullptr};
+                      bounds ? bounds->data() : nullptr};
     detail::check(ds_schedule_batch(&b, &pl, &out, device));
     std::vector<ScheduleScheme> res;
+    res.reserve(nd);
     for (std::size_t d = 0; d < nd; ++d) {
         detail::raise(st[d], "schedule: task " + std::to_string(d));
         const std::size_t n0 = p.node_off[d];
-        res.push_back(materialise(tasks[d], platform, ents.data() + 2 * n0, ne[d], grps.data() + n0, ng[d]));
+        res.push_back(materialise(*tasks[d], platform, ents.data() + 2 * n0, ne[d], grps.data() + n0, ng[d]));
     }
     return res;
 }
+}  // namespace detail
+
+std::vector<ScheduleScheme> schedule_batch(const std::vector<DagTask>& tasks, const Platform& platform, int device) {
+    std::vector<const DagTask*> ptrs;
+    for (const DagTask& t : tasks) ptrs.push_back(&t);
+    return detail::schedule_ptrs(ptrs, platform, device, nullptr);
+}
 
 ScheduleScheme schedule(const DagTask& task, const Platform& platform) {
-    return std::move(schedule_batch({task}, platform, detail::devices().front()).front());
+    return std::move(detail::schedule_ptrs({&task}, platform, detail::devices().front(), nullptr).front());
 }
 
 }  // namespace dagsched

@@ -28,7 +28,8 @@ namespace ds {
 // k4_validate.cu
 void k4_launch(u64 n_dags, const u32* node_off, const int32_t* status, const uint16_t* n_groups,
                const ds_group_rec* groups, const ds_entity_rec* ents, const int64_t* bounds, int samples,
-               long long lo, long long hi, u64 seed, unsigned char* over, double* ratio, int32_t* st);
+               long long lo, long long hi, u64 seed, unsigned char* over, double* ratio, int32_t* st,
+               cudaStream_t stream);
 
 thread_local std::string g_err;
 
@@ -132,12 +133,57 @@ __global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __r
     }
 }
 
+// pinned host staging (grows, never shrinks)
+struct PinBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 4096);
+        if (bytes <= cap) return DS_OK;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        DS_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+        cap = bytes;
+        return DS_OK;
+    }
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    ~PinBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+// Schedule-detail pass (ds_schedule_batch / ds_validate_batch): inputs and
+// outputs each live in one device arena carved per call, crossing PCIe as ONE
+// pinned copy each way, so a single-DAG call (the kept C++ API's schedule()
+// and analyze()) costs one H2D, the K1 launches and one D2H — no allocation.
+struct DetailView {
+    u32 *node_off, *edge_off, *edges;
+    u64 *ln, *ldn;
+    int32_t* status;
+    uint16_t *ne, *ng, *nd;
+    int16_t *nb, *ndg;
+    ds_entity_rec* ent;
+    ds_group_rec* grp;
+    int64_t* bounds;
+    size_t out_bytes;
+    size_t o_status, o_ne, o_ng, o_nd, o_nb, o_ndg, o_ent, o_grp, o_bounds;  // offsets in the out arena
+};
+struct DetailCtx {
+    DevBuf in, out, retry, retry_count, k4_over, k4_ratio, k4_st;
+    PinBuf in_stage, out_stage;
+    DetailView v{};
+};
+
 constexpr int kMaxSlots = 8;
 struct DeviceCtx {
     std::mutex mu;
     bool init = false;
     Slot slot[kMaxSlots];
     DevBuf retry, retry_count, handoff;  // scratch for the device-pointer entry point
+    DetailCtx det;
 };
 
 // The bounds pass runs as k1_front + k1_back (K1Handoff) unless DS_K1_SPLIT=0
@@ -315,9 +361,6 @@ int upload(const ds_dag_batch* b, Holder& H, cudaStream_t s) {
     return DS_OK;
 }
 
-struct DetailBufs {
-    DevBuf node_off, edge_off, ln, ldn, edges, status, ne, ng, nd, nb, ndg, ent, grp, bounds, retry, retry_count;
-};
 
 }  // namespace ds
 
@@ -480,54 +523,95 @@ int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_r
 int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
     return ds_analyze_batch16(b, p, mask, r, dev);
 }
-// K1 in detail mode over a host batch; results stay in B (device).
-int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DetailBufs& B) {
+// K1 in detail mode over a host batch; results stay in the device context's
+// out arena (ctx.det.v). The caller holds ctx.mu and the stream slot 0.
+int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx& ctx) {
     const u64 n = b->n_dags;
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
     if (int rc = configure(device, true, occ)) return rc;
-    cudaStream_t s = nullptr;
-    if (int rc = upload(b, B, s)) return rc;
-    const u64 N = b->node_off[n] - b->node_off[0];
-    if (int rc = B.status.ensure(n * 4)) return rc;
-    if (int rc = B.ne.ensure(n * 2)) return rc;
-    if (int rc = B.ng.ensure(n * 2)) return rc;
-    if (int rc = B.nd.ensure(n * 2)) return rc;
-    if (int rc = B.nb.ensure(N * 2)) return rc;
-    if (int rc = B.ndg.ensure(N * 2)) return rc;
-    if (int rc = B.ent.ensure(2 * N * sizeof(ds_entity_rec))) return rc;
-    if (int rc = B.grp.ensure(N * sizeof(ds_group_rec))) return rc;
-    if (int rc = B.bounds.ensure(n * 80)) return rc;
-    if (int rc = B.retry.ensure(2 * n * 4)) return rc;
-    if (int rc = B.retry_count.ensure(kK1Counters * 4)) return rc;
-    DS_CUDA(cudaMemset(B.nb.p, 0xff, N * 2));
-    DS_CUDA(cudaMemset(B.ndg.p, 0xff, N * 2));
-    DS_CUDA(cudaMemset(B.ent.p, 0, 2 * N * sizeof(ds_entity_rec)));
-    DS_CUDA(cudaMemset(B.grp.p, 0, N * sizeof(ds_group_rec)));
+    if (!ctx.init) {
+        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        ctx.init = true;
+    }
+    cudaStream_t s = ctx.slot[0].s;
+    DetailCtx& D = ctx.det;
+    DetailView& v = D.v;
+    const u32 nb0 = b->node_off[0], eb0 = b->edge_off[0];
+    const u64 N = b->node_off[n] - nb0, E = b->edge_off[n] - eb0;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    // ---- inputs: rebased offsets, loads, edges in one pinned stage -> one H2D
+    const size_t i_no = 0, i_eo = al(i_no + (n + 1) * 4), i_ln = al(i_eo + (n + 1) * 4), i_ld = al(i_ln + N * 8),
+                 i_ed = al(i_ld + (b->load_den ? N * 8 : 0)), in_bytes = al(i_ed + E * 4);
+    if (int rc = D.in_stage.ensure(in_bytes)) return rc;
+    if (int rc = D.in.ensure(in_bytes)) return rc;
+    char* st = static_cast<char*>(D.in_stage.p);
+    u32* no = reinterpret_cast<u32*>(st + i_no);
+    u32* eo = reinterpret_cast<u32*>(st + i_eo);
+    for (u64 i = 0; i <= n; ++i) {
+        no[i] = b->node_off[i] - nb0;
+        eo[i] = b->edge_off[i] - eb0;
+    }
+    std::memcpy(st + i_ln, b->load_num, N * 8);
+    if (b->load_den) std::memcpy(st + i_ld, b->load_den, N * 8);
+    std::memcpy(st + i_ed, b->edges, E * 4);
+    DS_CUDA(cudaMemcpyAsync(D.in.p, st, in_bytes, cudaMemcpyHostToDevice, s));
+    char* di = static_cast<char*>(D.in.p);
+    v.node_off = reinterpret_cast<u32*>(di + i_no);
+    v.edge_off = reinterpret_cast<u32*>(di + i_eo);
+    v.ln = reinterpret_cast<u64*>(di + i_ln);
+    v.ldn = b->load_den ? reinterpret_cast<u64*>(di + i_ld) : nullptr;
+    v.edges = reinterpret_cast<u32*>(di + i_ed);
+    // ---- outputs: one arena; node_block/node_div_group (0xff) and entity /
+    // group records (0) are adjacent so two memsets initialise them
+    v.o_nb = 0;
+    v.o_ndg = v.o_nb + N * 2;
+    v.o_ent = al(v.o_ndg + N * 2);
+    v.o_grp = v.o_ent + 2 * N * sizeof(ds_entity_rec);
+    v.o_status = al(v.o_grp + N * sizeof(ds_group_rec));
+    v.o_ne = al(v.o_status + n * 4);
+    v.o_ng = al(v.o_ne + n * 2);
+    v.o_nd = al(v.o_ng + n * 2);
+    v.o_bounds = al(v.o_nd + n * 2);
+    v.out_bytes = al(v.o_bounds + n * 80);
+    if (int rc = D.out.ensure(v.out_bytes)) return rc;
+    if (int rc = D.retry.ensure(2 * n * 4)) return rc;
+    if (int rc = D.retry_count.ensure(kK1Counters * 4)) return rc;
+    char* dout = static_cast<char*>(D.out.p);
+    v.nb = reinterpret_cast<int16_t*>(dout + v.o_nb);
+    v.ndg = reinterpret_cast<int16_t*>(dout + v.o_ndg);
+    v.ent = reinterpret_cast<ds_entity_rec*>(dout + v.o_ent);
+    v.grp = reinterpret_cast<ds_group_rec*>(dout + v.o_grp);
+    v.status = reinterpret_cast<int32_t*>(dout + v.o_status);
+    v.ne = reinterpret_cast<uint16_t*>(dout + v.o_ne);
+    v.ng = reinterpret_cast<uint16_t*>(dout + v.o_ng);
+    v.nd = reinterpret_cast<uint16_t*>(dout + v.o_nd);
+    v.bounds = reinterpret_cast<int64_t*>(dout + v.o_bounds);
+    DS_CUDA(cudaMemsetAsync(dout + v.o_nb, 0xff, N * 4, s));
+    DS_CUDA(cudaMemsetAsync(dout + v.o_ent, 0, v.o_status - v.o_ent, s));
     K1Args a{};
     a.n_dags = n;
-    a.node_off = B.node_off.as<const u32>();
-    a.edge_off = B.edge_off.as<const u32>();
-    a.load_num = B.ln.as<const u64>();
-    a.load_den = b->load_den ? B.ldn.as<const u64>() : nullptr;
-    a.edges = B.edges.as<const u32>();
+    a.node_off = v.node_off;
+    a.edge_off = v.edge_off;
+    a.load_num = v.ln;
+    a.load_den = v.ldn;
+    a.edges = v.edges;
     a.plat = P;
     a.mask = DS_M_ALL;
-    a.det.status = B.status.as<int32_t>();
-    a.det.n_entities = B.ne.as<uint16_t>();
-    a.det.n_groups = B.ng.as<uint16_t>();
-    a.det.n_div_groups = B.nd.as<uint16_t>();
-    a.det.node_block = B.nb.as<int16_t>();
-    a.det.node_div_group = B.ndg.as<int16_t>();
-    a.det.entities = B.ent.as<ds_entity_rec>();
-    a.det.groups = B.grp.as<ds_group_rec>();
-    a.det.bounds = B.bounds.as<int64_t>();
-    a.retry = B.retry.as<u32>();
-    a.retry_count = B.retry_count.as<u32>();
+    a.det.status = v.status;
+    a.det.n_entities = v.ne;
+    a.det.n_groups = v.ng;
+    a.det.n_div_groups = v.nd;
+    a.det.node_block = v.nb;
+    a.det.node_div_group = v.ndg;
+    a.det.entities = v.ent;
+    a.det.groups = v.grp;
+    a.det.bounds = v.bounds;
+    a.retry = D.retry.as<u32>();
+    a.retry_count = D.retry_count.as<u32>();
     a.retry2 = a.retry + n;
     a.retry2_count = a.retry_count + 1;
     DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, 0, n), true, s));
-    DS_CUDA(cudaDeviceSynchronize());
     return DS_OK;
 }
 }  // namespace ds
@@ -540,19 +624,30 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     if (int rc = check_platform(platform, P)) return rc;
     const u64 n = b->n_dags;
     if (n == 0) return DS_OK;
-    DetailBufs B;
-    if (int rc = run_detail(b, P, device, B)) return rc;
+    DeviceCtx& ctx = device_ctx(device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    if (int rc = run_detail(b, P, device, ctx)) return rc;
+    DetailCtx& D = ctx.det;
+    const DetailView& v = D.v;
+    cudaStream_t s = ctx.slot[0].s;
+    // one D2H of the whole out arena, then host copies into the caller's arrays
+    if (int rc = D.out_stage.ensure(v.out_bytes)) return rc;
+    DS_CUDA(cudaMemcpyAsync(D.out_stage.p, D.out.p, v.out_bytes, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaStreamSynchronize(s));
+    const char* h = static_cast<const char*>(D.out_stage.p);
     const u64 N = b->node_off[n] - b->node_off[0];
-    if (out->status) DS_CUDA(cudaMemcpy(out->status, B.status.p, n * 4, cudaMemcpyDeviceToHost));
-    if (out->n_entities) DS_CUDA(cudaMemcpy(out->n_entities, B.ne.p, n * 2, cudaMemcpyDeviceToHost));
-    if (out->n_groups) DS_CUDA(cudaMemcpy(out->n_groups, B.ng.p, n * 2, cudaMemcpyDeviceToHost));
-    if (out->n_div_groups) DS_CUDA(cudaMemcpy(out->n_div_groups, B.nd.p, n * 2, cudaMemcpyDeviceToHost));
-    if (out->node_block) DS_CUDA(cudaMemcpy(out->node_block, B.nb.p, N * 2, cudaMemcpyDeviceToHost));
-    if (out->node_div_group) DS_CUDA(cudaMemcpy(out->node_div_group, B.ndg.p, N * 2, cudaMemcpyDeviceToHost));
-    if (out->entities)
-        DS_CUDA(cudaMemcpy(out->entities, B.ent.p, 2 * N * sizeof(ds_entity_rec), cudaMemcpyDeviceToHost));
-    if (out->groups) DS_CUDA(cudaMemcpy(out->groups, B.grp.p, N * sizeof(ds_group_rec), cudaMemcpyDeviceToHost));
-    if (out->bounds) DS_CUDA(cudaMemcpy(out->bounds, B.bounds.p, n * 80, cudaMemcpyDeviceToHost));
+    auto put = [&](void* dst, size_t off, size_t bytes) {
+        if (dst) std::memcpy(dst, h + off, bytes);
+    };
+    put(out->status, v.o_status, n * 4);
+    put(out->n_entities, v.o_ne, n * 2);
+    put(out->n_groups, v.o_ng, n * 2);
+    put(out->n_div_groups, v.o_nd, n * 2);
+    put(out->node_block, v.o_nb, N * 2);
+    put(out->node_div_group, v.o_ndg, N * 2);
+    put(out->entities, v.o_ent, 2 * N * sizeof(ds_entity_rec));
+    put(out->groups, v.o_grp, N * sizeof(ds_group_rec));
+    put(out->bounds, v.o_bounds, n * 80);
     return DS_OK;
 }
 
@@ -574,23 +669,26 @@ int ds_validate_batch(const ds_dag_batch* b, const ds_platform* platform, int sa
     }
     const u64 n = b->n_dags;
     if (n == 0) return DS_OK;
-    DetailBufs B;
-    if (int rc = run_detail(b, P, device, B)) return rc;
+    DeviceCtx& ctx = device_ctx(device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    if (int rc = run_detail(b, P, device, ctx)) return rc;
+    DetailCtx& D = ctx.det;
+    const DetailView& v = D.v;
+    cudaStream_t s = ctx.slot[0].s;
     const u64 per = u64(samples) + 1, T = n * per;
-    DevBuf over, ratio, st;
-    if (int rc = over.ensure(T)) return rc;
-    if (int rc = ratio.ensure(T * 8)) return rc;
-    if (int rc = st.ensure(T * 4)) return rc;
-    k4_launch(n, B.node_off.as<const u32>(), B.status.as<int32_t>(), B.ng.as<uint16_t>(), B.grp.as<ds_group_rec>(),
-              B.ent.as<ds_entity_rec>(), B.bounds.as<int64_t>(), samples, lo, hi, seed, over.as<unsigned char>(),
-              ratio.as<double>(), st.as<int32_t>());
+    if (int rc = D.k4_over.ensure(T)) return rc;
+    if (int rc = D.k4_ratio.ensure(T * 8)) return rc;
+    if (int rc = D.k4_st.ensure(T * 4)) return rc;
+    k4_launch(n, v.node_off, v.status, v.ng, v.grp, v.ent, v.bounds, samples, lo, hi, seed,
+              D.k4_over.as<unsigned char>(), D.k4_ratio.as<double>(), D.k4_st.as<int32_t>(), s);
     DS_CUDA(cudaGetLastError());
     std::vector<unsigned char> h_over(T);
     std::vector<double> h_ratio(T);
     std::vector<int32_t> h_st(T);
-    DS_CUDA(cudaMemcpy(h_over.data(), over.p, T, cudaMemcpyDeviceToHost));
-    DS_CUDA(cudaMemcpy(h_ratio.data(), ratio.p, T * 8, cudaMemcpyDeviceToHost));
-    DS_CUDA(cudaMemcpy(h_st.data(), st.p, T * 4, cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaMemcpyAsync(h_over.data(), D.k4_over.p, T, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaMemcpyAsync(h_ratio.data(), D.k4_ratio.p, T * 8, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaMemcpyAsync(h_st.data(), D.k4_st.p, T * 4, cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaStreamSynchronize(s));
     // experiment.cpp:179-239 reductions, in the same order (samples, then tasks)
     ds_validation sum{int64_t(n), int64_t(n * per), 0, 0.0, 0.0};
     double worst_sum = 0.0, scaled_total = 0.0;

@@ -29,6 +29,22 @@ def test_reference_unit_tests_against_this_api(binary):
     assert "failed: 0" in r.stdout
 
 
+REF = os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF, "ref_rational_check")), reason="oracle/_ref not built")
+def test_rational_edge_cases_match_reference():
+    """tests/cpp/rational_check.cpp built against the reference's rational
+    (Boost 128-bit checked signed-magnitude, via oracle/shim) and against the
+    kept API: identical values and identical overflow points, including the
+    full +-(2^128 - 1) range and Boost.Rational's gcd-first intermediates."""
+    ref = subprocess.run([os.path.join(REF, "ref_rational_check")], capture_output=True, text=True, timeout=60)
+    api = subprocess.run([os.path.join(LIB, "api_rational_check")], capture_output=True, text=True, timeout=60)
+    assert ref.returncode == 0 and api.returncode == 0, ref.stderr + api.stderr
+    assert "2^128-1: 340282366920938463463374607431768211455" in api.stdout
+    assert api.stdout == ref.stdout
+
+
 @pytest.mark.gpu
 def test_cpp_api_parity_with_reference_goldens():
     r = subprocess.run([os.path.join(LIB, "api_parity")], capture_output=True, text=True, timeout=600)
