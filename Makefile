@@ -49,7 +49,7 @@ CPP_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(LIBDIR)/cpp_%.o,$(CPP_SRCS))
 API_INC  := -Iinclude -I$(PKG)/cpp
 REFPROJ  ?= /root/reference/proj
 
-cppapi: $(LIBDIR)/libdagsched_cpp.so $(LIBDIR)/api_parity $(LIBDIR)/api_division_dump $(LIBDIR)/api_bench $(LIBDIR)/api_rational_check $(if $(wildcard $(REFPROJ)/tests),$(LIBDIR)/api_test_dag_model $(LIBDIR)/api_test_exec_model)
+cppapi: $(LIBDIR)/libdagsched_cpp.so $(LIBDIR)/api_parity $(LIBDIR)/api_division_dump $(LIBDIR)/api_bench $(LIBDIR)/api_rational_check $(LIBDIR)/api_drivers_dump $(if $(wildcard $(REFPROJ)/tests),$(LIBDIR)/api_test_dag_model $(LIBDIR)/api_test_exec_model)
 
 $(LIBDIR)/cpp_%.o: $(PKG)/cpp/%.cpp $(wildcard include/dagsched/*.hpp) $(PKG)/cpp/device.hpp include/dagsched_b200.h
 	@mkdir -p $(LIBDIR)
@@ -62,6 +62,9 @@ $(LIBDIR)/api_parity: tests/cpp/api_parity.cpp $(LIBDIR)/libdagsched_cpp.so
 	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(LIBDIR)/api_rational_check: tests/cpp/rational_check.cpp $(LIBDIR)/libdagsched_cpp.so
+	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
+
+$(LIBDIR)/api_drivers_dump: tests/cpp/drivers_dump.cpp $(LIBDIR)/libdagsched_cpp.so
 	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(LIBDIR)/api_bench: tests/cpp/api_bench.cpp $(LIBDIR)/libdagsched_cpp.so

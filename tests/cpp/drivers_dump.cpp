@@ -1,0 +1,218 @@
+// §8(f) drivers through the C++ API — the SAME source compiles against the
+// reference's headers and library (oracle/_ref/ref_drivers_dump: its own CPU
+// code) and against the kept API (api_drivers_dump: K1/K4/K6 on the GPU), and
+// tests/test_cpp_drivers.py requires the two outputs to be identical:
+//   task_io     read_task (strings, integers, JSON floats, errors), write_task,
+//               write_scheme, write_trace  (task_io.cpp:16-157)
+//   simulator   simulate_scheme worst/scaled, simulate_greedy fifo/random,
+//               check_capacity / check_precedence  (simulator.cpp:44-224)
+//   experiment  run_experiment + write_csv, run_validation (summary doubles
+//               as exact bit patterns), run_benchmarks + write_bench_table
+//               (experiment.cpp:81-307)
+//
+// usage: drivers_dump <fixture dir> [--host-only]   (host-only: task_io parts
+//        that need no device: parse, validate, write_task)
+//        drivers_dump <fixture dir> --experiment N   (an M sweep at corpus size N)
+#include "dagsched/experiment.hpp"
+#include "dagsched/scheduler.hpp"
+#include "dagsched/simulator.hpp"
+#include "dagsched/task_io.hpp"
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+using namespace dagsched;
+
+namespace {
+
+void section(const std::string& s) { std::cout << "== " << s << "\n"; }
+
+void guarded(const std::string& what, const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const ValidationError& e) {
+        std::cout << what << ": ValidationError: " << e.what() << "\n";
+    } catch (const std::overflow_error& e) {
+        std::cout << what << ": overflow_error\n";
+    } catch (const std::invalid_argument& e) {
+        std::cout << what << ": invalid_argument\n";
+    } catch (const std::logic_error& e) {
+        std::cout << what << ": logic_error: " << e.what() << "\n";
+    } catch (const std::exception& e) {
+        std::cout << what << ": exception\n";  // parse / type errors (library-specific text)
+    }
+}
+
+std::string hexd(double x) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%a", x);
+    return b;
+}
+
+DagTask parse(const std::string& text) {
+    std::istringstream in(text);
+    return read_task(in);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: drivers_dump <fixture dir> [--host-only]\n");
+        return 2;
+    }
+    const std::string dir = argv[1];
+    const bool host_only = argc > 2 && std::strcmp(argv[2], "--host-only") == 0;
+    if (argc > 3 && std::strcmp(argv[2], "--experiment") == 0) {  // one M sweep at a given corpus size
+        ExperimentSpec spec;
+        spec.values = {4, 8, 32, 148};
+        spec.corpus_size = std::atoi(argv[3]);
+        guarded("sweep M", [&] { write_csv(run_experiment(spec), std::cout); });
+        return 0;
+    }
+    const std::vector<std::string> fixtures = {dir + "/fig2.json", dir + "/diamond.json", dir + "/fork_join.json",
+                                               dir + "/inception.json"};
+
+    section("read_task / write_task");
+    for (const std::string& f : fixtures) {
+        guarded(f, [&] {
+            const DagTask t = read_task_file(f);
+            write_task(t, std::cout, 42);
+        });
+    }
+    const char* cases[] = {
+        R"({"nodes": [{"id": 1, "load": 7.5}, {"id": 2, "load": "15/2"}], "edges": [[1, 2]]})",
+        R"({"nodes": [{"id": 1, "load": 0.1}, {"id": 2, "load": 3}], "edges": [[1, 2]], "period": "40"})",
+        R"({"nodes": [{"id": 1, "load": 1e-05}, {"id": 2, "load": 3}], "edges": [[1, 2]]})",
+        R"({"nodes": [{"id": 1, "load": "7.x"}], "edges": []})",
+        R"({"nodes": [{"id": 1, "load": true}], "edges": []})",
+        R"({"nodes": [{"id": 1, "load": 2}], "edges": [[1]]})",
+        R"({"nodes": [{"id": 1, "load": 2}]})",
+        R"({"nodes": [{"id": 1, "load": 2}, {"id": 2, "load": 2}], "edges": [[1, 2], [2, 1]]})",
+        R"({"nodes": [{"id": 1, "load": 2}, {"id": 2, "load": 2}], "edges": [[1, 3]]})",
+        R"({"nodes": [{"id": 1, "load": 0.5}], "edges": []})",
+        R"({"nodes": [{"id": 5, "load": "1"}], "edges": [], "period": 0})",
+        R"({"nodes": [{"id": 1, "load": 2}, {"id": 2, "load": 2}, {"id": 3, "load": 2}], "edges": [[1, 2], [1, 3]]})",
+        R"({"nodes": [{"id": 3, "load": "9/3"}, {"id": 1, "load": 2}], "edges": [[1, 3], [1, 3]], "seed": 7})",
+        R"([1, 2])",
+        R"({"nodes": [], "edges": []})",
+        R"({"nodes": [{"id": 1, "load": 2}], "edges": []} trailing)",
+    };
+    int k = 0;
+    for (const char* c : cases) {
+        guarded("case " + std::to_string(k++), [&] { write_task(parse(c), std::cout); });
+    }
+    if (host_only) return 0;
+
+    section("write_scheme / simulate_scheme / write_trace");
+    for (const std::string& f : fixtures) {
+        for (int M : {3, 8, 148}) {
+            guarded(f + " M" + std::to_string(M), [&] {
+                const DagTask t = read_task_file(f);
+                const Platform p{M, Rational(1)};
+                const ScheduleScheme s = schedule(t, p);
+                write_scheme(s, std::cout);
+                SimConfig sim;
+                sim.platform = p;
+                SimTrace tr = simulate_scheme(t, s, sim);
+                write_trace(tr, std::cout);
+                check_precedence(tr, s);
+                sim.time_model.kind = TimeModel::Kind::scaled;
+                sim.time_model.seed = 17;
+                sim.time_model.scale_min = Rational(1, 2);
+                sim.time_model.scale_max = Rational(9, 10);
+                tr = simulate_scheme(t, s, sim);
+                write_trace(tr, std::cout);
+                check_capacity(tr, M);
+            });
+        }
+    }
+    section("simulate_greedy");
+    for (const std::string& f : fixtures) {
+        for (int M : {3, 8, 148}) {
+            guarded(f + " greedy M" + std::to_string(M), [&] {
+                const DagTask t = read_task_file(f);
+                SimConfig g;
+                g.platform = Platform{M, Rational(1)};
+                g.mode = SimMode::greedy;
+                write_trace(simulate_greedy(t, g), std::cout);
+                g.policy = DispatchPolicy::random;
+                g.policy_seed = 5;
+                write_trace(simulate_greedy(t, g), std::cout);
+                g.time_model.kind = TimeModel::Kind::scaled;
+                g.time_model.seed = 3;
+                g.time_model.scale_min = Rational(1, 4);
+                write_trace(simulate_greedy(t, g), std::cout);
+            });
+        }
+    }
+    guarded("greedy in scheme mode", [&] {
+        SimConfig g;
+        g.platform = Platform{8, Rational(1)};
+        simulate_greedy(read_task_file(fixtures[0]), g);
+    });
+    guarded("bad scale range", [&] {
+        SimConfig g;
+        g.platform = Platform{8, Rational(1)};
+        g.mode = SimMode::greedy;
+        g.time_model.kind = TimeModel::Kind::scaled;
+        g.time_model.scale_min = Rational(3, 2);
+        simulate_greedy(read_task_file(fixtures[0]), g);
+    });
+    guarded("capacity violation", [&] {
+        SimTrace tr;
+        tr.events.push_back(SimEvent{"a", Rational(0), Rational(2), 5});
+        tr.events.push_back(SimEvent{"b", Rational(1), Rational(3), 5});
+        check_capacity(tr, 8);
+    });
+
+    section("run_experiment / write_csv");
+    {
+        ExperimentSpec spec;
+        spec.sweep = ExperimentSpec::SweepVar::sm_count;
+        spec.values = {4, 8, 32, 148};
+        spec.corpus_size = 20;
+        guarded("sweep M", [&] { write_csv(run_experiment(spec), std::cout); });
+        spec.sweep = ExperimentSpec::SweepVar::max_width;
+        spec.values = {2, 4, 8};
+        spec.platform.sm_count = 16;
+        spec.methods = {Method::proposed, Method::graham_para};
+        spec.normalize_to = Method::greedy;
+        guarded("sweep P", [&] { write_csv(run_experiment(spec), std::cout); });
+        spec.sweep = ExperimentSpec::SweepVar::depth;
+        spec.values = {3, 6};
+        spec.base.avg_load = Rational(15, 2);
+        spec.base.integer_loads = false;
+        guarded("sweep V", [&] { write_csv(run_experiment(spec), std::cout); });
+        spec.values = {};
+        guarded("no values", [&] { run_experiment(spec); });
+    }
+
+    section("run_validation");
+    {
+        GenConfig cfg;
+        for (int M : {8, 32, 148}) {
+            guarded("validation M" + std::to_string(M), [&] {
+                const ValidationSummary s =
+                    run_validation(cfg, 150, Platform{M, Rational(1)}, 4, Rational(1, 2), Rational(1));
+                std::cout << s.tasks << " " << s.runs << " " << s.violations << " " << hexd(s.mean_tightness_worst)
+                          << " " << hexd(s.mean_tightness_scaled) << " " << s.violation_details.size() << "\n";
+            });
+        }
+        // (a bad scale range is not exercised: the reference throws it inside
+        // an OpenMP region, which terminates the process)
+    }
+
+    section("run_benchmarks / write_bench_table");
+    guarded("benchmarks", [&] {
+        write_bench_table(run_benchmarks(fixtures, {4, 16, 148}, {4, 20}, 10, 1), std::cout);
+    });
+    guarded("missing fixture", [&] { run_benchmarks({dir + "/nope.json"}, {4}, {4}, 2, 1); });
+    return 0;
+}
