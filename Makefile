@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden
 CXXFLAGS:= -std=c++17 -O3 -fPIC -fopenmp -fvisibility=hidden -I/usr/local/cuda/include -Wall -Wno-comment
 LDOMP   := -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp -lpthread
 
-CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o $(LIBDIR)/k5_generate.o $(LIBDIR)/k6_greedy.o
+CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k1_small.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o $(LIBDIR)/k5_generate.o $(LIBDIR)/k6_greedy.o
 CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/dagsched_b200.h
 
 .PHONY: all product oracle ref clean
@@ -68,7 +68,7 @@ $(LIBDIR)/api_drivers_dump: tests/cpp/drivers_dump.cpp $(LIBDIR)/libdagsched_cpp
 	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(LIBDIR)/api_bench: tests/cpp/api_bench.cpp $(LIBDIR)/libdagsched_cpp.so
-	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
+	$(CXX) -std=c++20 -O2 -DDS_API_BENCH_RAW $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(LIBDIR)/api_division_dump: tests/cpp/division_dump.cpp $(LIBDIR)/libdagsched_cpp.so
 	$(CXX) -std=c++20 -O2 $(API_INC) $< -o $@ -L$(LIBDIR) -ldagsched_cpp -ldagsched_b200 -Wl,-rpath,'$$ORIGIN'

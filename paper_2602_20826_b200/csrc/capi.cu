@@ -31,6 +31,10 @@ void k4_launch(u64 n_dags, const u32* node_off, const int32_t* status, const uin
                long long lo, long long hi, u64 seed, unsigned char* over, double* ratio, int32_t* st,
                cudaStream_t stream);
 
+// k1_small.cu: the latency path (one kernel, zero-copy mapped buffers)
+cudaError_t k1_small_configure();
+cudaError_t k1_small_launch(const K1Args& a, bool detail, cudaStream_t s);
+
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -78,6 +82,7 @@ int configure(int device, bool detail, K1Occupancy& occ) {
         return DS_OK;
     }
     DS_CUDA(k1_configure(device, detail, occ));
+    DS_CUDA(k1_small_configure());
     cache[slot] = occ;
     ready[slot] = true;
     return DS_OK;
@@ -136,14 +141,16 @@ __global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __r
 // pinned host staging (grows, never shrinks)
 struct PinBuf {
     void* p = nullptr;
+    void* dev = nullptr;  // device alias when mapped
     size_t cap = 0;
-    int ensure(size_t bytes) {
+    int ensure(size_t bytes, bool mapped = false) {
         bytes = std::max<size_t>(bytes, 4096);
         if (bytes <= cap) return DS_OK;
         if (p) cudaFreeHost(p);
-        p = nullptr;
+        p = dev = nullptr;
         cap = 0;
-        DS_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+        DS_CUDA(cudaHostAlloc(&p, bytes, mapped ? cudaHostAllocMapped : cudaHostAllocDefault));
+        if (mapped) DS_CUDA(cudaHostGetDevicePointer(&dev, p, 0));
         cap = bytes;
         return DS_OK;
     }
@@ -184,7 +191,109 @@ struct DeviceCtx {
     Slot slot[kMaxSlots];
     DevBuf retry, retry_count, handoff;  // scratch for the device-pointer entry point
     DetailCtx det;
+    PinBuf small_in, small_out;  // latency path: mapped (zero-copy) inputs and outputs
 };
+
+DeviceCtx& device_ctx(int dev);
+
+// ------------------------------------------------------- latency path
+// Host batches of at most kSmallDags DAGs go through k1_small (k1_small.cu):
+// inputs packed into mapped pinned memory, one launch, results read back
+// from mapped pinned memory — no copy operations. DS_SMALL=0 disables it.
+constexpr u64 kSmallDags = 64;
+bool small_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("DS_SMALL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// A host batch in either wire form, read element-wise for packing.
+struct HostView {
+    u64 n;
+    const uint32_t *node_off, *edge_off;
+    const int64_t *ln, *ld;     // wide form
+    const uint16_t *ln16, *e16;  // compact form
+    const uint32_t* edges;
+    int64_t load(u64 i) const { return ln ? ln[i] : int64_t(ln16[i]); }
+    uint32_t edge(u64 i) const { return edges ? edges[i] : ((uint32_t(e16[i]) >> 8) << 16) | (e16[i] & 0xffu); }
+};
+inline HostView host_view(const ds_dag_batch* b) {
+    return HostView{b->n_dags, b->node_off, b->edge_off, b->load_num, b->load_den, nullptr, nullptr, b->edges};
+}
+inline HostView host_view(const ds_dag_batch16* b) {
+    return HostView{b->n_dags, b->node_off, b->edge_off, nullptr, nullptr, b->load, b->edges, nullptr};
+}
+
+// Packs `h` into ctx.small_in and points a's inputs at its device alias.
+int small_inputs(const HostView& h, DeviceCtx& ctx, K1Args& a) {
+    const u64 n = h.n;
+    const u32 nb = h.node_off[0], eb = h.edge_off[0];
+    const u64 N = h.node_off[n] - nb, E = h.edge_off[n] - eb;
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t o_eo = al((n + 1) * 4), o_ln = al(o_eo + (n + 1) * 4), o_ld = al(o_ln + N * 8),
+                 o_ed = al(o_ld + (h.ld ? N * 8 : 0)), bytes = o_ed + E * 4;
+    if (int rc = ctx.small_in.ensure(bytes, true)) return rc;
+    char* w = static_cast<char*>(ctx.small_in.p);
+    const char* dv = static_cast<const char*>(ctx.small_in.dev);
+    u32* no = reinterpret_cast<u32*>(w);
+    u32* eo = reinterpret_cast<u32*>(w + o_eo);
+    for (u64 i = 0; i <= n; ++i) {
+        no[i] = h.node_off[i] - nb;
+        eo[i] = h.edge_off[i] - eb;
+    }
+    int64_t* ln = reinterpret_cast<int64_t*>(w + o_ln);
+    for (u64 i = 0; i < N; ++i) ln[i] = h.load(i);
+    if (h.ld) std::memcpy(w + o_ld, h.ld, N * 8);
+    u32* ed = reinterpret_cast<u32*>(w + o_ed);
+    for (u64 i = 0; i < E; ++i) ed[i] = h.edge(i);
+    a.n_dags = n;
+    a.node_off = reinterpret_cast<const u32*>(dv);
+    a.edge_off = reinterpret_cast<const u32*>(dv + o_eo);
+    a.load_num = reinterpret_cast<const u64*>(dv + o_ln);
+    a.load_den = h.ld ? reinterpret_cast<const u64*>(dv + o_ld) : nullptr;
+    a.edges = reinterpret_cast<const u32*>(dv + o_ed);
+    return DS_OK;
+}
+
+int small_stream(int device, DeviceCtx& ctx, cudaStream_t& s) {
+    DS_CUDA(cudaSetDevice(device));
+    if (!ctx.init) {
+        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        ctx.init = true;
+    }
+    s = ctx.slot[0].s;
+    return DS_OK;
+}
+
+// bounds mode (ds_analyze_batch / ds_analyze_batch16 for small host batches)
+int analyze_small(const HostView& h, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
+    K1Occupancy occ;
+    if (int rc = configure(device, false, occ)) return rc;
+    DeviceCtx& ctx = device_ctx(device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    cudaStream_t s;
+    if (int rc = small_stream(device, ctx, s)) return rc;
+    K1Args a{};
+    if (int rc = small_inputs(h, ctx, a)) return rc;
+    const u64 n = h.n;
+    const size_t o_b = 0, o_st = n * 80, o_ng = o_st + n * 4;
+    if (int rc = ctx.small_out.ensure(o_ng + n * 2, true)) return rc;
+    char* dv = static_cast<char*>(ctx.small_out.dev);
+    a.plat = P;
+    a.mask = mask;
+    a.bounds = reinterpret_cast<int64_t*>(dv + o_b);
+    a.status = reinterpret_cast<int32_t*>(dv + o_st);
+    a.n_groups = reinterpret_cast<uint16_t*>(dv + o_ng);
+    DS_CUDA(k1_small_launch(a, false, s));
+    DS_CUDA(cudaStreamSynchronize(s));
+    const char* r = static_cast<const char*>(ctx.small_out.p);
+    std::memcpy(out->bounds, r + o_b, n * 80);
+    std::memcpy(out->status, r + o_st, n * 4);
+    if (out->n_groups) std::memcpy(out->n_groups, r + o_ng, n * 2);
+    return DS_OK;
+}
 
 // The bounds pass runs as k1_front + k1_back (K1Handoff) unless DS_K1_SPLIT=0
 // selects the single-kernel variant (kept for A/B measurement and tests).
@@ -215,6 +324,7 @@ constexpr u64 kDefaultChunks = 3;  // one per stream slot (1M C5 DAGs e2e: 3 chu
 template <class Batch>
 int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
     constexpr bool compact = std::is_same<Batch, ds_dag_batch16>::value;
+    if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small(host_view(b), P, mask, out, device);
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
     if (int rc = configure(device, false, occ)) return rc;
@@ -523,6 +633,53 @@ int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_r
 int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
     return ds_analyze_batch16(b, p, mask, r, dev);
 }
+// schedule-detail mode for a small host batch: one k1_small launch over
+// mapped buffers (see analyze_small)
+int schedule_small(const ds_dag_batch* b, const PlatT<u64>& P, ds_scheme_out* out, int device, DeviceCtx& ctx) {
+    K1Occupancy occ;
+    if (int rc = configure(device, true, occ)) return rc;
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    cudaStream_t s;
+    if (int rc = small_stream(device, ctx, s)) return rc;
+    K1Args a{};
+    const HostView h = host_view(b);
+    if (int rc = small_inputs(h, ctx, a)) return rc;
+    const u64 n = h.n, N = b->node_off[n] - b->node_off[0];
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t o_ent = 0, o_grp = al(o_ent + 2 * N * sizeof(ds_entity_rec)), o_b = al(o_grp + N * sizeof(ds_group_rec)),
+                 o_st = al(o_b + n * 80), o_ne = al(o_st + n * 4), o_ng = al(o_ne + n * 2), o_nd = al(o_ng + n * 2),
+                 o_nb = al(o_nd + n * 2), o_ndg = al(o_nb + N * 2), bytes = o_ndg + N * 2;
+    if (int rc = ctx.small_out.ensure(bytes, true)) return rc;
+    char* dv = static_cast<char*>(ctx.small_out.dev);
+    a.plat = P;
+    a.mask = DS_M_ALL;
+    a.det.entities = reinterpret_cast<ds_entity_rec*>(dv + o_ent);
+    a.det.groups = reinterpret_cast<ds_group_rec*>(dv + o_grp);
+    a.det.bounds = reinterpret_cast<int64_t*>(dv + o_b);
+    a.det.status = reinterpret_cast<int32_t*>(dv + o_st);
+    a.det.n_entities = reinterpret_cast<uint16_t*>(dv + o_ne);
+    a.det.n_groups = reinterpret_cast<uint16_t*>(dv + o_ng);
+    a.det.n_div_groups = reinterpret_cast<uint16_t*>(dv + o_nd);
+    a.det.node_block = reinterpret_cast<int16_t*>(dv + o_nb);
+    a.det.node_div_group = reinterpret_cast<int16_t*>(dv + o_ndg);
+    DS_CUDA(k1_small_launch(a, true, s));
+    DS_CUDA(cudaStreamSynchronize(s));
+    const char* r = static_cast<const char*>(ctx.small_out.p);
+    auto put = [&](void* dst, size_t off, size_t len) {
+        if (dst) std::memcpy(dst, r + off, len);
+    };
+    put(out->status, o_st, n * 4);
+    put(out->n_entities, o_ne, n * 2);
+    put(out->n_groups, o_ng, n * 2);
+    put(out->n_div_groups, o_nd, n * 2);
+    put(out->node_block, o_nb, N * 2);
+    put(out->node_div_group, o_ndg, N * 2);
+    put(out->entities, o_ent, 2 * N * sizeof(ds_entity_rec));
+    put(out->groups, o_grp, N * sizeof(ds_group_rec));
+    put(out->bounds, o_b, n * 80);
+    return DS_OK;
+}
+
 // K1 in detail mode over a host batch; results stay in the device context's
 // out arena (ctx.det.v). The caller holds ctx.mu and the stream slot 0.
 int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx& ctx) {
@@ -625,6 +782,7 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     const u64 n = b->n_dags;
     if (n == 0) return DS_OK;
     DeviceCtx& ctx = device_ctx(device);
+    if (n <= kSmallDags && small_enabled()) return schedule_small(b, P, out, device, ctx);
     std::lock_guard<std::mutex> lock(ctx.mu);
     if (int rc = run_detail(b, P, device, ctx)) return rc;
     DetailCtx& D = ctx.det;

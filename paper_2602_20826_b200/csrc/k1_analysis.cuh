@@ -1123,6 +1123,25 @@ struct K1Node {
     u64 pad;
 };
 static_assert(sizeof(K1Node) == 32, "K1Node is one sector");
+// Compact hand-off of a DAG with n <= 32 nodes and integer loads (k1_fast<32>):
+// per node a 16-byte record (u32 masks, load, rank | order << 8), then one u32
+// member mask per division group, all inside the DAG's own 32n-byte slice of
+// the K1Node array — 16n + 4 ndiv bytes in one contiguous run instead of 32n +
+// 2n + 8 ndiv over three arrays, so a lane's walk touches ~half the lines.
+// h.ndiv[d] carries kNdivCompact to say which layout a DAG has.
+struct K1Rec16 {
+    u32 pred;
+    u32 ad;  // anc | desc
+    u32 ln;  // integer load (den 1)
+    u32 ro;  // rank | order << 8
+};
+static_assert(sizeof(K1Rec16) == 16, "K1Rec16 is 16 bytes");
+constexpr uint16_t kNdivCompact = 0x8000;
+// walk-order sort key: the layout first (so a warp's lanes read one layout),
+// then the division-group shape (count, member counts of the first groups)
+__device__ __forceinline__ u32 walk_key(u32 shape, bool compact) {
+    return (compact ? 0u : 0x80000000u) | (shape & 0x03ffffffu);
+}
 struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] + v)
     K1Node* node;
     u64* anc;        // k1_mid's block construction
@@ -1380,7 +1399,7 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
             // within windows of kSortWindow consecutive DAGs (the window
             // index in the high bits), so a warp's walks stay near each other
             // in the hand-off and share L2 lines
-            if (a.h.skey) a.h.skey[d] = kSortWindow ? (u32(d / kSortWindow) << 20) | (shape >> 6) : shape;
+            if (a.h.skey) a.h.skey[d] = walk_key(shape, false);
         }
         __syncwarp();
     }
@@ -1407,12 +1426,35 @@ constexpr int kLaneWarps = 4;
 // fell to 12 warps/SM and the walk is latency bound). k1_back (warp per DAG)
 // 4.40.
 
-template <int QB>  // bits per packed quota field: 8 (M <= 255) or 16 (M <= 65535)
-__device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, const int n, const int ndiv,
-                                             const PlatT<u32> P, RatT<u32>& bound, int& n_groups) {
-    const K1Node* __restrict__ nodes = a.h.node + n0;
-    const uint16_t* __restrict__ ro = a.h.ro + n0;
-    const u64* __restrict__ divg = a.h.divg + n0;
+// The two hand-off layouts the walk reads (K1Node + ro + divg arrays, or the
+// compact per-DAG K1Rec16 run): node v's load, anc|desc, preds; ro(i) =
+// rank of node i | node at rank i << 8; division group g's member mask.
+struct LaneWide {
+    const K1Node* __restrict__ nodes;
+    const uint16_t* __restrict__ r;
+    const u64* __restrict__ g;
+    __device__ __forceinline__ LaneWide(const K1Args& a, u32 n0) : nodes(a.h.node + n0), r(a.h.ro + n0), g(a.h.divg + n0) {}
+    __device__ __forceinline__ RatT<u32> load(int v) const { return RatT<u32>{__ldg(&nodes[v].ln), __ldg(&nodes[v].ld)}; }
+    __device__ __forceinline__ u64 ad(int v) const { return __ldg(&nodes[v].ad); }
+    __device__ __forceinline__ u64 pred(int v) const { return __ldg(&nodes[v].pred); }
+    __device__ __forceinline__ u32 ro(int i) const { return __ldg(r + i); }
+    __device__ __forceinline__ u64 divg(int k) const { return __ldg(g + k); }
+};
+struct LaneCompact {
+    const K1Rec16* __restrict__ rec;
+    const u32* __restrict__ g;
+    __device__ __forceinline__ LaneCompact(const K1Args& a, u32 n0, int n)
+        : rec(reinterpret_cast<const K1Rec16*>(a.h.node + n0)), g(reinterpret_cast<const u32*>(rec + n)) {}
+    __device__ __forceinline__ RatT<u32> load(int v) const { return RatT<u32>{__ldg(&rec[v].ln), 1u}; }
+    __device__ __forceinline__ u64 ad(int v) const { return __ldg(&rec[v].ad); }
+    __device__ __forceinline__ u64 pred(int v) const { return __ldg(&rec[v].pred); }
+    __device__ __forceinline__ u32 ro(int i) const { return __ldg(&rec[i].ro); }
+    __device__ __forceinline__ u64 divg(int k) const { return __ldg(g + k); }
+};
+
+template <int QB, class R>  // QB: bits per packed quota field, 8 (M <= 255) or 16 (M <= 65535)
+__device__ __forceinline__ int schedule_lane(const R& H, const int n, const int ndiv, const PlatT<u32> P,
+                                             RatT<u32>& bound, int& n_groups) {
     // residual loads of segmented nodes (scheduler.cpp:318-328), newest last
     int n_over = 0;
     int over_v[kLaneSplits];
@@ -1421,18 +1463,18 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
         for (int k = n_over - 1; k >= 0; --k) {
             if (over_v[k] == v) return RatT<u32>{over_n[k], over_d[k]};
         }
-        return RatT<u32>{__ldg(&nodes[v].ln), __ldg(&nodes[v].ld)};
+        return H.load(v);
     };
     bool ovf = false;
     const u64 V = n >= 64 ? ~0ull : ((1ull << n) - 1);
     RatT<u32> proposed{0, 1};
     u64 done = 0;
     int gidx = 0;
-    u64 G_next = ndiv > 0 ? __ldg(divg) : 0;  // one group ahead: off the dependent-load chain
+    u64 G_next = ndiv > 0 ? H.divg(0) : 0;  // one group ahead: off the dependent-load chain
 #pragma unroll 1
     for (int g = 0; g < ndiv; ++g) {
         const u64 G = G_next;
-        if (g + 1 < ndiv) G_next = __ldg(divg + g + 1);
+        if (g + 1 < ndiv) G_next = H.divg(g + 1);
         const u64 org = G & ~done;
         if (!org) continue;  // fully absorbed by earlier launches
         RatT<u32> R{0, 1};
@@ -1451,7 +1493,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
             R = q_exec(l, cp, P);
             ovf |= R.d == 0;
             used = cp;
-            conc = ~__ldg(&nodes[v].ad);
+            conc = ~H.ad(v);
         } else {
             // apportion (scheduler.cpp:35-95) over the pending loads. Member k's
             // quota (<= M) lives in an 8-bit field (M <= 255) or a 16-bit
@@ -1545,7 +1587,7 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
                     first = false;
                 }
                 used += m;
-                conc |= ~__ldg(&nodes[v].ad);
+                conc |= ~H.ad(v);
             }
         }
         const int spare0 = P.M - used;
@@ -1563,17 +1605,17 @@ __device__ __forceinline__ int schedule_lane(const K1Args& a, const u32 n0, cons
                 b &= b - 1;
                 const int c1 = b ? __ffsll(b) - 1 : -1;
                 b &= b - 1;
-                const u64 p0 = __ldg(&nodes[c0].pred);
-                const u64 p1 = c1 >= 0 ? __ldg(&nodes[c1].pred) : ~0ull;
-                const uint16_t r0 = __ldg(ro + c0);
-                const uint16_t r1 = c1 >= 0 ? __ldg(ro + c1) : 0;
+                const u64 p0 = H.pred(c0);
+                const u64 p1 = c1 >= 0 ? H.pred(c1) : ~0ull;
+                const u32 r0 = H.ro(c0);
+                const u32 r1 = c1 >= 0 ? H.ro(c1) : 0;
                 if (!(p0 & pool) && !(p0 & ~done)) rm |= 1ull << (r0 & 0xff);
                 if (c1 >= 0 && !(p1 & pool) && !(p1 & ~done)) rm |= 1ull << (r1 & 0xff);
             }
             int spare = spare0;
 #pragma unroll 1
             for (; rm && spare >= 1; rm &= rm - 1) {
-                const int c = __ldg(ro + (__ffsll(rm) - 1)) >> 8;
+                const int c = int(H.ro(__ffsll(rm) - 1) >> 8);
                 const RatT<u32> l = load(c);
                 int mp = q_max_par(l, P);
                 if (mp < 0) {
@@ -1633,7 +1675,10 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
         const int n = int(a.node_off[d + 1] - nbase - n0);
         RatT<u32> bound{0, 0};
         int ng = 0;
-        const int st = schedule_lane<QB>(a, n0, n, a.h.ndiv[d], P, bound, ng);
+        const uint16_t nd = a.h.ndiv[d];
+        const int st = (nd & kNdivCompact)
+                           ? schedule_lane<QB>(LaneCompact(a, n0, n), n, nd & ~kNdivCompact, P, bound, ng)
+                           : schedule_lane<QB>(LaneWide(a, n0), n, nd, P, bound, ng);
         if (st == DS_EOVERFLOW || st == kLaneRetry) {  // recomputed from scratch in wider words
             a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
             a.status[d] = kStRetried;

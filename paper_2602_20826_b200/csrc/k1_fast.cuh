@@ -168,44 +168,81 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
         }
         return DS_OK;
     }
-    // ---- W^anc (dag.cpp:126-135)
+    // ---- W^anc = l + sum over ancestors, by load bit-planes (dag.cpp:126-135):
+    // O(load bits) ballots instead of O(n) shuffles
+    const int lbits = 32 - __clz(int(__reduce_or_sync(FULL, (ina ? la : 0u) | (inb ? lb : 0u))));
     u32 Wa = la, Wb = lb;
 #pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const u32 lk = __shfl_sync(FULL, k >= 32 ? lb : la, k & 31);
-        Wa += ((aa >> k) & 1) ? lk : 0u;
-        Wb += ((ab >> k) & 1) ? lk : 0u;
+    for (int b = 0; b < lbits; ++b) {
+        const u64 P = __ballot_sync(FULL, ina && ((la >> b) & 1)) |
+                      (u64(__ballot_sync(FULL, inb && ((lb >> b) & 1))) << 32);
+        Wa += u32(__popcll(aa & P)) << b;
+        Wb += u32(__popcll(ab & P)) << b;
     }
-    // ---- ranks (W desc, id asc) and join positions (W asc, id asc)
+    // ---- rank (W desc, id asc) and join position (W asc, id asc), bit-serial
+    // over W's bits: eq* hold the nodes (joins) whose W agrees so far
     const u64 J = __ballot_sync(FULL, ina && __popcll(pa) >= 2) | (u64(__ballot_sync(FULL, inb && __popcll(pb) >= 2)) << 32);
+    const int wbits = 32 - __clz(int(__reduce_or_sync(FULL, (ina ? Wa : 0u) | (inb ? Wb : 0u))));
+    u64 eqra = V, eqrb = V, eqja = J, eqjb = J;
     int ra = 0, rb = 0, ja = 0, jb = 0;
 #pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const u32 wk = __shfl_sync(FULL, k >= 32 ? Wb : Wa, k & 31);
-        const bool jk = (J >> k) & 1;
-        ra += (wk > Wa) | ((wk == Wa) & (k < va));
-        rb += (wk > Wb) | ((wk == Wb) & (k < vb));
-        ja += jk & ((wk < Wa) | ((wk == Wa) & (k < va)));
-        jb += jk & ((wk < Wb) | ((wk == Wb) & (k < vb)));
+    for (int b = wbits - 1; b >= 0; --b) {
+        const u64 B = __ballot_sync(FULL, ina && ((Wa >> b) & 1)) | (u64(__ballot_sync(FULL, inb && ((Wb >> b) & 1))) << 32);
+        if ((Wa >> b) & 1) {
+            ja += __popcll(eqja & ~B);
+            eqra &= B;
+            eqja &= B;
+        } else {
+            ra += __popcll(eqra & B);
+            eqra &= ~B;
+            eqja &= ~B;
+        }
+        if ((Wb >> b) & 1) {
+            jb += __popcll(eqjb & ~B);
+            eqrb &= B;
+            eqjb &= B;
+        } else {
+            rb += __popcll(eqrb & B);
+            eqrb &= ~B;
+            eqjb &= ~B;
+        }
     }
-    // ---- blocks: the earliest join (in join order) v is an ancestor of
+    {
+        const u64 lta = (1ull << va) - 1, ltb = (1ull << vb) - 1;  // equal W: smaller id first
+        ra += __popcll(eqra & lta);
+        ja += __popcll(eqja & lta);
+        rb += __popcll(eqrb & ltb);
+        jb += __popcll(eqjb & ltb);
+    }
+    // ---- block: the first join (in join order) v is an ancestor of, else the
+    // residual (division.cpp:10-30) = arg-min of jpos over desc(v) ∩ J, one
+    // jpos bit at a time (jpos < nj <= 63: six bits)
     const int nj = __popcll(J);
-    int ba = nj, bb = nj;
-#pragma unroll 1
-    for (u64 j = J; j; j &= j - 1) {
-        const int t = __ffsll(j) - 1;
-        const int pt = __shfl_sync(FULL, t >= 32 ? jb : ja, t & 31);
-        if ((da >> t) & 1) ba = min(ba, pt);
-        if ((db >> t) & 1) bb = min(bb, pt);
+    int ba = 0, bb = 0;
+    {
+        u64 Ca = da & J, Cb = db & J;
+#pragma unroll
+        for (int b = 5; b >= 0; --b) {
+            const u64 Z = __ballot_sync(FULL, ((J >> va) & 1) && !((ja >> b) & 1)) |
+                          (u64(__ballot_sync(FULL, ((J >> vb) & 1) && !((jb >> b) & 1))) << 32);
+            if (Ca & Z) Ca &= Z;
+            else ba |= 1 << b;
+            if (Cb & Z) Cb &= Z;
+            else bb |= 1 << b;
+        }
+        if (!(da & J)) ba = nj;
+        if (!(db & J)) bb = nj;
     }
-    // ---- in-block depth = |anc(v) ∩ block(v)|
-    int dpa = 0, dpb = 0;
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const int bk = __shfl_sync(FULL, k >= 32 ? bb : ba, k & 31);
-        dpa += ((aa >> k) & 1) & (bk == ba);
-        dpb += ((ab >> k) & 1) & (bk == bb);
-    }
+    // ---- in-block depth = |anc(v) ∩ block(v)|: block member masks by shared
+    // 64-bit atomics (S.pred is dead once pa / pb are in registers)
+    unsigned long long* bmask = reinterpret_cast<unsigned long long*>(S.pred);
+    bmask[lane] = 0;
+    bmask[lane + 32] = 0;
+    __syncwarp();
+    if (ina) atomicOr(bmask + ba, 1ull << va);
+    if (inb) atomicOr(bmask + bb, 1ull << vb);
+    __syncwarp();
+    const int dpa = ina ? __popcll(aa & bmask[ba]) : 0, dpb = inb ? __popcll(ab & bmask[bb]) : 0;
     // ---- division groups: (block, depth) in order; empty blocks vanish
     for (int i = lane; i < 68; i += 32) S.bdep[i] = 0;
     S.gcnt[lane] = 0;
@@ -286,7 +323,7 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
     if (lane == 0) {
         a.h.ndiv[d] = uint16_t(ndiv);
         a.status[d] = kStPending;
-        if (a.h.skey) a.h.skey[d] = kSortWindow ? (u32(d / kSortWindow) << 20) | (shape >> 6) : shape;
+        if (a.h.skey) a.h.skey[d] = walk_key(shape, false);
     }
     return DS_OK;
 }
@@ -439,30 +476,23 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     const u32 cnt = __popc(gm);
     // Rules 1-2 idle on every layer, else the general path
     if (__any_sync(FULL, in && (cnt > u32(M) || (cnt >= 2 && l >= u32(M))))) return -1;
-    // ---- hand-off for k1_back_lane
+    // ---- compact hand-off for k1_back_lane (K1Rec16 run + u32 group masks in
+    // the DAG's own slice of the K1Node array)
+    K1Rec16* rec = reinterpret_cast<K1Rec16*>(a.h.node + n0);
     const bool leader = in && (gm & lt) == 0;
     if (leader) {
-        a.h.divg[n0 + gidx] = u64(gm);
+        reinterpret_cast<u32*>(rec + n)[gidx] = gm;
         S.gcnt[gidx] = cnt;
     }
     if (in) S.ord[rank] = (unsigned char)lane;
     __syncwarp();
-    if (in) {
-        K1Node nd;
-        nd.pred = p;
-        nd.ad = an | de;
-        nd.ln = l;
-        nd.ld = 1;
-        nd.pad = 0;
-        a.h.node[n0 + lane] = nd;
-        a.h.ro[n0 + lane] = uint16_t(rank | (S.ord[lane] << 8));
-    }
+    if (in) rec[lane] = K1Rec16{p, an | de, l, u32(rank) | (u32(S.ord[lane]) << 8)};
     const u32 c3 = lane < int(ndiv) && lane < 10 ? min(S.gcnt[lane], 3u) : 0u;
     const u32 shape = (min(ndiv, 63u) << 20) | __reduce_or_sync(FULL, c3 << (18 - 2 * min(lane, 9)));
     if (lane == 0) {
-        a.h.ndiv[d] = uint16_t(ndiv);
+        a.h.ndiv[d] = uint16_t(ndiv) | kNdivCompact;
         a.status[d] = kStPending;
-        if (a.h.skey) a.h.skey[d] = kSortWindow ? (u32(d / kSortWindow) << 20) | (shape >> 6) : shape;
+        if (a.h.skey) a.h.skey[d] = walk_key(shape, true);
     }
     return DS_OK;
 }

@@ -17,6 +17,10 @@
 #include "dagsched/generator.hpp"
 #include "dagsched/scheduler.hpp"
 
+#ifdef DS_API_BENCH_RAW  // this repo's build: also time the bare C-ABI calls
+#include "dagsched_b200.h"
+#endif
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -77,6 +81,32 @@ int main(int argc, char** argv) {
     std::size_t groups = 0;
     const Lat ls = latency(reps, [&] { groups = schedule(c1, p148).groups.size(); });
 
+    std::string raw = "";
+#ifdef DS_API_BENCH_RAW
+    {  // the C-ABI calls alone on the packed C1 task (no DagTask packing / materialisation)
+        const uint32_t no[2] = {0, 10}, eo[2] = {0, 16};
+        int64_t ln[10] = {1, 20, 20, 20, 20, 20, 20, 20, 20, 1};
+        uint32_t ed[16];
+        for (int i = 1; i <= 8; ++i) ed[i - 1] = (0u << 16) | uint32_t(i), ed[7 + i] = (uint32_t(i) << 16) | 9u;
+        std::sort(ed, ed + 16);
+        const ds_dag_batch b{1, no, eo, ln, nullptr, ed};
+        const ds_platform pl{148, 0, 1, 1};
+        int32_t st = 0;
+        int64_t bounds[10];
+        uint16_t ne = 0, ng = 0, nd = 0;
+        int16_t nb[10], ndg[10];
+        ds_entity_rec ents[20];
+        ds_group_rec grps[10];
+        ds_results r{&st, bounds, nullptr};
+        ds_scheme_out so{&st, &ne, &ng, &nd, nb, ndg, ents, grps, bounds};
+        const Lat ra = latency(reps, [&] { ds_analyze_batch(&b, &pl, DS_M_ALL, &r, 0, nullptr, 0); });
+        const Lat rs = latency(reps, [&] { ds_schedule_batch(&b, &pl, &so, 0); });
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "\"c1_raw_ds_analyze_batch_us\": {\"p50\": %.2f, \"p99\": %.2f}, "
+                      "\"c1_raw_ds_schedule_batch_us\": {\"p50\": %.2f, \"p99\": %.2f}, ", ra.p50, ra.p99, rs.p50, rs.p99);
+        raw = buf;
+    }
+#endif
     GenConfig cfg;
     auto t0 = Clock::now();
     const std::vector<DagTask> corpus = generate_corpus(cfg, n);
@@ -96,12 +126,12 @@ int main(int argc, char** argv) {
                 for (char c : format_exact(q) + ";") h = (h ^ (unsigned char)c) * 1099511628211ull;
         check = std::to_string(h);
     }
-    std::printf("{\"c1_analyze_us\": {\"p50\": %.2f, \"p99\": %.2f, \"mean\": %.2f}, "
+    std::printf("{%s\"c1_analyze_us\": {\"p50\": %.2f, \"p99\": %.2f, \"mean\": %.2f}, "
                 "\"c1_schedule_us\": {\"p50\": %.2f, \"p99\": %.2f, \"mean\": %.2f}, \"c1_proposed\": \"%s\", "
                 "\"c1_groups\": %zu, \"corpus_dags\": %d, \"corpus_generate_s\": %.3f, "
                 "\"corpus_evaluate_s\": %.4f, \"corpus_dags_per_s\": %.1f, \"corpus_checksum\": \"%s\", "
                 "\"reps\": %d}\n",
-                la.p50, la.p99, la.mean, ls.p50, ls.p99, ls.mean, proposed.c_str(), groups, n, gen_s, best,
+                raw.c_str(), la.p50, la.p99, la.mean, ls.p50, ls.p99, ls.mean, proposed.c_str(), groups, n, gen_s, best,
                 n / best, check.c_str(), reps);
     return 0;
 }

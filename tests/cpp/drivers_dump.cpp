@@ -184,11 +184,13 @@ int main(int argc, char** argv) {
         spec.platform.sm_count = 16;
         spec.methods = {Method::proposed, Method::graham_para};
         spec.normalize_to = Method::greedy;
+        spec.corpus_size = 8;  // the reference's 128-bit running sums overflow above ~10-20 DAGs here
         guarded("sweep P", [&] { write_csv(run_experiment(spec), std::cout); });
         spec.sweep = ExperimentSpec::SweepVar::depth;
         spec.values = {3, 6};
         spec.base.avg_load = Rational(15, 2);
         spec.base.integer_loads = false;
+        spec.corpus_size = 3;
         guarded("sweep V", [&] { write_csv(run_experiment(spec), std::cout); });
         spec.values = {};
         guarded("no values", [&] { run_experiment(spec); });

@@ -91,6 +91,40 @@ def test_seeded_corpora_vs_oracle(orc, cfg, Ms):
         assert len(bad) == 0, (M, bad[:5])
 
 
+@pytest.mark.parametrize("cfg,Ms", [
+    (dict(seed=2024), (1, 8, 148)),
+    (dict(seed=7, avg_load=200, max_width=12), (8, 300)),  # u64 / u128 word tiers
+    (dict(seed=99, integer_loads=False, avg_load=5), (4, 148)),
+    (dict(seed=5, t_min="1/2", avg_load=9), (6, 148)),
+    (dict(seed=13, depth_min=6, depth_max=10, max_width=24, avg_load=40), (32, 148)),  # n > 64
+])
+def test_latency_path_vs_oracle(orc, cfg, Ms):
+    """Host batches of <= 64 DAGs take the one-kernel latency path (k1_small:
+    zero-copy mapped buffers, in-warp 32/64/128-bit tiers); its bounds,
+    statuses and (detail mode) schedules equal the oracle's and the
+    throughput path's."""
+    gen = _lib.Corpus(640, **cfg)
+    b = gen.batch()
+    tmin = cfg.get("t_min", 1)
+    c = orc.corpus(b, min_load=tmin)
+    for M in Ms:
+        st_o, b_o, _ = c.evaluate(M, tmin)
+        for lo in range(0, 640, 64):
+            st, bounds, _ = _lib.analyze(b.slice(lo, lo + 64), M, tmin)
+            assert np.array_equal(st, st_o[lo:lo + 64]), (M, lo)
+            assert np.array_equal(bounds, b_o[lo:lo + 64]), (M, lo)
+        if b.integer_loads() and b.compact16_ok():
+            st, bounds, _ = _lib.analyze16(b.slice(0, 50), M, tmin)
+            assert np.array_equal(st, st_o[:50]) and np.array_equal(bounds, b_o[:50])
+        big, st_big = scheme.schedule_batch(b.slice(0, 130), M, tmin)  # > 64: throughput (detail arena) path
+        for lo in (0, 64):
+            small, st_small = scheme.schedule_batch(b.slice(lo, lo + 64), M, tmin)
+            assert np.array_equal(st_small, st_big[lo:lo + 64])
+            for k, sch in enumerate(small):
+                if sch is not None:
+                    assert scheme.to_reference_json(sch) == scheme.to_reference_json(big[lo + k]), (M, lo + k)
+
+
 def test_method_mask_subsets(orc):
     b = _lib.Corpus(500, seed=3).batch()
     _, full, _ = _lib.analyze(b, 148)
