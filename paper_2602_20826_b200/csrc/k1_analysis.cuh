@@ -1137,11 +1137,36 @@ struct K1Rec16 {
 };
 static_assert(sizeof(K1Rec16) == 16, "K1Rec16 is 16 bytes");
 constexpr uint16_t kNdivCompact = 0x8000;
-// walk-order sort key: the layout first (so a warp's lanes read one layout),
-// then the division-group shape (count, member counts of the first groups)
-__device__ __forceinline__ u32 walk_key(u32 shape, bool compact) {
-    return (compact ? 0u : 0x80000000u) | (shape & 0x03ffffffu);
+// Walk-order sort key (52 bits; k1_wsort appends the 12-bit window index):
+// the hand-off layout first (a warp's lanes then read one layout), then the
+// division-group shape. Called by every lane of the warp with c = the member
+// count of division group `lane` and c2 = that of group lane + 32 (0 when
+// absent). mode (K1Args::key_mode, DS_WALK_KEY):
+//   0  group count (6 bits) + member counts clipped to 3 of groups 0..9
+//   1  group count (5 bits) + member counts clipped to 3 of groups 0..22
+//   2  group count (5 bits) + one "several members" bit for groups 0..45
+__device__ __forceinline__ u64 walk_key(const int lane, const u32 ndiv, const u32 c, const u32 c2, const bool compact,
+                                        const int mode) {
+    const u64 top = (compact ? 0ull : 1ull) << 51;
+    if (mode == 1) {
+        const u32 f = lane < 23 ? min(c, 3u) : 0u;
+        const int sh = 2 * (22 - min(lane, 22));  // group g at bits 45-2g..44-2g
+        const u32 lo = __reduce_or_sync(FULL, sh < 32 ? f << sh : 0u);
+        const u32 hi = __reduce_or_sync(FULL, sh >= 32 ? f << (sh - 32) : 0u);
+        return top | (u64(min(ndiv, 31u)) << 46) | (u64(hi) << 32) | lo;
+    }
+    if (mode == 2) {
+        const u32 b1 = __ballot_sync(FULL, c >= 2), b2 = __ballot_sync(FULL, lane < 14 && c2 >= 2);
+        // group g at bit 45-g
+        const u64 bits = (u64(__brev(b1)) << 14) | (u64(__brev(b2) >> 18) & 0x3fffull);
+        return top | (u64(min(ndiv, 31u)) << 46) | bits;
+    }
+    const u32 f = lane < 10 ? min(c, 3u) : 0u;
+    const u32 shape = (min(ndiv, 63u) << 20) | __reduce_or_sync(FULL, f << (18 - 2 * min(lane, 9)));
+    return top | shape;
 }
+constexpr int kDefaultWalkKey = 0;
+constexpr u64 kWalkKeyNone = ~0ull;  // never walked (k1_fast left it to the general kernels)
 struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] + v)
     K1Node* node;
     u64* anc;        // k1_mid's block construction
@@ -1152,7 +1177,7 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     // count, which division groups have several members), k1_wsort orders
     // the DAG indices by it within windows of kSortWindow DAGs, and the lanes
     // of a warp then walk DAGs that take the same branches
-    u32* skey;       // per DAG: walk-order key (k1_fast / k1_mid)
+    u64* skey;       // per DAG: walk-order key (k1_fast / k1_mid), walk_key()
     u32* perm;       // walk order out of k1_wsort
     u32* fb;         // DAGs k1_fast left to the general kernels (count: retry_count[7])
     u32* l64;        // DAGs with 32 < n <= 64 for k1_fast<64> (count: retry_count[8])
@@ -1178,6 +1203,7 @@ struct K1Args {
     K1Handoff h;           // split mode when h.node != nullptr (bounds mode only)
     const u32* perm;       // k1_back_lane's DAG order (nullptr: index order)
     int fb_only;           // k1_front / k1_mid take only the DAGs k1_fast queued (h.fb)
+    int key_mode;          // walk_key() layout (DS_WALK_KEY)
 };
 
 template <int W, class T, bool DETAIL>
@@ -1288,7 +1314,7 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
         const u64 d = a.fb_only ? a.h.fb[t] : t;
         if (d >= a.n_dags) break;
         if (!a.fb_only && a.h.skey && lane == 0) {
-            a.h.skey[d] = 0xffffffffu;  // not walked by k1_back_lane unless k1_mid keys it
+            a.h.skey[d] = kWalkKeyNone;  // not walked by k1_back_lane unless k1_mid keys it
         }
         const u32 n0 = a.node_off[d] - nbase, e0 = a.edge_off[d] - ebase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
@@ -1391,15 +1417,16 @@ __global__ void __launch_bounds__(128) k1_mid(const K1Args a) {
         // 19-2g..18-2g — measured best of the keys tried (back 2.08 ms; with
         // only "which groups are multi-member" 2.11, member counts of 13
         // groups without the count 2.39, with the node count 2.20)
-        const u32 cnt = lane < ndiv && lane < 10 ? u32(min(__popcll(S.divg[lane][0]), 3)) : 0u;
-        const u32 shape = (u32(min(ndiv, 63)) << 20) | __reduce_or_sync(FULL, cnt << (18 - 2 * min(lane, 9)));
+        const u32 cg = lane < ndiv ? u32(__popcll(S.divg[lane][0])) : 0u;
+        const u32 cg2 = lane + 32 < ndiv ? u32(__popcll(S.divg[lane + 32][0])) : 0u;
+        const u64 key = walk_key(lane, u32(ndiv), cg, cg2, false, a.key_mode);
         if (lane == 0) {
             a.h.ndiv[d] = uint16_t(ndiv);
             a.status[d] = kStPending;
             // within windows of kSortWindow consecutive DAGs (the window
             // index in the high bits), so a warp's walks stay near each other
             // in the hand-off and share L2 lines
-            if (a.h.skey) a.h.skey[d] = walk_key(shape, false);
+            if (a.h.skey) a.h.skey[d] = key;
         }
         __syncwarp();
     }

@@ -164,7 +164,7 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
         if (lane == 0) {
             a.status[d] = DS_OK;
             if (a.n_groups) a.n_groups[d] = 0;
-            if (a.h.skey) a.h.skey[d] = 0xffffffffu;
+            if (a.h.skey) a.h.skey[d] = kWalkKeyNone;
         }
         return DS_OK;
     }
@@ -317,13 +317,13 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
             if (int(g & ~31u) + lane < int(ndiv)) a.h.divg[n0 + (g & ~31u) + lane] = mine;
         }
     }
-    // walk-order key (as k1_mid): group count, member counts of the first 10
-    const u32 cnt = lane < int(ndiv) && lane < 10 ? min(ca, 3u) : 0u;
-    const u32 shape = (min(ndiv, 63u) << 20) | __reduce_or_sync(FULL, cnt << (18 - 2 * min(lane, 9)));
+    // walk-order key (walk_key): group count and member counts
+    const u64 key = walk_key(lane, ndiv, lane < int(ndiv) ? ca : 0u, lane + 32 < int(ndiv) ? cb : 0u, false,
+                             a.key_mode);
     if (lane == 0) {
         a.h.ndiv[d] = uint16_t(ndiv);
         a.status[d] = kStPending;
-        if (a.h.skey) a.h.skey[d] = walk_key(shape, false);
+        if (a.h.skey) a.h.skey[d] = key;
     }
     return DS_OK;
 }
@@ -415,7 +415,7 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
         if (lane == 0) {
             a.status[d] = DS_OK;
             if (a.n_groups) a.n_groups[d] = 0;
-            if (a.h.skey) a.h.skey[d] = 0xffffffffu;
+            if (a.h.skey) a.h.skey[d] = kWalkKeyNone;
         }
         return DS_OK;
     }
@@ -487,12 +487,11 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     if (in) S.ord[rank] = (unsigned char)lane;
     __syncwarp();
     if (in) rec[lane] = K1Rec16{p, an | de, l, u32(rank) | (u32(S.ord[lane]) << 8)};
-    const u32 c3 = lane < int(ndiv) && lane < 10 ? min(S.gcnt[lane], 3u) : 0u;
-    const u32 shape = (min(ndiv, 63u) << 20) | __reduce_or_sync(FULL, c3 << (18 - 2 * min(lane, 9)));
+    const u64 key = walk_key(lane, ndiv, lane < int(ndiv) ? S.gcnt[lane] : 0u, 0u, true, a.key_mode);
     if (lane == 0) {
         a.h.ndiv[d] = uint16_t(ndiv) | kNdivCompact;
         a.status[d] = kStPending;
-        if (a.h.skey) a.h.skey[d] = walk_key(shape, true);
+        if (a.h.skey) a.h.skey[d] = key;
     }
     return DS_OK;
 }
@@ -532,7 +531,7 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
         }
         if (st != DS_OK && lane == 0) {
             a.h.fb[atomicAdd(a.retry_count + kFbCounter, 1u)] = u32(d);
-            if (a.h.skey) a.h.skey[d] = 0xffffffffu;  // not walked unless k1_mid takes it over
+            if (a.h.skey) a.h.skey[d] = kWalkKeyNone;  // not walked unless k1_mid takes it over
         }
         __syncwarp();
     }
@@ -547,13 +546,13 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
 constexpr int kWsortThreads = 1024;
 static_assert(kSortWindow == 4096, "k1_wsort sorts 4096-DAG windows");
 template <bool UNUSED = false>
-__global__ void __launch_bounds__(kWsortThreads) k1_wsort(const u32* __restrict__ skey, u32* __restrict__ perm,
+__global__ void __launch_bounds__(kWsortThreads) k1_wsort(const u64* __restrict__ skey, u32* __restrict__ perm,
                                                            u64 n_dags) {
     __shared__ u64 k[kSortWindow];
     const u64 base = u64(blockIdx.x) * kSortWindow;
     for (int i = threadIdx.x; i < int(kSortWindow); i += kWsortThreads) {
         const u64 d = base + u64(i);
-        k[i] = d < n_dags ? (u64(skey[d]) << 32) | u32(d) : ~0ull;
+        k[i] = d < n_dags ? (skey[d] << 12) | u64(i) : ~0ull;  // 52-bit key, window-relative index
     }
     __syncthreads();
 #pragma unroll 1
@@ -574,7 +573,7 @@ __global__ void __launch_bounds__(kWsortThreads) k1_wsort(const u32* __restrict_
     }
     for (int i = threadIdx.x; i < int(kSortWindow); i += kWsortThreads) {
         const u64 d = base + u64(i);
-        if (d < n_dags) perm[d] = u32(k[i]);
+        if (d < n_dags) perm[d] = u32(base + (k[i] & 0xfffull));
     }
 }
 

@@ -26,7 +26,7 @@ constexpr int kK1Counters = 12;  // u32 work counters at K1Args::retry_count (48
 
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
-    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 16;
+    return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 20;
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;
@@ -37,8 +37,8 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     h.ro = reinterpret_cast<uint16_t*>(m + 2 * n_nodes);
     h.ndiv = h.ro + n_nodes;
     uintptr_t p = (reinterpret_cast<uintptr_t>(h.ndiv + n_dags) + 255) & ~uintptr_t(255);
-    h.skey = reinterpret_cast<u32*>(p);
-    h.perm = h.skey + n_dags;
+    h.skey = reinterpret_cast<u64*>(p);
+    h.perm = reinterpret_cast<u32*>(h.skey + n_dags);
     h.fb = h.perm + n_dags;
     h.l64 = h.fb + n_dags;
     return h;

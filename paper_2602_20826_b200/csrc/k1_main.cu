@@ -102,8 +102,14 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
     }();
     const bool fast = split && fast_on && a.load_den == nullptr && a.plat.tmin.n == 1 && a.plat.tmin.d == 1 &&
                       a.plat.M <= 1023;
+    // walk-key layout (walk_key in k1_analysis.cuh); DS_WALK_KEY overrides
+    static const int key_mode = [] {
+        const char* env = getenv("DS_WALK_KEY");
+        return env ? atoi(env) : kDefaultWalkKey;
+    }();
     K1Args af = a;
     af.fb_only = fast ? 1 : 0;
+    af.key_mode = key_mode;
     if (fast) {
         const u64 need = (a.n_dags + kFastWarps - 1) / kFastWarps;
         const int gf = int(need < u64(occ.grid_fast) ? need : u64(occ.grid_fast));
