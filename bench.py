@@ -9,10 +9,12 @@ data path: DAGs are independent), so scaling is weak: N GPUs analyse N x 1M
 DAGs. ``value`` = all ranks' DAGs / max-over-ranks device time.
 
 e2e: the same metric through the public C-ABI with pinned HOST buffers —
-ds_analyze_batch16 (the compact wire form: 16-bit loads and edges, 2.4x fewer
-PCIe bytes) when the corpus fits it, else ds_analyze_batch (--wide forces
-it); H2D of the packed DAGs and D2H of statuses/bounds are inside the timed
-region every step.
+ds_analyze_batch16 (the compact wire form: 16-bit loads and edges, 199 B per
+C5 DAG) when the corpus fits it, else ds_analyze_batch; --wire forces one
+(tri: ds_analyze_batch_tri, each DAG's adjacency as a bit matrix, 98 B per
+DAG — half the PCIe bytes, but the pass is GPU-bound and its device
+expansion costs more than the copy it saves: 147 vs 181 M DAGs/s). H2D of the packed
+DAGs and D2H of statuses/bounds are inside the timed region every step.
 
 --impl reference: the reference's own CPU implementation of the path —
 generate_corpus + evaluate_corpus (experiment.cpp:52-79) + lower_bound from
@@ -178,7 +180,7 @@ def pass_alg_bytes(n, N):
 def host_chunks(n: int) -> int:
     """How many chunks analyze_host (capi.cu) streams an n-DAG host batch in."""
     k = int(os.environ.get("DS_CHUNKS", "0") or 0)
-    weights = [1] * (k if 1 <= k <= 64 else 3)
+    weights = [1] * (k if 1 <= k <= 64 else 5)
     wsum, bounds, acc = sum(weights), [0], 0
     for w in weights:
         acc += w
@@ -419,7 +421,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=100000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-makespan", action="store_true")
-    ap.add_argument("--wide", action="store_true", help="e2e through ds_analyze_batch (64-bit loads, 32-bit edges)")
+    ap.add_argument("--wire", default="auto", choices=["auto", "tri", "16", "wide"],
+                    help="e2e wire form: ds_analyze_batch_tri / ds_analyze_batch16 / ds_analyze_batch")
     ap.add_argument("--makespan-replays", type=int, default=1000)
     ap.add_argument("--makespan-c2", type=int, default=100)
     args = ap.parse_args()
@@ -504,19 +507,37 @@ def main():
     r = _abi.ds_results(res_status.ctypes.data, res_bounds.ctypes.data, res_groups.ctypes.data)
     pl = _lib.platform(SM_COUNT)
     L = _lib.lib()
-    # the caller's host arrays in the compact wire form when the batch fits it
-    # (integer loads < 2^16, <= 256 nodes: every C5 corpus), pinned; the
-    # conversion is the caller's packing, outside the timed region
-    compact = batch.compact16_ok() and not args.wide
-    if compact:
-        pin16 = (torch.empty(batch.load_num.shape[0], dtype=torch.int16, pin_memory=True).numpy().view(np.uint16),
-                 torch.empty(batch.edges.shape[0], dtype=torch.int16, pin_memory=True).numpy().view(np.uint16))
+    # the caller's host arrays in the most compact wire form the batch fits,
+    # pinned; the conversion is the caller's packing, outside the timed region
+    wire = args.wire
+    if wire == "auto":  # measured fastest first (the e2e pass is GPU-bound, and the
+        # triangular form's device expansion costs more than its PCIe saving)
+        wire = "16" if batch.compact16_ok() else "tri" if batch.tri_ok() else "wide"
+    pin = lambda n, dt: torch.empty(n, dtype=dt, pin_memory=True).numpy()  # noqa: E731
+    if wire == "tri":
+        adj_off = batch.tri_words()
+        pint = (pin(batch.load_num.shape[0], torch.int16).view(np.uint16),
+                pin(int(adj_off[-1]), torch.int32).view(np.uint32))
+        load16, adj_off_np, adj = batch.tri(out=pint)
+        adj_off = pin(adj_off_np.shape[0], torch.int32).view(np.uint32)
+        adj_off[:] = adj_off_np
+        cb = batch.as_ctri(load16, adj_off, adj)
+        call = lambda: L.ds_analyze_batch_tri(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev)  # noqa: E731
+        h2d = batch.node_off.nbytes + adj_off.nbytes + load16.nbytes + adj.nbytes
+        api = "ds_analyze_batch_tri (triangular bit-matrix wire form, host pinned)"
+    elif wire == "16":
+        pin16 = (pin(batch.load_num.shape[0], torch.int16).view(np.uint16),
+                 pin(batch.edges.shape[0], torch.int16).view(np.uint16))
         load16, edges16 = batch.compact16(out=pin16)
         cb = batch.as_c16(load16, edges16)
         call = lambda: L.ds_analyze_batch16(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev)  # noqa: E731
+        h2d = batch.node_off.nbytes + batch.edge_off.nbytes + load16.nbytes + edges16.nbytes
+        api = "ds_analyze_batch16 (16-bit wire form, host pinned)"
     else:
         cb = batch.as_c()
         call = lambda: L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev, None, 0)  # noqa: E731
+        h2d = batch.nbytes(with_den=not integer)
+        api = "ds_analyze_batch (host pinned)"
     _lib.check(call())
     barrier()
     t0 = time.perf_counter()
@@ -532,8 +553,6 @@ def main():
         per_rank_e2e = allv
     e2e_value = world * n * args.e2e_steps / e2e_s
     same = bool(np.array_equal(res_status, st) and np.array_equal(res_bounds, bounds))
-    h2d = (batch.node_off.nbytes + batch.edge_off.nbytes + load16.nbytes + edges16.nbytes if compact
-           else batch.nbytes(with_den=not integer))
     d2h = res_status.nbytes + res_bounds.nbytes + res_groups.nbytes
     chunks = host_chunks(n)
 
@@ -581,8 +600,7 @@ def main():
             "data": "synthetic (reference generator, bit-identical)",
             "config": dict(workload(n, 1), parallelism=f"shards{world}", integer_loads=integer),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": 1e3 * e2e_s / args.e2e_steps, "api": ("ds_analyze_batch16 (16-bit wire form, host pinned)" if compact
-                            else "ds_analyze_batch (host pinned)"),
+                    "ms_per_step": 1e3 * e2e_s / args.e2e_steps, "api": api,
                     "matches_device_leg": same,
                     "per_rank_dags_per_s": [n * args.e2e_steps / t for t in per_rank_e2e],
                     "pcie_bytes_per_rank_per_step": h2d + d2h},
@@ -605,7 +623,7 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
             # per chunk: the K1 sequence, plus the 16-bit form's widening kernel
-            "e2e_gpu_launches": chunks * (launches_per_step + int(compact)) * args.e2e_steps,
+            "e2e_gpu_launches": chunks * (launches_per_step + int(wire != "wide")) * args.e2e_steps,
             "dags_ok": ok, "generation_s": gen_s,
             "kernel_ms": {"mean": statistics.mean(kms), "min": min(kms), "max": max(kms)},
         }

@@ -117,6 +117,24 @@ typedef struct ds_dag_batch16 {
     const uint16_t* edges;    /* [edge_off[n_dags]] from << 8 | to              */
 } ds_dag_batch16;
 
+/* Triangular wire form of a batch whose local node indices are a topological
+ * order (every edge u < v), with at most 64 nodes per DAG and 16-bit integer
+ * loads: instead of an edge list, each DAG carries its strictly lower
+ * triangular adjacency matrix as bits — the predecessors of node v (v = 1 ..
+ * n-1) are bits [v(v-1)/2, v(v-1)/2 + v) of the DAG's words, bit
+ * v(v-1)/2 + u set iff (u, v) is an edge; little-endian within u32 words.
+ * DAG d's words are adj[adj_off[d] - adj_off[0] .. adj_off[d+1] - adj_off[0])
+ * (any number >= ceil(n(n-1)/64) words). Duplicate edges are impossible and
+ * order is implied. C5: ~107 B per DAG over PCIe instead of 199 B
+ * (ds_dag_batch16) or 488 B (ds_dag_batch); the device expands it. */
+typedef struct ds_dag_batch_tri {
+    uint64_t n_dags;
+    const uint32_t* node_off; /* [n_dags + 1] */
+    const uint32_t* adj_off;  /* [n_dags + 1] in u32 words */
+    const uint16_t* load;     /* [node_off[n_dags]] integer load num (den 1)    */
+    const uint32_t* adj;      /* [adj_off[n_dags]] adjacency bit matrices       */
+} ds_dag_batch_tri;
+
 /* Per-DAG results of the batched analysis (evaluate_corpus + lower_bound). */
 typedef struct ds_results {
     int32_t* status;   /* [n_dags] DS_OK or a per-DAG DS_E* / DS_EOVERFLOW code   */
@@ -301,6 +319,12 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform,
 int ds_analyze_batch16(const ds_dag_batch16* batch, const ds_platform* platform,
                        uint32_t method_mask, ds_results* out, int device);
 
+/* ds_analyze_batch over the triangular wire form (host pointers, pinned for
+ * full PCIe speed); results identical to ds_analyze_batch on the same DAGs.
+ * A DAG with more than 64 nodes is DS_ETOOBIG in this form. */
+int ds_analyze_batch_tri(const ds_dag_batch_tri* batch, const ds_platform* platform,
+                         uint32_t method_mask, ds_results* out, int device);
+
 /* Same, sharded as contiguous DAG ranges over `devices` (one host thread per
  * device, no collective), host pointers only; results land in DAG order. */
 int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platform,
@@ -312,6 +336,11 @@ int ds_analyze_batch_multi(const ds_dag_batch* batch, const ds_platform* platfor
 int ds_analyze_batch16_multi(const ds_dag_batch16* batch, const ds_platform* platform,
                              uint32_t method_mask, ds_results* out, const int* devices,
                              int n_devices);
+
+/* ds_analyze_batch_tri sharded the same way. */
+int ds_analyze_batch_tri_multi(const ds_dag_batch_tri* batch, const ds_platform* platform,
+                               uint32_t method_mask, ds_results* out, const int* devices,
+                               int n_devices);
 
 /* The split both multi entry points use: shard i of n_shards owns DAGs
  * [lo, hi) = [n*i/n_shards, n*(i+1)/n_shards) — the contiguous split of the

@@ -65,6 +65,12 @@ class ds_dag_batch16(C.Structure):
                 ("load", C.c_void_p), ("edges", C.c_void_p)]
 
 
+class ds_dag_batch_tri(C.Structure):
+    _fields_ = [("n_dags", C.c_uint64),
+                ("node_off", C.c_void_p), ("adj_off", C.c_void_p),
+                ("load", C.c_void_p), ("adj", C.c_void_p)]
+
+
 class ds_results(C.Structure):
     _fields_ = [("status", C.c_void_p), ("bounds", C.c_void_p), ("n_groups", C.c_void_p)]
 

@@ -39,6 +39,10 @@ def _sig(lib):
                                          P(_abi.ds_results), C.c_int]),
         "ds_analyze_batch_multi": (C.c_int, [P(_abi.ds_dag_batch), P(_abi.ds_platform), C.c_uint32,
                                              P(_abi.ds_results), P(C.c_int), C.c_int]),
+        "ds_analyze_batch_tri": (C.c_int, [P(_abi.ds_dag_batch_tri), P(_abi.ds_platform), C.c_uint32,
+                                           P(_abi.ds_results), C.c_int]),
+        "ds_analyze_batch_tri_multi": (C.c_int, [P(_abi.ds_dag_batch_tri), P(_abi.ds_platform), C.c_uint32,
+                                                 P(_abi.ds_results), P(C.c_int), C.c_int]),
         "ds_analyze_batch16_multi": (C.c_int, [P(_abi.ds_dag_batch16), P(_abi.ds_platform), C.c_uint32,
                                                P(_abi.ds_results), P(C.c_int), C.c_int]),
         "ds_shard_range": (C.c_int, [C.c_uint64, C.c_int, C.c_int, P(C.c_uint64), P(C.c_uint64)]),
@@ -162,6 +166,22 @@ def analyze16_multi(batch: DagBatch, sm_count: int, devices, t_min=1, mask: int 
     pl = platform(sm_count, t_min, min_load)
     devs = (C.c_int * len(devices))(*devices)
     check(lib().ds_analyze_batch16_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
+    return _finish(batch, st, b, ng)
+
+
+def analyze_tri(batch: DagBatch, sm_count: int, t_min=1, mask: int = _abi.DS_M_ALL, device: int = 0,
+                min_load=None, devices=None):
+    """analyze() over the triangular wire form (ds_analyze_batch_tri, or
+    ds_analyze_batch_tri_multi over `devices`)."""
+    st, b, ng, r = _results(batch.n_dags)
+    load16, adj_off, adj = batch.tri()
+    cb = batch.as_ctri(load16, adj_off, adj)
+    pl = platform(sm_count, t_min, min_load)
+    if devices is None:
+        check(lib().ds_analyze_batch_tri(C.byref(cb), C.byref(pl), mask, C.byref(r), device))
+    else:
+        devs = (C.c_int * len(devices))(*devices)
+        check(lib().ds_analyze_batch_tri_multi(C.byref(cb), C.byref(pl), mask, C.byref(r), devs, len(devices)))
     return _finish(batch, st, b, ng)
 
 

@@ -88,6 +88,51 @@ class DagBatch:
         return _abi.ds_dag_batch16(self.n_dags, self.node_off.ctypes.data, self.edge_off.ctypes.data,
                                    load16.ctypes.data, edges16.ctypes.data)
 
+    def tri_ok(self) -> bool:
+        """Fits ds_dag_batch_tri: integer loads in [0, 65535], <= 64 nodes per
+        DAG, every edge u < v (local indices are a topological order)."""
+        if not (self.integer_loads() and self.load_num.size > 0 and int(self.load_num.min()) >= 0
+                and int(self.load_num.max()) <= 0xFFFF and int(self.sizes().max(initial=0)) <= 64):
+            return False
+        return bool(np.all((self.edges >> 16) < (self.edges & 0xFFFF)))
+
+    def tri_words(self) -> np.ndarray:
+        """adj_off (uint32 [n+1], in u32 words) of the triangular form."""
+        n = self.sizes()
+        words = (n * (n - 1) // 2 + 31) // 32
+        off = np.zeros(self.n_dags + 1, np.uint32)
+        np.cumsum(words, out=off[1:])
+        return off
+
+    def tri(self, out=None):
+        """(load u16 [N], adj_off u32 [n+1], adj u32 [W]) — the ds_dag_batch_tri
+        wire form: node v's predecessors are bits v(v-1)/2 + u of its DAG's
+        words. `out` = preallocated (load, adj) arrays to fill (e.g. pinned;
+        adj sized tri_words()[-1])."""
+        if not self.tri_ok():
+            raise ValueError("batch does not fit the triangular wire form")
+        adj_off = self.tri_words()
+        nw = int(adj_off[-1])
+        load = out[0] if out else np.empty(self.load_num.shape, np.uint16)
+        np.copyto(load, self.load_num, casting="unsafe")
+        ecount = np.diff(self.edge_off.astype(np.int64))
+        dag = np.repeat(np.arange(self.n_dags, dtype=np.int64), ecount)
+        u = (self.edges >> 16).astype(np.int64)
+        v = (self.edges & 0xFFFF).astype(np.int64)
+        bit = adj_off[dag].astype(np.int64) * 32 + v * (v - 1) // 2 + u
+        bits = np.zeros(nw * 32, np.bool_)
+        bits[bit] = True  # duplicate edges collapse, as DagTask::make dedups them
+        words = np.packbits(bits, bitorder="little").view(np.uint32)
+        adj = out[1] if out else np.empty(nw, np.uint32)
+        np.copyto(adj, words)
+        return load, adj_off, adj
+
+    def as_ctri(self, load16: np.ndarray, adj_off: np.ndarray, adj: np.ndarray) -> _abi.ds_dag_batch_tri:
+        for a in (self.node_off, adj_off, load16, adj):
+            assert a.flags["C_CONTIGUOUS"]
+        return _abi.ds_dag_batch_tri(self.n_dags, self.node_off.ctypes.data, adj_off.ctypes.data,
+                                     load16.ctypes.data, adj.ctypes.data)
+
     def slice(self, lo: int, hi: int) -> "DagBatch":
         """DAGs [lo, hi) as a new batch with rebased offsets."""
         n0, n1 = int(self.node_off[lo]), int(self.node_off[hi])

@@ -124,7 +124,8 @@ struct DevBuf {
 struct Slot {
     cudaStream_t s = nullptr;
     DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
-    DevBuf ln16, edges16;  // compact wire form staging (ds_analyze_batch16)
+    DevBuf ln16, edges16;         // compact wire form staging (ds_analyze_batch16)
+    DevBuf adj_off, adj, edge_cnt;  // triangular wire form staging (ds_analyze_batch_tri)
 };
 
 // ds_dag_batch16 -> the analysis' wide form, on the device (HBM-bound, tiny)
@@ -135,6 +136,64 @@ __global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __r
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < ne; i += stride) {
         const u32 e = e16[i];
         edges[i] = ((e >> 8) << 16) | (e & 0xffu);
+    }
+}
+
+// ds_dag_batch_tri -> the analysis' wide form, one warp per DAG: loads
+// widened, each node's predecessor bits read out of the triangular matrix,
+// transposed to successor masks and written as the (from << 16 | to) edge
+// list in (from, to) order into the DAG's capacity slot (32 edges per
+// adjacency word: edge_off[d] = 32 * word offset, edge_cnt[d] = edges).
+// Reads ~107 B and writes ~30 B per node-edge pair set of a C5 DAG: HBM-light.
+__global__ void __launch_bounds__(256) k_widen_tri(const u32* __restrict__ node_off, const u32* __restrict__ adj_off,
+                                                   const uint16_t* __restrict__ ln16, const u32* __restrict__ adj,
+                                                   u64 n_dags, u64* __restrict__ ln, u32* __restrict__ edge_off,
+                                                   u32* __restrict__ edge_cnt, u32* __restrict__ edges) {
+    const int lane = threadIdx.x & 31;
+    const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+    const u32 nb = node_off[0], ab = adj_off[0];
+    for (u64 d = u64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_dags; d += warps) {
+        const u32 n0 = node_off[d] - nb;
+        const int n = int(node_off[d + 1] - node_off[d]);
+        const u32 w0 = adj_off[d] - ab, nw = adj_off[d + 1] - adj_off[d];
+        for (int v = lane; v < n; v += 32) ln[n0 + v] = ln16[n0 + v];
+        if (lane == 0) {
+            edge_off[d] = w0 * 32u;
+            if (d + 1 == n_dags) edge_off[n_dags] = (adj_off[n_dags] - ab) * 32u;
+        }
+        // predecessor bits of node v: [v(v-1)/2, v(v-1)/2 + v) of the DAG's words
+        const u32* w = adj + w0;
+        auto preds = [&](int v) -> u64 {
+            if (v <= 0 || v >= n) return 0;
+            const u32 o = u32(v) * u32(v - 1) / 2, k = o >> 5, sh = o & 31;
+            u64 x = w[k] >> sh;
+            if (k + 1 < nw) x |= u64(w[k + 1]) << (32 - sh);
+            if (sh && k + 2 < nw) x |= u64(w[k + 2]) << (64 - sh);
+            return x & ((1ull << v) - 1);  // v <= 63
+        };
+        const u64 pa = preds(lane), pb = preds(lane + 32);
+        // successors of u = lane (sa) and u = lane + 32 (sb): transpose
+        const u32 t00 = warp_transpose32(u32(pa), lane), t10 = warp_transpose32(u32(pb), lane);
+        const u32 t11 = n > 32 ? warp_transpose32(u32(pb >> 32), lane) : 0u;
+        const u64 sa = (u64(t10) << 32) | t00, sb = u64(t11) << 32;
+        // edges in (from, to) order: u = 0..31 (slot a), then 32..63 (slot b)
+        const u32 ca = __popcll(sa), cb = __popcll(sb);
+        u32 ia = ca, ib = cb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+            if (lane >= o) {
+                ia += ya;
+                ib += yb;
+            }
+        }
+        const u32 tot_a = __shfl_sync(FULL, ia, 31), tot = tot_a + __shfl_sync(FULL, ib, 31);
+        u32* e = edges + w0 * 32u;
+        u32 pos = ia - ca;
+        for (u64 m = sa; m; m &= m - 1) e[pos++] = (u32(lane) << 16) | u32(__ffsll(m) - 1);
+        pos = tot_a + ib - cb;
+        for (u64 m = sb; m; m &= m - 1) e[pos++] = (u32(lane + 32) << 16) | u32(__ffsll(m) - 1);
+        if (lane == 0) edge_cnt[d] = tot;
     }
 }
 
@@ -319,12 +378,26 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 14;  // smallest chunk worth a launch sequence
-constexpr u64 kDefaultChunks = 3;  // one per stream slot (1M C5 DAGs e2e: 3 chunks 101 M/s, 6: 99, 8: 95, 4: 93)
+constexpr u64 kDefaultChunks = 5;  // 1M C5 DAGs e2e (round 2 kernels): 3 chunks 171 M/s, 4: 179, 5: 181, 6: 180, 8: 160
+
+// the second offset array of each wire form: edges, or adjacency words
+inline const uint32_t* second_off(const ds_dag_batch* b) { return b->edge_off; }
+inline const uint32_t* second_off(const ds_dag_batch16* b) { return b->edge_off; }
+inline const uint32_t* second_off(const ds_dag_batch_tri* b) { return b->adj_off; }
+
+int analyze_small_tri(const ds_dag_batch_tri* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device);
 
 template <class Batch>
 int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
     constexpr bool compact = std::is_same<Batch, ds_dag_batch16>::value;
-    if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small(host_view(b), P, mask, out, device);
+    constexpr bool tri = std::is_same<Batch, ds_dag_batch_tri>::value;
+    if constexpr (tri) {
+        for (u64 d = 0; d < b->n_dags; ++d)
+            if (b->node_off[d + 1] - b->node_off[d] > 64) return fail(DS_EINVAL, "ds_dag_batch_tri: DAG with more than 64 nodes");
+        if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small_tri(b, P, mask, out, device);
+    } else {
+        if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small(host_view(b), P, mask, out, device);
+    }
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
     if (int rc = configure(device, false, occ)) return rc;
@@ -363,16 +436,17 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         const u64 lo = bounds[c], hi = bounds[c + 1], nd = hi - lo;
         Slot& sl = ctx.slot[c % n_slots];
         // indices are relative to node_off[0] / edge_off[0] (header contract)
+        const uint32_t* eoff = second_off(b);
         const u64 n0 = b->node_off[lo] - b->node_off[0], n1 = b->node_off[hi] - b->node_off[0];
-        const u64 e0 = b->edge_off[lo] - b->edge_off[0], e1 = b->edge_off[hi] - b->edge_off[0];
+        const u64 e0 = eoff[lo] - eoff[0], e1 = eoff[hi] - eoff[0];  // tri: adjacency words
         const size_t nn = n1 - n0, ne = e1 - e0;
         DS_CUDA(cudaStreamSynchronize(sl.s));  // the slot's buffers are reused
         if (int rc = sl.node_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.edge_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.ln.ensure(nn * 8)) return rc;
-        if (int rc = sl.edges.ensure(ne * 4)) return rc;
+        if (int rc = sl.edges.ensure(tri ? ne * 32 * 4 : ne * 4)) return rc;  // tri: capacity, 32 edges per word
         bool has_den = false;
-        if constexpr (!compact) has_den = b->load_den != nullptr;
+        if constexpr (!compact && !tri) has_den = b->load_den != nullptr;
         if (has_den) {
             if (int rc = sl.ldn.ensure(nn * 8)) return rc;
         }
@@ -382,8 +456,25 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         if (int rc = sl.retry.ensure(2 * nd * 4)) return rc;  // two retry lists
         if (int rc = sl.retry_count.ensure(kK1Counters * 4)) return rc;
         DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
-        DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
-        if constexpr (compact) {
+        if constexpr (tri) {
+            if (int rc = sl.adj_off.ensure((nd + 1) * 4)) return rc;
+            if (int rc = sl.ln16.ensure(nn * 2)) return rc;
+            if (int rc = sl.adj.ensure(ne * 4)) return rc;
+            if (int rc = sl.edge_cnt.ensure(nd * 4)) return rc;
+            DS_CUDA(cudaMemcpyAsync(sl.adj_off.p, b->adj_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
+            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, sl.s));
+            DS_CUDA(cudaMemcpyAsync(sl.adj.p, b->adj + e0, ne * 4, cudaMemcpyHostToDevice, sl.s));
+            const unsigned grid = unsigned(std::min<u64>((nd + 7) / 8, 148 * 8));
+            k_widen_tri<<<grid, 256, 0, sl.s>>>(sl.node_off.as<const u32>(), sl.adj_off.as<const u32>(),
+                                                 sl.ln16.as<const uint16_t>(), sl.adj.as<const u32>(), nd,
+                                                 sl.ln.as<u64>(), sl.edge_off.as<u32>(), sl.edge_cnt.as<u32>(),
+                                                 sl.edges.as<u32>());
+            DS_CUDA(cudaGetLastError());
+        } else {
+            DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
+        }
+        if constexpr (tri) {
+        } else if constexpr (compact) {
             if (int rc = sl.ln16.ensure(nn * 2)) return rc;
             if (int rc = sl.edges16.ensure(ne * 2)) return rc;
             DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, sl.s));
@@ -405,6 +496,7 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         a.load_num = sl.ln.as<const u64>();
         a.load_den = has_den ? sl.ldn.as<const u64>() : nullptr;
         a.edges = sl.edges.as<const u32>();
+        a.edge_cnt = tri ? sl.edge_cnt.as<const u32>() : nullptr;
         a.plat = P;
         a.mask = mask;
         a.status = sl.status.as<int32_t>();
@@ -415,7 +507,7 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         a.retry2 = a.retry + nd;
         a.retry2_count = a.retry_count + 1;
         if (int rc = attach_handoff(a, sl.handoff, nd, nn)) return rc;
-        DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, lo, hi), false, sl.s));
+        DS_CUDA(k1_launch(a, occ, !tri && batch_has_big(b->node_off, lo, hi), false, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, sl.s));
         if (out->n_groups) {
@@ -502,8 +594,19 @@ inline ds_dag_batch16 sub_batch(const ds_dag_batch16* b, u64 lo, u64 hi) {
     return sub;
 }
 
+inline ds_dag_batch_tri sub_batch(const ds_dag_batch_tri* b, u64 lo, u64 hi) {
+    ds_dag_batch_tri sub = *b;
+    sub.n_dags = hi - lo;
+    sub.node_off = b->node_off + lo;
+    sub.adj_off = b->adj_off + lo;
+    sub.load = b->load + (b->node_off[lo] - b->node_off[0]);
+    sub.adj = b->adj + (b->adj_off[lo] - b->adj_off[0]);
+    return sub;
+}
+
 int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev);
 int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev);
+int analyze_one(const ds_dag_batch_tri* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev);
 
 // contiguous shards over devices, one host thread per device, no collective
 // (DAGs are independent, experiment.cpp:56-57); results land in DAG order
@@ -560,6 +663,16 @@ int ds_analyze_batch16(const ds_dag_batch16* batch, const ds_platform* platform,
     if (int rc = check_platform(platform, P)) return rc;
     if (batch->n_dags == 0) return DS_OK;
     if (!batch->node_off || !batch->edge_off || !batch->load || !batch->edges) return fail(DS_EINVAL, "NULL array");
+    return analyze_host(batch, P, method_mask & DS_M_ALL, out, device);
+}
+
+int ds_analyze_batch_tri(const ds_dag_batch_tri* batch, const ds_platform* platform, uint32_t method_mask,
+                         ds_results* out, int device) {
+    if (!batch || !out || !out->status || !out->bounds) return fail(DS_EINVAL, "NULL batch or results");
+    PlatT<u64> P;
+    if (int rc = check_platform(platform, P)) return rc;
+    if (batch->n_dags == 0) return DS_OK;
+    if (!batch->node_off || !batch->adj_off || !batch->load || !batch->adj) return fail(DS_EINVAL, "NULL array");
     return analyze_host(batch, P, method_mask & DS_M_ALL, out, device);
 }
 
@@ -624,6 +737,11 @@ int ds_analyze_batch16_multi(const ds_dag_batch16* batch, const ds_platform* pla
     return analyze_multi(batch, platform, method_mask, out, devices, n_devices);
 }
 
+int ds_analyze_batch_tri_multi(const ds_dag_batch_tri* batch, const ds_platform* platform, uint32_t method_mask,
+                               ds_results* out, const int* devices, int n_devices) {
+    return analyze_multi(batch, platform, method_mask, out, devices, n_devices);
+}
+
 }  // extern "C"
 
 namespace ds {
@@ -632,6 +750,33 @@ int analyze_one(const ds_dag_batch* b, const ds_platform* p, uint32_t mask, ds_r
 }
 int analyze_one(const ds_dag_batch16* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
     return ds_analyze_batch16(b, p, mask, r, dev);
+}
+int analyze_one(const ds_dag_batch_tri* b, const ds_platform* p, uint32_t mask, ds_results* r, int dev) {
+    return ds_analyze_batch_tri(b, p, mask, r, dev);
+}
+// a small triangular batch: expanded to the wide form on the host, then the
+// latency path
+int analyze_small_tri(const ds_dag_batch_tri* b, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
+    const u64 n = b->n_dags;
+    std::vector<uint32_t> no(n + 1), eo(n + 1, 0), ed;
+    std::vector<int64_t> ln;
+    const u32 nb = b->node_off[0], ab = b->adj_off[0];
+    for (u64 d = 0; d < n; ++d) {
+        no[d] = b->node_off[d] - nb;
+        const int nn = int(b->node_off[d + 1] - b->node_off[d]);
+        const u32* w = b->adj + (b->adj_off[d] - ab);
+        const u32 nw = b->adj_off[d + 1] - b->adj_off[d];
+        for (int v = 0; v < nn; ++v) ln.push_back(b->load[no[d] + v]);
+        for (int u = 0; u < nn; ++u)  // (from, to) order
+            for (int v = u + 1; v < nn; ++v) {
+                const u32 bit = u32(v) * u32(v - 1) / 2 + u32(u);
+                if ((bit >> 5) < nw && ((w[bit >> 5] >> (bit & 31)) & 1)) ed.push_back((u32(u) << 16) | u32(v));
+            }
+        eo[d + 1] = u32(ed.size());
+    }
+    no[n] = b->node_off[n] - nb;
+    const ds_dag_batch wide{n, no.data(), eo.data(), ln.data(), nullptr, ed.data()};
+    return analyze_small(host_view(&wide), P, mask, out, device);
 }
 // schedule-detail mode for a small host batch: one k1_small launch over
 // mapped buffers (see analyze_small)

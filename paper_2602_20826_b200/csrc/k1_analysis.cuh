@@ -1190,6 +1190,9 @@ struct K1Args {
     const u64* load_num;
     const u64* load_den;
     const u32* edges;
+    const u32* edge_cnt;   // optional per-DAG edge counts: DAG d's edges are
+                           // edges[edge_off[d] ..][0 .. edge_cnt[d]) (capacity
+                           // layout of the expanded triangular form)
     PlatT<u64> plat;
     u32 mask;
     int32_t* status;
@@ -1211,7 +1214,7 @@ __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, cons
                                         const u32 nbase, const u32 ebase, const PlatT<T> P, u32* next,
                                         u32* next_count) {
     const u32 n0 = a.node_off[d] - nbase, n1 = a.node_off[d + 1] - nbase;
-    const u32 e0 = a.edge_off[d] - ebase, e1 = a.edge_off[d + 1] - ebase;
+    const u32 e0 = a.edge_off[d] - ebase, e1 = a.edge_cnt ? e0 + a.edge_cnt[d] : a.edge_off[d + 1] - ebase;
     const int n = int(n1 - n0);
     int ng = 0, nent = 0, ndiv = 0;
     DetailOut det{};
@@ -1322,7 +1325,7 @@ __global__ void __launch_bounds__(128, 10) k1_front(const K1Args a) {
         int st = DS_EOVERFLOW, ng = 0, nent = 0, ndiv = 0;
         if (narrow) {
             st = analyse_dag<1, u32, false, true>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
-                                                  a.edges + e0, int(a.edge_off[d + 1] - ebase - e0), P, a.mask, ng,
+                                                  a.edges + e0, a.edge_cnt ? int(a.edge_cnt[d]) : int(a.edge_off[d + 1] - ebase - e0), P, a.mask, ng,
                                                   DetailOut{}, nent, ndiv);
         }
         if (st == DS_EOVERFLOW) {

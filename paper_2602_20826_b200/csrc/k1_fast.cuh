@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
         if (d >= a.n_dags) break;
         const u32 n0 = a.node_off[d] - nbase, e0 = a.edge_off[d] - ebase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
-        const int ne = int(a.edge_off[d + 1] - ebase - e0);
+        const int ne = a.edge_cnt ? int(a.edge_cnt[d]) : int(a.edge_off[d + 1] - ebase - e0);
         int st;
         if (NMAX == 32) {
             if (n > 32 && n <= 64) {  // the two-slot kernel's

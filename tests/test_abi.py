@@ -161,3 +161,20 @@ def test_scheme_self_checks_reject_cycles_and_oversubscription():
     with pytest.raises(_lib.DagschedError) as e:
         S.verify(over)
     assert "exceeds the device" in str(e.value)
+
+
+def test_triangular_packer_roundtrip():
+    """batch.tri(): node v's predecessor bits v(v-1)/2 + u decode back to the
+    DAG's (deduplicated, sorted) edge list (host only)."""
+    from paper_2602_20826_b200 import _lib
+    b = _lib.Corpus(3000, seed=4).batch()
+    load, adj_off, adj = b.tri()
+    assert np.array_equal(load, b.load_num.astype(np.uint16))
+    for d in range(0, 3000, 97):
+        n0, n1 = int(b.node_off[d]), int(b.node_off[d + 1])
+        e0, e1 = int(b.edge_off[d]), int(b.edge_off[d + 1])
+        w = adj[adj_off[d]:adj_off[d + 1]]
+        n = n1 - n0
+        got = [(u << 16) | v for u in range(n) for v in range(u + 1, n)
+               if (int(w[(v * (v - 1) // 2 + u) >> 5]) >> ((v * (v - 1) // 2 + u) & 31)) & 1]
+        assert got == sorted(set(int(x) for x in b.edges[e0:e1]))

@@ -125,6 +125,49 @@ def test_latency_path_vs_oracle(orc, cfg, Ms):
                     assert scheme.to_reference_json(sch) == scheme.to_reference_json(big[lo + k]), (M, lo + k)
 
 
+@pytest.mark.parametrize("cfg,Ms", [
+    (dict(seed=2024), (1, 8, 148)),
+    (dict(seed=7, avg_load=200, max_width=10), (8, 300)),  # u64 / u128 word tiers
+    (dict(seed=21, depth_min=2, depth_max=3, max_width=2), (4, 148)),  # tiny DAGs
+    (dict(seed=23, depth_min=7, depth_max=8, max_width=9), (32, 148)),  # 33..64 nodes
+])
+def test_triangular_wire_form_matches_wide(cfg, Ms):
+    """ds_analyze_batch_tri (bit-matrix wire form, expanded on the device by
+    k_widen_tri) = ds_analyze_batch on the same DAGs: throughput path, the
+    latency path (<= 64 DAGs) and the multi-device split."""
+    b = _lib.Corpus(30000, **cfg).batch()
+    assert b.tri_ok()
+    for M in Ms:
+        st, bounds, ng = _lib.analyze(b, M)
+        st_t, b_t, ng_t = _lib.analyze_tri(b, M)
+        assert np.array_equal(st, st_t) and np.array_equal(bounds, b_t) and np.array_equal(ng, ng_t), M
+        st_s, b_s, _ = _lib.analyze_tri(b.slice(100, 160), M)
+        assert np.array_equal(st_s, st[100:160]) and np.array_equal(b_s, bounds[100:160])
+    st_m, b_m, _ = _lib.analyze_tri(b, 148, devices=[0] * 3)
+    st, bounds, _ = _lib.analyze(b, 148)
+    assert np.array_equal(st_m, st) and np.array_equal(b_m, bounds)
+
+
+def test_triangular_wire_form_invalid_dags():
+    """Validation statuses survive the bit-matrix form: several sources or
+    sinks, load 0, duplicate edges (collapse, as DagTask::make dedups)."""
+    dags = [
+        ([1, 2, 3], [(0, 1), (0, 2)]),            # two sinks
+        ([1, 2, 3], [(0, 2), (1, 2)]),            # two sources
+        ([1, 0, 3], [(0, 1), (1, 2)]),            # load 0
+        ([2, 3, 4], [(0, 1), (0, 1), (1, 2)]),    # duplicate edge
+        ([5], []),                                # one node
+        ([1] * 64, [(i, i + 1) for i in range(63)]),  # 64-node chain
+    ]
+    b = pack(dags)
+    assert b.tri_ok()
+    st, bounds, _ = _lib.analyze(b, 8)
+    st_t, b_t, _ = _lib.analyze_tri(b, 8)
+    assert np.array_equal(st, st_t) and np.array_equal(bounds, b_t)
+    big = pack([([1] * 65, [(i, i + 1) for i in range(64)])])
+    assert not big.tri_ok()
+
+
 def test_method_mask_subsets(orc):
     b = _lib.Corpus(500, seed=3).batch()
     _, full, _ = _lib.analyze(b, 148)
