@@ -236,6 +236,32 @@ def cpu_baseline_run(batch, kind_pref="ref", target_s=10.0, min_dags=4000, max_d
                       else "oracle/src restatement"}
 
 
+def cpp_api_bench(n_ours=1_000_000, n_ref=100_000, reps=300):
+    """The kept C++ API against the reference's, the same program
+    (tests/cpp/api_bench.cpp) built against each library: C1's
+    (make_fan(8, 20, 1)) analyze() / schedule() latency, and
+    evaluate_corpus over generate_corpus(GenConfig{}, n) end to end
+    (DagTask packing and Rational results included; generation excluded).
+    The reference side runs its own CPU code on the host cores (bounded
+    sample); this side runs the GPU path."""
+    out = {}
+    for name, path, n in (("ours", os.path.join(ROOT, "paper_2602_20826_b200", "_lib", "api_bench"), n_ours),
+                          ("reference", os.path.join(ROOT, "oracle", "_ref", "ref_api_bench"), n_ref)):
+        if not os.path.exists(path):
+            out[name] = {"error": f"{path} not built"}
+            continue
+        try:
+            r = subprocess.run([path, str(n), str(reps)], capture_output=True, text=True, timeout=300)
+            out[name] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-300:]}
+        except Exception as e:  # reported, never required
+            out[name] = {"error": str(e)}
+    out["source"] = "tests/cpp/api_bench.cpp (Makefile api_bench / oracle/Makefile ref_api_bench)"
+    out["reference_threads"] = cpu_cores()
+    return out
+
+
+PLATFORM_BLOCKING_US = 3000.0  # longest whole-context preemption observed on this platform (2.87 ms) + margin
+
 MAKESPAN_MAIN = ("dynamic_prio", "multistream_host", "multistream")
 MAKESPAN_OTHER = ("proposed", "proposed_deps", "dynamic_deps", "serial")
 
@@ -298,7 +324,7 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
 
     proposed_kinds = ("dynamic_prio", "proposed", "proposed_deps", "dynamic_deps")
     per = {}  # (config, kind) -> list of per-DAG arrays
-    ratios, over, stall_like, launches = {}, {}, {}, 0
+    ratios, over, over_b, stall_like, launches = {}, {}, {}, {}, 0
     p50 = {}
     contracts = {"checked_replays": 0, "precedence_violations": 0, "sm_overlap_violations": 0}
     c2_seen = 0
@@ -330,6 +356,7 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
             if kind in proposed_kinds:
                 ratios.setdefault(kind, []).append(mk / bus)
                 over[kind] = over.get(kind, 0) + int((mk > bus).sum())
+                over_b[kind] = over_b.get(kind, 0) + int((mk > bus + PLATFORM_BLOCKING_US).sum())
             launches += (2 if engine == X.ENGINE_DYNAMIC else len(plan.entities) + 1) * (reps + 3)
     configs = {}
     for (cfg, kind), arrs in per.items():
@@ -357,6 +384,15 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
             "tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
             "configs": configs, "measured_over_bound": mob,
             "replays_over_bound_raw": over, "stall_like_replays": stall_like,
+            "platform_blocking": {
+                "B_us": PLATFORM_BLOCKING_US,
+                "replays_over_bound_plus_B": over_b,
+                "rule": "response-time analysis with a blocking term: the Theorem-1 bound assumes a dedicated "
+                        "GPU; on this platform the whole context is preempted for 1.5-2.9 ms every 0.3-10 s "
+                        "(all 148 SMs stop at once; host-side time-slicing through the VM's GPU proxy), so "
+                        "a replay that meets one can exceed the bound by at most B (stalls are >= 0.3 s apart, "
+                        "longer than any makespan here)",
+                "evidence": "profiles/r02_stall_root.txt, profiles/r01_stall_probe.txt (tools/heartbeat.cu)"},
             "trace_contracts_dynamic_prio": contracts, "executor_kernel_launches": launches}
 
 
@@ -585,6 +621,10 @@ def main():
         except Exception as e:  # reported, never required for the headline line
             makespan = {"error": str(e)}
 
+    cpp_api = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpp_api = cpp_api_bench()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -619,6 +659,7 @@ def main():
                                   "frac": alg_bytes / (step_ms / 1e3) / 1e9 / peak},
                          "note": "integer issue/latency-bound exact-rational greedy per DAG; HBM is not the limiter"},
             "cpu_baseline": cpu,
+            "cpp_api": cpp_api,
             "makespan": makespan,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
