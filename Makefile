@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden
 CXXFLAGS:= -std=c++17 -O3 -fPIC -fopenmp -fvisibility=hidden -I/usr/local/cuda/include -Wall -Wno-comment
 LDOMP   := -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp -lpthread
 
-CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k1_small.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o $(LIBDIR)/k5_generate.o $(LIBDIR)/k6_greedy.o
+CU_OBJS := $(LIBDIR)/capi.o $(LIBDIR)/k1_main.o $(LIBDIR)/k1_detail.o $(LIBDIR)/k1_small.o $(LIBDIR)/k3_executor.o $(LIBDIR)/k4_validate.o $(LIBDIR)/k5_generate.o $(LIBDIR)/k6_greedy.o $(LIBDIR)/k1_big8.o $(LIBDIR)/k1_big16_u32.o $(LIBDIR)/k1_big16_u64.o $(LIBDIR)/k1_big16_u128.o
 CU_DEPS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/dagsched_b200.h
 
 .PHONY: all product oracle ref clean

@@ -42,8 +42,11 @@ extern "C" {
 #define DS_E_SINKS 18      /* "expected a single sink node"               dag.cpp:106-108 */
 #define DS_E_LOAD_TMIN 19  /* "load below the platform time unit"         scheduler.cpp:177-182 */
 
-/* Largest DAG the device path accepts (node-index masks are 4 x 64 bits). */
-#define DS_MAX_NODES 256
+/* Largest DAG the device path accepts. Size classes: n <= 64 one warp per
+ * DAG with 1-word masks (k1_fast / k1_front / k1_analyse<1>), <= 256 four
+ * words (k1_analyse<4>), <= 512 eight words in 191 KB of shared memory and
+ * <= 1024 sixteen words in a global-memory warp state (k1_big). */
+#define DS_MAX_NODES 1024
 
 /* Bound slots / method mask bits. Methods mirror experiment.hpp:14
  * (Method::{proposed, greedy, greedy_unaware, graham_para}); LOWER is
@@ -180,8 +183,6 @@ typedef struct ds_group_rec {
     uint16_t n_launches;
     uint16_t n_members;
     uint16_t reserved;
-    uint64_t unlaunched[4];      /* node mask: candidates not launched whole
-                                    (they get the extra dep v_R -> candidate)    */
 } ds_group_rec;
 
 /* Capacities: entities per DAG <= 2 n, executed groups per DAG <= n. Slot bases
@@ -196,6 +197,13 @@ typedef struct ds_scheme_out {
     ds_entity_rec* entities;  /* [2N]                                            */
     ds_group_rec* groups;     /* [N]                                             */
     int64_t* bounds;          /* [n_dags * 10] as in ds_results                  */
+    uint64_t* unlaunched;     /* per executed group, the node mask of candidates
+                                 not launched whole (they get the extra dep
+                                 v_R -> candidate): DAG d (n nodes, w =
+                                 ceil(n/64) words per mask) group g at
+                                 unlaunched[u_d + g*w .. + w), u_d = the sum
+                                 over earlier DAGs k of n_k * w_k (0 when
+                                 NULL: not returned)                          */
 } ds_scheme_out;
 
 /* ------------------------------------------------------ executor (K2/K3) */

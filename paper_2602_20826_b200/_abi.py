@@ -27,7 +27,7 @@ DS_E_LOAD_TMIN = 19
 DS_PF_MIN_LOAD_ONE = 1  # ds_platform.flags: DagTask::make floor = 1 (else t_min)
 DS_PF_PREMADE = 2       # tasks made on the host: only load > 0 is checked
 
-DS_MAX_NODES = 256
+DS_MAX_NODES = 1024
 
 DS_BOUND_PROPOSED, DS_BOUND_GREEDY, DS_BOUND_GREEDY_UNAWARE, DS_BOUND_GRAHAM_PARA, DS_BOUND_LOWER = range(5)
 BOUND_NAMES = ("proposed", "greedy", "greedy_unaware", "graham_para", "lower")
@@ -99,7 +99,7 @@ class ds_group_rec(C.Structure):
                 ("spare_sms", C.c_int32), ("div_group", C.c_uint16),
                 ("bottleneck", C.c_uint16), ("first_entity", C.c_uint16),
                 ("n_launches", C.c_uint16), ("n_members", C.c_uint16),
-                ("reserved", C.c_uint16), ("unlaunched", C.c_uint64 * 4)]
+                ("reserved", C.c_uint16)]
 
 
 class ds_scheme_out(C.Structure):
@@ -107,7 +107,7 @@ class ds_scheme_out(C.Structure):
                 ("n_groups", C.c_void_p), ("n_div_groups", C.c_void_p),
                 ("node_block", C.c_void_p), ("node_div_group", C.c_void_p),
                 ("entities", C.c_void_p), ("groups", C.c_void_p),
-                ("bounds", C.c_void_p)]
+                ("bounds", C.c_void_p), ("unlaunched", C.c_void_p)]
 
 
 class ds_validation(C.Structure):

@@ -54,7 +54,7 @@ BalancedGroupList build_groups(const DagTask& task, const Platform& platform) {
     int32_t st = 0;
     uint16_t ne = 0, ng = 0, nd = 0;
     std::vector<int16_t> blk(n), div(n);
-    ds_scheme_out out{&st, &ne, &ng, &nd, blk.data(), div.data(), nullptr, nullptr, nullptr};
+    ds_scheme_out out{&st, &ne, &ng, &nd, blk.data(), div.data(), nullptr, nullptr, nullptr, nullptr};
     detail::check(ds_schedule_batch(&b, &pl, &out, 0));
     // build_groups has no t_min check of its own (division.cpp:67-126): the
     // device still fills the division when only schedule() would refuse

@@ -114,7 +114,7 @@ void verify(const ScheduleScheme& s, int M) {
 }
 
 ScheduleScheme materialise(const DagTask& t, const Platform& plat, const ds_entity_rec* er, int ne,
-                           const ds_group_rec* gr, int ng) {
+                           const ds_group_rec* gr, int ng, const std::uint64_t* unl) {
     ScheduleScheme s;
     s.platform = plat;
     const std::size_t n = t.size();
@@ -151,8 +151,9 @@ ScheduleScheme materialise(const DagTask& t, const Platform& plat, const ds_enti
         }
         for (int i = L0; i < L1; ++i)  // launched -> successors of the bottleneck
             for (std::uint32_t sc : succ[er[G.bottleneck].origin]) pending[sc].push_back(Dep{eid(t, er[i]), true});
+        const std::uint64_t* unl_g = unl + std::size_t(g) * ((n + 63) / 64);
         for (std::size_t c = 0; c < n; ++c)  // bottleneck -> unlaunched candidates
-            if ((G.unlaunched[c >> 6] >> (c & 63)) & 1) pending[c].push_back(Dep{plan.bottleneck, true});
+            if ((unl_g[c >> 6] >> (c & 63)) & 1) pending[c].push_back(Dep{plan.bottleneck, true});
         for (int i = L1; i < M1; ++i) {
             const ds_entity_rec& r = er[i];
             rec[i] = pending[r.origin];
@@ -239,16 +240,24 @@ std::vector<ScheduleScheme> schedule_ptrs(const std::vector<const DagTask*>& tas
     std::vector<uint16_t> ne(nd), ng(nd), ndv(nd);
     std::vector<ds_entity_rec> ents(std::max<std::size_t>(2 * N, 1));
     std::vector<ds_group_rec> grps(std::max<std::size_t>(N, 1));
+    // unlaunched-candidate masks: n * ceil(n / 64) words per DAG (header layout)
+    std::vector<std::size_t> ubase(nd + 1, 0);
+    for (std::size_t d = 0; d < nd; ++d) {
+        const std::size_t k = tasks[d]->size();
+        ubase[d + 1] = ubase[d] + k * ((k + 63) / 64);
+    }
+    std::vector<std::uint64_t> unl(std::max<std::size_t>(ubase[nd], 1));
     if (bounds) bounds->assign(nd * 10, 0);
     ds_scheme_out out{st.data(), ne.data(), ng.data(), ndv.data(), nullptr, nullptr, ents.data(), grps.data(),
-                      bounds ? bounds->data() : nullptr};
+                      bounds ? bounds->data() : nullptr, unl.data()};
     detail::check(ds_schedule_batch(&b, &pl, &out, device));
     std::vector<ScheduleScheme> res;
     res.reserve(nd);
     for (std::size_t d = 0; d < nd; ++d) {
         detail::raise(st[d], "schedule: task " + std::to_string(d));
         const std::size_t n0 = p.node_off[d];
-        res.push_back(materialise(*tasks[d], platform, ents.data() + 2 * n0, ne[d], grps.data() + n0, ng[d]));
+        res.push_back(
+            materialise(*tasks[d], platform, ents.data() + 2 * n0, ne[d], grps.data() + n0, ng[d], unl.data() + ubase[d]));
     }
     return res;
 }

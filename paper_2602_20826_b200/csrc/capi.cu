@@ -88,11 +88,24 @@ int configure(int device, bool detail, K1Occupancy& occ) {
     return DS_OK;
 }
 
-bool batch_has_big(const uint32_t* node_off, u64 lo, u64 hi) {
-    for (u64 d = lo; d < hi; ++d) {
-        if (node_off[d + 1] - node_off[d] > 64) return true;
+// the largest DAG of DAGs [lo, hi): picks the size-class kernels k1_launch runs
+u32 batch_max_n(const uint32_t* node_off, u64 lo, u64 hi) {
+    u32 m = 0;
+    for (u64 d = lo; d < hi; ++d) m = std::max(m, node_off[d + 1] - node_off[d]);
+    return m;
+}
+
+// detail mode: DAG d's unlaunched-candidate masks start at word base[d] of
+// ds_scheme_out::unlaunched (n_k * ceil(n_k / 64) words per earlier DAG k);
+// returns the total word count
+u64 unl_layout(const uint32_t* node_off, u64 n, u64* base) {
+    u64 w = 0;
+    for (u64 d = 0; d < n; ++d) {
+        const u64 k = node_off[d + 1] - node_off[d];
+        if (base) base[d] = w;
+        w += k * ((k + 63) / 64);
     }
-    return false;
+    return w;
 }
 
 struct DevBuf {
@@ -126,6 +139,7 @@ struct Slot {
     DevBuf node_off, edge_off, ln, ldn, edges, status, bounds, ngroups, retry, retry_count, handoff;
     DevBuf ln16, edges16;         // compact wire form staging (ds_analyze_batch16)
     DevBuf adj_off, adj, edge_cnt;  // triangular wire form staging (ds_analyze_batch_tri)
+    DevBuf big_q, big_scratch;      // DAGs above 256 nodes (k1_big)
 };
 
 // ds_dag_batch16 -> the analysis' wide form, on the device (HBM-bound, tiny)
@@ -235,10 +249,12 @@ struct DetailView {
     ds_group_rec* grp;
     int64_t* bounds;
     size_t out_bytes;
-    size_t o_status, o_ne, o_ng, o_nd, o_nb, o_ndg, o_ent, o_grp, o_bounds;  // offsets in the out arena
+    uint64_t* unl;
+    u64 unl_words;
+    size_t o_status, o_ne, o_ng, o_nd, o_nb, o_ndg, o_ent, o_grp, o_bounds, o_unl;  // offsets in the out arena
 };
 struct DetailCtx {
-    DevBuf in, out, retry, retry_count, k4_over, k4_ratio, k4_st;
+    DevBuf in, out, retry, retry_count, k4_over, k4_ratio, k4_st, big_q, big_scratch;
     PinBuf in_stage, out_stage;
     DetailView v{};
 };
@@ -248,7 +264,7 @@ struct DeviceCtx {
     std::mutex mu;
     bool init = false;
     Slot slot[kMaxSlots];
-    DevBuf retry, retry_count, handoff;  // scratch for the device-pointer entry point
+    DevBuf retry, retry_count, handoff, big_q, big_scratch;  // scratch for the device-pointer entry point
     DetailCtx det;
     PinBuf small_in, small_out;  // latency path: mapped (zero-copy) inputs and outputs
 };
@@ -372,6 +388,21 @@ int attach_handoff(K1Args& a, DevBuf& buf, u64 n_dags, u64 n_nodes) {
     return DS_OK;
 }
 
+// DAGs above 256 nodes: k1_big's tier queues and, above 512, its HBM warp
+// states (allocated on first use, kept with the context's other scratch)
+int attach_big(K1Args& a, DevBuf& q, DevBuf& scratch, u64 n_dags, u32 max_n) {
+    a.big_q = nullptr;
+    a.big_scratch = nullptr;
+    if (max_n <= 256) return DS_OK;
+    if (int rc = q.ensure(2 * n_dags * 4)) return rc;
+    a.big_q = q.as<u32>();
+    if (max_n > 512) {
+        if (int rc = scratch.ensure(size_t(kBigGrid) * kBigScratchPerCta)) return rc;
+        a.big_scratch = scratch.as<unsigned char>();
+    }
+    return DS_OK;
+}
+
 DeviceCtx& device_ctx(int dev) {
     static DeviceCtx ctx[64];
     return ctx[dev & 63];
@@ -396,7 +427,9 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
             if (b->node_off[d + 1] - b->node_off[d] > 64) return fail(DS_EINVAL, "ds_dag_batch_tri: DAG with more than 64 nodes");
         if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small_tri(b, P, mask, out, device);
     } else {
-        if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small(host_view(b), P, mask, out, device);
+        // the latency kernel covers DAGs up to 256 nodes; bigger ones take k1_big
+        if (b->n_dags <= kSmallDags && small_enabled() && batch_max_n(b->node_off, 0, b->n_dags) <= 256)
+            return analyze_small(host_view(b), P, mask, out, device);
     }
     DS_CUDA(cudaSetDevice(device));
     K1Occupancy occ;
@@ -507,7 +540,9 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         a.retry2 = a.retry + nd;
         a.retry2_count = a.retry_count + 1;
         if (int rc = attach_handoff(a, sl.handoff, nd, nn)) return rc;
-        DS_CUDA(k1_launch(a, occ, !tri && batch_has_big(b->node_off, lo, hi), false, sl.s));
+        const u32 max_n = tri ? 64u : batch_max_n(b->node_off, lo, hi);
+        if (int rc = attach_big(a, sl.big_q, sl.big_scratch, nd, max_n)) return rc;
+        DS_CUDA(k1_launch(a, occ, max_n, false, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, sl.s));
         DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, sl.s));
         if (out->n_groups) {
@@ -527,7 +562,8 @@ struct Session {
     K1Args args{};
     K1Occupancy occ;
     K1Marks marks;
-    bool any_big = false;
+    u32 max_n = 0;
+    DevBuf big_q, big_scratch;
     u64 n_dags = 0;
     ~Session() {
         for (int i = 0; i < K1Marks::kMax; ++i)
@@ -712,9 +748,11 @@ int ds_analyze_batch(const ds_dag_batch* batch, const ds_platform* platform, uin
     a.retry2 = a.retry + batch->n_dags;
     a.retry2_count = a.retry_count + 1;
     if (int rc = attach_handoff(a, ctx.handoff, batch->n_dags, u64(ends[1] - ends[0]))) return rc;
-    // device pointers: size classes are unknown on the host, so the n <= 256
-    // kernel always runs (it skips DAGs with n <= 64 after two offset loads)
-    DS_CUDA(k1_launch(a, occ, true, false, s));
+    // device pointers: size classes are unknown on the host, so every
+    // size-class kernel runs (each skips the DAGs of other classes after two
+    // offset loads)
+    if (int rc = attach_big(a, ctx.big_q, ctx.big_scratch, batch->n_dags, DS_MAX_NODES)) return rc;
+    DS_CUDA(k1_launch(a, occ, DS_MAX_NODES, false, s));
     // the scratch is reused by the next call: finish before releasing it
     DS_CUDA(cudaStreamSynchronize(s));
     return DS_OK;
@@ -793,7 +831,9 @@ int schedule_small(const ds_dag_batch* b, const PlatT<u64>& P, ds_scheme_out* ou
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
     const size_t o_ent = 0, o_grp = al(o_ent + 2 * N * sizeof(ds_entity_rec)), o_b = al(o_grp + N * sizeof(ds_group_rec)),
                  o_st = al(o_b + n * 80), o_ne = al(o_st + n * 4), o_ng = al(o_ne + n * 2), o_nd = al(o_ng + n * 2),
-                 o_nb = al(o_nd + n * 2), o_ndg = al(o_nb + N * 2), bytes = o_ndg + N * 2;
+                 o_nb = al(o_nd + n * 2), o_ndg = al(o_nb + N * 2), o_ub = al(o_ndg + N * 2), o_unl = al(o_ub + n * 8);
+    const u64 unl_words = unl_layout(b->node_off, n, nullptr);
+    const size_t bytes = o_unl + unl_words * 8;
     if (int rc = ctx.small_out.ensure(bytes, true)) return rc;
     char* dv = static_cast<char*>(ctx.small_out.dev);
     a.plat = P;
@@ -807,6 +847,9 @@ int schedule_small(const ds_dag_batch* b, const PlatT<u64>& P, ds_scheme_out* ou
     a.det.n_div_groups = reinterpret_cast<uint16_t*>(dv + o_nd);
     a.det.node_block = reinterpret_cast<int16_t*>(dv + o_nb);
     a.det.node_div_group = reinterpret_cast<int16_t*>(dv + o_ndg);
+    a.det.unlaunched = reinterpret_cast<uint64_t*>(dv + o_unl);
+    unl_layout(b->node_off, n, reinterpret_cast<u64*>(static_cast<char*>(ctx.small_out.p) + o_ub));
+    a.unl_base = reinterpret_cast<const u64*>(dv + o_ub);
     DS_CUDA(k1_small_launch(a, true, s));
     DS_CUDA(cudaStreamSynchronize(s));
     const char* r = static_cast<const char*>(ctx.small_out.p);
@@ -822,6 +865,7 @@ int schedule_small(const ds_dag_batch* b, const PlatT<u64>& P, ds_scheme_out* ou
     put(out->entities, o_ent, 2 * N * sizeof(ds_entity_rec));
     put(out->groups, o_grp, N * sizeof(ds_group_rec));
     put(out->bounds, o_b, n * 80);
+    put(out->unlaunched, o_unl, unl_words * 8);
     return DS_OK;
 }
 
@@ -844,7 +888,7 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     // ---- inputs: rebased offsets, loads, edges in one pinned stage -> one H2D
     const size_t i_no = 0, i_eo = al(i_no + (n + 1) * 4), i_ln = al(i_eo + (n + 1) * 4), i_ld = al(i_ln + N * 8),
-                 i_ed = al(i_ld + (b->load_den ? N * 8 : 0)), in_bytes = al(i_ed + E * 4);
+                 i_ed = al(i_ld + (b->load_den ? N * 8 : 0)), i_ub = al(i_ed + E * 4), in_bytes = al(i_ub + n * 8);
     if (int rc = D.in_stage.ensure(in_bytes)) return rc;
     if (int rc = D.in.ensure(in_bytes)) return rc;
     char* st = static_cast<char*>(D.in_stage.p);
@@ -857,6 +901,7 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     std::memcpy(st + i_ln, b->load_num, N * 8);
     if (b->load_den) std::memcpy(st + i_ld, b->load_den, N * 8);
     std::memcpy(st + i_ed, b->edges, E * 4);
+    v.unl_words = unl_layout(b->node_off, n, reinterpret_cast<u64*>(st + i_ub));
     DS_CUDA(cudaMemcpyAsync(D.in.p, st, in_bytes, cudaMemcpyHostToDevice, s));
     char* di = static_cast<char*>(D.in.p);
     v.node_off = reinterpret_cast<u32*>(di + i_no);
@@ -875,7 +920,8 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     v.o_ng = al(v.o_ne + n * 2);
     v.o_nd = al(v.o_ng + n * 2);
     v.o_bounds = al(v.o_nd + n * 2);
-    v.out_bytes = al(v.o_bounds + n * 80);
+    v.o_unl = al(v.o_bounds + n * 80);
+    v.out_bytes = al(v.o_unl + v.unl_words * 8);
     if (int rc = D.out.ensure(v.out_bytes)) return rc;
     if (int rc = D.retry.ensure(2 * n * 4)) return rc;
     if (int rc = D.retry_count.ensure(kK1Counters * 4)) return rc;
@@ -889,6 +935,7 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     v.ng = reinterpret_cast<uint16_t*>(dout + v.o_ng);
     v.nd = reinterpret_cast<uint16_t*>(dout + v.o_nd);
     v.bounds = reinterpret_cast<int64_t*>(dout + v.o_bounds);
+    v.unl = reinterpret_cast<uint64_t*>(dout + v.o_unl);
     DS_CUDA(cudaMemsetAsync(dout + v.o_nb, 0xff, N * 4, s));
     DS_CUDA(cudaMemsetAsync(dout + v.o_ent, 0, v.o_status - v.o_ent, s));
     K1Args a{};
@@ -909,11 +956,15 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     a.det.entities = v.ent;
     a.det.groups = v.grp;
     a.det.bounds = v.bounds;
+    a.det.unlaunched = v.unl;
+    a.unl_base = reinterpret_cast<const u64*>(di + i_ub);
     a.retry = D.retry.as<u32>();
     a.retry_count = D.retry_count.as<u32>();
     a.retry2 = a.retry + n;
     a.retry2_count = a.retry_count + 1;
-    DS_CUDA(k1_launch(a, occ, batch_has_big(b->node_off, 0, n), true, s));
+    const u32 max_n = batch_max_n(b->node_off, 0, n);
+    if (int rc = attach_big(a, D.big_q, D.big_scratch, n, max_n)) return rc;
+    DS_CUDA(k1_launch(a, occ, max_n, true, s));
     return DS_OK;
 }
 }  // namespace ds
@@ -927,7 +978,8 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     const u64 n = b->n_dags;
     if (n == 0) return DS_OK;
     DeviceCtx& ctx = device_ctx(device);
-    if (n <= kSmallDags && small_enabled()) return schedule_small(b, P, out, device, ctx);
+    if (n <= kSmallDags && small_enabled() && batch_max_n(b->node_off, 0, n) <= 256)
+        return schedule_small(b, P, out, device, ctx);
     std::lock_guard<std::mutex> lock(ctx.mu);
     if (int rc = run_detail(b, P, device, ctx)) return rc;
     DetailCtx& D = ctx.det;
@@ -951,6 +1003,7 @@ int ds_schedule_batch(const ds_dag_batch* b, const ds_platform* platform, ds_sch
     put(out->entities, v.o_ent, 2 * N * sizeof(ds_entity_rec));
     put(out->groups, v.o_grp, N * sizeof(ds_group_rec));
     put(out->bounds, v.o_bounds, n * 80);
+    put(out->unlaunched, v.o_unl, v.unl_words * 8);
     return DS_OK;
 }
 
@@ -1045,7 +1098,7 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     }
     if (int rc = upload(b, *S, S->s)) return bail(rc);
     const u64 n = b->n_dags;
-    S->any_big = batch_has_big(b->node_off, 0, n);
+    S->max_n = batch_max_n(b->node_off, 0, n);
     int rc = DS_OK;
     rc = rc ? rc : S->status.ensure(n * 4);
     rc = rc ? rc : S->bounds.ensure(n * 80);
@@ -1070,6 +1123,7 @@ int ds_session_create(const ds_dag_batch* b, const ds_platform* platform, uint32
     a.retry2 = a.retry + n;
     a.retry2_count = a.retry_count + 1;
     if (int rc2 = attach_handoff(a, S->handoff, n, u64(b->node_off[n] - b->node_off[0]))) return bail(rc2);
+    if (int rc2 = attach_big(a, S->big_q, S->big_scratch, n, S->max_n)) return bail(rc2);
     *session = S;
     return DS_OK;
 }
@@ -1078,7 +1132,7 @@ int ds_session_run(void* session, float* kernel_ms) {
     auto* S = static_cast<Session*>(session);
     DS_CUDA(cudaSetDevice(S->device));
     DS_CUDA(cudaEventRecord(S->e0, S->s));
-    DS_CUDA(k1_launch(S->args, S->occ, S->any_big, false, S->s, &S->marks));
+    DS_CUDA(k1_launch(S->args, S->occ, S->max_n, false, S->s, &S->marks));
     DS_CUDA(cudaEventRecord(S->e1, S->s));
     DS_CUDA(cudaEventSynchronize(S->e1));
     if (kernel_ms) DS_CUDA(cudaEventElapsedTime(kernel_ms, S->e0, S->e1));

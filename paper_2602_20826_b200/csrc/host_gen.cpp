@@ -189,6 +189,8 @@ int ds_corpus_generate(const ds_gen_config* g, int64_t count, uint32_t flags, vo
     if (2 + int64_t(c.dmax - 2) * c.width > DS_MAX_NODES)
         return fail(DS_ETOOBIG, "generated DAGs could exceed DS_MAX_NODES nodes");
     if (flags & DS_F_GPU_GENERATE) {
+        if (2 + int64_t(c.dmax - 2) * c.width > 256)
+            return fail(DS_ETOOBIG, "GPU generation (K5) covers DAGs up to 256 nodes; generate larger ones on the host");
         ds::K5Params p;
         p.count = uint64_t(count);
         p.seed = g->seed;

@@ -219,6 +219,8 @@ struct DetailOut {
     ds_group_rec* grp;   // this DAG's group slots
     short* node_block;
     short* node_div_group;
+    uint64_t* unl;       // this DAG's unlaunched-candidate masks (NULL: not kept)
+    int unl_w;           // words per mask: ceil(n / 64)
 };
 
 // --------------------------------------------------------------- phase: loads
@@ -1023,8 +1025,9 @@ K1_PHASE long long p_schedule(WarpState<W, T>& S, const int lane, const int n, c
                 gr.n_launches = (unsigned short)n_launch;
                 gr.n_members = (unsigned short)n_mem;
                 gr.reserved = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) gr.unlaunched[k] = k < W ? (cands.w[k] & ~whole.w[k]) : 0;
+                if (det.unl) {
+                    for (int k = 0; k < det.unl_w; ++k) det.unl[gidx * det.unl_w + k] = cands.w[k] & ~whole.w[k];
+                }
             }
         }
 #pragma unroll
@@ -1190,6 +1193,11 @@ struct K1Args {
     const u64* load_num;
     const u64* load_den;
     const u32* edges;
+    const u64* unl_base;   // detail mode: per DAG, its first word in det.unlaunched
+    u32* big_q;            // n > 256: DAG indices queued from the 32- to the 64-bit
+                           // tier ([0, n)) and from the 64- to the 128-bit tier
+                           // ([n, 2n)); counts at retry_count[10], [11]
+    unsigned char* big_scratch;  // n > 512: global-memory warp states (k1_big<16>)
     const u32* edge_cnt;   // optional per-DAG edge counts: DAG d's edges are
                            // edges[edge_off[d] ..][0 .. edge_cnt[d]) (capacity
                            // layout of the expanded triangular form)
@@ -1223,6 +1231,8 @@ __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, cons
         det.grp = a.det.groups + n0;
         det.node_block = a.det.node_block + n0;
         det.node_div_group = a.det.node_div_group + n0;
+        det.unl = a.det.unlaunched && a.unl_base ? a.det.unlaunched + a.unl_base[d] : nullptr;
+        det.unl_w = (n + 63) / 64;
     }
     int st = analyse_dag<W, T, DETAIL>(S, lane, n, a.load_num + n0, a.load_den ? a.load_den + n0 : nullptr,
                                        a.edges + e0, int(e1 - e0), P, a.mask, ng, det, nent, ndiv);
@@ -1257,7 +1267,8 @@ __device__ __forceinline__ void run_one(WarpState<W, T>& S, const int lane, cons
     __syncwarp();
 }
 
-// Main pass: every DAG of its size class (W=1: n <= 64; W=4: 64 < n <= 256),
+// Main pass: every DAG of its size class (W=1: n <= 64; W=4: 64 < n <= 256;
+// larger ones: k1_big),
 // persistent warps striding over the batch, in 32-bit words. A DAG whose
 // 32-bit pass overflows is queued for the 64-bit retry, and from there for
 // the 128-bit one (k1_analyse_retry).
@@ -1286,8 +1297,8 @@ __global__ void __launch_bounds__(128) k1_analyse(const K1Args a) {
         }
         if (d >= a.n_dags) break;
         const int n = int(a.node_off[d + 1] - a.node_off[d]);
-        if (W > 1 && n <= 64) continue;
-        if (W == 1 && n > 64 && n <= DS_MAX_NODES) continue;
+        if (W > 1 && (n <= 64 || n > 256)) continue;  // k1_analyse<4>: 64 < n <= 256
+        if (W == 1 && n > 64 && n <= DS_MAX_NODES) continue;  // the bigger kernels
         if (!narrow) {
             if (lane == 0) a.retry[atomicAdd(a.retry_count, 1u)] = u32(d);
             __syncwarp();

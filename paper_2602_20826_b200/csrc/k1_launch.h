@@ -44,6 +44,25 @@ inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     return h;
 }
 
+// k1_big*.cu: DAGs above 256 nodes, one launcher per (W, word type, detail);
+// configure = true sets the kernel's shared-memory limit instead of launching
+#define DS_K1_BIG_DECL(NAME) cudaError_t NAME(const K1Args& a, int grid, cudaStream_t s, bool configure);
+DS_K1_BIG_DECL(k1_big_8_u32_b)
+DS_K1_BIG_DECL(k1_big_8_u64_b)
+DS_K1_BIG_DECL(k1_big_8_u128_b)
+DS_K1_BIG_DECL(k1_big_8_u32_d)
+DS_K1_BIG_DECL(k1_big_8_u64_d)
+DS_K1_BIG_DECL(k1_big_8_u128_d)
+DS_K1_BIG_DECL(k1_big_16_u32_b)
+DS_K1_BIG_DECL(k1_big_16_u64_b)
+DS_K1_BIG_DECL(k1_big_16_u128_b)
+DS_K1_BIG_DECL(k1_big_16_u32_d)
+DS_K1_BIG_DECL(k1_big_16_u64_d)
+DS_K1_BIG_DECL(k1_big_16_u128_d)
+#undef DS_K1_BIG_DECL
+constexpr size_t kBigScratchPerCta = sizeof(WarpState<16, u128>);  // HBM warp state of k1_big<16>
+constexpr int kBigGrid = 148;
+
 // Query occupancy once per device and set the dynamic shared-memory limits.
 cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ);
 
@@ -57,8 +76,11 @@ struct K1Marks {
 };
 
 // Launch the main pass(es) and the 128-bit retry pass on `s`. `a.retry` and
-// `a.retry_count` must point to device scratch (count zeroed here).
-cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s,
+// `a.retry_count` must point to device scratch (count zeroed here). max_n:
+// the largest DAG of the batch (DS_MAX_NODES when unknown); above 256 nodes
+// `a.big_q` [2 n_dags] and, above 512, `a.big_scratch` [kBigGrid x
+// kBigScratchPerCta] must be set.
+cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, u32 max_n, bool detail, cudaStream_t s,
                       K1Marks* marks = nullptr);
 
 }  // namespace ds

@@ -36,6 +36,14 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&orr, k1_analyse_retry<DETAIL, u128>, 32, kSmemR128)))
         return e;
     if (o1 < 1 || o4 < 1 || orr < 1) return cudaErrorInvalidConfiguration;
+    {
+        using L = cudaError_t (*)(const K1Args&, int, cudaStream_t, bool);
+        const L cfg[6] = {DETAIL ? k1_big_8_u32_d : k1_big_8_u32_b, DETAIL ? k1_big_8_u64_d : k1_big_8_u64_b,
+                          DETAIL ? k1_big_8_u128_d : k1_big_8_u128_b, DETAIL ? k1_big_16_u32_d : k1_big_16_u32_b,
+                          DETAIL ? k1_big_16_u64_d : k1_big_16_u64_b, DETAIL ? k1_big_16_u128_d : k1_big_16_u128_b};
+        for (L f : cfg)
+            if ((e = f(K1Args{}, 0, nullptr, true)) != cudaSuccess) return e;
+    }
     if (!DETAIL) {
         if ((e = cudaFuncSetAttribute(k1_front<>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemSmall))))
             return e;
@@ -76,7 +84,7 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
 }
 
 template <bool DETAIL>
-cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* marks) {
+cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* marks) {
     if (marks) marks->n = 0;
     if (a.n_dags == 0) return cudaSuccess;
     int mark_i = 0;
@@ -126,7 +134,7 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
         k1_analyse<1, DETAIL><<<cap(occ.grid_small), 32 * kWarpsSmall, kSmemSmall, s>>>(a);
         if ((e = mark("k1_analyse<1>")) != cudaSuccess) return e;
     }
-    if (any_big) {
+    if (max_n > 64) {
         const int gb = int(a.n_dags < u64(occ.grid_big) ? a.n_dags : u64(occ.grid_big));
         k1_analyse<4, DETAIL><<<gb, 32 * kWarpsBig, kSmemBig, s>>>(a);
         if ((e = mark("k1_analyse<4>")) != cudaSuccess) return e;
@@ -155,6 +163,25 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
             if ((e = mark("k1_back_lane")) != cudaSuccess) return e;
         }
     }
+    // DAGs above 256 nodes (k1_big*.cu): 32-bit pass, then the 64- and
+    // 128-bit passes over what overflowed
+    if (max_n > 256) {
+        if (!a.big_q || (max_n > 512 && !a.big_scratch)) return cudaErrorInvalidValue;
+        const bool w16 = max_n > 512;
+        using L = cudaError_t (*)(const K1Args&, int, cudaStream_t, bool);
+        const L w8[3] = {DETAIL ? k1_big_8_u32_d : k1_big_8_u32_b, DETAIL ? k1_big_8_u64_d : k1_big_8_u64_b,
+                         DETAIL ? k1_big_8_u128_d : k1_big_8_u128_b};
+        const L w16f[3] = {DETAIL ? k1_big_16_u32_d : k1_big_16_u32_b, DETAIL ? k1_big_16_u64_d : k1_big_16_u64_b,
+                           DETAIL ? k1_big_16_u128_d : k1_big_16_u128_b};
+        for (int t = 0; t < 3; ++t) {
+            if ((e = w8[t](a, kBigGrid, s, false)) != cudaSuccess) return e;
+            if ((e = mark("k1_big<8>")) != cudaSuccess) return e;
+            if (w16) {
+                if ((e = w16f[t](a, kBigGrid, s, false)) != cudaSuccess) return e;
+                if ((e = mark("k1_big<16>")) != cudaSuccess) return e;
+            }
+        }
+    }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
     // nothing queued each kernel reads the count and exits
     const int gr = int(a.n_dags < u64(occ.grid_retry) ? a.n_dags : u64(occ.grid_retry));
@@ -167,19 +194,19 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, bool any_big, c
 
 #ifndef K1_DETAIL_TU
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ);
-cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* m);
+cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* m);
 
 cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ) {
     return detail ? k1_configure_detail(device, occ) : k1_configure_t<false>(device, occ);
 }
-cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, bool any_big, bool detail, cudaStream_t s,
+cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, u32 max_n, bool detail, cudaStream_t s,
                       K1Marks* marks) {
-    return detail ? k1_launch_detail(a, occ, any_big, s, marks) : k1_launch_t<false>(a, occ, any_big, s, marks);
+    return detail ? k1_launch_detail(a, occ, max_n, s, marks) : k1_launch_t<false>(a, occ, max_n, s, marks);
 }
 #else
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ) { return k1_configure_t<true>(device, occ); }
-cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, bool any_big, cudaStream_t s, K1Marks* m) {
-    return k1_launch_t<true>(a, occ, any_big, s, m);
+cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* m) {
+    return k1_launch_t<true>(a, occ, max_n, s, m);
 }
 #endif
 

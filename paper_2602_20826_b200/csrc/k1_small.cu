@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(32) k1_small(const K1Args a) {
         u64* g = reinterpret_cast<u64*>(a.det.groups + n0);
         for (u64 k = lane; k < u64(n) * sizeof(ds_group_rec) / 8; k += 32) g[k] = 0;
     }
+    if (n > 256 && n <= DS_MAX_NODES) return;  // k1_big (launched after this kernel) takes it
     if (lane == 0) qc = 0;
     __syncwarp();
     const bool narrow = ((a.plat.tmin.n | a.plat.tmin.d) >> 32) == 0;

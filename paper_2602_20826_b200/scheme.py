@@ -106,9 +106,13 @@ def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0, min
     ents = (_abi.ds_entity_rec * max(2 * N, 1))()
     grps = (_abi.ds_group_rec * max(N, 1))()
     bnd = np.zeros((n, 10), np.int64)
+    # unlaunched-candidate masks: n_d * ceil(n_d / 64) words per DAG (header layout)
+    sizes = np.diff(batch.node_off.astype(np.int64))
+    ubase = np.concatenate([[0], np.cumsum(sizes * ((sizes + 63) // 64))]).astype(np.int64)
+    unl = np.zeros(max(int(ubase[-1]), 1), np.uint64)
     out = _abi.ds_scheme_out(st.ctypes.data, ne.ctypes.data, ng.ctypes.data, nd.ctypes.data,
                              nb.ctypes.data, ndg.ctypes.data, C.addressof(ents), C.addressof(grps),
-                             bnd.ctypes.data)
+                             bnd.ctypes.data, unl.ctypes.data)
     cb = batch.as_c()
     pl = platform(sm_count, t_min, min_load)
     check(lib().ds_schedule_batch(C.byref(cb), C.byref(pl), C.byref(out), device))
@@ -131,15 +135,18 @@ def schedule_batch(batch: DagBatch, sm_count: int, t_min=1, device: int = 0, min
         schemes.append(_materialise(
             sm_count, tmin, [ents[2 * n0 + i] for i in range(int(ne[d]))],
             [grps[n0 + i] for i in range(int(ng[d]))], pred, succ,
-            [int(x) for x in nb[n0:n1]], [int(x) for x in ndg[n0:n1]], int(nd[d]), bnd[d]))
+            [int(x) for x in nb[n0:n1]], [int(x) for x in ndg[n0:n1]], int(nd[d]), bnd[d],
+            unl[ubase[d]:ubase[d + 1]]))
         if batch.node_ids is not None:
             schemes[-1].node_ids = list(batch.node_ids[d])
     return schemes, status
 
 
-def _materialise(M, tmin, erecs, grecs, pred, succ, node_block, node_div, n_div, brow) -> Scheme:
-    """Replay of scheduler.cpp:286-385 bookkeeping over the device records."""
+def _materialise(M, tmin, erecs, grecs, pred, succ, node_block, node_div, n_div, brow, unl) -> Scheme:
+    """Replay of scheduler.cpp:286-385 bookkeeping over the device records
+    (``unl``: this DAG's unlaunched-candidate masks, ceil(n/64) words per group)."""
     n = len(pred)
+    uw = (n + 63) // 64
     ents = []
     for r in erecs:
         e = Entity(EntityId(r.origin, r.generation, r.part), _q(r.load_num, r.load_den), r.parallelism,
@@ -169,7 +176,7 @@ def _materialise(M, tmin, erecs, grecs, pred, succ, node_block, node_div, n_div,
         for e in launches:  # scheduler.cpp:336-341
             for s in succ[bott.origin]:
                 eps[s].append((e.id, True))
-        mask = sum(int(g.unlaunched[k]) << (64 * k) for k in range(4))
+        mask = sum(int(unl[gi * uw + k]) << (64 * k) for k in range(uw))
         for c in range(n):  # scheduler.cpp:342-346
             if (mask >> c) & 1:
                 eps[c].append((bott, True))

@@ -1,0 +1,157 @@
+"""GPU parity for DAGs above 256 nodes (k1_big: W = 8 shared-memory and
+W = 16 HBM warp states, all three word tiers) through the C-ABI.
+
+The reference has no size limit (boost::dynamic_bitset,
+/root/reference/proj/include/dagsched/dag.hpp:89-90); the paper's |V| sweep
+at P = 32 passes 256 nodes at depth ~9. Corpora come from the
+reference's own generate_corpus (oracle/_ref) and every status, bound and
+write_scheme JSON is compared bit-exact with the reference's.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import bindings
+from paper_2602_20826_b200 import _abi, _lib, scheme
+from paper_2602_20826_b200.batch import from_arrays, pack
+from tests import helpers
+
+pytestmark = pytest.mark.gpu
+
+# generate_corpus configs: P = 32 as in the paper's |V| sweep, 186..483
+# nodes (mostly the W = 8 class), and 483..940 nodes (the W = 16 class)
+CFG_MID = dict(depth_min=16, depth_max=26, max_width=32)
+CFG_HUGE = dict(depth_min=26, depth_max=34, max_width=48)
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return bindings.Checker("ref")
+
+
+def _corpus(ref, count, seed, **cfg):
+    c = ref.generate(count, seed=seed, **cfg)
+    return c, c.pack()
+
+
+def _analyze_device(b, M):
+    """ds_analyze_batch over device pointers (DS_F_DEVICE_PTRS)."""
+    import torch
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(getattr(b, k).view(np.int32) if getattr(b, k).dtype == np.uint32
+                             else getattr(b, k)).to(dev) for k in ("node_off", "edge_off", "load_num", "edges")}
+    out_st = torch.zeros(b.n_dags, dtype=torch.int32, device=dev)
+    out_b = torch.zeros(b.n_dags * 10, dtype=torch.int64, device=dev)
+    ld = torch.from_numpy(b.load_den).to(dev)
+    cb = _abi.ds_dag_batch(b.n_dags, t["node_off"].data_ptr(), t["edge_off"].data_ptr(), t["load_num"].data_ptr(),
+                           ld.data_ptr(), t["edges"].data_ptr())
+    r = _abi.ds_results(out_st.data_ptr(), out_b.data_ptr(), None)
+    pl = _lib.platform(M)
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), 0,
+                                           C.c_void_p(stream), _abi.DS_F_DEVICE_PTRS))
+    torch.cuda.synchronize()
+    return out_st.cpu().numpy(), out_b.cpu().numpy().reshape(-1, 10)
+
+
+def _check_bounds(c, b, M, t_min=1):
+    st_ref, b_ref, _ = c.evaluate(M, t_min)
+    st, bounds, _ = _lib.analyze(b, M, t_min)
+    assert np.array_equal(st, st_ref), (M, t_min, np.nonzero(st != st_ref)[0][:5])
+    bad = np.nonzero((bounds != b_ref).any(1))[0]
+    assert len(bad) == 0, (M, t_min, bad[:5], bounds[bad[:1]], b_ref[bad[:1]])
+    return st
+
+
+@pytest.mark.parametrize("cfg,integer", [(CFG_MID, True), (CFG_MID, False), (CFG_HUGE, True), (CFG_HUGE, False)])
+def test_big_bounds_match_reference(ref, cfg, integer):
+    c, b = _corpus(ref, 48, 11 if integer else 12, integer_loads=integer, **cfg)
+    sizes = b.sizes()
+    assert sizes.max() <= _abi.DS_MAX_NODES
+    if cfg is CFG_MID:
+        assert (sizes > 256).sum() >= 30
+    else:
+        assert (sizes > 512).sum() >= 40
+    for M in (8, 32, 148):
+        st = _check_bounds(c, b, M)
+        assert (st == _abi.DS_OK).all()
+
+
+def test_big_fractional_tmin_and_wide_words(ref):
+    """t_min = 7/3 and fractional loads push DAGs through the 64- and 128-bit
+    tiers; a t_min wider than 32 bits starts in the 64-bit tier."""
+    c, b = _corpus(ref, 24, 21, integer_loads=False, t_min="7/3", avg_load="131/7", **CFG_HUGE)
+    for M in (5, 32, 148):
+        _check_bounds(c, b, M, "7/3")
+    c2, b2 = _corpus(ref, 16, 22, t_min="5000000001/1000000000", avg_load=20, **CFG_MID)
+    _check_bounds(c2, b2, 32, "5000000001/1000000000")
+
+
+def test_big_schemes_match_reference_write_scheme(ref):
+    for cfg, seed in ((CFG_MID, 31), (CFG_HUGE, 32)):
+        c, b = _corpus(ref, 6, seed, integer_loads=seed % 2 == 0, **cfg)
+        for M in (8, 148):
+            schemes, st = scheme.schedule_batch(b, M)
+            for d in range(b.n_dags):
+                assert st[d] == _abi.DS_OK
+                got = helpers.normalise_scheme(scheme.to_reference_json(schemes[d]))
+                want = helpers.normalise_scheme(c.scheme(d, M))
+                assert got == want, (cfg, M, d)
+
+
+def test_mixed_size_classes_in_one_batch(ref):
+    """Small, W = 4, W = 8 and W = 16 DAGs interleaved: every size-class
+    kernel picks out its own DAGs (host batch, session, device pointers)."""
+    torch = pytest.importorskip("torch")
+    parts = [_corpus(ref, 40, 41, depth_min=3, depth_max=6, max_width=8)[1],
+             _corpus(ref, 10, 42, depth_min=6, depth_max=9, max_width=30)[1],
+             _corpus(ref, 10, 43, **CFG_MID)[1],
+             _corpus(ref, 10, 44, **CFG_HUGE)[1]]
+    # interleave DAG by DAG
+    order = []
+    for k in range(40):
+        for p, part in enumerate(parts):
+            if k < part.n_dags:
+                order.append((p, k))
+    no, eo, ln, ld, ed = [0], [0], [], [], []
+    for p, k in order:
+        part = parts[p]
+        n0, n1 = part.node_off[k], part.node_off[k + 1]
+        e0, e1 = part.edge_off[k], part.edge_off[k + 1]
+        ln.append(part.load_num[n0:n1])
+        ld.append(part.load_den[n0:n1])
+        ed.append(part.edges[e0:e1])
+        no.append(no[-1] + int(n1 - n0))
+        eo.append(eo[-1] + int(e1 - e0))
+    b = from_arrays(np.array(no, np.uint32), np.array(eo, np.uint32), np.concatenate(ln), np.concatenate(ld),
+                    np.concatenate(ed))
+    c = ref.corpus(b)
+    st = _check_bounds(c, b, 148)
+    assert (st == _abi.DS_OK).all()
+    st_ref, b_ref, _ = c.evaluate(148)
+    s = _lib.Session(b, 148)
+    s.run()
+    st2, b2, _ = s.results()
+    assert np.array_equal(st2, st_ref) and np.array_equal(b2, b_ref)
+    # device pointers: size classes unknown to the host
+    st3, b3 = _analyze_device(b, 148)
+    assert np.array_equal(st3, st_ref) and np.array_equal(b3, b_ref)
+
+
+def test_small_host_batch_with_a_big_dag_takes_the_throughput_path(ref):
+    c, b = _corpus(ref, 3, 51, **CFG_HUGE)
+    _check_bounds(c, b, 32)
+    schemes, st = scheme.schedule_batch(b, 32)
+    for d in range(3):
+        assert helpers.normalise_scheme(scheme.to_reference_json(schemes[d])) == \
+            helpers.normalise_scheme(c.scheme(d, 32))
+
+
+def test_limit_is_1024_nodes(ref):
+    chain = lambda n: (list(range(1, n + 1)), [(i, i + 1) for i in range(n - 1)])  # noqa: E731
+    b = pack([chain(1024), chain(1025)])
+    st, bounds, _ = _lib.analyze(b, 4)
+    assert st[0] == _abi.DS_OK and st[1] == _abi.DS_ETOOBIG
+    b1 = pack([chain(1024)])
+    _check_bounds(ref.corpus(b1), b1, 4)

@@ -191,7 +191,7 @@ def test_invalid_and_edge_dags():
         ([(0, 1), (1, 1), (2, 1)], [(0, 1), (0, 2)]),      # two sinks
         ([(0, "1/2")], []),                                # load below t_min
         ([(0, 5)], []),                                    # single node
-        (list(range(1, 258)), [(i, i + 1) for i in range(256)]),  # 257 nodes: too big
+        (list(range(1, 1026)), [(i, i + 1) for i in range(1024)]),  # 1025 nodes: too big
         ([(5, 3), (9, 4), (40, 2)], [(5, 9), (9, 40), (5, 40), (5, 9)]),  # sparse ids + duplicate edge
     ]
     b = pack(dags)
