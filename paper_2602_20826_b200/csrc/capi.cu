@@ -265,11 +265,43 @@ struct DeviceCtx {
     bool init = false;
     Slot slot[kMaxSlots];
     DevBuf retry, retry_count, handoff, big_q, big_scratch;  // scratch for the device-pointer entry point
+    // host-batch pipeline (analyze_host): copy-in, front kernels, back
+    // kernels, copy-out streams and per-slot events between them
+    cudaStream_t pipe[4] = {};
+    cudaEvent_t pev[kMaxSlots][4] = {};
+    bool pev_live[kMaxSlots] = {};  // slot's copy-out event recorded (buffers in use)
     DetailCtx det;
     PinBuf small_in, small_out;  // latency path: mapped (zero-copy) inputs and outputs
 };
 
 DeviceCtx& device_ctx(int dev);
+
+// The slots' streams, in decreasing priority: slot k (the k-th chunk of a
+// host batch) outranks every later slot, so when chunks overlap, the block
+// scheduler serves the earliest chunk first and later chunks fill its tails
+// (each K1 pass ends in a ~0.25 ms tail of long lane walks) instead of
+// slowing it down. DS_STREAM_PRIO=0: equal priorities.
+int create_slot_streams(DeviceCtx& ctx) {
+    static const bool prio = [] {
+        const char* e = getenv("DS_STREAM_PRIO");
+        return !(e && e[0] == '0');
+    }();
+    int least = 0, greatest = 0;
+    DS_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    for (int k = 0; k < kMaxSlots; ++k) {
+        const int p = prio ? std::min(least, greatest + k) : least;
+        DS_CUDA(cudaStreamCreateWithPriority(&ctx.slot[k].s, cudaStreamNonBlocking, p));
+    }
+    // pipeline: the back kernels (lane walks) outrank the next chunk's front
+    // kernels, so a chunk's walks finish first and the front work fills
+    // their tail
+    const int pp[4] = {least, std::min(least, greatest + 1), greatest, least};
+    for (int k = 0; k < 4; ++k) DS_CUDA(cudaStreamCreateWithPriority(&ctx.pipe[k], cudaStreamNonBlocking, pp[k]));
+    for (auto& row : ctx.pev)
+        for (auto& e : row) DS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx.init = true;
+    return DS_OK;
+}
 
 // ------------------------------------------------------- latency path
 // Host batches of at most kSmallDags DAGs go through k1_small (k1_small.cu):
@@ -335,7 +367,7 @@ int small_inputs(const HostView& h, DeviceCtx& ctx, K1Args& a) {
 int small_stream(int device, DeviceCtx& ctx, cudaStream_t& s) {
     DS_CUDA(cudaSetDevice(device));
     if (!ctx.init) {
-        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        if (int rc = create_slot_streams(ctx)) return rc;
         ctx.init = true;
     }
     s = ctx.slot[0].s;
@@ -437,7 +469,7 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     DeviceCtx& ctx = device_ctx(device);
     std::lock_guard<std::mutex> lock(ctx.mu);
     if (!ctx.init) {
-        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        if (int rc = create_slot_streams(ctx)) return rc;
         ctx.init = true;
     }
     const u64 n = b->n_dags;
@@ -459,21 +491,67 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     }
     if (bounds.back() != n) bounds.back() = n;  // small batches: one (or few) chunks
     if (bounds.size() == 1) bounds.push_back(n);
-    // streams (and buffer sets) the chunks rotate over; DS_STREAMS overrides
-    static const int n_slots = [] {
+    // streams (and buffer sets) the chunks rotate over: one per chunk (up to
+    // kMaxSlots), so no chunk waits for an earlier one's buffers and stream
+    // priority follows chunk order; DS_STREAMS overrides
+    static const int env_slots = [] {
         const char* e = getenv("DS_STREAMS");
         const int v = e ? atoi(e) : 0;
-        return v >= 1 && v <= kMaxSlots ? v : 3;
+        return v >= 1 && v <= kMaxSlots ? v : 0;
     }();
+    const int n_slots = env_slots ? env_slots : int(std::min<size_t>(bounds.size() - 1, kMaxSlots));
+    // DS_E2E_TRACE=1: per-chunk event timeline on stderr (tuning aid)
+    static const bool trace = [] {
+        const char* e = getenv("DS_E2E_TRACE");
+        return e && e[0] == '1';
+    }();
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st) -> int {
+        if (!trace) return DS_OK;
+        cudaEvent_t e;
+        DS_CUDA(cudaEventCreate(&e));
+        DS_CUDA(cudaEventRecord(e, st));
+        tev.push_back(e);
+        return DS_OK;
+    };
+    // DS_PIPE=0: each chunk's copies and kernels on its own slot stream
+    // (chunks overlap as whole launch sequences). Default: four streams —
+    // copy-in, front kernels (k1_fast .. k1_mid), back kernels (walk sort,
+    // lane walks, retries), copy-out — chained by events, so chunk c's walks
+    // run beside chunk c+1's front kernels and both directions of PCIe stay
+    // busy.
+    static const bool pipe = [] {
+        const char* e = getenv("DS_PIPE");
+        return !(e && e[0] == '0');
+    }();
+    // DS_PIPE_SPLIT=0: front and back kernels on one stream (tuning knob)
+    static const bool pipe_split = [] {
+        const char* e = getenv("DS_PIPE_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    if (pipe) {  // the previous call's copy-out finished (its results were read)
+        for (int k = 0; k < kMaxSlots; ++k) ctx.pev_live[k] = false;
+    }
+    if (int rc = tmark(pipe ? ctx.pipe[0] : ctx.slot[0].s)) return rc;
     for (size_t c = 0; c + 1 < bounds.size(); ++c) {
         const u64 lo = bounds[c], hi = bounds[c + 1], nd = hi - lo;
-        Slot& sl = ctx.slot[c % n_slots];
+        const int si = int(c % size_t(n_slots));
+        Slot& sl = ctx.slot[si];
+        cudaStream_t s_in = sl.s, s_front = sl.s, s_back = nullptr, s_out = sl.s;
+        if (pipe) {
+            s_in = ctx.pipe[0];
+            s_front = ctx.pipe[1];
+            s_back = pipe_split ? ctx.pipe[2] : ctx.pipe[1];
+            s_out = ctx.pipe[3];
+            // the slot's buffers are reused once its previous chunk's results left
+            if (ctx.pev_live[si]) DS_CUDA(cudaEventSynchronize(ctx.pev[si][3]));
+        }
         // indices are relative to node_off[0] / edge_off[0] (header contract)
         const uint32_t* eoff = second_off(b);
         const u64 n0 = b->node_off[lo] - b->node_off[0], n1 = b->node_off[hi] - b->node_off[0];
         const u64 e0 = eoff[lo] - eoff[0], e1 = eoff[hi] - eoff[0];  // tri: adjacency words
         const size_t nn = n1 - n0, ne = e1 - e0;
-        DS_CUDA(cudaStreamSynchronize(sl.s));  // the slot's buffers are reused
+        if (!pipe) DS_CUDA(cudaStreamSynchronize(sl.s));  // the slot's buffers are reused
         if (int rc = sl.node_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.edge_off.ensure((nd + 1) * 4)) return rc;
         if (int rc = sl.ln.ensure(nn * 8)) return rc;
@@ -488,39 +566,46 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         if (int rc = sl.ngroups.ensure(nd * 2)) return rc;
         if (int rc = sl.retry.ensure(2 * nd * 4)) return rc;  // two retry lists
         if (int rc = sl.retry_count.ensure(kK1Counters * 4)) return rc;
-        DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
+        DS_CUDA(cudaMemcpyAsync(sl.node_off.p, b->node_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, s_in));
         if constexpr (tri) {
             if (int rc = sl.adj_off.ensure((nd + 1) * 4)) return rc;
             if (int rc = sl.ln16.ensure(nn * 2)) return rc;
             if (int rc = sl.adj.ensure(ne * 4)) return rc;
             if (int rc = sl.edge_cnt.ensure(nd * 4)) return rc;
-            DS_CUDA(cudaMemcpyAsync(sl.adj_off.p, b->adj_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
-            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, sl.s));
-            DS_CUDA(cudaMemcpyAsync(sl.adj.p, b->adj + e0, ne * 4, cudaMemcpyHostToDevice, sl.s));
-            const unsigned grid = unsigned(std::min<u64>((nd + 7) / 8, 148 * 8));
-            k_widen_tri<<<grid, 256, 0, sl.s>>>(sl.node_off.as<const u32>(), sl.adj_off.as<const u32>(),
-                                                 sl.ln16.as<const uint16_t>(), sl.adj.as<const u32>(), nd,
-                                                 sl.ln.as<u64>(), sl.edge_off.as<u32>(), sl.edge_cnt.as<u32>(),
-                                                 sl.edges.as<u32>());
-            DS_CUDA(cudaGetLastError());
-        } else {
-            DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, sl.s));
-        }
-        if constexpr (tri) {
+            DS_CUDA(cudaMemcpyAsync(sl.adj_off.p, b->adj_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, s_in));
+            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, s_in));
+            DS_CUDA(cudaMemcpyAsync(sl.adj.p, b->adj + e0, ne * 4, cudaMemcpyHostToDevice, s_in));
         } else if constexpr (compact) {
             if (int rc = sl.ln16.ensure(nn * 2)) return rc;
             if (int rc = sl.edges16.ensure(ne * 2)) return rc;
-            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, sl.s));
-            DS_CUDA(cudaMemcpyAsync(sl.edges16.p, b->edges + e0, ne * 2, cudaMemcpyHostToDevice, sl.s));
-            k_widen16<<<296, 512, 0, sl.s>>>(sl.ln16.as<const uint16_t>(), sl.edges16.as<const uint16_t>(), nn, ne,
-                                             sl.ln.as<u64>(), sl.edges.as<u32>());
-            DS_CUDA(cudaGetLastError());
+            DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, s_in));
+            DS_CUDA(cudaMemcpyAsync(sl.ln16.p, b->load + n0, nn * 2, cudaMemcpyHostToDevice, s_in));
+            DS_CUDA(cudaMemcpyAsync(sl.edges16.p, b->edges + e0, ne * 2, cudaMemcpyHostToDevice, s_in));
         } else {
-            DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
+            DS_CUDA(cudaMemcpyAsync(sl.edge_off.p, b->edge_off + lo, (nd + 1) * 4, cudaMemcpyHostToDevice, s_in));
+            DS_CUDA(cudaMemcpyAsync(sl.ln.p, b->load_num + n0, nn * 8, cudaMemcpyHostToDevice, s_in));
             if (has_den) {
-                DS_CUDA(cudaMemcpyAsync(sl.ldn.p, b->load_den + n0, nn * 8, cudaMemcpyHostToDevice, sl.s));
+                DS_CUDA(cudaMemcpyAsync(sl.ldn.p, b->load_den + n0, nn * 8, cudaMemcpyHostToDevice, s_in));
             }
-            DS_CUDA(cudaMemcpyAsync(sl.edges.p, b->edges + e0, ne * 4, cudaMemcpyHostToDevice, sl.s));
+            DS_CUDA(cudaMemcpyAsync(sl.edges.p, b->edges + e0, ne * 4, cudaMemcpyHostToDevice, s_in));
+        }
+        if (pipe) {
+            DS_CUDA(cudaEventRecord(ctx.pev[si][0], s_in));
+            DS_CUDA(cudaStreamWaitEvent(s_front, ctx.pev[si][0], 0));
+        }
+        if (int rc = tmark(s_in)) return rc;
+        // the compact wire forms widen on the device (the front stream)
+        if constexpr (tri) {
+            const unsigned grid = unsigned(std::min<u64>((nd + 7) / 8, 148 * 8));
+            k_widen_tri<<<grid, 256, 0, s_front>>>(sl.node_off.as<const u32>(), sl.adj_off.as<const u32>(),
+                                                    sl.ln16.as<const uint16_t>(), sl.adj.as<const u32>(), nd,
+                                                    sl.ln.as<u64>(), sl.edge_off.as<u32>(), sl.edge_cnt.as<u32>(),
+                                                    sl.edges.as<u32>());
+            DS_CUDA(cudaGetLastError());
+        } else if constexpr (compact) {
+            k_widen16<<<296, 512, 0, s_front>>>(sl.ln16.as<const uint16_t>(), sl.edges16.as<const uint16_t>(), nn, ne,
+                                                sl.ln.as<u64>(), sl.edges.as<u32>());
+            DS_CUDA(cudaGetLastError());
         }
         K1Args a{};
         a.n_dags = nd;
@@ -542,14 +627,38 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         if (int rc = attach_handoff(a, sl.handoff, nd, nn)) return rc;
         const u32 max_n = tri ? 64u : batch_max_n(b->node_off, lo, hi);
         if (int rc = attach_big(a, sl.big_q, sl.big_scratch, nd, max_n)) return rc;
-        DS_CUDA(k1_launch(a, occ, max_n, false, sl.s));
-        DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, sl.s));
-        DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, sl.s));
-        if (out->n_groups) {
-            DS_CUDA(cudaMemcpyAsync(out->n_groups + lo, sl.ngroups.p, nd * 2, cudaMemcpyDeviceToHost, sl.s));
+        DS_CUDA(k1_launch(a, occ, max_n, false, s_front, nullptr, pipe && pipe_split ? s_back : nullptr,
+                          pipe && pipe_split ? ctx.pev[si][1] : nullptr));
+        if (pipe) {
+            DS_CUDA(cudaEventRecord(ctx.pev[si][2], s_back));
+            DS_CUDA(cudaStreamWaitEvent(s_out, ctx.pev[si][2], 0));
         }
+        if (int rc = tmark(s_out)) return rc;
+        DS_CUDA(cudaMemcpyAsync(out->status + lo, sl.status.p, nd * 4, cudaMemcpyDeviceToHost, s_out));
+        DS_CUDA(cudaMemcpyAsync(out->bounds + 10 * lo, sl.bounds.p, nd * 80, cudaMemcpyDeviceToHost, s_out));
+        if (out->n_groups) {
+            DS_CUDA(cudaMemcpyAsync(out->n_groups + lo, sl.ngroups.p, nd * 2, cudaMemcpyDeviceToHost, s_out));
+        }
+        if (pipe) {
+            DS_CUDA(cudaEventRecord(ctx.pev[si][3], s_out));
+            ctx.pev_live[si] = true;
+        }
+        if (int rc = tmark(s_out)) return rc;
     }
-    for (auto& sl : ctx.slot) DS_CUDA(cudaStreamSynchronize(sl.s));
+    if (pipe) {
+        DS_CUDA(cudaStreamSynchronize(ctx.pipe[3]));
+    } else {
+        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamSynchronize(sl.s));
+    }
+    if (trace) {
+        // per chunk: inputs landed, K1 done, results landed (ms from the start)
+        for (size_t i = 1; i + 2 < tev.size(); i += 3) {
+            float t[3];
+            for (int k = 0; k < 3; ++k) DS_CUDA(cudaEventElapsedTime(&t[k], tev[0], tev[i + k]));
+            fprintf(stderr, "[e2e] chunk %zu: h2d %.3f  k1 %.3f  d2h %.3f ms\n", i / 3, t[0], t[1], t[2]);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     return DS_OK;
 }
 
@@ -877,7 +986,7 @@ int run_detail(const ds_dag_batch* b, const PlatT<u64>& P, int device, DeviceCtx
     K1Occupancy occ;
     if (int rc = configure(device, true, occ)) return rc;
     if (!ctx.init) {
-        for (auto& sl : ctx.slot) DS_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+        if (int rc = create_slot_streams(ctx)) return rc;
         ctx.init = true;
     }
     cudaStream_t s = ctx.slot[0].s;

@@ -80,7 +80,10 @@ struct K1Marks {
 // the largest DAG of the batch (DS_MAX_NODES when unknown); above 256 nodes
 // `a.big_q` [2 n_dags] and, above 512, `a.big_scratch` [kBigGrid x
 // kBigScratchPerCta] must be set.
+// With s_back and ev_split (bounds mode), the kernels from the walk-order sort
+// on are launched on s_back after ev_split is recorded on s (and s_back waits
+// for it): the caller's later work on s overlaps them.
 cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, u32 max_n, bool detail, cudaStream_t s,
-                      K1Marks* marks = nullptr);
+                      K1Marks* marks = nullptr, cudaStream_t s_back = nullptr, cudaEvent_t ev_split = nullptr);
 
 }  // namespace ds

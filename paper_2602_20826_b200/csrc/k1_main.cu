@@ -84,7 +84,8 @@ cudaError_t k1_configure_t(int device, K1Occupancy& occ) {
 }
 
 template <bool DETAIL>
-cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* marks) {
+cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* marks,
+                        cudaStream_t s_back, cudaEvent_t ev_split) {
     if (marks) marks->n = 0;
     if (a.n_dags == 0) return cudaSuccess;
     int mark_i = 0;
@@ -142,6 +143,16 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
     if (split && (a.mask & DS_M_PROPOSED)) {
         k1_mid<><<<cap(occ.grid_mid), 32 * kWarpsSmall, kSmemSmall, s>>>(af);
         if ((e = mark("k1_mid")) != cudaSuccess) return e;
+    }
+    // two-stream form: the walk-order sort, the lane walks, the big-DAG and
+    // retry kernels go to s_back after an event, so the caller can overlap
+    // this batch's walks with the next batch's front kernels
+    if (s_back && ev_split) {
+        if ((e = cudaEventRecord(ev_split, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s_back, ev_split, 0)) != cudaSuccess) return e;
+        s = s_back;
+    }
+    if (split && (a.mask & DS_M_PROPOSED)) {
         // shape-sorted walk order for the lane kernel (DS_K1_SORT=0: index order)
         static const bool sort_walks = [] {
             const char* env = getenv("DS_K1_SORT");
@@ -200,13 +211,14 @@ cudaError_t k1_configure(int device, bool detail, K1Occupancy& occ) {
     return detail ? k1_configure_detail(device, occ) : k1_configure_t<false>(device, occ);
 }
 cudaError_t k1_launch(const K1Args& a, const K1Occupancy& occ, u32 max_n, bool detail, cudaStream_t s,
-                      K1Marks* marks) {
-    return detail ? k1_launch_detail(a, occ, max_n, s, marks) : k1_launch_t<false>(a, occ, max_n, s, marks);
+                      K1Marks* marks, cudaStream_t s_back, cudaEvent_t ev_split) {
+    return detail ? k1_launch_detail(a, occ, max_n, s, marks)
+                  : k1_launch_t<false>(a, occ, max_n, s, marks, s_back, ev_split);
 }
 #else
 cudaError_t k1_configure_detail(int device, K1Occupancy& occ) { return k1_configure_t<true>(device, occ); }
 cudaError_t k1_launch_detail(const K1Args& a, const K1Occupancy& occ, u32 max_n, cudaStream_t s, K1Marks* m) {
-    return k1_launch_t<true>(a, occ, max_n, s, m);
+    return k1_launch_t<true>(a, occ, max_n, s, m, nullptr, nullptr);
 }
 #endif
 

@@ -332,3 +332,26 @@ def test_lane_walk_wide_platform_matches_oracle(orc):
         st, bounds, _ = _lib.analyze(b, M)
         st_o, b_o, _ = orc.corpus(b).evaluate(M)
         assert np.array_equal(st, st_o) and np.array_equal(bounds, b_o), M
+
+
+def test_host_pipeline_matches_slot_streams():
+    """The four-stream host pipeline (default) and the per-chunk slot streams
+    (DS_PIPE=0) give the same results over every wire form, with several
+    chunks (8 chunks x 25k DAGs, more chunks than stream slots reuse them)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = ("import json,sys,hashlib; sys.path.insert(0,'.'); from paper_2602_20826_b200 import _lib; "
+            "b=_lib.Corpus(200000, seed=6).batch(); h=[]\n"
+            "for f in (_lib.analyze, _lib.analyze16, _lib.analyze_tri):\n"
+            "    st,bo,ng=f(b,148); h.append(hashlib.sha1(st.tobytes()+bo.tobytes()+ng.tobytes()).hexdigest())\n"
+            "print(json.dumps(h))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_kv in ({"DS_CHUNKS": "8"}, {"DS_CHUNKS": "8", "DS_PIPE": "0"}, {"DS_CHUNKS": "12"}):
+        env = dict(os.environ, **env_kv)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, check=True)
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1] == outs[2]
+    assert len(set(outs[0])) == 1  # the three wire forms agree too
