@@ -45,6 +45,8 @@ def make_dags(spec, M):
 
 
 def plan_for(kind, sch, loads, edges, M, unit):
+    if kind == "dynamic_ms":  # naive multi-stream's plan (original edges, m = min(m^max, M)) on the dynamic engine
+        return X.plan_baseline("multistream", loads, edges, M, unit)
     if kind.endswith("_prio"):
         return X.plan_from_scheme(sch, loads, unit, mode=X.PLAN_PRIORITY)
     if kind.startswith(("proposed", "dynamic")):
@@ -65,8 +67,9 @@ def main():
     ap.add_argument("--unit", type=int, default=1 << 17)
     ap.add_argument("--windows", default="c4_0")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "exec_study.json"))
+    ap.add_argument("--sm-limit", type=int, default=0, help="green context of this many SMs (0: the whole GPU)")
     args = ap.parse_args()
-    M = 148
+    M = args.sm_limit or 148
     dags = make_dags(args.dags, M)
     schemes, st = scheme.schedule_batch(pack([d for _, d in dags]), M)
     res = []
@@ -76,7 +79,7 @@ def main():
         row["work_us_at_6539"] = tot_bytes / 6539.2e3
         for kind in args.variants.split(","):
             plan = plan_for(kind, sch, loads, edges, M, args.unit)
-            ex = X.Executor(plan, workload=X.WL_MIX32_TMA, engine=engine_for(kind))
+            ex = X.Executor(plan, workload=X.WL_MIX32_TMA, engine=engine_for(kind), sm_limit=args.sm_limit)
             r = ex.run(args.replays, warmup=3, stamps=True)
             ex.close()
             mk = r.makespan_us
