@@ -186,8 +186,11 @@ int ds_corpus_generate(const ds_gen_config* g, int64_t count, uint32_t flags, vo
     if (c.avg < c.tmin) return fail(DS_EINVAL, "avg_load must be >= t_min");
     c.avg_d = double(g->avg_load_num) / double(g->avg_load_den);
     c.tmin_d = double(g->tmin_num) / double(g->tmin_den);
-    if (2 + int64_t(c.dmax - 2) * c.width > DS_MAX_NODES)
-        return fail(DS_ETOOBIG, "generated DAGs could exceed DS_MAX_NODES nodes");
+    // the packed form indexes nodes in 16 bits and generate_one keeps <= 512
+    // layers; a generated DAG above DS_MAX_NODES gets DS_ETOOBIG from the
+    // analysis, like any other
+    if (c.dmax > 513 || 2 + int64_t(c.dmax - 2) * c.width > 65535)
+        return fail(DS_ETOOBIG, "generated DAGs could exceed 65535 nodes or 512 layers");
     if (flags & DS_F_GPU_GENERATE) {
         if (2 + int64_t(c.dmax - 2) * c.width > 256)
             return fail(DS_ETOOBIG, "GPU generation (K5) covers DAGs up to 256 nodes; generate larger ones on the host");

@@ -85,8 +85,31 @@ std::vector<std::vector<std::vector<NodeId>>> read_groups(const char* path, std:
 
 int main(int argc, char** argv) {
     const bool host_only = argc > 2 && std::strcmp(argv[1], "--host-only") == 0;
+    // --big: only generated DAGs of ~190-940 nodes (the paper's P = 32 sweep
+    // and deeper), compared live against the reference's build of this file
+    const bool big = argc > 1 && std::strcmp(argv[1], "--big") == 0;
     std::vector<Case> cases;
-    for (int M : {3, 4, 5, 6, 8, 148}) cases.push_back({"fig2", fig2(), M});
+    if (big) {
+        GenConfig mid;
+        mid.seed = 700;
+        mid.max_width = 32;
+        mid.depth_min = 16;
+        mid.depth_max = 26;
+        const auto a = generate_corpus(mid, 6);
+        for (int M : {8, 32, 148})
+            for (std::size_t i = 0; i < a.size(); ++i) cases.push_back({"p32_seed" + std::to_string(700 + i), a[i], M});
+        GenConfig huge = mid;
+        huge.seed = 800;
+        huge.max_width = 48;
+        huge.depth_min = 26;
+        huge.depth_max = 34;
+        const auto h = generate_corpus(huge, 3);
+        for (int M : {8, 148})
+            for (std::size_t i = 0; i < h.size(); ++i) cases.push_back({"p48_seed" + std::to_string(800 + i), h[i], M});
+    }
+    if (!big)
+        for (int M : {3, 4, 5, 6, 8, 148}) cases.push_back({"fig2", fig2(), M});
+    if (!big) {
     cases.push_back({"chain3", chain3(), 4});
     cases.push_back({"diamond_1_5_2_1", diamond(1, 5, 2, 1), 4});
     cases.push_back({"diamond_1_5_2_1", diamond(1, 5, 2, 1), 148});
@@ -116,6 +139,7 @@ int main(int argc, char** argv) {
         const auto h = generate_corpus(heavy, 20);
         for (int M : {8, 148})
             for (std::size_t i = 0; i < h.size(); ++i) cases.push_back({"heavy_seed" + std::to_string(100 + i), h[i], M});
+    }
     }
     std::vector<std::vector<std::vector<NodeId>>> given;
     if (host_only) given = read_groups(argv[2], cases.size());

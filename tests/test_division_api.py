@@ -116,3 +116,23 @@ def test_device_node_block_and_div_group_match_reference(golden):
                 assert s.n_div_groups == len(want["groups"])
                 checked += 1
     assert checked == 60 * 4 + 20 * 3 + 20 * 2
+
+
+REF_DUMP = os.path.join(ROOT, "oracle", "_ref", "ref_division_dump")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_DUMP), reason="oracle/_ref not built (make ref)")
+def test_big_dags_division_match_reference():
+    """DAGs of ~190-940 nodes (the device's k1_big size classes behind
+    build_groups): blocks, local paths, groups, scaling and candidates from
+    the kept API equal the reference's own build of the same program."""
+    got = subprocess.run([DUMP, "--big"], capture_output=True, text=True, timeout=600)
+    want = subprocess.run([REF_DUMP, "--big"], capture_output=True, text=True, timeout=600)
+    assert got.returncode == 0, got.stderr[-2000:]
+    assert want.returncode == 0, want.stderr[-2000:]
+    g, w = json.loads(got.stdout)["cases"], json.loads(want.stdout)["cases"]
+    assert len(g) == len(w) == 24
+    assert max(len(sum(c["groups"], [])) for c in w) > 512  # the W = 16 class is covered
+    for a, b in zip(g, w):
+        assert a == b, (a["name"], a["sm_count"])
