@@ -1,4 +1,5 @@
 // K6 launcher + C-ABI entry (ds_simulate_greedy_batch).
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -53,12 +54,13 @@ extern "C" int ds_simulate_greedy_batch(const ds_dag_batch* b, const ds_platform
     const u64 nb = b->node_off[0], eb = b->edge_off[0];
     const u64 N = b->node_off[n] - nb, E = b->edge_off[n] - eb;
     const u64 P = n * u64(cfg->runs);
-    bool big = false;
+    bool big = false, huge = false;
     std::vector<u32> no(n + 1), eo(n + 1);
     for (u64 i = 0; i <= n; ++i) {
         no[i] = u32(b->node_off[i] - nb);
         eo[i] = u32(b->edge_off[i] - eb);
         if (i && no[i] - no[i - 1] > 64) big = true;
+        if (i && no[i] - no[i - 1] > 256) huge = true;
     }
     K6_CUDA(cudaSetDevice(device));
     cudaStream_t s;
@@ -67,7 +69,7 @@ extern "C" int ds_simulate_greedy_batch(const ds_dag_batch* b, const ds_platform
         cudaStream_t s;
         ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{s};
-    Buf dno, deo, dln, dld, ded, dst, dmk, dev;
+    Buf dno, deo, dln, dld, ded, dst, dmk, dev, dscr;
     K6_CUDA(cudaMalloc(&dno.p, (n + 1) * 4));
     K6_CUDA(cudaMalloc(&deo.p, (n + 1) * 4));
     K6_CUDA(cudaMalloc(&dln.p, std::max<u64>(N, 1) * 8));
@@ -113,6 +115,15 @@ extern "C" int ds_simulate_greedy_batch(const ds_dag_batch* b, const ds_platform
     }
     k6_greedy<256, u128><<<grid(4), 64, 0, s>>>(a);  // the runs that overflowed 64 bits
     K6_CUDA(cudaGetLastError());
+    if (huge) {  // n > 256: run state in HBM, one slot per resident thread (u128-sized, ~238 KB)
+        K6_CUDA(cudaMalloc(&dscr.p, size_t(kK6BigThreads) * K6Slot<1024, u128>::kBytes));
+        a.scratch = static_cast<unsigned char*>(dscr.p);
+        const unsigned gb = unsigned(std::min<u64>((P + 31) / 32, kK6BigThreads / 32));
+        k6_greedy<1024, u64><<<gb, 32, 0, s>>>(a);
+        K6_CUDA(cudaGetLastError());
+        k6_greedy<1024, u128><<<gb, 32, 0, s>>>(a);
+        K6_CUDA(cudaGetLastError());
+    }
     K6_CUDA(cudaMemcpyAsync(status, dst.p, P * 4, cudaMemcpyDeviceToHost, s));
     K6_CUDA(cudaMemcpyAsync(makespan, dmk.p, P * 16, cudaMemcpyDeviceToHost, s));
     if (events) K6_CUDA(cudaMemcpyAsync(events, dev.p, N * cfg->runs * 32, cudaMemcpyDeviceToHost, s));

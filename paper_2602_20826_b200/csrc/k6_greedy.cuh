@@ -26,6 +26,8 @@
 #include "rat.cuh"
 #include "rng.cuh"
 
+#include <type_traits>
+
 namespace ds {
 
 constexpr int32_t kK6Retry = -2000;
@@ -48,7 +50,43 @@ struct K6Args {
     int32_t* status;   // [n_dags * runs]
     int64_t* makespan; // [n_dags * runs * 2]
     int64_t* events;   // optional [N * runs * 4]: start n/d, finish n/d
+    unsigned char* scratch;  // n > 256: per-thread run state (K6Big), kK6BigThreads slots
 };
+
+// Per-run state: local arrays (n <= 256) or one HBM slot per thread (n <= 1024)
+template <int NMAX, class T>
+struct K6Local {
+    static constexpr int NW = NMAX / 64;
+    u64 succ[NMAX][NW];
+    RatT<T> dur[NMAX], rel[NMAX], fin[NMAX];
+    int m[NMAX];
+    u64 tie[NMAX];
+    unsigned short left[NMAX];
+    static constexpr size_t kBytes = 0;
+    __device__ __forceinline__ void bind(unsigned char*) {}
+};
+template <int NMAX, class T>
+struct K6Slot {
+    static constexpr int NW = NMAX / 64;
+    u64 (*succ)[NW];
+    RatT<T>*dur, *rel, *fin;
+    int* m;
+    u64* tie;
+    unsigned short* left;
+    static constexpr size_t kBytes = size_t(NMAX) * (NW * 8 + 3 * sizeof(RatT<T>) + 4 + 8 + 2);
+    __device__ __forceinline__ void bind(unsigned char* base) {
+        succ = reinterpret_cast<u64(*)[NW]>(base);
+        base += size_t(NMAX) * NW * 8;
+        dur = reinterpret_cast<RatT<T>*>(base);
+        rel = dur + NMAX;
+        fin = rel + NMAX;
+        base += size_t(NMAX) * 3 * sizeof(RatT<T>);
+        tie = reinterpret_cast<u64*>(base);
+        m = reinterpret_cast<int*>(tie + NMAX);
+        left = reinterpret_cast<unsigned short*>(m + NMAX);
+    }
+};
+constexpr int kK6BigThreads = 148 * 32;  // resident threads of the n > 256 kernels (one HBM slot each)
 
 template <class T>
 __device__ __forceinline__ bool fits_i64_any(T v) {
@@ -60,29 +98,38 @@ __device__ __forceinline__ bool q_less(const RatT<T>& a, const RatT<T>& b) {
     return rat_cmp(a, b) < 0;
 }
 
+// Size classes: NMAX = 64 takes n <= 64, 256 takes 64 < n <= 256, 1024 (HBM
+// slots) takes the rest (n > 1024: DS_ETOOBIG); the u128 passes take the runs
+// of their class flagged kK6Retry.
 template <int NMAX, class T>
 __global__ void __launch_bounds__(64) k6_greedy(const K6Args a) {
     constexpr int NW = NMAX / 64;
+    constexpr bool kSlot = NMAX > 256;
     const u64 total = a.n_dags * u64(a.runs);
-    for (u64 p = u64(blockIdx.x) * blockDim.x + threadIdx.x; p < total; p += u64(gridDim.x) * blockDim.x) {
+    const u64 tid = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    using Arr = typename std::conditional<kSlot, K6Slot<NMAX, T>, K6Local<NMAX, T>>::type;
+    for (u64 p = tid; p < total; p += u64(gridDim.x) * blockDim.x) {
         const u64 d = p / u64(a.runs);
         const int run = int(p - d * u64(a.runs));
         const u32 n0 = a.node_off[d] - a.node_off[0];
         const int n = int(a.node_off[d + 1] - a.node_off[d]);
-        if (sizeof(T) == 16) {
-            if (a.status[p] != kK6Retry) continue;
-        } else {
-            if (NMAX == 64 ? (n > 64) : (n <= 64)) continue;
-        }
+        const bool mine = sizeof(T) == 16 ? (NMAX == 256 ? n <= 256 : n > 256)
+                                          : (NMAX == 64 ? n <= 64 : NMAX == 256 ? (n > 64 && n <= 256) : n > 256);
+        if (!mine) continue;  // another class
+        if (sizeof(T) == 16 && a.status[p] != kK6Retry) continue;
         int st = DS_OK;
         if (n <= 0) st = DS_E_EMPTY;
         if (n > NMAX) st = DS_ETOOBIG;
         bool ovf = false;
-        u64 succ[NMAX][NW];
-        RatT<T> dur[NMAX], rel[NMAX], fin[NMAX];
-        int m[NMAX];
-        u64 tie[NMAX];
-        unsigned short left[NMAX];
+        Arr A;
+        A.bind(a.scratch + tid * Arr::kBytes);
+        auto& succ = A.succ;
+        auto& dur = A.dur;
+        auto& rel = A.rel;
+        auto& fin = A.fin;
+        auto& m = A.m;
+        auto& tie = A.tie;
+        auto& left = A.left;
         const PlatT<T> P{a.M, RatT<T>{T(a.tmin_n), T(a.tmin_d)}};
         Mt64 g;
         if (st == DS_OK) {

@@ -108,3 +108,23 @@ def test_greedy_rejects_bad_args():
                                                                                    Fraction(1, 2)))
     with pytest.raises(_lib.DagschedError):
         simulator.simulate_greedy_batch(b, 8, 0)
+
+
+@pytest.mark.parametrize("policy,scaled", [("random", False), ("fifo", True)])
+def test_greedy_big_dags_match_reference_live(policy, scaled):
+    """K6 on DAGs of ~190-940 nodes (the HBM-slot class, n > 256, and the
+    64 < n <= 256 class side by side) against the reference's simulate_greedy
+    on the same generated corpus, computed live by oracle/_ref."""
+    from oracle import bindings
+    cfgs = [dict(depth_min=16, depth_max=26, max_width=32, seed=910), dict(depth_min=26, depth_max=34, max_width=48,
+                                                                           seed=911)]
+    for cfg in cfgs:
+        runs, M = 3, 32
+        tm = simulator.TimeModel(scaled, 7, Fraction(1, 2), Fraction(1))
+        corp = _lib.Corpus(6, **cfg)
+        st, num, den, _ = simulator.simulate_greedy_batch(corp.batch(), M, runs, policy, 5, tm)
+        rc = bindings.Checker("ref").generate(6, **cfg)
+        st_r, mk_r = bindings.ref_sim_greedy(rc, M, runs, policy, 5, scaled, 7, "1/2", 1)
+        assert int(corp.batch().sizes().max()) > 256
+        assert np.array_equal(st, st_r), (cfg, st, st_r)
+        assert np.array_equal(num, mk_r[:, :, 0]) and np.array_equal(den, mk_r[:, :, 1]), cfg
