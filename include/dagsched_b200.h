@@ -311,6 +311,11 @@ typedef struct ds_exec_trace {
 const char* ds_last_error(void);
 const char* ds_version(void);
 int ds_device_count(int* count);
+/* Page-locked host memory for the batch entry points' arrays (their copies
+ * then run at full PCIe rate and asynchronously): cudaMallocHost / cudaFreeHost.
+ * No reference equivalent (the reference has no device). */
+int ds_pinned_alloc(size_t bytes, void** out);
+int ds_pinned_free(void* p);
 
 /* Batched bound analysis — replaces evaluate_corpus (experiment.cpp:52-79 with
  * method_bound :27-39) plus lower_bound (analysis.cpp:72-81). One warp per DAG.

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <exception>
+#include <mutex>
 #include <sstream>
 #include <stdexcept>
 #include <thread>
@@ -34,41 +35,134 @@ void parallel_for(std::size_t n, const std::function<void(std::size_t, std::size
         if (e) std::rethrow_exception(e);
 }
 
-Packed pack(const std::vector<const DagTask*>& tasks) {
+struct Packed::Store {
+    std::unique_lock<std::mutex> lease;      // the pinned arena, held while the batch lives
+    std::unique_ptr<unsigned char[]> heap;   // else a heap block (default-initialised: untouched)
+};
+
+namespace {
+struct PinnedArena {
+    std::mutex mu;
+    void* p = nullptr;
+    std::size_t cap = 0;
+};
+PinnedArena& pinned_arena() {
+    static PinnedArena* a = new PinnedArena;  // never destroyed: cudaFreeHost after the runtime's teardown is unsafe
+    return *a;
+}
+bool arena_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DAGSCHED_PINNED_ARENA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+constexpr std::size_t kArenaMin = std::size_t(4) << 20;  // smaller batches: heap (the latency path copies anyway)
+
+// `bytes` of storage for a batch: the arena when it is free and big enough
+// (grown on demand), else the heap
+unsigned char* acquire(Packed& p, std::size_t bytes) {
+    p.store = std::make_shared<Packed::Store>();
+    if (bytes >= kArenaMin && arena_enabled()) {
+        PinnedArena& a = pinned_arena();
+        std::unique_lock<std::mutex> lk(a.mu, std::try_to_lock);
+        if (lk.owns_lock()) {
+            if (a.cap < bytes) {
+                if (a.p) ds_pinned_free(a.p);
+                a.p = nullptr;
+                a.cap = 0;
+                const std::size_t want = bytes + bytes / 4;
+                if (ds_pinned_alloc(want, &a.p) == DS_OK) a.cap = want;
+            }
+            if (a.cap >= bytes) {
+                p.store->lease = std::move(lk);
+                p.pinned = true;
+                return static_cast<unsigned char*>(a.p);
+            }
+        }
+    }
+    p.store->heap.reset(new unsigned char[bytes ? bytes : 1]);
+    return p.store->heap.get();
+}
+}  // namespace
+
+Packed pack(const std::vector<const DagTask*>& tasks, bool with_results) {
     Packed p;
     const std::size_t nd = tasks.size();
-    p.node_off.assign(nd + 1, 0);
-    p.edge_off.assign(nd + 1, 0);
-    for (std::size_t d = 0; d < nd; ++d) {
-        if (tasks[d]->size() > DS_MAX_NODES) throw std::invalid_argument("DAG larger than DS_MAX_NODES nodes");
-        p.node_off[d + 1] = p.node_off[d] + std::uint32_t(tasks[d]->size());
-        p.edge_off[d + 1] = p.edge_off[d] + std::uint32_t(tasks[d]->edges().size());
+    p.n_dags = nd;
+    // the host's cores each take a contiguous run of tasks, the same runs in
+    // every pass below
+    const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t parts = std::max<std::size_t>(1, std::min(hw, nd / 2048));
+    auto run = [&](std::size_t i) { return nd * i / parts; };
+    std::vector<std::size_t> pn(parts + 1, 0), pe(parts + 1, 0);
+    parallel_for(parts, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            std::size_t a = 0, b = 0;
+            for (std::size_t d = run(i); d < run(i + 1); ++d) {
+                if (tasks[d]->size() > DS_MAX_NODES) throw std::invalid_argument("DAG larger than DS_MAX_NODES nodes");
+                a += tasks[d]->size();
+                b += tasks[d]->edges().size();
+            }
+            pn[i + 1] = a;
+            pe[i + 1] = b;
+        }
+    }, 1);
+    for (std::size_t i = 0; i < parts; ++i) {
+        pn[i + 1] += pn[i];
+        pe[i + 1] += pe[i];
     }
-    p.num.resize(p.node_off[nd]);
-    p.den.resize(p.node_off[nd]);
-    p.edges.resize(p.edge_off[nd]);
+    p.n_nodes = pn[parts];
+    p.n_edges = pe[parts];
+    if (p.n_nodes > 0xffffffffull || p.n_edges > 0xffffffffull)
+        throw std::invalid_argument("batch exceeds 2^32 nodes or edges");
+    // layout (8-byte aligned): num, den, bounds | node_off, edge_off, edges, status
+    const std::size_t N = p.n_nodes, E = p.n_edges, R = with_results ? nd : 0;
+    const std::size_t bytes = 8 * (2 * N + 10 * R) + 4 * (2 * (nd + 1) + E + R) + 64;
+    unsigned char* base = acquire(p, bytes);
+    p.num = reinterpret_cast<std::int64_t*>(base);
+    p.den = p.num + N;
+    p.bounds = with_results ? p.den + N : nullptr;
+    p.node_off = reinterpret_cast<std::uint32_t*>(p.den + N + 10 * R);
+    p.edge_off = p.node_off + nd + 1;
+    p.edges = p.edge_off + nd + 1;
+    p.status = with_results ? reinterpret_cast<std::int32_t*>(p.edges + E) : nullptr;
+    p.node_off[0] = 0;
+    p.edge_off[0] = 0;
     std::atomic<bool> frac{false};
     constexpr BigInt::u128 kMax = BigInt::u128(INT64_MAX);
-    parallel_for(nd, [&](std::size_t lo, std::size_t hi) {
-        bool f = false;
-        for (std::size_t d = lo; d < hi; ++d) {
-            std::size_t i = p.node_off[d];
-            for (const DagNode& v : tasks[d]->nodes()) {
-                const BigInt& n = v.load.num();
-                const BigInt& dn = v.load.den();
-                if (n.magnitude() > kMax || dn.magnitude() > kMax)
-                    throw std::overflow_error("load outside the C-ABI's int64 range");
-                p.num[i] = n.negative() ? -std::int64_t(n.magnitude()) : std::int64_t(n.magnitude());
-                p.den[i] = std::int64_t(dn.magnitude());
-                f |= p.den[i] != 1;
-                ++i;
+    parallel_for(parts, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t r = lo; r < hi; ++r) {
+            bool f = false;
+            std::size_t i = pn[r], e = pe[r];
+            for (std::size_t d = run(r); d < run(r + 1); ++d) {
+                const DagTask& t = *tasks[d];
+                for (const DagNode& v : t.nodes()) {
+                    const BigInt& n = v.load.num();
+                    const BigInt& dn = v.load.den();
+                    if (n.magnitude() > kMax || dn.magnitude() > kMax)
+                        throw std::overflow_error("load outside the C-ABI's int64 range");
+                    p.num[i++] = n.negative() ? -std::int64_t(n.magnitude()) : std::int64_t(n.magnitude());
+                    f |= dn.magnitude() != 1;
+                }
+                t.edge_words_into(p.edges + e);
+                e += t.edges().size();
+                p.node_off[d + 1] = std::uint32_t(i);
+                p.edge_off[d + 1] = std::uint32_t(e);
             }
-            std::size_t e = p.edge_off[d];
-            for (std::uint32_t w : tasks[d]->edge_words()) p.edges[e++] = w;
+            if (f) frac = true;
         }
-        if (f) frac = true;
-    });
+    }, 1);
     p.integer = !frac;
+    if (!p.integer) {  // denominators only when some load is fractional
+        parallel_for(parts, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t r = lo; r < hi; ++r) {
+                std::size_t i = pn[r];
+                for (std::size_t d = run(r); d < run(r + 1); ++d)
+                    for (const DagNode& v : tasks[d]->nodes()) p.den[i++] = std::int64_t(v.load.den().magnitude());
+            }
+        }, 1);
+    }
     return p;
 }
 

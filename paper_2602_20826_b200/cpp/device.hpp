@@ -8,22 +8,34 @@
 
 #include <cstddef>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
 namespace dagsched::detail {
 
+// A batch of DagTasks in the C-ABI's packed form (ds_dag_batch), plus
+// result staging (status[n_dags], bounds[10 n_dags]) when asked for. Large
+// batches are packed into a process-wide pinned arena (the C-ABI's copies then
+// run at full PCIe rate; one batch holds it at a time, others fall back to
+// the heap; DAGSCHED_PINNED_ARENA=0 disables it); the arrays are filled by
+// the host's cores, each first touching its own slice.
 struct Packed {
-    std::vector<std::uint32_t> node_off{0}, edge_off{0}, edges;
-    std::vector<std::int64_t> num, den;
+    std::size_t n_dags = 0, n_nodes = 0, n_edges = 0;
+    std::uint32_t *node_off = nullptr, *edge_off = nullptr, *edges = nullptr;
+    std::int64_t *num = nullptr, *den = nullptr;
+    std::int32_t* status = nullptr;
+    std::int64_t* bounds = nullptr;
     bool integer = true;
+    bool pinned = false;
+    struct Store;
+    std::shared_ptr<Store> store;  // the arena lease or the heap block
     ds_dag_batch view() const {
-        return ds_dag_batch{node_off.size() - 1, node_off.data(), edge_off.data(), num.data(),
-                            integer ? nullptr : den.data(), edges.data()};
+        return ds_dag_batch{n_dags, node_off, edge_off, num, integer ? nullptr : den, edges};
     }
 };
 
-Packed pack(const std::vector<const DagTask*>& tasks);
+Packed pack(const std::vector<const DagTask*>& tasks, bool with_results = false);
 // f(lo, hi) over [0, n) split into contiguous chunks on the host's cores
 // (std::thread; the first exception, in chunk order, is rethrown). Host
 // bookkeeping around the device calls: packing DagTasks, building results.

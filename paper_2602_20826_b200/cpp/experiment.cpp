@@ -84,21 +84,25 @@ std::vector<std::vector<Rational>> evaluate_corpus(const std::vector<DagTask>& c
     std::vector<const DagTask*> ptrs;
     ptrs.reserve(corpus.size());
     for (const DagTask& t : corpus) ptrs.push_back(&t);
-    const detail::Packed p = detail::pack(ptrs);
+    // inputs and result staging in one packed block (the pinned arena for a
+    // large corpus), so both copy directions run at full PCIe rate
+    const detail::Packed p = detail::pack(ptrs, true);
     const ds_dag_batch b = p.view();
     const ds_platform pl = detail::platform_of(platform);
-    std::vector<int32_t> st(corpus.size());
-    std::vector<int64_t> bounds(corpus.size() * 10);
-    ds_results r{st.data(), bounds.data(), nullptr};
+    ds_results r{p.status, p.bounds, nullptr};
     const std::vector<int> devs = detail::devices();
     detail::check(ds_analyze_batch_multi(&b, &pl, method_mask(methods), &r, devs.data(), int(devs.size())));
     for (std::size_t i = 0; i < corpus.size(); ++i)  // the first failing task, in order
-        if (st[i] != DS_OK) detail::raise(st[i], "evaluate_corpus: task " + std::to_string(i));
+        if (p.status[i] != DS_OK) detail::raise(p.status[i], "evaluate_corpus: task " + std::to_string(i));
     std::vector<std::vector<Rational>> out(corpus.size());
+    const int64_t* bounds = p.bounds;
     detail::parallel_for(corpus.size(), [&](std::size_t lo, std::size_t hi) {
         for (std::size_t i = lo; i < hi; ++i) {
             out[i].reserve(methods.size());
-            for (Method m : methods) out[i].push_back(bound_at(bounds, i, int(m)));
+            for (Method m : methods) {
+                const int k = int(m);
+                out[i].push_back(Rational::reduced(BigInt(bounds[10 * i + 2 * k]), BigInt(bounds[10 * i + 2 * k + 1])));
+            }
         }
     });
     return out;

@@ -235,7 +235,7 @@ std::vector<ScheduleScheme> schedule_ptrs(const std::vector<const DagTask*>& tas
     const detail::Packed p = detail::pack(tasks);
     const ds_dag_batch b = p.view();
     const ds_platform pl = detail::platform_of(platform);
-    const std::size_t nd = tasks.size(), N = p.num.size();
+    const std::size_t nd = tasks.size(), N = p.n_nodes;
     std::vector<int32_t> st(nd);
     std::vector<uint16_t> ne(nd), ng(nd), ndv(nd);
     std::vector<ds_entity_rec> ents(std::max<std::size_t>(2 * N, 1));

@@ -790,6 +790,18 @@ extern "C" {
 const char* ds_last_error(void) { return g_err.c_str(); }
 const char* ds_version(void) { return "dagsched_b200 0.2 (sm_100a)"; }
 
+int ds_pinned_alloc(size_t bytes, void** out) {
+    if (!out) return fail(DS_EINVAL, "NULL output pointer");
+    *out = nullptr;
+    DS_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    return DS_OK;
+}
+
+int ds_pinned_free(void* p) {
+    if (p) DS_CUDA(cudaFreeHost(p));
+    return DS_OK;
+}
+
 int ds_device_count(int* count) {
     int c = 0;
     cudaError_t e = cudaGetDeviceCount(&c);
