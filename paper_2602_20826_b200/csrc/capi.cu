@@ -529,7 +529,10 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         const char* e = getenv("DS_PIPE_SPLIT");
         return !(e && e[0] == '0');
     }();
-    if (pipe) {  // the previous call's copy-out finished (its results were read)
+    if (pipe) {
+        // a previous call that failed part-way may have left work in flight
+        // on the slot buffers: drain it (free when the streams are idle)
+        for (cudaStream_t st : ctx.pipe) DS_CUDA(cudaStreamSynchronize(st));
         for (int k = 0; k < kMaxSlots; ++k) ctx.pev_live[k] = false;
     }
     if (int rc = tmark(pipe ? ctx.pipe[0] : ctx.slot[0].s)) return rc;

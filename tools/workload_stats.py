@@ -33,8 +33,11 @@ def main():
     ents = np.zeros(2 * N, dtype=np.dtype(_abi.ds_entity_rec))
     grps = np.zeros(N, dtype=np.dtype(_abi.ds_group_rec))
     bnd = np.zeros((n, 10), np.int64)
+    sizes = np.diff(b.node_off.astype(np.int64))
+    ubase = np.concatenate([[0], np.cumsum(sizes * ((sizes + 63) // 64))]).astype(np.int64)
+    unl_w = np.zeros(max(int(ubase[-1]), 1), np.uint64)  # unlaunched-candidate masks (header layout)
     out = _abi.ds_scheme_out(st.ctypes.data, ne.ctypes.data, ng.ctypes.data, nd.ctypes.data, nb.ctypes.data,
-                             ndg.ctypes.data, ents.ctypes.data, grps.ctypes.data, bnd.ctypes.data)
+                             ndg.ctypes.data, ents.ctypes.data, grps.ctypes.data, bnd.ctypes.data, unl_w.ctypes.data)
     _lib.check(_lib.lib().ds_schedule_batch(C.byref(b.as_c()), C.byref(_lib.platform(a.M)), C.byref(out), 0))
     nodes = np.diff(b.node_off.astype(np.int64))
     edges = np.diff(b.edge_off.astype(np.int64))
@@ -47,7 +50,8 @@ def main():
             r = grps[base + j]
             mem.append(int(r["n_members"]))
             lau.append(int(r["n_launches"]))
-            unl.append(sum(bin(int(x)).count("1") for x in r["unlaunched"]))
+            w = (int(sizes[d]) + 63) // 64
+            unl.append(sum(bin(int(x)).count("1") for x in unl_w[ubase[d] + j * w: ubase[d] + (j + 1) * w]))
             withl += r["n_launches"] > 0
     splits = int(sum(1 for d in range(n) for k in range(int(ne[d]))
                      if ents[2 * int(b.node_off[d]) + k]["part"] == 1))
