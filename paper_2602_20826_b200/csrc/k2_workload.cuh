@@ -400,64 +400,94 @@ __global__ void k3_dyn_reset(const DArgs a) {
     if (threadIdx.x == 0 && a.idle) *a.idle = 0;
 }
 
-template <bool kTma>
+// One probe pass of a warp over the plan from `cur`: claims a rank of the
+// first entity that can start (pend_done = 0), else of the first whose
+// predecessors are all claimed (pend_claim = 0), window by window; ent = ~0u
+// when nothing is open now. Advances `cur` past fully handed-out entities.
+// (Measured: looking for a startable rank in every window before reserving
+// one is no faster, at M = 148, 32 or 8.)
+__device__ __forceinline__ void dyn_probe(const DArgs& a, const int lane, uint32_t& cur, uint32_t& ent,
+                                          uint32_t& rank) {
+    ent = ~0u;
+    rank = 0;
+    bool got = false;
+    uint32_t gcur = ~0u;  // group of `cur` (priority plans)
+    bool stop = false;
+#pragma unroll 1
+    for (uint32_t base = cur; base < a.n && !got && !stop; base += 32) {
+        const uint32_t e = base + lane;
+        const bool valid = e < a.n;
+        const uint32_t m = valid ? __ldg(a.quota + e) : 0;
+        const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
+        const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
+        const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
+        bool open = valid && cl < m;
+        const unsigned open_mask = __ballot_sync(~0u, open);
+        if (base == cur) {
+            cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
+            if (a.egroup && cur < a.n) gcur = __ldg(a.egroup + cur);
+        }
+        if (a.egroup) {  // later groups wait until this one is fully claimed
+            const bool later = valid && __ldg(a.egroup + e) > gcur;
+            open = open && !later;
+            stop = __any_sync(~0u, later);  // plan order = group order: nothing after
+        }
+        unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
+        if (!pick) pick = __ballot_sync(~0u, open && pc == 0);
+        while (pick && !got) {
+            const int l = __ffs(pick) - 1;
+            pick &= pick - 1;
+            uint32_t c = 0;
+            if (lane == l) c = atomicAdd(a.claimed + e, 1u);
+            c = __shfl_sync(~0u, c, l);
+            const uint32_t ml = __shfl_sync(~0u, m, l);
+            if (c < ml) {
+                got = true;
+                ent = base + l;
+                rank = c;
+            }
+        }
+    }
+}
+
+// a claimed rank of `ent` counts as claimed for its successors (lane 0)
+__device__ __forceinline__ void dyn_commit(const DArgs& a, uint32_t ent) {
+    const DEnt& d = a.ents[ent];
+    for (uint32_t k = 0; k < d.n_succ; ++k) atomicSub(a.pend_claim + a.succs[d.succ_off + k], 1u);
+}
+
+// kAhead (TMA ring, fixed slices): the producer warp schedules — once it has
+// issued an item's last load it already claims the CTA's next item while the
+// consumer warps drain the ring, so the claim's round trips leave the gap
+// between items (the rank still waits for its predecessors after the item
+// ends; deadlock-free as before: the earliest claimed-but-waiting rank has
+// every predecessor rank claimed, and claimed ranks ahead of it are running).
+template <bool kTma, bool kAhead = false>
 __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const DArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ TmaRing ring;
     __shared__ unsigned long long t0s;
     __shared__ uint32_t s_ent, s_rank, s_chunk;
     if (kTma && threadIdx.x == 0) tma_ring_init(&ring);
-    const int lane = threadIdx.x & 31;
+    constexpr int kSched = (kTma && kAhead) ? kTmaConsumerWarps : 0;  // the scheduling warp
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t it = 0;   // TMA ring chunks used by this CTA
-    uint32_t cur = 0;  // entities before cur are fully handed out (warp 0)
+    uint32_t cur = 0;  // entities before cur are fully handed out (scheduling warp)
+    uint32_t next_ent = ~0u, next_rank = 0;  // claimed ahead (kAhead)
 #pragma unroll 1
     while (true) {
-        if (threadIdx.x < 32) {
-            uint32_t ent = ~0u, rank = 0;
-            while (cur < a.n) {
-                bool got = false;
-                uint32_t gcur = ~0u;  // group of `cur` (priority plans)
-                bool stop = false;
-                for (uint32_t base = cur; base < a.n && !got && !stop; base += 32) {
-                    const uint32_t e = base + lane;
-                    const bool valid = e < a.n;
-                    const uint32_t m = valid ? __ldg(a.quota + e) : 0;
-                    const uint32_t cl = valid ? ld_relaxed(a.claimed + e) : 0;
-                    const uint32_t pc = valid ? ld_relaxed(a.pend_claim + e) : 1;
-                    const uint32_t pd = valid ? ld_relaxed(a.pend_done + e) : 1;
-                    bool open = valid && cl < m;
-                    const unsigned open_mask = __ballot_sync(~0u, open);
-                    if (base == cur) {
-                        cur = open_mask ? base + __ffs(open_mask) - 1 : base + 32;
-                        if (a.egroup && cur < a.n) gcur = __ldg(a.egroup + cur);
-                    }
-                    if (a.egroup) {  // later groups wait until this one is fully claimed
-                        const bool later = valid && __ldg(a.egroup + e) > gcur;
-                        open = open && !later;
-                        stop = __any_sync(~0u, later);  // plan order = group order: nothing after
-                    }
-                    unsigned pick = __ballot_sync(~0u, open && pc == 0 && pd == 0);
-                    if (!pick) pick = __ballot_sync(~0u, open && pc == 0);
-                    while (pick && !got) {
-                        const int l = __ffs(pick) - 1;
-                        pick &= pick - 1;
-                        uint32_t c = 0;
-                        if (lane == l) c = atomicAdd(a.claimed + e, 1u);
-                        c = __shfl_sync(~0u, c, l);
-                        const uint32_t ml = __shfl_sync(~0u, m, l);
-                        if (c < ml) {
-                            got = true;
-                            ent = base + l;
-                            rank = c;
-                        }
-                    }
+        if (warp == kSched) {
+            uint32_t ent = next_ent, rank = next_rank;
+            next_ent = ~0u;
+            while (ent == ~0u && cur < a.n) {
+                dyn_probe(a, lane, cur, ent, rank);
+                if (ent != ~0u) {
+                    if (lane == 0) dyn_commit(a, ent);
+                    break;
                 }
-                if (got) break;
                 __nanosleep(32);
             }
             if (lane == 0 && ent != ~0u) {
-                const DEnt& d = a.ents[ent];
-                for (uint32_t k = 0; k < d.n_succ; ++k) atomicSub(a.pend_claim + a.succs[d.succ_off + k], 1u);
                 while (ld_acquire(a.pend_done + ent) != 0) {
                 }  // tight: every reserved rank of ent starts within one L2 round trip
                 t0s = gtimer();
@@ -477,6 +507,10 @@ __global__ void __launch_bounds__(kTma ? kTmaThreads : 1024, 1) k3_dynamic(const
             const unsigned long long s0 = e.lo + len * rank / e.m, s1 = e.lo + len * (rank + 1) / e.m;
             if constexpr (kTma) tma_mix_slice(e.x, e.y, s0, s1, sm, &ring, it);
             else mix_ldg_slice<4>(e.x, e.y, s0, s1);
+            if (kAhead && warp == kSched && cur < a.n) {  // loads issued: claim the next item now
+                dyn_probe(a, lane, cur, next_ent, next_rank);
+                if (next_ent != ~0u && lane == 0) dyn_commit(a, next_ent);
+            }
         } else {
             // chunked ranks: claim chunk after chunk of the entity's range; the
             // next claim is issued before the current chunk is processed

@@ -77,6 +77,21 @@ struct Exec {
 // barriers), sorted by plan index so entities released together enter the
 // ready queue in schedule order; with DS_PLAN_PRIORITY also each entity's
 // group, which the kernel's claim rule reads.
+// The dynamic engine's kernel. On a partition of the GPU (green context:
+// many ranks per SM in sequence) the producer warp claims each CTA's next
+// item while the ring drains (k3_dynamic<true, true>): measured -2..3% on
+// C2/C4 at M = 32 and 8, +0.7% at M = 148, where it stays off.
+// DS_DYN_AHEAD=0/1 forces it (A/B knob).
+void* dynamic_kernel(bool tma, bool partition) {
+    static const int forced = [] {
+        const char* e = getenv("DS_DYN_AHEAD");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool ahead = forced >= 0 ? forced == 1 : partition;
+    if (!tma) return reinterpret_cast<void*>(k3_dynamic<false>);
+    return ahead ? reinterpret_cast<void*>(k3_dynamic<true, true>) : reinterpret_cast<void*>(k3_dynamic<true, false>);
+}
+
 int build_dynamic(Exec* E, const ds_exec_plan* plan) {
     const int n = plan->n_entities;
     int max_group = -1;
@@ -168,8 +183,8 @@ int build_dynamic(Exec* E, const ds_exec_plan* plan) {
     }
     a.chunk = E->chunk_elems;
     const bool tma = E->workload == DS_WL_MIX32_TMA;
-    void* k = tma ? reinterpret_cast<void*>(k3_dynamic<true>) : reinterpret_cast<void*>(k3_dynamic<false>);
-    DS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tma ? kTmaSmem : kNodeSmem));
+    DS_CUDA(cudaFuncSetAttribute(dynamic_kernel(tma, E->gctx != nullptr), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tma ? kTmaSmem : kNodeSmem));
     E->grid = uint32_t(E->sm_count);
     return DS_OK;
 }
@@ -602,7 +617,7 @@ int ds_exec_run(void* exec, int warmup, int replays, ds_exec_trace* trace) {
             // cooperative: every CTA (one per SM) resident at once; they wait
             // on each other's completion counters
             DS_CUDA(cudaLaunchCooperativeKernel(
-                tma ? reinterpret_cast<void*>(k3_dynamic<true>) : reinterpret_cast<void*>(k3_dynamic<false>),
+                dynamic_kernel(tma, E->gctx != nullptr),
                 dim3(E->grid), dim3(tma ? unsigned(kTmaThreads) : 1024u), kargs, size_t(tma ? kTmaSmem : kNodeSmem),
                 E->s));
         } else if (E->engine == DS_ENGINE_STREAMS) {
