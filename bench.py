@@ -546,9 +546,9 @@ def main():
     # the caller's host arrays in the most compact wire form the batch fits,
     # pinned; the conversion is the caller's packing, outside the timed region
     wire = args.wire
-    if wire == "auto":  # measured fastest first (the e2e pass is GPU-bound, and the
-        # triangular form's device expansion costs more than its PCIe saving)
-        wire = "16" if batch.compact16_ok() else "tri" if batch.tri_ok() else "wide"
+    if wire == "auto":  # measured fastest first: the triangular form (half the 16-bit
+        # form's PCIe bytes; k1_fast reads it as is), then the 16-bit one
+        wire = "tri" if batch.tri_ok() else "16" if batch.compact16_ok() else "wide"
     pin = lambda n, dt: torch.empty(n, dtype=dt, pin_memory=True).numpy()  # noqa: E731
     if wire == "tri":
         adj_off = batch.tri_words()
@@ -664,7 +664,10 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
             # per chunk: the K1 sequence, plus the 16-bit form's widening kernel
-            "e2e_gpu_launches": chunks * (launches_per_step + int(wire != "wide")) * args.e2e_steps,
+            # per chunk: the session's kernels + the wire form's widening
+            # (16-bit: k_widen16; triangular: k_widen_tri_list over the
+            # fallback and retry queues)
+            "e2e_gpu_launches": chunks * (launches_per_step + {"tri": 2, "16": 1, "wide": 0}[wire]) * args.e2e_steps,
             "dags_ok": ok, "generation_s": gen_s,
             "kernel_ms": {"mean": statistics.mean(kms), "min": min(kms), "max": max(kms)},
         }

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -150,64 +151,6 @@ __global__ void k_widen16(const uint16_t* __restrict__ ln16, const uint16_t* __r
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < ne; i += stride) {
         const u32 e = e16[i];
         edges[i] = ((e >> 8) << 16) | (e & 0xffu);
-    }
-}
-
-// ds_dag_batch_tri -> the analysis' wide form, one warp per DAG: loads
-// widened, each node's predecessor bits read out of the triangular matrix,
-// transposed to successor masks and written as the (from << 16 | to) edge
-// list in (from, to) order into the DAG's capacity slot (32 edges per
-// adjacency word: edge_off[d] = 32 * word offset, edge_cnt[d] = edges).
-// Reads ~107 B and writes ~30 B per node-edge pair set of a C5 DAG: HBM-light.
-__global__ void __launch_bounds__(256) k_widen_tri(const u32* __restrict__ node_off, const u32* __restrict__ adj_off,
-                                                   const uint16_t* __restrict__ ln16, const u32* __restrict__ adj,
-                                                   u64 n_dags, u64* __restrict__ ln, u32* __restrict__ edge_off,
-                                                   u32* __restrict__ edge_cnt, u32* __restrict__ edges) {
-    const int lane = threadIdx.x & 31;
-    const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
-    const u32 nb = node_off[0], ab = adj_off[0];
-    for (u64 d = u64(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_dags; d += warps) {
-        const u32 n0 = node_off[d] - nb;
-        const int n = int(node_off[d + 1] - node_off[d]);
-        const u32 w0 = adj_off[d] - ab, nw = adj_off[d + 1] - adj_off[d];
-        for (int v = lane; v < n; v += 32) ln[n0 + v] = ln16[n0 + v];
-        if (lane == 0) {
-            edge_off[d] = w0 * 32u;
-            if (d + 1 == n_dags) edge_off[n_dags] = (adj_off[n_dags] - ab) * 32u;
-        }
-        // predecessor bits of node v: [v(v-1)/2, v(v-1)/2 + v) of the DAG's words
-        const u32* w = adj + w0;
-        auto preds = [&](int v) -> u64 {
-            if (v <= 0 || v >= n) return 0;
-            const u32 o = u32(v) * u32(v - 1) / 2, k = o >> 5, sh = o & 31;
-            u64 x = w[k] >> sh;
-            if (k + 1 < nw) x |= u64(w[k + 1]) << (32 - sh);
-            if (sh && k + 2 < nw) x |= u64(w[k + 2]) << (64 - sh);
-            return x & ((1ull << v) - 1);  // v <= 63
-        };
-        const u64 pa = preds(lane), pb = preds(lane + 32);
-        // successors of u = lane (sa) and u = lane + 32 (sb): transpose
-        const u32 t00 = warp_transpose32(u32(pa), lane), t10 = warp_transpose32(u32(pb), lane);
-        const u32 t11 = n > 32 ? warp_transpose32(u32(pb >> 32), lane) : 0u;
-        const u64 sa = (u64(t10) << 32) | t00, sb = u64(t11) << 32;
-        // edges in (from, to) order: u = 0..31 (slot a), then 32..63 (slot b)
-        const u32 ca = __popcll(sa), cb = __popcll(sb);
-        u32 ia = ca, ib = cb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
-            if (lane >= o) {
-                ia += ya;
-                ib += yb;
-            }
-        }
-        const u32 tot_a = __shfl_sync(FULL, ia, 31), tot = tot_a + __shfl_sync(FULL, ib, 31);
-        u32* e = edges + w0 * 32u;
-        u32 pos = ia - ca;
-        for (u64 m = sa; m; m &= m - 1) e[pos++] = (u32(lane) << 16) | u32(__ffsll(m) - 1);
-        pos = tot_a + ib - cb;
-        for (u64 m = sb; m; m &= m - 1) e[pos++] = (u32(lane + 32) << 16) | u32(__ffsll(m) - 1);
-        if (lane == 0) edge_cnt[d] = tot;
     }
 }
 
@@ -374,6 +317,31 @@ int small_stream(int device, DeviceCtx& ctx, cudaStream_t& s) {
     return DS_OK;
 }
 
+// DS_SMALL_TRACE=1: the latency path's kernel time (CUDA events) on stderr
+int small_launch_traced(const K1Args& a, bool detail, cudaStream_t s) {
+    static const bool trace = [] {
+        const char* e = getenv("DS_SMALL_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!trace) {
+        DS_CUDA(k1_small_launch(a, detail, s));
+        return DS_OK;
+    }
+    cudaEvent_t e0, e1;
+    DS_CUDA(cudaEventCreate(&e0));
+    DS_CUDA(cudaEventCreate(&e1));
+    DS_CUDA(cudaEventRecord(e0, s));
+    DS_CUDA(k1_small_launch(a, detail, s));
+    DS_CUDA(cudaEventRecord(e1, s));
+    DS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    DS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    fprintf(stderr, "[small] k1_small<%d> %llu DAGs: %.1f us\n", int(detail), (unsigned long long)a.n_dags, 1e3 * ms);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return DS_OK;
+}
+
 // bounds mode (ds_analyze_batch / ds_analyze_batch16 for small host batches)
 int analyze_small(const HostView& h, const PlatT<u64>& P, uint32_t mask, ds_results* out, int device) {
     K1Occupancy occ;
@@ -393,7 +361,7 @@ int analyze_small(const HostView& h, const PlatT<u64>& P, uint32_t mask, ds_resu
     a.bounds = reinterpret_cast<int64_t*>(dv + o_b);
     a.status = reinterpret_cast<int32_t*>(dv + o_st);
     a.n_groups = reinterpret_cast<uint16_t*>(dv + o_ng);
-    DS_CUDA(k1_small_launch(a, false, s));
+    if (int rc = small_launch_traced(a, false, s)) return rc;
     DS_CUDA(cudaStreamSynchronize(s));
     const char* r = static_cast<const char*>(ctx.small_out.p);
     std::memcpy(out->bounds, r + o_b, n * 80);
@@ -455,9 +423,12 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     constexpr bool compact = std::is_same<Batch, ds_dag_batch16>::value;
     constexpr bool tri = std::is_same<Batch, ds_dag_batch_tri>::value;
     if constexpr (tri) {
-        for (u64 d = 0; d < b->n_dags; ++d)
-            if (b->node_off[d + 1] - b->node_off[d] > 64) return fail(DS_EINVAL, "ds_dag_batch_tri: DAG with more than 64 nodes");
-        if (b->n_dags <= kSmallDags && small_enabled()) return analyze_small_tri(b, P, mask, out, device);
+        // (the size check of bigger batches runs per chunk, beside the GPU work)
+        if (b->n_dags <= kSmallDags && small_enabled()) {
+            if (batch_max_n(b->node_off, 0, b->n_dags) > 64)
+                return fail(DS_EINVAL, "ds_dag_batch_tri: DAG with more than 64 nodes");
+            return analyze_small_tri(b, P, mask, out, device);
+        }
     } else {
         // the latency kernel covers DAGs up to 256 nodes; bigger ones take k1_big
         if (b->n_dags <= kSmallDags && small_enabled() && batch_max_n(b->node_off, 0, b->n_dags) <= 256)
@@ -535,6 +506,7 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         for (cudaStream_t st : ctx.pipe) DS_CUDA(cudaStreamSynchronize(st));
         for (int k = 0; k < kMaxSlots; ++k) ctx.pev_live[k] = false;
     }
+    const auto h0 = std::chrono::steady_clock::now();
     if (int rc = tmark(pipe ? ctx.pipe[0] : ctx.slot[0].s)) return rc;
     for (size_t c = 0; c + 1 < bounds.size(); ++c) {
         const u64 lo = bounds[c], hi = bounds[c + 1], nd = hi - lo;
@@ -597,15 +569,9 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
             DS_CUDA(cudaStreamWaitEvent(s_front, ctx.pev[si][0], 0));
         }
         if (int rc = tmark(s_in)) return rc;
-        // the compact wire forms widen on the device (the front stream)
-        if constexpr (tri) {
-            const unsigned grid = unsigned(std::min<u64>((nd + 7) / 8, 148 * 8));
-            k_widen_tri<<<grid, 256, 0, s_front>>>(sl.node_off.as<const u32>(), sl.adj_off.as<const u32>(),
-                                                    sl.ln16.as<const uint16_t>(), sl.adj.as<const u32>(), nd,
-                                                    sl.ln.as<u64>(), sl.edge_off.as<u32>(), sl.edge_cnt.as<u32>(),
-                                                    sl.edges.as<u32>());
-            DS_CUDA(cudaGetLastError());
-        } else if constexpr (compact) {
+        // the 16-bit form widens on the device (the front stream); the
+        // triangular one inside k1_launch (only what the general kernels take)
+        if constexpr (compact) {
             k_widen16<<<296, 512, 0, s_front>>>(sl.ln16.as<const uint16_t>(), sl.edges16.as<const uint16_t>(), nn, ne,
                                                 sl.ln.as<u64>(), sl.edges.as<u32>());
             DS_CUDA(cudaGetLastError());
@@ -618,6 +584,15 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         a.load_den = has_den ? sl.ldn.as<const u64>() : nullptr;
         a.edges = sl.edges.as<const u32>();
         a.edge_cnt = tri ? sl.edge_cnt.as<const u32>() : nullptr;
+        if constexpr (tri) {
+            a.tri.adj = sl.adj.as<const u32>();
+            a.tri.adj_off = sl.adj_off.as<const u32>();
+            a.tri.ln16 = sl.ln16.as<const uint16_t>();
+            a.tri.ln = sl.ln.as<u64>();
+            a.tri.edge_off = sl.edge_off.as<u32>();
+            a.tri.edge_cnt = sl.edge_cnt.as<u32>();
+            a.tri.edges = sl.edges.as<u32>();
+        }
         a.plat = P;
         a.mask = mask;
         a.status = sl.status.as<int32_t>();
@@ -628,7 +603,12 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         a.retry2 = a.retry + nd;
         a.retry2_count = a.retry_count + 1;
         if (int rc = attach_handoff(a, sl.handoff, nd, nn)) return rc;
-        const u32 max_n = tri ? 64u : batch_max_n(b->node_off, lo, hi);
+        const u32 max_n = batch_max_n(b->node_off, lo, hi);
+        if (tri && max_n > 64) {  // nothing of this chunk is queued yet; drain the earlier ones
+            for (cudaStream_t st : ctx.pipe) cudaStreamSynchronize(st);
+            for (auto& slot : ctx.slot) cudaStreamSynchronize(slot.s);
+            return fail(DS_EINVAL, "ds_dag_batch_tri: DAG with more than 64 nodes");
+        }
         if (int rc = attach_big(a, sl.big_q, sl.big_scratch, nd, max_n)) return rc;
         DS_CUDA(k1_launch(a, occ, max_n, false, s_front, nullptr, pipe && pipe_split ? s_back : nullptr,
                           pipe && pipe_split ? ctx.pev[si][1] : nullptr));
@@ -648,12 +628,18 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         }
         if (int rc = tmark(s_out)) return rc;
     }
+    const auto h1 = std::chrono::steady_clock::now();
     if (pipe) {
         DS_CUDA(cudaStreamSynchronize(ctx.pipe[3]));
     } else {
         for (auto& sl : ctx.slot) DS_CUDA(cudaStreamSynchronize(sl.s));
     }
     if (trace) {
+        const auto h2 = std::chrono::steady_clock::now();
+        auto us = [&](std::chrono::steady_clock::time_point t) {
+            return std::chrono::duration<double, std::micro>(t - h0).count();
+        };
+        fprintf(stderr, "[e2e] host: enqueue done %.0f us, synchronised %.0f us\n", us(h1), us(h2));
         // per chunk: inputs landed, K1 done, results landed (ms from the start)
         for (size_t i = 1; i + 2 < tev.size(); i += 3) {
             float t[3];
@@ -974,7 +960,7 @@ int schedule_small(const ds_dag_batch* b, const PlatT<u64>& P, ds_scheme_out* ou
     a.det.unlaunched = reinterpret_cast<uint64_t*>(dv + o_unl);
     unl_layout(b->node_off, n, reinterpret_cast<u64*>(static_cast<char*>(ctx.small_out.p) + o_ub));
     a.unl_base = reinterpret_cast<const u64*>(dv + o_ub);
-    DS_CUDA(k1_small_launch(a, true, s));
+    if (int rc = small_launch_traced(a, true, s)) return rc;
     DS_CUDA(cudaStreamSynchronize(s));
     const char* r = static_cast<const char*>(ctx.small_out.p);
     auto put = [&](void* dst, size_t off, size_t len) {

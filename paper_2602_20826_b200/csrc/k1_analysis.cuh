@@ -1186,6 +1186,30 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     u32* l64;        // DAGs with 32 < n <= 64 for k1_fast<64> (count: retry_count[8])
 };
 
+// The triangular wire form (ds_dag_batch_tri) as K1 reads it: the fast path
+// takes each node's predecessor mask straight out of the adjacency bits; the
+// wide arrays (u64 loads, capacity-layout edge list) are written on demand
+// for the DAGs the general kernels take (k1_tri.cuh).
+struct TriWire {
+    const u32* adj = nullptr;       // strictly lower-triangular bits, node v's preds at v(v-1)/2 ..
+    const u32* adj_off = nullptr;   // [n + 1] word offsets (relative to adj_off[0])
+    const uint16_t* ln16 = nullptr; // [N] integer loads
+    u64* ln = nullptr;              // widened: the K1Args::load_num array
+    u32* edge_off = nullptr;        // widened: K1Args::edge_off (32 edges per adjacency word)
+    u32* edge_cnt = nullptr;        // widened: K1Args::edge_cnt
+    u32* edges = nullptr;           // widened: K1Args::edges
+};
+
+// node v's predecessor mask (v < 64) from a DAG's triangular words w[0 .. nw)
+__device__ __forceinline__ u64 tri_preds(const u32* w, u32 nw, int n, int v) {
+    if (v <= 0 || v >= n) return 0;
+    const u32 o = u32(v) * u32(v - 1) / 2, k = o >> 5, sh = o & 31;
+    u64 x = w[k] >> sh;
+    if (k + 1 < nw) x |= u64(w[k + 1]) << (32 - sh);
+    if (sh && k + 2 < nw) x |= u64(w[k + 2]) << (64 - sh);
+    return x & ((1ull << v) - 1);
+}
+
 struct K1Args {
     u64 n_dags;
     const u32* node_off;
@@ -1215,6 +1239,7 @@ struct K1Args {
     const u32* perm;       // k1_back_lane's DAG order (nullptr: index order)
     int fb_only;           // k1_front / k1_mid take only the DAGs k1_fast queued (h.fb)
     int key_mode;          // walk_key() layout (DS_WALK_KEY)
+    TriWire tri;           // triangular wire form (tri.adj != nullptr)
 };
 
 template <int W, class T, bool DETAIL>

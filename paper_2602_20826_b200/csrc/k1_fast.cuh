@@ -66,29 +66,42 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
     const bool hi = n > 32;
     const int va = lane, vb = lane + 32;
     const bool ina = va < n, inb = vb < n;
-    // ---- loads: integers in [1, 65535]
-    const long long la_ = ina ? (long long)a.load_num[n0 + va] : 1;
-    const long long lb_ = inb ? (long long)a.load_num[n0 + vb] : 1;
-    if (__any_sync(FULL, la_ < 1 || la_ > 65535 || lb_ < 1 || lb_ > 65535)) return -1;
-    const u32 la = u32(la_), lb = u32(lb_);
-    // ---- edges (sorted (from, to) words): all u < v < n, scattered to pred
-    S.pred[lane] = 0;
-    S.pred[lane + 32] = 0;
-    __syncwarp();
-    bool bad = false;
+    u32 la, lb;
+    u64 pa, pb;
+    if (a.tri.adj) {  // triangular wire form: u16 loads, predecessor bits
+        la = ina ? u32(a.tri.ln16[n0 + va]) : 1u;
+        lb = inb ? u32(a.tri.ln16[n0 + vb]) : 1u;
+        if (__any_sync(FULL, la < 1 || lb < 1)) return -1;
+        const u32 w0 = a.tri.adj_off[d] - a.tri.adj_off[0], nw = a.tri.adj_off[d + 1] - a.tri.adj_off[d];
+        pa = tri_preds(a.tri.adj + w0, nw, n, va);
+        pb = hi ? tri_preds(a.tri.adj + w0, nw, n, vb) : 0ull;
+    } else {
+        // ---- loads: integers in [1, 65535]
+        const long long la_ = ina ? (long long)a.load_num[n0 + va] : 1;
+        const long long lb_ = inb ? (long long)a.load_num[n0 + vb] : 1;
+        if (__any_sync(FULL, la_ < 1 || la_ > 65535 || lb_ < 1 || lb_ > 65535)) return -1;
+        la = u32(la_);
+        lb = u32(lb_);
+        // ---- edges (sorted (from, to) words): all u < v < n, scattered to pred
+        S.pred[lane] = 0;
+        S.pred[lane + 32] = 0;
+        __syncwarp();
+        bool bad = false;
 #pragma unroll 1
-    for (int e = lane; e < ne; e += 32) {
-        const u32 w = a.edges[e0 + e];
-        const u32 u = w >> 16, v = w & 0xffffu;
-        if (u >= v || v >= u32(n)) {
-            bad = true;
-        } else {
-            atomicOr(reinterpret_cast<unsigned int*>(&S.pred[v]) + (u >> 5), 1u << (u & 31));
+        for (int e = lane; e < ne; e += 32) {
+            const u32 w = a.edges[e0 + e];
+            const u32 u = w >> 16, v = w & 0xffffu;
+            if (u >= v || v >= u32(n)) {
+                bad = true;
+            } else {
+                atomicOr(reinterpret_cast<unsigned int*>(&S.pred[v]) + (u >> 5), 1u << (u & 31));
+            }
         }
+        if (__any_sync(FULL, bad)) return -1;
+        __syncwarp();
+        pa = S.pred[va];
+        pb = hi ? S.pred[vb] : 0ull;
     }
-    if (__any_sync(FULL, bad)) return -1;
-    __syncwarp();
-    const u64 pa = S.pred[va], pb = hi ? S.pred[vb] : 0ull;
     // ---- exactly one source and one sink (dag.cpp:97-108): in index order
     // node 0 is a source and node n-1 a sink, so check there are no others
     const u32 hs_lo = __reduce_or_sync(FULL, u32(pa) | u32(pb)), hs_hi = __reduce_or_sync(FULL, u32(pa >> 32) | u32(pb >> 32));
@@ -339,24 +352,32 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     const bool in = lane < n;
     const u32 V = n == 32 ? FULL : ((1u << n) - 1);
     const u32 lt = (1u << lane) - 1;  // lanes below this one
-    const long long l_ = in ? (long long)a.load_num[n0 + lane] : 1;
-    if (__any_sync(FULL, l_ < 1 || l_ > 65535)) return -1;
-    const u32 l = u32(l_);
-    // ---- edges: every u < v < n (index order is topological), scattered to pred
-    unsigned int* pr = reinterpret_cast<unsigned int*>(S.pred);
-    pr[lane] = 0;
-    __syncwarp();
-    bool bad = false;
+    u32 l, p;
+    if (a.tri.adj) {  // triangular wire form: u16 loads, predecessor bits
+        l = in ? u32(a.tri.ln16[n0 + lane]) : 1u;
+        if (__any_sync(FULL, l < 1)) return -1;
+        const u32 w0 = a.tri.adj_off[d] - a.tri.adj_off[0], nw = a.tri.adj_off[d + 1] - a.tri.adj_off[d];
+        p = u32(tri_preds(a.tri.adj + w0, nw, n, lane));
+    } else {
+        const long long l_ = in ? (long long)a.load_num[n0 + lane] : 1;
+        if (__any_sync(FULL, l_ < 1 || l_ > 65535)) return -1;
+        l = u32(l_);
+        // ---- edges: every u < v < n (index order is topological), scattered to pred
+        unsigned int* pr = reinterpret_cast<unsigned int*>(S.pred);
+        pr[lane] = 0;
+        __syncwarp();
+        bool bad = false;
 #pragma unroll 1
-    for (int e = lane; e < ne; e += 32) {
-        const u32 w = a.edges[e0 + e];
-        const u32 u = w >> 16, v = w & 0xffffu;
-        if (u >= v || v >= u32(n)) bad = true;
-        else atomicOr(pr + v, 1u << u);
+        for (int e = lane; e < ne; e += 32) {
+            const u32 w = a.edges[e0 + e];
+            const u32 u = w >> 16, v = w & 0xffffu;
+            if (u >= v || v >= u32(n)) bad = true;
+            else atomicOr(pr + v, 1u << u);
+        }
+        if (__any_sync(FULL, bad)) return -1;
+        __syncwarp();
+        p = in ? pr[lane] : 0u;
     }
-    if (__any_sync(FULL, bad)) return -1;
-    __syncwarp();
-    const u32 p = in ? pr[lane] : 0u;
     // ---- one source, one sink (dag.cpp:97-108)
     const u32 has_succ = __reduce_or_sync(FULL, p);
     if (__popc(__ballot_sync(FULL, in && p == 0)) != 1 || __popc(V & ~has_succ) != 1) return -1;
@@ -505,7 +526,8 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
     __shared__ FastWarp ws[kFastWarps];
     const int lane = threadIdx.x & 31;
     FastWarp& S = ws[threadIdx.x >> 5];
-    const u32 nbase = a.node_off[0], ebase = a.edge_off[0];
+    const bool tri = a.tri.adj != nullptr;  // no edge list (widened later for the DAGs queued here)
+    const u32 nbase = a.node_off[0], ebase = tri ? 0u : a.edge_off[0];
     const int M = a.plat.M;
     const u32 n_l64 = NMAX == 64 ? a.retry_count[kL64Counter] : 0u;
 #pragma unroll 1
@@ -516,9 +538,9 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
         if (NMAX == 64 && t >= n_l64) break;
         const u64 d = NMAX == 64 ? a.h.l64[t] : t;
         if (d >= a.n_dags) break;
-        const u32 n0 = a.node_off[d] - nbase, e0 = a.edge_off[d] - ebase;
+        const u32 n0 = a.node_off[d] - nbase, e0 = tri ? 0u : a.edge_off[d] - ebase;
         const int n = int(a.node_off[d + 1] - nbase - n0);
-        const int ne = a.edge_cnt ? int(a.edge_cnt[d]) : int(a.edge_off[d + 1] - ebase - e0);
+        const int ne = tri ? 0 : a.edge_cnt ? int(a.edge_cnt[d]) : int(a.edge_off[d + 1] - ebase - e0);
         int st;
         if (NMAX == 32) {
             if (n > 32 && n <= 64) {  // the two-slot kernel's

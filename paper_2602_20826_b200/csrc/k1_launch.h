@@ -7,6 +7,7 @@
 #include "k1_analysis.cuh"
 
 #include "k1_fast.cuh"
+#include "k1_tri.cuh"
 
 namespace ds {
 

@@ -2,6 +2,7 @@
 // file) and schedule-detail mode (k1_detail.cu defines K1_DETAIL_TU).
 #include "k1_launch.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace ds {
@@ -119,6 +120,15 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
     K1Args af = a;
     af.fb_only = fast ? 1 : 0;
     af.key_mode = key_mode;
+    // triangular wire form: the fast path reads it as is and only the DAGs
+    // the general kernels take are widened (k1_tri.cuh); without the fast
+    // path every DAG is widened first
+    const bool tri = a.tri.adj != nullptr;
+    const int gw = int(std::min<u64>((a.n_dags + 7) / 8, 148 * 8));  // 8 warps (DAGs) per CTA
+    if (tri && !fast) {
+        k_widen_tri<><<<gw, 256, 0, s>>>(a.tri, a.node_off, a.n_dags);
+        if ((e = mark("k_widen_tri")) != cudaSuccess) return e;
+    }
     if (fast) {
         const u64 need = (a.n_dags + kFastWarps - 1) / kFastWarps;
         const int gf = int(need < u64(occ.grid_fast) ? need : u64(occ.grid_fast));
@@ -128,6 +138,10 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
         if ((e = mark("k1_fast<64>")) != cudaSuccess) return e;
     }
     if (split) {
+        if (tri && fast) {  // the DAGs k1_fast queued for the general kernels
+            k_widen_tri_list<><<<148, 256, 0, s>>>(a.tri, a.node_off, a.n_dags, a.h.fb, a.retry_count + kFbCounter);
+            if ((e = mark("k_widen_tri_list")) != cudaSuccess) return e;
+        }
         // every DAG, or (fast path) only those k1_fast queued
         k1_front<><<<cap(occ.grid_front), 32 * kWarpsSmall, kSmemSmall, s>>>(af);
         if ((e = mark("k1_front")) != cudaSuccess) return e;
@@ -195,6 +209,10 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
     }
     // wider-word retries of the DAGs that overflowed 32 (then 64) bits; with
     // nothing queued each kernel reads the count and exits
+    if (tri && fast) {  // lane walks the fast path fed go back to the general kernels
+        k_widen_tri_list<><<<148, 256, 0, s>>>(a.tri, a.node_off, a.n_dags, a.retry, a.retry_count);
+        if ((e = mark("k_widen_tri_list")) != cudaSuccess) return e;
+    }
     const int gr = int(a.n_dags < u64(occ.grid_retry) ? a.n_dags : u64(occ.grid_retry));
     k1_analyse_retry<DETAIL, u64><<<gr, 32, kSmemR64, s>>>(a);
     if ((e = mark("k1_analyse_retry<u64>")) != cudaSuccess) return e;

@@ -168,6 +168,43 @@ def test_triangular_wire_form_invalid_dags():
     assert not big.tri_ok()
 
 
+@pytest.mark.parametrize("n_small", [3, 40000])
+def test_triangular_wire_form_rejects_dags_above_64_nodes(n_small):
+    """A DAG above 64 nodes in a ds_dag_batch_tri is DS_EINVAL, whether the
+    batch takes the latency path or the chunked pipeline (checked per chunk
+    there, here in the last chunk)."""
+    import ctypes as C
+    from paper_2602_20826_b200.batch import DagBatch
+    b = _lib.Corpus(n_small, seed=2).batch()
+    big = pack([([1] * 65, [(i, i + 1) for i in range(64)])])
+    tw = lambda x: x.tri_words()  # noqa: E731
+    # the triangular arrays of b + big, packed by hand (tri() refuses the big DAG)
+    both = DagBatch(np.concatenate([b.node_off, b.node_off[-1] + big.node_off[1:]]).astype(np.uint32),
+                    np.concatenate([b.edge_off, b.edge_off[-1] + big.edge_off[1:]]).astype(np.uint32),
+                    np.concatenate([b.load_num, big.load_num]), np.concatenate([b.load_den, big.load_den]),
+                    np.concatenate([b.edges, big.edges]), np.zeros(b.n_dags + 1, np.int32))
+    adj_off = tw(both)
+    n = both.sizes()
+    ecount = np.diff(both.edge_off.astype(np.int64))
+    dag = np.repeat(np.arange(both.n_dags, dtype=np.int64), ecount)
+    u = (both.edges >> 16).astype(np.int64)
+    v = (both.edges & 0xFFFF).astype(np.int64)
+    bits = np.zeros(int(adj_off[-1]) * 32, np.bool_)
+    bits[adj_off[dag].astype(np.int64) * 32 + v * (v - 1) // 2 + u] = True
+    adj = np.packbits(bits, bitorder="little").view(np.uint32).copy()
+    load16 = both.load_num.astype(np.uint16)
+    assert int(n.max()) == 65
+    cb = both.as_ctri(load16, adj_off, adj)
+    st, bo, ng, r = _lib._results(both.n_dags)
+    rc = _lib.lib().ds_analyze_batch_tri(C.byref(cb), C.byref(_lib.platform(148)), _abi.DS_M_ALL, C.byref(r), 0)
+    assert rc == _abi.DS_EINVAL
+    assert "more than 64" in _lib.lib().ds_last_error().decode()
+    # the library is still usable afterwards
+    st2, b2, _ = _lib.analyze_tri(b, 148)
+    st1, b1, _ = _lib.analyze(b, 148)
+    assert np.array_equal(st1, st2) and np.array_equal(b1, b2)
+
+
 def test_method_mask_subsets(orc):
     b = _lib.Corpus(500, seed=3).batch()
     _, full, _ = _lib.analyze(b, 148)
