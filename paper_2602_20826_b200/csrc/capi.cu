@@ -210,7 +210,7 @@ struct DeviceCtx {
     DevBuf retry, retry_count, handoff, big_q, big_scratch;  // scratch for the device-pointer entry point
     // host-batch pipeline (analyze_host): copy-in, front kernels, back
     // kernels, copy-out streams and per-slot events between them
-    cudaStream_t pipe[4] = {};
+    cudaStream_t pipe[6] = {};  // copy-in, front, back 0, copy-out, back 1, back 2
     cudaEvent_t pev[kMaxSlots][4] = {};
     bool pev_live[kMaxSlots] = {};  // slot's copy-out event recorded (buffers in use)
     DetailCtx det;
@@ -238,8 +238,8 @@ int create_slot_streams(DeviceCtx& ctx) {
     // pipeline: the back kernels (lane walks) outrank the next chunk's front
     // kernels, so a chunk's walks finish first and the front work fills
     // their tail
-    const int pp[4] = {least, std::min(least, greatest + 1), greatest, least};
-    for (int k = 0; k < 4; ++k) DS_CUDA(cudaStreamCreateWithPriority(&ctx.pipe[k], cudaStreamNonBlocking, pp[k]));
+    const int pp[6] = {least, std::min(least, greatest + 1), greatest, least, greatest, greatest};
+    for (int k = 0; k < 6; ++k) DS_CUDA(cudaStreamCreateWithPriority(&ctx.pipe[k], cudaStreamNonBlocking, pp[k]));
     for (auto& row : ctx.pev)
         for (auto& e : row) DS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx.init = true;
@@ -495,6 +495,11 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         const char* e = getenv("DS_PIPE");
         return !(e && e[0] == '0');
     }();
+    static const int pipe_backs = [] {
+        const char* e = getenv("DS_PIPE_BACKS");
+        const int v = e ? atoi(e) : 2;
+        return v >= 1 && v <= 3 ? v : 2;
+    }();
     // DS_PIPE_SPLIT=0: front and back kernels on one stream (tuning knob)
     static const bool pipe_split = [] {
         const char* e = getenv("DS_PIPE_SPLIT");
@@ -516,7 +521,10 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
         if (pipe) {
             s_in = ctx.pipe[0];
             s_front = ctx.pipe[1];
-            s_back = pipe_split ? ctx.pipe[2] : ctx.pipe[1];
+            // back streams in rotation: chunk c+1's lane walks fill the tail
+            // of chunk c's (DS_PIPE_BACKS = 1..3 streams)
+            static const int kBackStream[3] = {2, 4, 5};
+            s_back = pipe_split ? ctx.pipe[kBackStream[c % size_t(pipe_backs)]] : ctx.pipe[1];
             s_out = ctx.pipe[3];
             // the slot's buffers are reused once its previous chunk's results left
             if (ctx.pev_live[si]) DS_CUDA(cudaEventSynchronize(ctx.pev[si][3]));
