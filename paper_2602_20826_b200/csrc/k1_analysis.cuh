@@ -1184,6 +1184,7 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     u32* perm;       // walk order out of k1_wsort
     u32* fb;         // DAGs k1_fast left to the general kernels (count: retry_count[7])
     u32* l64;        // DAGs with 32 < n <= 64 for k1_fast<64> (count: retry_count[8])
+    u32* wcnt;       // per sort window: walked compact / wide DAGs (k1_wsort)
 };
 
 // The triangular wire form (ds_dag_batch_tri) as K1 reads it: the fast path
@@ -1727,14 +1728,33 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
     const int lane = threadIdx.x & 31;
     const u32 nbase = a.node_off[0];
     const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
+    // Task order. Default: 32 consecutive walk-order positions per task. With
+    // wcnt (wide-first): two phases of per-window task slots (128 per window)
+    // — first every window's wide DAGs (n > 32, the longest walks), then its
+    // compact ones — so the last wave of tasks holds short walks and the
+    // kernel's tail shrinks; windows stay in order within a phase (L2
+    // locality), and empty slots are skipped after one counter read.
+    const u64 nwin = (a.n_dags + kSortWindow - 1) / kSortWindow;
+    const u64 slots = nwin * (kSortWindow / 32);
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
-        if (lane == 0) t = atomicAdd(a.retry_count + 5, 32u);
+        if (lane == 0) t = atomicAdd(a.retry_count + 5, a.h.wcnt ? 1u : 32u);
         t = __shfl_sync(FULL, t, 0);
-        if (t >= a.n_dags) break;
-        const u64 q = u64(t) + lane;
-        if (q >= a.n_dags) continue;
+        u64 q;
+        if (a.h.wcnt) {
+            if (t >= 2 * slots) break;
+            const bool wide = t < slots;
+            const u64 sl = wide ? t : t - slots, w = sl / (kSortWindow / 32), k = sl % (kSortWindow / 32);
+            const u32 cc = a.h.wcnt[2 * w], cnt = wide ? a.h.wcnt[2 * w + 1] : cc;
+            if (32 * k >= cnt) continue;
+            if (32 * k + lane >= cnt) continue;
+            q = w * kSortWindow + (wide ? cc : 0) + 32 * k + lane;
+        } else {
+            if (t >= a.n_dags) break;
+            q = u64(t) + lane;
+            if (q >= a.n_dags) continue;
+        }
         const u64 d = a.perm ? u64(a.perm[q]) : q;
         if (a.status[d] != kStPending) continue;
         const u32 n0 = a.node_off[d] - nbase;

@@ -174,11 +174,18 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
         }();
         K1Args b = a;
         b.perm = nullptr;
+        // DS_K1_WIDE_FIRST=0: lane walks in window order only (tuning knob)
+        static const bool wide_first = [] {
+            const char* env = getenv("DS_K1_WIDE_FIRST");
+            return !(env && env[0] == '0');
+        }();
+        b.h.wcnt = nullptr;
         if (sort_walks && a.h.skey) {
-            k1_wsort<><<<int((a.n_dags + kSortWindow - 1) / kSortWindow), kWsortThreads, 0, s>>>(a.h.skey, a.h.perm,
-                                                                                                a.n_dags);
+            k1_wsort<><<<int((a.n_dags + kSortWindow - 1) / kSortWindow), kWsortThreads, 0, s>>>(
+                a.h.skey, a.h.perm, a.n_dags, wide_first ? a.h.wcnt : nullptr);
             if ((e = mark("k1_wsort")) != cudaSuccess) return e;
             b.perm = a.h.perm;
+            if (wide_first) b.h.wcnt = a.h.wcnt;
         }
         {
             const u64 need = (a.n_dags + 32 * kLaneWarps - 1) / (32 * kLaneWarps);
