@@ -1169,6 +1169,18 @@ __device__ __forceinline__ u64 walk_key(const int lane, const u32 ndiv, const u3
     return top | shape;
 }
 constexpr int kDefaultWalkKey = 0;
+// Smallest compact walk key with at least `groups` division groups (the
+// group count sits above the shape bits: bits 20-25 in layout 0, 46-50 in
+// layouts 1 and 2) — the heavy class of k1_back_lane's task order.
+// DS_K1_HEAVY_GROUPS overrides the default of 15 (C5: 14.5 groups per DAG).
+inline u64 walk_key_heavy(int mode) {
+    static const u64 groups = [] {
+        const char* env = getenv("DS_K1_HEAVY_GROUPS");
+        const long v = env ? atol(env) : 15;
+        return u64(v >= 0 && v < 64 ? v : 15);
+    }();
+    return mode == 0 ? (groups << 20) : (std::min<u64>(groups, 31) << 46);
+}
 constexpr u64 kWalkKeyNone = ~0ull;  // never walked (k1_fast left it to the general kernels)
 struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] + v)
     K1Node* node;
@@ -1184,7 +1196,7 @@ struct K1Handoff {   // over the batch's node index (node_off[d] - node_off[0] +
     u32* perm;       // walk order out of k1_wsort
     u32* fb;         // DAGs k1_fast left to the general kernels (count: retry_count[7])
     u32* l64;        // DAGs with 32 < n <= 64 for k1_fast<64> (count: retry_count[8])
-    u32* wcnt;       // per sort window: walked compact / wide DAGs (k1_wsort)
+    u32* wcnt;       // per sort window: walked light compact / heavy compact / wide DAGs (k1_wsort)
 };
 
 // The triangular wire form (ds_dag_batch_tri) as K1 reads it: the fast path
@@ -1729,11 +1741,12 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
     const u32 nbase = a.node_off[0];
     const PlatT<u32> P{a.plat.M, RatT<u32>{u32(a.plat.tmin.n), u32(a.plat.tmin.d)}, a.plat.minl};
     // Task order. Default: 32 consecutive walk-order positions per task. With
-    // wcnt (wide-first): two phases of per-window task slots (128 per window)
-    // — first every window's wide DAGs (n > 32, the longest walks), then its
-    // compact ones — so the last wave of tasks holds short walks and the
-    // kernel's tail shrinks; windows stay in order within a phase (L2
-    // locality), and empty slots are skipped after one counter read.
+    // wcnt (heavy-first): three phases of per-window task slots (128 per
+    // window) — every window's wide DAGs (n > 32, the longest walks), then
+    // its compact DAGs with many division groups, then the rest — so the last
+    // wave of tasks holds short walks and the kernel's tail shrinks; windows
+    // stay in order within a phase (L2 locality), and empty slots are skipped
+    // after one counter read.
     const u64 nwin = (a.n_dags + kSortWindow - 1) / kSortWindow;
     const u64 slots = nwin * (kSortWindow / 32);
 #pragma unroll 1
@@ -1743,13 +1756,14 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
         t = __shfl_sync(FULL, t, 0);
         u64 q;
         if (a.h.wcnt) {
-            if (t >= 2 * slots) break;
-            const bool wide = t < slots;
-            const u64 sl = wide ? t : t - slots, w = sl / (kSortWindow / 32), k = sl % (kSortWindow / 32);
-            const u32 cc = a.h.wcnt[2 * w], cnt = wide ? a.h.wcnt[2 * w + 1] : cc;
+            if (t >= 3 * slots) break;
+            const int cls = 2 - int(t / slots);  // 2 wide, 1 heavy compact, 0 light compact
+            const u64 sl = t % slots, w = sl / (kSortWindow / 32), k = sl % (kSortWindow / 32);
+            const u32* c = a.h.wcnt + 3 * w;
+            const u32 cnt = c[cls], start = cls == 0 ? 0u : cls == 1 ? c[0] : c[0] + c[1];
             if (32 * k >= cnt) continue;
             if (32 * k + lane >= cnt) continue;
-            q = w * kSortWindow + (wide ? cc : 0) + 32 * k + lane;
+            q = w * kSortWindow + start + 32 * k + lane;
         } else {
             if (t >= a.n_dags) break;
             q = u64(t) + lane;

@@ -567,33 +567,30 @@ __global__ void __launch_bounds__(32 * kFastWarps) k1_fast(const K1Args a) {
 // index order, as a stable sort would.
 constexpr int kWsortThreads = 1024;
 static_assert(kSortWindow == 4096, "k1_wsort sorts 4096-DAG windows");
-// With `wcnt`, the window's walked DAGs are also counted by layout —
-// wcnt[2w] compact (k1_fast<32> hand-off, sorted first), wcnt[2w + 1] wide —
-// for k1_back_lane's wide-first task order.
+// With `wcnt`, the window's walked DAGs are also counted by weight class, in
+// sort order: wcnt[3w] light compact (key < heavy_key), wcnt[3w + 1] heavy
+// compact (k1_fast<32> hand-offs with many division groups), wcnt[3w + 2]
+// wide (K1Node hand-offs) — for k1_back_lane's heavy-first task order.
 template <bool UNUSED = false>
 __global__ void __launch_bounds__(kWsortThreads) k1_wsort(const u64* __restrict__ skey, u32* __restrict__ perm,
-                                                           u64 n_dags, u32* __restrict__ wcnt) {
+                                                           u64 n_dags, u32* __restrict__ wcnt, u64 heavy_key) {
     __shared__ u64 k[kSortWindow];
     const u64 base = u64(blockIdx.x) * kSortWindow;
-    int nc = 0, nw = 0;
+    int c[3] = {0, 0, 0};
     for (int i = threadIdx.x; i < int(kSortWindow); i += kWsortThreads) {
         const u64 d = base + u64(i);
         const u64 key = d < n_dags ? skey[d] : kWalkKeyNone;
         k[i] = d < n_dags ? (key << 12) | u64(i) : ~0ull;  // 52-bit key, window-relative index
-        nc += key != kWalkKeyNone && !((key >> 51) & 1);
-        nw += key != kWalkKeyNone && ((key >> 51) & 1);
+        if (key != kWalkKeyNone) ++c[((key >> 51) & 1) ? 2 : key >= heavy_key ? 1 : 0];
     }
     if (wcnt) {
-        __shared__ int sc, sw;
-        if (threadIdx.x == 0) sc = sw = 0;
+        __shared__ int sc[3];
+        if (threadIdx.x < 3) sc[threadIdx.x] = 0;
         __syncthreads();
-        if (nc) atomicAdd(&sc, nc);
-        if (nw) atomicAdd(&sw, nw);
+        for (int j = 0; j < 3; ++j)
+            if (c[j]) atomicAdd(&sc[j], c[j]);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            wcnt[2 * blockIdx.x] = u32(sc);
-            wcnt[2 * blockIdx.x + 1] = u32(sw);
-        }
+        if (threadIdx.x < 3) wcnt[3 * blockIdx.x + threadIdx.x] = u32(sc[threadIdx.x]);
     }
     __syncthreads();
 #pragma unroll 1

@@ -28,7 +28,7 @@ constexpr int kK1Counters = 12;  // u32 work counters at K1Args::retry_count (48
 // Scratch for the front/back split (K1Handoff), carved from one buffer.
 inline size_t k1_handoff_bytes(u64 n_dags, u64 n_nodes) {
     return size_t(n_nodes) * (sizeof(K1Node) + 2 * 8 + 2) + size_t(n_dags) * 2 + 64 + 256 + size_t(n_dags) * 20 +
-           size_t(n_dags / kSortWindow + 2) * 8;
+           size_t(n_dags / kSortWindow + 2) * 12;
 }
 inline K1Handoff k1_handoff_carve(void* base, u64 n_dags, u64 n_nodes) {
     K1Handoff h;

@@ -174,7 +174,9 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
         }();
         K1Args b = a;
         b.perm = nullptr;
-        // DS_K1_WIDE_FIRST=0: lane walks in window order only (tuning knob)
+        // DS_K1_WIDE_FIRST=0: lane walks in window order only (tuning knob);
+        // DS_K1_HEAVY_GROUPS: the division-group count from which a compact
+        // DAG's walk counts as heavy (walk_key_heavy)
         static const bool wide_first = [] {
             const char* env = getenv("DS_K1_WIDE_FIRST");
             return !(env && env[0] == '0');
@@ -182,7 +184,7 @@ cudaError_t k1_launch_t(const K1Args& a, const K1Occupancy& occ, u32 max_n, cuda
         b.h.wcnt = nullptr;
         if (sort_walks && a.h.skey) {
             k1_wsort<><<<int((a.n_dags + kSortWindow - 1) / kSortWindow), kWsortThreads, 0, s>>>(
-                a.h.skey, a.h.perm, a.n_dags, wide_first ? a.h.wcnt : nullptr);
+                a.h.skey, a.h.perm, a.n_dags, wide_first ? a.h.wcnt : nullptr, walk_key_heavy(key_mode));
             if ((e = mark("k1_wsort")) != cudaSuccess) return e;
             b.perm = a.h.perm;
             if (wide_first) b.h.wcnt = a.h.wcnt;
