@@ -1747,18 +1747,26 @@ __global__ void __launch_bounds__(32 * kLaneWarps, DS_LANE_MIN_BLOCKS) k1_back_l
     // wave of tasks holds short walks and the kernel's tail shrinks; windows
     // stay in order within a phase (L2 locality), and empty slots are skipped
     // after one counter read.
+    // Only the last ~two waves of windows are phased (the tail is the last
+    // wave); earlier windows go in plain window order, which keeps a warp's
+    // hand-off reads inside a compact address range (L2 hits).
     const u64 nwin = (a.n_dags + kSortWindow - 1) / kSortWindow;
-    const u64 slots = nwin * (kSortWindow / 32);
+    const u64 wave = u64(gridDim.x) * (blockDim.x >> 5) * 32;  // DAGs one wave of warp tasks covers
+    const u64 w0 = a.n_dags > 2 * wave ? (a.n_dags - 2 * wave) / kSortWindow : 0;  // first phased window
+    const u64 plain = w0 * (kSortWindow / 32), slots = (nwin - w0) * (kSortWindow / 32);
 #pragma unroll 1
     for (;;) {
         u32 t = 0;
         if (lane == 0) t = atomicAdd(a.retry_count + 5, a.h.wcnt ? 1u : 32u);
         t = __shfl_sync(FULL, t, 0);
         u64 q;
-        if (a.h.wcnt) {
-            if (t >= 3 * slots) break;
-            const int cls = 2 - int(t / slots);  // 2 wide, 1 heavy compact, 0 light compact
-            const u64 sl = t % slots, w = sl / (kSortWindow / 32), k = sl % (kSortWindow / 32);
+        if (a.h.wcnt && t < plain) {
+            q = u64(t) * 32 + lane;  // windows [0, w0): walk order as sorted
+        } else if (a.h.wcnt) {
+            const u64 tp = t - plain;
+            if (tp >= 3 * slots) break;
+            const int cls = 2 - int(tp / slots);  // 2 wide, 1 heavy compact, 0 light compact
+            const u64 sl = tp % slots, w = w0 + sl / (kSortWindow / 32), k = sl % (kSortWindow / 32);
             const u32* c = a.h.wcnt + 3 * w;
             const u32 cnt = c[cls], start = cls == 0 ? 0u : cls == 1 ? c[0] : c[0] + c[1];
             if (32 * k >= cnt) continue;
