@@ -448,6 +448,19 @@ int analyze_host(const Batch* b, const PlatT<u64>& P, uint32_t mask, ds_results*
     // enough that every launch sequence fills the GPU (smaller first/last
     // chunks measured slower too). DS_CHUNKS=k overrides (tuning knob).
     static const std::vector<u64> weights = [] {
+        // DS_CHUNK_WEIGHTS=a,b,c,... (relative chunk sizes) overrides both
+        if (const char* w = getenv("DS_CHUNK_WEIGHTS")) {
+            std::vector<u64> out;
+            for (const char* p = w; *p;) {
+                char* end = nullptr;
+                const long v = strtol(p, &end, 10);
+                if (end == p || v < 1) break;
+                out.push_back(u64(v));
+                p = *end == ',' ? end + 1 : end;
+                if (!*end) break;
+            }
+            if (!out.empty() && out.size() <= 64) return out;
+        }
         const char* e = getenv("DS_CHUNKS");
         const long v = e ? atol(e) : 0;
         return std::vector<u64>(size_t(v >= 1 && v <= 64 ? v : long(kDefaultChunks)), 1);
