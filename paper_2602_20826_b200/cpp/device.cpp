@@ -166,6 +166,80 @@ Packed pack(const std::vector<const DagTask*>& tasks, bool with_results) {
     return p;
 }
 
+Packed pack_compact(const std::vector<const DagTask*>& tasks, bool with_results) {
+    const std::size_t nd = tasks.size();
+    const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t parts = std::max<std::size_t>(1, std::min(hw, nd / 2048));
+    auto run = [&](std::size_t i) { return nd * i / parts; };
+    // sizes: nodes and adjacency words per run; any DAG above 64 nodes -> wide form
+    std::vector<std::size_t> pn(parts + 1, 0), pw(parts + 1, 0);
+    std::atomic<bool> fits{nd > 0};
+    parallel_for(parts, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            std::size_t a = 0, w = 0;
+            for (std::size_t d = run(i); d < run(i + 1); ++d) {
+                const std::size_t n = tasks[d]->size();
+                if (n > 64) fits = false;
+                a += n;
+                w += (n * (n - 1) / 2 + 31) / 32;
+            }
+            pn[i + 1] = a;
+            pw[i + 1] = w;
+        }
+    }, 1);
+    if (!fits) return pack(tasks, with_results);
+    for (std::size_t i = 0; i < parts; ++i) {
+        pn[i + 1] += pn[i];
+        pw[i + 1] += pw[i];
+    }
+    Packed p;
+    p.n_dags = nd;
+    p.n_nodes = pn[parts];
+    p.tri = true;
+    const std::size_t N = p.n_nodes, Wd = pw[parts], R = with_results ? nd : 0;
+    if (N > 0xffffffffull || Wd > 0xffffffffull) return pack(tasks, with_results);
+    // layout (8-byte aligned first): bounds | node_off, adj_off, adj, status | ln16
+    const std::size_t bytes = 8 * 10 * R + 4 * (2 * (nd + 1) + Wd + R) + 2 * N + 64;
+    unsigned char* base = acquire(p, bytes);
+    p.bounds = with_results ? reinterpret_cast<std::int64_t*>(base) : nullptr;
+    p.node_off = reinterpret_cast<std::uint32_t*>(base + 8 * 10 * R);
+    p.adj_off = p.node_off + nd + 1;
+    p.adj = p.adj_off + nd + 1;
+    p.status = with_results ? reinterpret_cast<std::int32_t*>(p.adj + Wd) : nullptr;
+    p.ln16 = reinterpret_cast<std::uint16_t*>(p.adj + Wd + R);
+    p.node_off[0] = 0;
+    p.adj_off[0] = 0;
+    std::atomic<bool> ok{true};
+    parallel_for(parts, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t r = lo; r < hi && ok; ++r) {
+            std::size_t i = pn[r], w = pw[r];
+            for (std::size_t d = run(r); d < run(r + 1); ++d) {
+                const DagTask& t = *tasks[d];
+                const std::size_t n = t.size();
+                for (const DagNode& v : t.nodes()) {
+                    const BigInt& num = v.load.num();
+                    if (v.load.den().magnitude() != 1 || num.negative() || num.magnitude() > 0xffff) {
+                        ok = false;
+                        return;
+                    }
+                    p.ln16[i++] = std::uint16_t(num.magnitude());
+                }
+                const std::size_t nw = (n * (n - 1) / 2 + 31) / 32;
+                std::fill(p.adj + w, p.adj + w + nw, 0u);
+                if (!t.tri_bits_into(p.adj + w)) {
+                    ok = false;
+                    return;
+                }
+                w += nw;
+                p.node_off[d + 1] = std::uint32_t(i);
+                p.adj_off[d + 1] = std::uint32_t(w);
+            }
+        }
+    }, 1);
+    if (!ok) return pack(tasks, with_results);  // a fractional or >= 2^16 load, or a non-topological order
+    return p;
+}
+
 ds_platform platform_of(const Platform& p) {
     p.check();
     return ds_platform{p.sm_count, DS_PF_PREMADE, to_int64(numerator(p.t_min)), to_int64(denominator(p.t_min))};

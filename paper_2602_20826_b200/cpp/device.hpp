@@ -28,14 +28,24 @@ struct Packed {
     std::int64_t* bounds = nullptr;
     bool integer = true;
     bool pinned = false;
+    // the triangular wire form instead (pack_compact): node_off, adj_off,
+    // u16 loads, adjacency bits; num / den / edge_off / edges unused
+    bool tri = false;
+    std::uint32_t *adj_off = nullptr, *adj = nullptr;
+    std::uint16_t* ln16 = nullptr;
     struct Store;
     std::shared_ptr<Store> store;  // the arena lease or the heap block
     ds_dag_batch view() const {
         return ds_dag_batch{n_dags, node_off, edge_off, num, integer ? nullptr : den, edges};
     }
+    ds_dag_batch_tri view_tri() const { return ds_dag_batch_tri{n_dags, node_off, adj_off, ln16, adj}; }
 };
 
 Packed pack(const std::vector<const DagTask*>& tasks, bool with_results = false);
+// The triangular wire form when every task fits it (<= 64 nodes, integer
+// loads < 2^16, local order topological: ~5x fewer bytes over PCIe, read by
+// the device's fast path as is), else pack().
+Packed pack_compact(const std::vector<const DagTask*>& tasks, bool with_results = false);
 // f(lo, hi) over [0, n) split into contiguous chunks on the host's cores
 // (std::thread; the first exception, in chunk order, is rethrown). Host
 // bookkeeping around the device calls: packing DagTasks, building results.

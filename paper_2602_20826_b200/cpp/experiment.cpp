@@ -86,12 +86,17 @@ std::vector<std::vector<Rational>> evaluate_corpus(const std::vector<DagTask>& c
     for (const DagTask& t : corpus) ptrs.push_back(&t);
     // inputs and result staging in one packed block (the pinned arena for a
     // large corpus), so both copy directions run at full PCIe rate
-    const detail::Packed p = detail::pack(ptrs, true);
-    const ds_dag_batch b = p.view();
+    const detail::Packed p = detail::pack_compact(ptrs, true);
     const ds_platform pl = detail::platform_of(platform);
     ds_results r{p.status, p.bounds, nullptr};
     const std::vector<int> devs = detail::devices();
-    detail::check(ds_analyze_batch_multi(&b, &pl, method_mask(methods), &r, devs.data(), int(devs.size())));
+    if (p.tri) {
+        const ds_dag_batch_tri b = p.view_tri();
+        detail::check(ds_analyze_batch_tri_multi(&b, &pl, method_mask(methods), &r, devs.data(), int(devs.size())));
+    } else {
+        const ds_dag_batch b = p.view();
+        detail::check(ds_analyze_batch_multi(&b, &pl, method_mask(methods), &r, devs.data(), int(devs.size())));
+    }
     for (std::size_t i = 0; i < corpus.size(); ++i)  // the first failing task, in order
         if (p.status[i] != DS_OK) detail::raise(p.status[i], "evaluate_corpus: task " + std::to_string(i));
     std::vector<std::vector<Rational>> out(corpus.size());
