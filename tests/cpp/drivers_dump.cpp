@@ -211,6 +211,46 @@ int main(int argc, char** argv) {
         // an OpenMP region, which terminates the process)
     }
 
+    section("evaluate_corpus (wire forms)");
+    {
+        // a corpus that fits the triangular wire form, then the same plus one
+        // task that does not: local order not topological, a fractional
+        // load, more than 64 nodes (the kept API then packs the wide form)
+        GenConfig cfg;
+        cfg.seed = 77;
+        const std::vector<DagTask> base = generate_corpus(cfg, 300);
+        const DagTask reversed = DagTask::make({{1, Rational(3)}, {2, Rational(5)}, {3, Rational(2)}, {9, Rational(4)}},
+                                               {{9, 1}, {9, 2}, {1, 3}, {2, 3}});
+        const DagTask fractional = DagTask::make({{0, Rational(7, 2)}, {1, Rational(5)}, {2, Rational(1)}},
+                                                 {{0, 1}, {1, 2}});
+        std::vector<DagNode> chain_nodes;
+        std::vector<std::pair<NodeId, NodeId>> chain_edges;
+        for (NodeId i = 0; i < 70; ++i) {
+            chain_nodes.push_back({i, Rational(1 + i % 9)});
+            if (i) chain_edges.push_back({i - 1, i});
+        }
+        const DagTask chain = DagTask::make(chain_nodes, chain_edges);
+        const std::vector<Method> methods{Method::proposed, Method::greedy, Method::greedy_unaware,
+                                          Method::graham_para};
+        const std::pair<const char*, const DagTask*> extra[] = {
+            {"tri", nullptr}, {"reversed ids", &reversed}, {"fractional", &fractional}, {"70 nodes", &chain}};
+        for (const auto& [name, t] : extra) {
+            guarded(std::string("evaluate ") + name, [&] {
+                std::vector<DagTask> corpus = base;
+                if (t) corpus.insert(corpus.begin() + 150, *t);
+                for (int M : {8, 148}) {
+                    const auto rows = evaluate_corpus(corpus, Platform{M, Rational(1)}, methods, true);
+                    std::size_t h = 1469598103934665603ull;
+                    for (const auto& row : rows)
+                        for (const Rational& x : row)
+                            for (char c : format_exact(x) + ";") h = (h ^ std::size_t((unsigned char)c)) * 1099511628211ull;
+                    std::cout << name << " M" << M << " rows " << rows.size() << " h " << h << " row150 "
+                              << format_exact(rows[150][0]) << " " << format_exact(rows[150][3]) << "\n";
+                }
+            });
+        }
+    }
+
     section("run_benchmarks / write_bench_table");
     guarded("benchmarks", [&] {
         write_bench_table(run_benchmarks(fixtures, {4, 16, 148}, {4, 20}, 10, 1), std::cout);
