@@ -192,6 +192,15 @@ int main(int argc, char** argv) {
         spec.base.integer_loads = false;
         spec.corpus_size = 3;
         guarded("sweep V", [&] { write_csv(run_experiment(spec), std::cout); });
+        // the paper's |V| sweep at P = 32 (Fig. 6): depth 20 gives DAGs of
+        // ~300-600 nodes (the device's k1_big classes)
+        ExperimentSpec big;
+        big.sweep = ExperimentSpec::SweepVar::depth;
+        big.values = {12, 20};
+        big.base.max_width = 32;
+        big.platform.sm_count = 32;
+        big.corpus_size = 4;
+        guarded("sweep V at P=32", [&] { write_csv(run_experiment(big), std::cout); });
         spec.values = {};
         guarded("no values", [&] { run_experiment(spec); });
     }
