@@ -6,14 +6,14 @@
 // copies — ~130 us for one 10-node DAG, 6x the reference's CPU. Here one
 // kernel does everything for a batch of up to kSmallDags DAGs, one CTA (one
 // warp) per DAG:
-//   * inputs are read straight from mapped pinned host memory (zero-copy:
-//     no H2D copy operation) and results are written straight back into
-//     mapped pinned host memory (no D2H copy);
+//   * inputs arrive in one H2D copy of the packed batch (or, DS_SMALL_COPY=0,
+//     are read zero-copy from mapped pinned memory) and results are written
+//     straight back into mapped pinned host memory (no D2H copy);
 //   * the 32 -> 64 -> 128-bit word tiers run back to back in the same warp
 //     (the overflow queue is a shared-memory slot, not a relaunch);
 //   * in schedule-detail mode the warp first initialises its DAG's record
 //     slices (what the throughput path's memsets do).
-// So a call is: pack on the host, one launch, one stream synchronise.
+// So a call is: pack on the host, one copy, one launch, one stream synchronise.
 #include "k1_launch.h"
 
 namespace ds {
