@@ -10,7 +10,8 @@ import random
 from fractions import Fraction
 
 
-def random_dag(rng: random.Random, n: int, density: float, frac: bool, tmin: Fraction, big_frac: float = 0.1):
+def random_dag(rng: random.Random, n: int, density: float, frac: bool, tmin: Fraction, big_frac: float = 0.1,
+               scale: int = 1):
     order = list(range(n))
     ids = rng.sample(range(10 * n + 5), n)  # sparse, shuffled ids
     edges = set()
@@ -31,6 +32,8 @@ def random_dag(rng: random.Random, n: int, density: float, frac: bool, tmin: Fra
         else:
             base = rng.randint(1, 40)
         l = Fraction(base, rng.choice([1, 1, 2, 3, 7])) if frac else Fraction(base)
+        if scale > 1:  # wide values: the 64- and 128-bit tiers, and the 128-bit ceiling
+            l = l * rng.randint(1, scale) / rng.choice([1, 1, 3, 7, 65537])
         loads.append(max(l, tmin))
     nodes = [(ids[i], loads[i]) for i in range(n)]
     return nodes, [(ids[u], ids[v]) for u, v in edges]
@@ -43,6 +46,13 @@ def corpus(seed: int, count: int, max_n: int = 96, tmin=Fraction(1)):
         n = rng.choice([1, 2, 3, rng.randint(4, 16), rng.randint(10, 40), rng.randint(30, max_n)])
         dags.append(random_dag(rng, n, rng.choice([0.0, 0.05, 0.15, 0.4]), rng.random() < 0.4, Fraction(tmin)))
     return dags
+
+
+def corpus_sized(seed: int, count: int, n_lo: int, n_hi: int, tmin=Fraction(1), scale: int = 1):
+    """`count` random DAGs with n in [n_lo, n_hi] (e.g. the big-DAG classes)."""
+    rng = random.Random(seed)
+    return [random_dag(rng, rng.randint(n_lo, n_hi), rng.choice([0.0, 0.01, 0.03]), rng.random() < 0.4,
+                       Fraction(tmin), scale=scale) for _ in range(count)]
 
 
 def broken(seed: int, count: int):

@@ -37,6 +37,27 @@ def test_fuzz_bounds(seed, tmin, max_n):
             assert len(bad) == 0, (chk.kind, M, bad[:5])
 
 
+@pytest.mark.parametrize("seed,n_lo,n_hi,scale,Ms", [
+    (31, 257, 700, 1, (2, 37, 148)),          # big classes, shuffled ids, fractional loads
+    (32, 600, 1024, 1, (8, 148)),             # W = 16 class up to the limit
+    (33, 2, 60, 1 << 20, (1, 3, 148)),        # wide values: 64/128-bit tiers, 128-bit overflow
+    (34, 257, 400, 3, (5, 148)),              # scaled fractional loads in the big classes
+])
+def test_fuzz_big_and_wide(seed, n_lo, n_hi, scale, Ms):
+    dags = fuzz_dags.corpus_sized(seed, 40, n_lo, n_hi, scale=scale)
+    b = pack(dags)
+    chk = bindings.Checker("ref" if bindings.available("ref") else "oracle")
+    c = chk.corpus(helpers_raw(b))
+    for M in Ms:
+        st, bounds, _ = _lib.analyze(b, M)
+        st_o, b_o, _ = c.evaluate(M, parallel=False)  # (an overflow inside the reference's OpenMP loop aborts it)
+        assert np.array_equal(st, st_o), (M, np.nonzero(st != st_o)[0][:5], st[st != st_o][:5], st_o[st != st_o][:5])
+        bad = np.nonzero((bounds != b_o).any(1))[0]
+        assert len(bad) == 0, (M, bad[:5])
+    if scale > 1:
+        assert (st == 0).any()  # the tiers carry most DAGs
+
+
 def test_fuzz_invalid_statuses():
     dags = fuzz_dags.broken(7, 200)
     b = pack(dags)
