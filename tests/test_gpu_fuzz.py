@@ -86,6 +86,25 @@ def test_fuzz_schemes_vs_reference(M):
         assert helpers.normalise_scheme(got) == helpers.normalise_scheme(ref.scheme(d, M)), d
 
 
+@pytest.mark.skipif(not bindings.available("ref"), reason="needs oracle/_ref")
+@pytest.mark.parametrize("M", [8, 148])
+def test_fuzz_big_schemes_vs_reference(M):
+    """write_scheme JSON of big DAGs (k1_big in detail mode: variable-width
+    unlaunched masks) with sparse, shuffled node ids on both sides."""
+    dags = fuzz_dags.corpus_sized(41, 6, 257, 600)
+    b = pack(dags)
+    schemes, st = scheme.schedule_batch(b, M)
+    ref = bindings.Checker("ref").corpus_with_ids(helpers_raw(b), np.concatenate([np.asarray(i) for i in b.node_ids]))
+    st_r, _, _ = ref.evaluate(M, parallel=False)
+    assert np.array_equal(st, st_r)
+    assert (st == 0).sum() >= 3
+    for d in range(len(dags)):
+        if st[d] != 0:
+            continue
+        got = scheme.to_reference_json(schemes[d])
+        assert helpers.normalise_scheme(got) == helpers.normalise_scheme(ref.scheme(d, M)), d
+
+
 def helpers_raw(b):
     """The packed batch as the checkers take it (same arrays, id-free)."""
     from paper_2602_20826_b200.batch import from_arrays
