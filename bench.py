@@ -663,7 +663,6 @@ def main():
             "makespan": makespan,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
-            # per chunk: the K1 sequence, plus the 16-bit form's widening kernel
             # per chunk: the session's kernels + the wire form's widening
             # (16-bit: k_widen16; triangular: k_widen_tri_list over the
             # fallback and retry queues)
