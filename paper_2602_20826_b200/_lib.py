@@ -15,7 +15,8 @@ from . import _abi
 from .batch import DagBatch, combine_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libdagsched_b200.so")
+# DAGSCHED_LIB: another build of the library (A/B measurements only)
+LIB_PATH = os.environ.get("DAGSCHED_LIB") or os.path.join(HERE, "_lib", "libdagsched_b200.so")
 
 _lock = threading.Lock()
 _lib = None
