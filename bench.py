@@ -262,7 +262,7 @@ def cpp_api_bench(n_ours=1_000_000, n_ref=100_000, reps=300):
 
 PLATFORM_BLOCKING_US = 3000.0  # longest whole-context preemption observed on this platform (2.87 ms) + margin
 
-MAKESPAN_MAIN = ("dynamic_prio", "multistream_host", "multistream")
+MAKESPAN_MAIN = ("dynamic_prio", "graph_prio", "multistream_host", "multistream")
 MAKESPAN_OTHER = ("proposed", "proposed_deps", "dynamic_deps", "serial")
 
 
@@ -275,6 +275,9 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
     Variants (all on the same K2 TMA node kernel, same SMs):
       dynamic_prio     the schedule on the dynamic engine, precedence edges +
                        group-priority claiming (DS_PLAN_PRIORITY) — the product
+      graph_prio       the same plan as a CUDA graph, each kernel node at its
+                       group's launch priority (hardware CTA dispatch order) —
+                       the product on the graph engine
       proposed         the schedule as a CUDA graph with group barriers
                        (simulate_scheme semantics, the Theorem-1 setting)
       proposed_deps    the schedule's augmented graph (Ē) as a CUDA graph
@@ -313,8 +316,9 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
     schemes, st = scheme.schedule_batch(pack([d for _, _, d in dags]), M, device=device)
 
     def plan_of(kind, sch, loads, edges):
-        if kind == "dynamic_prio":
-            return X.plan_from_scheme(sch, loads, unit, mode=X.PLAN_PRIORITY), X.ENGINE_DYNAMIC
+        if kind in ("dynamic_prio", "graph_prio"):
+            return (X.plan_from_scheme(sch, loads, unit, mode=X.PLAN_PRIORITY),
+                    X.ENGINE_DYNAMIC if kind == "dynamic_prio" else X.ENGINE_GRAPH)
         if kind in ("proposed", "proposed_deps", "dynamic_deps"):
             mode = X.PLAN_BARRIERS if kind == "proposed" else X.PLAN_DEPS
             return (X.plan_from_scheme(sch, loads, unit, mode=mode),
@@ -322,7 +326,7 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
         engine = X.ENGINE_STREAMS if kind == "multistream_host" else X.ENGINE_GRAPH
         return X.plan_baseline(kind.replace("_host", ""), loads, edges, M, unit), engine
 
-    proposed_kinds = ("dynamic_prio", "proposed", "proposed_deps", "dynamic_deps")
+    proposed_kinds = ("dynamic_prio", "graph_prio", "proposed", "proposed_deps", "dynamic_deps")
     per = {}  # (config, kind) -> list of per-DAG arrays
     ratios, over, over_b, stall_like, launches = {}, {}, {}, {}, 0
     p50 = {}
@@ -342,7 +346,7 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
             r = ex.run(reps, warmup=3, stamps=False)
             wall["setup"] += t1 - t0
             wall["replays"] += time.perf_counter() - t1
-            if kind == "dynamic_prio" and (cfg != "C2" or name in ("c2_seed2", "c2_seed3")):
+            if kind in ("dynamic_prio", "graph_prio") and (cfg != "C2" or name in ("c2_seed2", "c2_seed3")):
                 rs = ex.run(10, warmup=1, stamps=True)  # trace contracts on stamped replays
                 for k in range(10):
                     contracts["precedence_violations"] += len(X.check_precedence(plan, rs, k))
@@ -371,6 +375,10 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
                                                                for n in names))
         c["dynamic_prio_beats_multistream_p50"] = int(sum(p50["dynamic_prio"][n] < p50["multistream"][n]
                                                           for n in names))
+        c["graph_prio_beats_multistream_host_p50"] = int(sum(p50["graph_prio"][n] < p50["multistream_host"][n]
+                                                             for n in names))
+        c["graph_prio_beats_multistream_p50"] = int(sum(p50["graph_prio"][n] < p50["multistream"][n]
+                                                        for n in names))
     mob = {}
     for k, v in ratios.items():
         v = np.concatenate(v)
@@ -393,7 +401,70 @@ def makespan_summary(device, replays=1000, replays_other=200, n_c2=100, n_c2_oth
                         "a replay that meets one can exceed the bound by at most B (stalls are >= 0.3 s apart, "
                         "longer than any makespan here)",
                 "evidence": "profiles/r02_stall_root.txt, profiles/r01_stall_probe.txt (tools/heartbeat.cu)"},
-            "trace_contracts_dynamic_prio": contracts, "executor_kernel_launches": launches}
+            "trace_contracts_prio": contracts, "executor_kernel_launches": launches}
+
+
+CONTENDED_VARIANTS = ("graph_prio", "dynamic_prio", "multistream_host", "multistream")
+
+
+def makespan_contended(device, sms=(32, 8), replays=200, n_c2=12, unit=1 << 17):
+    """The paper's contended regime: the DAG runs inside a green context of M
+    SMs (M = 32, 8), scheduled and bounded for that M (calibration inside the
+    same partition). Per config the mean over its DAGs of the per-DAG p50 /
+    p99 in us, the max over all replays, and the proposed variants' replays
+    over the bound counted raw."""
+    from paper_2602_20826_b200 import _lib, executor as X, scheme, workloads
+    from paper_2602_20826_b200.batch import pack
+
+    wl = X.WL_MIX32_TMA
+    t_start = time.perf_counter()
+    out = {"replays": replays, "c2_dags": n_c2, "variants": list(CONTENDED_VARIANTS)}
+    b = _lib.Corpus(400, seed=1).batch()
+    sizes = np.diff(b.node_off.astype(np.int64))
+    c2 = []
+    for d in [d for d in range(b.n_dags) if 20 <= sizes[d] <= 50][:n_c2]:
+        n0, n1, e0, e1 = (int(b.node_off[d]), int(b.node_off[d + 1]), int(b.edge_off[d]), int(b.edge_off[d + 1]))
+        c2.append(("C2", ([int(x) for x in b.load_num[n0:n1]],
+                          [(int(w) >> 16, int(w) & 0xFFFF) for w in b.edges[e0:e1]])))
+
+    def norm(nodes, edges):
+        if isinstance(nodes[0], tuple):
+            idx = {i: k for k, (i, _) in enumerate(sorted(nodes))}
+            return [l for _, l in sorted(nodes)], [(idx[u], idx[v]) for u, v in edges]
+        return list(nodes), list(edges)
+
+    for M in sms:
+        cal = X.calibrate(unit, sm_limit=M, device=device, workload=wl)
+        dags = [("C1", norm(*workloads.c1_fork_join())), ("C3", norm(*workloads.inception_dag()))]
+        dags += [("C4", norm(*workloads.oversized_dag(s, M))) for s in range(3)] + c2
+        schemes, _ = scheme.schedule_batch(pack([d for _, d in dags]), M, device=device)
+        per, over, ratio = {}, {}, {}
+        for (cfg, (loads, edges)), sch in zip(dags, schemes):
+            bus = X.bound_us(sch, cal)
+            for kind in CONTENDED_VARIANTS:
+                if kind.endswith("_prio"):
+                    plan = X.plan_from_scheme(sch, loads, unit, mode=X.PLAN_PRIORITY)
+                    engine = X.ENGINE_GRAPH if kind == "graph_prio" else X.ENGINE_DYNAMIC
+                else:
+                    plan = X.plan_baseline(kind.replace("_host", ""), loads, edges, M, unit)
+                    engine = X.ENGINE_STREAMS if kind == "multistream_host" else X.ENGINE_GRAPH
+                ex = X.Executor(plan, device=device, workload=wl, engine=engine, sm_limit=M)
+                mk = ex.run(replays, warmup=3, stamps=False).makespan_us
+                ex.close()
+                per.setdefault((cfg, kind), []).append(mk)
+                if kind.endswith("_prio"):
+                    over[kind] = over.get(kind, 0) + int((mk > bus).sum())
+                    ratio[kind] = max(ratio.get(kind, 0.0), float((mk / bus).max()))
+        cf = {}
+        for (cfg, kind), arrs in per.items():
+            cf.setdefault(cfg, {})[kind] = {
+                "dags": len(arrs), "p50_us": float(np.mean([np.median(a) for a in arrs])),
+                "p99_us": float(np.mean([np.percentile(a, 99) for a in arrs])),
+                "max_us": float(np.concatenate(arrs).max())}
+        out[f"M{M}"] = {"tau_us": cal["tau_us"], "delta_us": cal["delta_us"], "eps_us": cal["eps_us"],
+                        "configs": cf, "replays_over_bound_raw": over, "max_measured_over_bound": ratio}
+    out["wall_s"] = time.perf_counter() - t_start
+    return out
 
 
 def run_reference(args):
@@ -620,6 +691,10 @@ def main():
             makespan = makespan_summary(dev, args.makespan_replays, n_c2=args.makespan_c2)
         except Exception as e:  # reported, never required for the headline line
             makespan = {"error": str(e)}
+        try:
+            makespan["contended"] = makespan_contended(dev)
+        except Exception as e:
+            makespan["contended"] = {"error": str(e)}
 
     cpp_api = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

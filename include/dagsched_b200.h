@@ -245,14 +245,21 @@ typedef struct ds_exec_plan {
 /* ds_exec_plan.barrier_groups. DEPS: only the plan's edges order entities
  * (the augmented graph: original edges + extra dependencies Ē). BARRIERS:
  * group g+1 starts after all of group g (simulate_scheme semantics,
- * simulator.cpp:44-94). PRIORITY (DS_ENGINE_DYNAMIC only): the plan's edges
+ * simulator.cpp:44-94). PRIORITY (DS_ENGINE_DYNAMIC or DS_ENGINE_GRAPH): the plan's edges
  * are the precedence edges alone (original edges resolved to segment chains,
  * no Ē) and the engine enforces the group order itself — no rank of a
  * group-(g+1) entity is claimed while a group-g entity still has unclaimed
  * ranks — so a group's entities always find their quota of SMs free, every
  * group ends within its response after the previous group's last rank (the
  * Theorem-1 induction), and SMs that finish early take the next group's
- * ranks instead of idling behind Ē. */
+ * ranks instead of idling behind Ē. On DS_ENGINE_GRAPH the same order is
+ * requested from the hardware: each kernel node carries the launch priority
+ * of its group (group 0 highest; groups beyond the device's priority range
+ * share its lowest level) and the graph is instantiated with
+ * cudaGraphInstantiateFlagUseNodePriority, so a freed SM takes a pending CTA
+ * of the earliest ready group — best effort (the dispatcher's order, not a
+ * device-side claim), checked against the bound per replay like every
+ * variant. */
 #define DS_PLAN_DEPS 0
 #define DS_PLAN_BARRIERS 1
 #define DS_PLAN_PRIORITY 2
@@ -273,7 +280,7 @@ typedef struct ds_exec_cfg {
 } ds_exec_cfg;
 
 /* Executor engines. GRAPH: one CUDA Graph kernel node per entity (plans
- * DS_PLAN_DEPS / DS_PLAN_BARRIERS). (1 and 4 are retired engines: a static
+ * DS_PLAN_DEPS / DS_PLAN_BARRIERS / DS_PLAN_PRIORITY). (1 and 4 are retired engines: a static
  * list-scheduled persistent kernel and a ring-streaming variant of DYNAMIC,
  * both measured slower than DYNAMIC.) */
 #define DS_ENGINE_GRAPH 0
@@ -287,8 +294,8 @@ typedef struct ds_exec_cfg {
 /* DYNAMIC: one resident CTA per SM, work-conserving: an entity enters a
  * device-side ready queue (plan order = schedule priority) when its last
  * predecessor completes, and idle CTAs claim its m ranks, so it never holds
- * more than its quota of SMs. Any topologically ordered plan, and the only
- * engine for DS_PLAN_PRIORITY; workloads DS_WL_MIX32 and DS_WL_MIX32_TMA. */
+ * more than its quota of SMs. Any topologically ordered plan (for
+ * DS_PLAN_PRIORITY the exact device-side claim order); workloads DS_WL_MIX32 and DS_WL_MIX32_TMA. */
 #define DS_ENGINE_DYNAMIC 3
 /* STREAMS: no graph — every replay the host launches each entity's kernel on
  * its own stream after cudaStreamWaitEvent on its predecessors' events (and,

@@ -320,6 +320,14 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
     int max_group = -1;
     for (int i = 0; i < n; ++i) max_group = std::max(max_group, int(plan->entities[i].group));
     const bool barriers = plan->barrier_groups == DS_PLAN_BARRIERS && max_group > 0;
+    // DS_PLAN_PRIORITY on a graph: per-node launch priorities from the group
+    // index (group 0 the highest; groups past the device's range share the
+    // lowest level), honoured by instantiating with UseNodePriority — the
+    // hardware CTA dispatcher then plays the dynamic engine's group-priority
+    // claiming (an earlier group's pending CTAs take a freed SM first).
+    const bool prio = plan->barrier_groups == DS_PLAN_PRIORITY;
+    int prio_least = 0, prio_greatest = 0;
+    if (prio) DS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
     std::vector<std::vector<int>> members(max_group + 1);
     for (int i = 0; i < n; ++i) {
         if (plan->entities[i].group >= 0) members[plan->entities[i].group].push_back(i);
@@ -387,6 +395,11 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
         }
         kp.kernelParams = params;
         DS_CUDA(cudaGraphAddKernelNode(&node[i], E->graph, deps.data(), deps.size(), &kp));
+        if (prio) {  // group g's CTAs dispatch before group g+1's whenever both are ready
+            cudaKernelNodeAttrValue v{};
+            v.priority = std::min(prio_least, prio_greatest + std::max(0, int(e.group)));
+            DS_CUDA(cudaGraphKernelNodeSetAttribute(node[i], cudaKernelNodeAttributePriority, &v));
+        }
     }
     // tail: advance the replay counter after every sink entity
     std::vector<char> has_succ(n, 0);
@@ -407,7 +420,7 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
     tp.blockDim = dim3(1);
     tp.kernelParams = tparams;
     DS_CUDA(cudaGraphAddKernelNode(&tail, E->graph, sinks.data(), sinks.size(), &tp));
-    DS_CUDA(cudaGraphInstantiate(&E->exec, E->graph, 0));
+    DS_CUDA(cudaGraphInstantiate(&E->exec, E->graph, prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
     return DS_OK;
 }
 
@@ -451,8 +464,8 @@ int ds_exec_create(const ds_exec_plan* plan, const ds_exec_cfg* cfg, int device,
         return fail(DS_EINVAL, "bad workload");
     if (plan->barrier_groups < DS_PLAN_DEPS || plan->barrier_groups > DS_PLAN_PRIORITY)
         return fail(DS_EINVAL, "bad plan ordering mode");
-    if (plan->barrier_groups == DS_PLAN_PRIORITY && cfg->engine != DS_ENGINE_DYNAMIC)
-        return fail(DS_EINVAL, "DS_PLAN_PRIORITY runs on DS_ENGINE_DYNAMIC only (a graph cannot express priorities)");
+    if (plan->barrier_groups == DS_PLAN_PRIORITY && cfg->engine != DS_ENGINE_DYNAMIC && cfg->engine != DS_ENGINE_GRAPH)
+        return fail(DS_EINVAL, "DS_PLAN_PRIORITY runs on DS_ENGINE_DYNAMIC or DS_ENGINE_GRAPH (node priorities)");
     const int threads = cfg->block_threads > 0 ? cfg->block_threads : 1024;
     if (threads > 1024 || threads % 32) return fail(DS_EINVAL, "block_threads must be a multiple of 32 <= 1024");
     auto* H = new ExecHandle();

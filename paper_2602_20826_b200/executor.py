@@ -214,7 +214,8 @@ class Executor:
                  sm_limit: int = 0, engine: int = ENGINE_GRAPH, chunk_elems: int = 0):
         """sm_limit > 0 runs inside a green context of that many SMs; engine
         ENGINE_DYNAMIC runs the plan as one resident CTA per SM claiming
-        entity ranks (the only engine for PLAN_PRIORITY plans)."""
+        entity ranks (exact group-priority claiming for PLAN_PRIORITY plans;
+        ENGINE_GRAPH runs them with per-node launch priorities instead)."""
         L = _sig()
         self.plan = plan
         self.workload = workload

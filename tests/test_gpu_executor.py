@@ -214,11 +214,35 @@ def test_host_streams_engine(workload):
         ex.close()
 
 
-def test_priority_plans_need_the_dynamic_engine():
-    """A CUDA graph (or host streams) cannot express claim priorities: a
-    DS_PLAN_PRIORITY plan is refused there instead of running without Ē."""
+def test_priority_plans_need_a_priority_engine():
+    """Host streams cannot express the group order: a DS_PLAN_PRIORITY plan is
+    refused there instead of running without Ē (the dynamic engine claims in
+    group order, the graph engine carries per-node launch priorities)."""
     s, loads, edges = _scheme_and_loads(workloads.make_example_task(), 8)
     plan = X.plan_from_scheme(s, loads, 4096, mode=X.PLAN_PRIORITY)
-    for engine in (X.ENGINE_GRAPH, X.ENGINE_STREAMS):
+    for engine in (X.ENGINE_STREAMS, X.ENGINE_GRAPH_FREE):
         with pytest.raises(_lib.DagschedError):
             X.Executor(plan, engine=engine)
+
+
+@pytest.mark.parametrize("workload", [X.WL_MIX32, X.WL_MIX32_TMA])
+def test_graph_priority_plans(workload):
+    """DS_PLAN_PRIORITY on DS_ENGINE_GRAPH: the precedence edges alone (no Ē)
+    as graph edges, each kernel node at its group's launch priority
+    (cudaGraphInstantiateFlagUseNodePriority). Every CTA runs once per
+    replay, outputs are bit-exact, precedence and SM exclusivity hold."""
+    cases = [(workloads.make_example_task(), 8), (workloads.oversized_dag(2, 148), 148),
+             (workloads.inception_dag(), 148), (workloads.c1_fork_join(), 148)]
+    for dag, M in cases:
+        s, loads, edges = _scheme_and_loads(dag, M)
+        plan = X.plan_from_scheme(s, loads, UNIT + 5, mode=X.PLAN_PRIORITY)
+        ex = X.Executor(plan, workload=workload, engine=X.ENGINE_GRAPH, sm_limit=0 if M == 148 else 8)
+        res = ex.run(6, warmup=2)
+        for r in range(6):
+            st = res.stamps[r]
+            assert (st[:, 0] > 0).all() and (st[:, 1] >= st[:, 0]).all()
+            assert X.check_precedence(plan, res, r) == []
+            assert X.check_sm_exclusive(plan, res, r) == 0
+        for v in range(len(loads)):
+            assert np.array_equal(ex.output(v), X.mix32(X.node_input(1, v, plan.node_elems[v])))
+        ex.close()
