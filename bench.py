@@ -524,7 +524,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-dags", type=int, default=N_PER_GPU)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-sample", type=int, default=100000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-makespan", action="store_true")
@@ -645,7 +645,8 @@ def main():
         call = lambda: L.ds_analyze_batch(C.byref(cb), C.byref(pl), _abi.DS_M_ALL, C.byref(r), dev, None, 0)  # noqa: E731
         h2d = batch.nbytes(with_den=not integer)
         api = "ds_analyze_batch (host pinned)"
-    _lib.check(call())
+    for _ in range(3):  # warm-up: pinned staging, stream pool, first-touch of the result arrays
+        _lib.check(call())
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
