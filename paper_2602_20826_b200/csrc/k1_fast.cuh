@@ -12,8 +12,10 @@
 // broadcast by a shuffle — no divergent per-lane loops:
 //   closure     ids in topological order (every edge u < v): one pass in
 //               index order folds anc[k] | {k} into k's successors (Warshall
-//               in topological order), with the hop level and the weighted
-//               prefix (dag.cpp:69-124, analysis.cpp:11-24);
+//               in topological order), with the weighted prefix; the hop
+//               level (longest path in nodes) by peeling sources layer by
+//               layer, one ballot per layer (dag.cpp:69-124,
+//               analysis.cpp:11-24);
 //   W^anc       sum of the ancestors' loads (dag.cpp:126-135);
 //   ranks       (W^anc desc, id asc) for heads/candidates, joins (W^anc asc,
 //               id asc) (division.cpp:88-93, dag.cpp:218-230);
@@ -113,27 +115,41 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
     const bool flat = !__any_sync(FULL, (ina && la > u32(M)) || (inb && lb > u32(M)));
     const u32 wa = la > u32(M) ? la : u32(M), wb = lb > u32(M) ? lb : u32(M);  // exec in units of 1/M
     u64 aa = 0, ab = 0;     // ancestors
-    int lva = 0, lvb = 0;   // longest incoming path (nodes)
     u32 cpa = 0, cpb = 0;   // longest incoming weighted path (units of 1/M)
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const bool kb = k >= 32;
-        const int src = k & 31;
-        const u64 ak = shfl64(kb ? ab : aa, src) | (1ull << k);
-        const int lk = __shfl_sync(FULL, kb ? lvb : lva, src) + 1;
+    // index order is topological, so node k < 32 has only ancestors < 32 (a
+    // 32-bit word, one shuffle) and only slot-b nodes (v >= 32) can have a
+    // predecessor k >= 32: two loops without per-k slot selects
+    const int n1 = n < 32 ? n : 32;
+#pragma unroll 4
+    for (int k = 0; k < n1; ++k) {
+        const u32 ak = __shfl_sync(FULL, u32(aa), k) | (1u << k);
         u32 ck = 0;
-        if (!flat) ck = __shfl_sync(FULL, kb ? cpb + wb : cpa + wa, src);
+        if (!flat) ck = __shfl_sync(FULL, cpa + wa, k);
         if ((pa >> k) & 1) {
             aa |= ak;
-            lva = max(lva, lk);
             cpa = max(cpa, ck);
         }
         if ((pb >> k) & 1) {
             ab |= ak;
-            lvb = max(lvb, lk);
             cpb = max(cpb, ck);
         }
     }
+#pragma unroll 4
+    for (int k = 32; k < n; ++k) {
+        const u64 ak = shfl64(ab, k - 32) | (1ull << k);
+        u32 ck = 0;
+        if (!flat) ck = __shfl_sync(FULL, cpb + wb, k - 32);
+        if ((pb >> k) & 1) {
+            ab |= ak;
+            cpb = max(cpb, ck);
+        }
+    }
+    // longest path in nodes: peel sources layer by layer (node v leaves in
+    // round lv(v) + 1)
+    u32 rounds64 = 0;
+    for (u64 R = V; R; ++rounds64)
+        R &= ~(u64(__ballot_sync(FULL, ina && ((R >> va) & 1) && !(pa & R))) |
+               (u64(__ballot_sync(FULL, inb && ((R >> vb) & 1) && !(pb & R))) << 32));
     // ---- descendants: transpose of the ancestor matrix (dag.cpp:119-124)
     u64 da, db = 0;
     {
@@ -155,7 +171,7 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
         const u32 GU = __reduce_add_sync(FULL, (ina ? (la + u32(M) - 1) / u32(M) : 0u) +
                                                    (inb ? (lb + u32(M) - 1) / u32(M) : 0u));
         const u32 G = flat ? u32(n) * u32(M) : __reduce_add_sync(FULL, (ina ? wa : 0u) + (inb ? wb : 0u));
-        const u32 rounds = u32(__reduce_max_sync(FULL, u32(max(ina ? lva + 1 : 0, inb ? lvb + 1 : 0))));
+        const u32 rounds = rounds64;  // longest path in nodes
         const u32 cp = flat ? rounds * u32(M)
                             : __reduce_max_sync(FULL, max(ina ? cpa + wa : 0u, inb ? cpb + wb : 0u));
         // lanes 0..3 reduce one bound each: greedy, greedy_unaware, graham_para, lower
@@ -385,29 +401,27 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     const bool flat = !__any_sync(FULL, in && l > u32(M));
     const u32 w = l > u32(M) ? l : u32(M);  // exec(l, min(l, M)) in units of 1/M
     u32 an = 0, cpi = 0, pm = p;
-    int lv = 0;
+    u32 rounds = 0;  // longest path in nodes
     if (flat) {
-#pragma unroll 2
+        // closure alone (one shuffle per node); the longest path in nodes by
+        // peeling sources layer by layer: node v leaves in round lv(v) + 1
+#pragma unroll 8
         for (int k = 0; k < n; ++k, pm >>= 1) {
             const u32 ak = __shfl_sync(FULL, an, k) | (1u << k);
-            const int lk = __shfl_sync(FULL, lv, k) + 1;
-            if (pm & 1) {
-                an |= ak;
-                lv = max(lv, lk);
-            }
+            if (pm & 1) an |= ak;
         }
+        for (u32 R = V; R; ++rounds) R &= ~__ballot_sync(FULL, ((R >> lane) & 1) && !(p & R));
     } else {
 #pragma unroll 1
         for (int k = 0; k < n; ++k, pm >>= 1) {
             const u32 ak = __shfl_sync(FULL, an, k) | (1u << k);
-            const int lk = __shfl_sync(FULL, lv, k) + 1;
             const u32 ck = __shfl_sync(FULL, cpi + w, k);
             if (pm & 1) {
                 an |= ak;
-                lv = max(lv, lk);
                 cpi = max(cpi, ck);
             }
         }
+        for (u32 R = V; R; ++rounds) R &= ~__ballot_sync(FULL, ((R >> lane) & 1) && !(p & R));
     }
     const u32 de = warp_transpose32(an, lane);  // descendants (dag.cpp:119-124)
     // ---- bounds 1..4 (analysis.cpp:40-81)
@@ -417,7 +431,6 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
         const u32 U = __reduce_add_sync(FULL, in ? l : 0u);
         const u32 GU = flat ? u32(n) : __reduce_add_sync(FULL, in ? (l + u32(M) - 1) / u32(M) : 0u);
         const u32 G = flat ? u32(n) * u32(M) : __reduce_add_sync(FULL, in ? w : 0u);
-        const u32 rounds = __reduce_max_sync(FULL, in ? u32(lv + 1) : 0u);
         const u32 cp = flat ? rounds * u32(M) : __reduce_max_sync(FULL, in ? cpi + w : 0u);
         if (lane < 4) {  // greedy, greedy_unaware, graham_para, lower: one lane each
             const int k = lane + 1;

@@ -13,7 +13,7 @@ import sass_hotspots as sh  # noqa: E402
 
 rep, kname, sass = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base", os.environ.get("NCU_NAME_BASE", "function"), "-k",
                       f"regex:{kname}"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(txt)))
 for i, row in enumerate(r):
