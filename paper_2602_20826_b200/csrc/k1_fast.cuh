@@ -120,28 +120,52 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
     // 32-bit word, one shuffle) and only slot-b nodes (v >= 32) can have a
     // predecessor k >= 32: two loops without per-k slot selects
     const int n1 = n < 32 ? n : 32;
-#pragma unroll 4
-    for (int k = 0; k < n1; ++k) {
-        const u32 ak = __shfl_sync(FULL, u32(aa), k) | (1u << k);
-        u32 ck = 0;
-        if (!flat) ck = __shfl_sync(FULL, cpa + wa, k);
-        if ((pa >> k) & 1) {
-            aa |= ak;
-            cpa = max(cpa, ck);
+    if (flat) {  // ancestors-or-self words, constant-k predecessor tests (cf. fast_dag32)
+        u32 xa = ina ? (1u << va) : 0u;
+        u64 xb = inb ? (1ull << vb) : 0ull;
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+            if (k0 >= n1) break;
+#pragma unroll
+            for (int k = k0; k < k0 + 4; ++k) {
+                const u32 ak = __shfl_sync(FULL, xa, k);
+                if ((pa >> k) & 1) xa |= ak;
+                if ((pb >> k) & 1) xb |= ak;
+            }
         }
-        if ((pb >> k) & 1) {
-            ab |= ak;
-            cpb = max(cpb, ck);
+#pragma unroll
+        for (int k0 = 32; k0 < 64; k0 += 4) {
+            if (k0 >= n) break;
+#pragma unroll
+            for (int k = k0; k < k0 + 4; ++k) {
+                const u64 ak = shfl64(xb, k - 32);
+                if ((pb >> k) & 1) xb |= ak;
+            }
         }
-    }
+        aa = xa & ~(1u << va);
+        ab = inb ? xb & ~(1ull << vb) : 0ull;
+    } else {  // some load > M: the weighted prefix rides along
 #pragma unroll 4
-    for (int k = 32; k < n; ++k) {
-        const u64 ak = shfl64(ab, k - 32) | (1ull << k);
-        u32 ck = 0;
-        if (!flat) ck = __shfl_sync(FULL, cpb + wb, k - 32);
-        if ((pb >> k) & 1) {
-            ab |= ak;
-            cpb = max(cpb, ck);
+        for (int k = 0; k < n1; ++k) {
+            const u32 ak = __shfl_sync(FULL, u32(aa), k) | (1u << k);
+            const u32 ck = __shfl_sync(FULL, cpa + wa, k);
+            if ((pa >> k) & 1) {
+                aa |= ak;
+                cpa = max(cpa, ck);
+            }
+            if ((pb >> k) & 1) {
+                ab |= ak;
+                cpb = max(cpb, ck);
+            }
+        }
+#pragma unroll 4
+        for (int k = 32; k < n; ++k) {
+            const u64 ak = shfl64(ab, k - 32) | (1ull << k);
+            const u32 ck = __shfl_sync(FULL, cpb + wb, k - 32);
+            if ((pb >> k) & 1) {
+                ab |= ak;
+                cpb = max(cpb, ck);
+            }
         }
     }
     // longest path in nodes: peel sources layer by layer (node v leaves in
@@ -337,15 +361,17 @@ __device__ __forceinline__ int fast_dag(FastWarp& S, const K1Args& a, const int 
         a.h.node[n0 + vb] = nd;
         a.h.ro[n0 + vb] = uint16_t(rb | (S.ord[vb] << 8));
     }
-    u64 mine = 0;  // division group lane (and lane + 32)'s member mask
-#pragma unroll 1
-    for (u32 g = 0; g < ndiv; ++g) {
-        const u64 m = __ballot_sync(FULL, ga == int(g)) | (u64(__ballot_sync(FULL, gb == int(g))) << 32);
-        if (lane == int(g & 31)) mine = m;
-        if ((g & 31) == 31 || g + 1 == ndiv) {
-            if (int(g & ~31u) + lane < int(ndiv)) a.h.divg[n0 + (g & ~31u) + lane] = mine;
-        }
-    }
+    // division group member masks by shared 64-bit atomics (S.pred's block
+    // masks are dead by now), then one coalesced store per group
+    unsigned long long* gmask = reinterpret_cast<unsigned long long*>(S.pred);
+    gmask[lane] = 0;
+    gmask[lane + 32] = 0;
+    __syncwarp();
+    if (ina) atomicOr(gmask + ga, 1ull << va);
+    if (inb) atomicOr(gmask + gb, 1ull << vb);
+    __syncwarp();
+    if (lane < int(ndiv)) a.h.divg[n0 + lane] = gmask[lane];
+    if (lane + 32 < int(ndiv)) a.h.divg[n0 + lane + 32] = gmask[lane + 32];
     // walk-order key (walk_key): group count and member counts
     const u64 key = walk_key(lane, ndiv, lane < int(ndiv) ? ca : 0u, lane + 32 < int(ndiv) ? cb : 0u, false,
                              a.key_mode);
@@ -403,13 +429,22 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     u32 an = 0, cpi = 0, pm = p;
     u32 rounds = 0;  // longest path in nodes
     if (flat) {
-        // closure alone (one shuffle per node); the longest path in nodes by
-        // peeling sources layer by layer: node v leaves in round lv(v) + 1
-#pragma unroll 8
-        for (int k = 0; k < n; ++k, pm >>= 1) {
-            const u32 ak = __shfl_sync(FULL, an, k) | (1u << k);
-            if (pm & 1) an |= ak;
+        // closure alone, one shuffle per node, over ancestors-or-self words x
+        // (node k's word is shuffled as is; with k a compile-time constant
+        // the predecessor test is one LOP3; one warp-uniform bound check per
+        // 4 nodes — nodes >= n have x = 0 and no p bit). The longest path in
+        // nodes by peeling sources layer by layer: v leaves in round lv(v) + 1
+        u32 x = in ? (1u << lane) : 0u;
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+            if (k0 >= n) break;
+#pragma unroll
+            for (int k = k0; k < k0 + 4; ++k) {
+                const u32 ak = __shfl_sync(FULL, x, k);
+                if ((p >> k) & 1) x |= ak;
+            }
         }
+        an = x & ~(1u << lane);
         for (u32 R = V; R; ++rounds) R &= ~__ballot_sync(FULL, ((R >> lane) & 1) && !(p & R));
     } else {
 #pragma unroll 1
