@@ -491,8 +491,14 @@ __device__ __forceinline__ int fast_dag32(FastWarp& S, const K1Args& a, const in
     // ---- W^anc = l + sum over ancestors, by load bit-planes (dag.cpp:126-135)
     const int lbits = 32 - __clz(int(__reduce_or_sync(FULL, in ? l : 0u)));
     u32 W = l;
-#pragma unroll 1
-    for (int b = 0; b < lbits; ++b) W += u32(__popc(an & __ballot_sync(FULL, in && ((l >> b) & 1)))) << b;
+    // compile-time bit index (loads < 2^16), one bound check per 2 planes;
+    // planes at or above lbits are empty and add nothing
+#pragma unroll
+    for (int b0 = 0; b0 < 16; b0 += 2) {
+        if (b0 >= lbits) break;
+#pragma unroll
+        for (int b = b0; b < b0 + 2; ++b) W += u32(__popc(an & __ballot_sync(FULL, in && ((l >> b) & 1)))) << b;
+    }
     // ---- rank (W desc, id asc) and join position (W asc, id asc), bit-serial
     const u32 J = __ballot_sync(FULL, in && __popc(p) >= 2);
     const int nj = __popc(J);
