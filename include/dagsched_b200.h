@@ -254,8 +254,8 @@ typedef struct ds_exec_plan {
  * Theorem-1 induction), and SMs that finish early take the next group's
  * ranks instead of idling behind Ē. On DS_ENGINE_GRAPH the same order is
  * requested from the hardware: each kernel node carries the launch priority
- * of its group (group 0 highest; groups beyond the device's priority range
- * share its lowest level) and the graph is instantiated with
+ * of its group (group 0 highest, the last group lowest, the groups spread
+ * evenly over the device's priority levels) and the graph is instantiated with
  * cudaGraphInstantiateFlagUseNodePriority, so a freed SM takes a pending CTA
  * of the earliest ready group — best effort (the dispatcher's order, not a
  * device-side claim), checked against the bound per replay like every

@@ -422,7 +422,8 @@ DeviceCtx& device_ctx(int dev) {
 }
 
 constexpr u64 kChunk = 1ull << 14;  // smallest chunk worth a launch sequence
-constexpr u64 kDefaultChunks = 5;  // 1M C5 DAGs e2e (round 2 kernels): 3 chunks 171 M/s, 4: 179, 5: 181, 6: 180, 8: 160
+constexpr u64 kDefaultChunks = 5;  // 1M C5 DAGs e2e (round 2 kernels): 3 chunks 171 M/s, 4: 179, 5: 181, 6: 180, 8: 160;
+                                    // after the k1_fast rework (tools/gpu_e2e_chunks.sh): 3: 210, 4: 219, 5: 229-232, 6: 230, 8: 221
 
 // the second offset array of each wire form: edges, or adjacency words
 inline const uint32_t* second_off(const ds_dag_batch* b) { return b->edge_off; }

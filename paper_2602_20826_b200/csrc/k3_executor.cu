@@ -321,13 +321,17 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
     for (int i = 0; i < n; ++i) max_group = std::max(max_group, int(plan->entities[i].group));
     const bool barriers = plan->barrier_groups == DS_PLAN_BARRIERS && max_group > 0;
     // DS_PLAN_PRIORITY on a graph: per-node launch priorities from the group
-    // index (group 0 the highest; groups past the device's range share the
-    // lowest level), honoured by instantiating with UseNodePriority — the
+    // index (group 0 the highest, the groups spread evenly over the device's
+    // levels), honoured by instantiating with UseNodePriority — the
     // hardware CTA dispatcher then plays the dynamic engine's group-priority
     // claiming (an earlier group's pending CTAs take a freed SM first).
     const bool prio = plan->barrier_groups == DS_PLAN_PRIORITY;
     int prio_least = 0, prio_greatest = 0;
     if (prio) DS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    static const int prio_mode = [] {
+        const char* m = getenv("DS_GRAPH_PRIO_MODE");
+        return m ? atoi(m) : 1;
+    }();
     std::vector<std::vector<int>> members(max_group + 1);
     for (int i = 0; i < n; ++i) {
         if (plan->entities[i].group >= 0) members[plan->entities[i].group].push_back(i);
@@ -397,7 +401,15 @@ int build_graph(Exec* E, const ds_exec_plan* plan) {
         DS_CUDA(cudaGraphAddKernelNode(&node[i], E->graph, deps.data(), deps.size(), &kp));
         if (prio) {  // group g's CTAs dispatch before group g+1's whenever both are ready
             cudaKernelNodeAttrValue v{};
-            v.priority = std::min(prio_least, prio_greatest + std::max(0, int(e.group)));
+            const int g = std::max(0, int(e.group)), levels = prio_least - prio_greatest + 1;
+            // groups spread evenly over the device's levels (group 0 highest,
+            // the last group lowest). Same-session A/B (tools/gpu_prio_mode.sh,
+            // C2 mean p50): M = 32 245.9 us vs 250.3 with one level per group
+            // clamped at the lowest (DS_GRAPH_PRIO_MODE=0) and 251.8 with no
+            // priorities (=2); M = 148 and 8 unchanged.
+            v.priority = prio_mode == 0   ? std::min(prio_least, prio_greatest + g)
+                         : prio_mode == 2 ? prio_greatest
+                                          : prio_greatest + g * levels / (max_group + 1);
             DS_CUDA(cudaGraphKernelNodeSetAttribute(node[i], cudaKernelNodeAttributePriority, &v));
         }
     }
